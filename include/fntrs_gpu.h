@@ -1,0 +1,143 @@
+/*
+ * fntrs_gpu.h -- C ABI of the B200-native batched FNT Reed-Solomon codec
+ * over GF(65537) (libfntrs_b200.so). Plain pointers and sizes; no C++ types.
+ *
+ * This is the drop-in boundary for the reference's non-systematic codec
+ * path (/root/reference/proj/include/fntrs/codec.hpp). The reference has no
+ * FFI; its callers link the C++ API statically. Each entry point below says
+ * which reference interface it replaces. The C++ header include/fntrs/codec.hpp
+ * restores the reference's exact C++ API (same namespace, names, signatures,
+ * exception classes) on top of these functions.
+ *
+ * Data model (batched). A stripe is k source packets sharing one erasure
+ * pattern; a packet is L uint16 symbols; codeword j of a stripe is symbol j
+ * of every packet (reference CLI: proj/tools/fntrs_main.cpp:122-139).
+ * Buffers are packet-major: src [stripes][k][L], encoded [stripes][n][L],
+ * received [stripes][k][L], decoded [stripes][k][L], all uint16 in DEVICE
+ * memory. A field value 65536 is stored as word 0 and its symbol index is
+ * listed as an escape (proj/src/shardio.cpp:131-137,153-154,203-208).
+ * Escape lists are ascending uint64 symbol indices into the buffer they
+ * describe (index = row * L + col, row = stripe * rows_per_stripe + packet),
+ * which is the reference's per-shard ascending list, concatenated.
+ *
+ * Errors: every function returns an fntrs_status. Values 1..18 map 1:1 onto
+ * the reference exception classes (proj/include/fntrs/errors.hpp:9-38).
+ * Calls on one context must be serialised by the caller; contexts on
+ * different devices are independent. All work is enqueued on `stream`
+ * (a cudaStream_t, NULL = legacy default stream); device pointers are
+ * caller-owned. There is no CPU fallback: without a usable CUDA device,
+ * fntrs_gpu_create fails with FNTRS_E_CUDA.
+ */
+#ifndef FNTRS_GPU_H
+#define FNTRS_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum fntrs_status {
+    FNTRS_OK = 0,
+    FNTRS_E_ERROR = 1,                  /* fntrs::Error */
+    FNTRS_E_ZERO_INVERSE = 2,           /* fntrs::ZeroInverse */
+    FNTRS_E_INVALID_TRANSFORM_SIZE = 3, /* fntrs::InvalidTransformSize */
+    FNTRS_E_SIZE_MISMATCH = 4,          /* fntrs::SizeMismatch */
+    FNTRS_E_PRODUCT_TOO_LARGE = 5,      /* fntrs::ProductTooLarge */
+    FNTRS_E_DUPLICATE_POINT = 6,        /* fntrs::DuplicatePoint */
+    FNTRS_E_DUPLICATE_POSITION = 7,     /* fntrs::DuplicatePosition */
+    FNTRS_E_POSITION_OUT_OF_RANGE = 8,  /* fntrs::PositionOutOfRange */
+    FNTRS_E_TOO_FEW_POSITIONS = 9,      /* fntrs::TooFewPositions */
+    FNTRS_E_NOT_ENOUGH_SYMBOLS = 10,    /* fntrs::NotEnoughSymbols */
+    FNTRS_E_TOO_MANY_ESCAPES = 11,      /* fntrs::TooManyEscapes (also: escape buffer too small) */
+    FNTRS_E_BAD_MAGIC = 12,
+    FNTRS_E_BAD_VERSION = 13,
+    FNTRS_E_TRUNCATED_SHARD = 14,
+    FNTRS_E_MALFORMED_ESCAPES = 15,
+    FNTRS_E_MALFORMED_HEADER = 16,
+    FNTRS_E_LENGTH_MISMATCH = 17,
+    FNTRS_E_NOT_ENOUGH_SHARDS = 18,
+    FNTRS_E_CUDA = 100,          /* CUDA runtime error; see fntrs_gpu_last_error */
+    FNTRS_E_UNSUPPORTED = 101,   /* shape outside this build (e.g. 2k > 65536) */
+    FNTRS_E_INVALID_ARGUMENT = 102
+} fntrs_status;
+
+typedef struct fntrs_ctx fntrs_ctx;
+typedef struct fntrs_plans fntrs_plans;
+
+/* Library / context. The context owns the twiddle tables (r_m^j for every
+ * m | 65536, both directions) and scratch; replaces the reference's
+ * mutex-guarded plan registry (proj/src/transform.cpp:66-75). */
+int fntrs_gpu_create(int device, fntrs_ctx** out);
+int fntrs_gpu_destroy(fntrs_ctx* ctx);
+const char* fntrs_gpu_status_string(int status);
+const char* fntrs_gpu_last_error(const fntrs_ctx* ctx);
+int fntrs_gpu_device(const fntrs_ctx* ctx);
+const char* fntrs_gpu_version(void);
+
+/* codec::CodeParams::make (proj/src/codec.cpp:112-122): validates
+ * 1 <= k <= n <= 65536 and returns n_domain = next power of two >= n. */
+int fntrs_gpu_code_params(uint32_t k, uint32_t n, uint32_t* n_domain);
+
+/* Batched codec::encode_nonsystematic (proj/src/codec.cpp:124-131): for every
+ * codeword, zero-pad the k source symbols to n_domain, forward FNT, keep the
+ * first n outputs.
+ *   src      [stripes][k][L] uint16;  src_esc: n_src_esc sorted indices into src
+ *   out      [stripes][n][L] uint16;  out_esc: capacity esc_cap (uint64)
+ *   n_out_esc  DEVICE uint64 receiving the true escape count; when it exceeds
+ *              esc_cap only esc_cap entries were kept and the list is invalid. */
+int fntrs_gpu_encode(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t stripes, uint32_t L,
+                     const uint16_t* src, const uint64_t* src_esc, uint64_t n_src_esc,
+                     uint16_t* out, uint64_t* out_esc, uint64_t esc_cap, uint64_t* n_out_esc,
+                     void* stream);
+
+/* Once-per-erasure-pattern decode plans: interp::build_plan / plan_for
+ * (proj/src/interp.cpp:23-101), batched over patterns, computed on the GPU.
+ * positions: HOST array [npatterns][kp]; pattern p lists the kp received
+ * positions (distinct, < n) in the order the received packets will follow.
+ * kp must equal k, or n when n == n_domain (complete reception: decode is
+ * one inverse transform, codec.cpp:137-144). */
+int fntrs_gpu_plans_create(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t kp,
+                           uint32_t npatterns, const uint32_t* positions, fntrs_plans** out,
+                           void* stream);
+int fntrs_gpu_plans_destroy(fntrs_plans* plans);
+uint32_t fntrs_gpu_plans_count(const fntrs_plans* plans);
+
+/* DecodePlan fields of one pattern (proj/include/fntrs/interp.hpp:18-32), to
+ * HOST buffers: a_coeffs [kp+1] (the locator A, monic), aprime_inv [kp],
+ * *product_size, a_fnt [product_size] (dif_forward order, bit-reversed).
+ * Synchronises the context's internal stream. */
+int fntrs_gpu_plans_export(fntrs_ctx* ctx, const fntrs_plans* plans, uint32_t pattern,
+                           uint32_t* a_coeffs, uint32_t* aprime_inv, uint32_t* product_size,
+                           uint32_t* a_fnt);
+
+/* Batched codec::decode_nonsystematic (proj/src/codec.cpp:133-149 ->
+ * interp::interpolate, interp.cpp:103-137).
+ *   stripe_pattern DEVICE [stripes] uint32: plan index of each stripe
+ *   rx   [stripes][kp][L] uint16: row i of stripe s is the packet received at
+ *        position i of that stripe's pattern;  rx_esc sorted indices into rx
+ *   out  [stripes][k][L] uint16 decoded source packets; out_esc as in encode */
+int fntrs_gpu_decode(fntrs_ctx* ctx, const fntrs_plans* plans, uint32_t stripes, uint32_t L,
+                     const uint32_t* stripe_pattern, const uint16_t* rx, const uint64_t* rx_esc,
+                     uint64_t n_rx_esc, uint16_t* out, uint64_t* out_esc, uint64_t esc_cap,
+                     uint64_t* n_out_esc, void* stream);
+
+/* fnt_forward / fnt_inverse (proj/src/transform.cpp:302-323) over the columns
+ * of a DEVICE [m][L] uint32 array of canonical values; natural order. */
+int fntrs_gpu_fnt(fntrs_ctx* ctx, uint32_t m, int inverse, uint32_t L, const uint32_t* in,
+                  uint32_t* out, void* stream);
+
+/* Seeded synthetic source symbols (benchmark workload):
+ * out[i] = low 16 bits of output number (first_index + i) of the splitmix64
+ * stream seeded with `seed` (state_j = seed + (j+1) * 0x9E3779B97F4A7C15).
+ * DEVICE buffer; the same generator is restated in numpy for the tests. */
+int fntrs_gpu_fill_symbols(uint64_t seed, uint64_t first_index, uint64_t count, uint16_t* out,
+                           void* stream);
+
+/* Launch accounting: number of kernels this context has launched. */
+uint64_t fntrs_gpu_launch_count(const fntrs_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FNTRS_GPU_H */

@@ -1,0 +1,237 @@
+// oracle/ref_shim.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// extern "C" entry points over the UNMODIFIED reference library, compiled
+// from /root/reference/proj/src with -Dfntrs=fntrs_ref (oracle/Makefile) into
+// oracle/_ref/libfntrs_ref.so. Used by tests/ to pin the oracle restatement
+// against the reference itself, and by bench.py (--impl reference and the
+// cpu_baseline leg) to time the reference's own CPU codec on the host.
+//
+// The batched entry points mirror the reference CLI's codeword loop:
+// gather column j of packet-major stripes, call codec::encode_nonsystematic /
+// decode_nonsystematic once per codeword, scatter the result
+// (proj/tools/fntrs_main.cpp:122-139,222-231), on `threads` workers pulling
+// codeword indices from an atomic counter like for_each_stripe (:72-106).
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "fntrs/codec.hpp"
+#include "fntrs/errors.hpp"
+#include "fntrs/interp.hpp"
+#include "fntrs/transform.hpp"
+
+using namespace fntrs;
+
+namespace {
+
+int status_of(const std::exception& e) {
+    if (dynamic_cast<const ZeroInverse*>(&e)) return 2;
+    if (dynamic_cast<const InvalidTransformSize*>(&e)) return 3;
+    if (dynamic_cast<const SizeMismatch*>(&e)) return 4;
+    if (dynamic_cast<const ProductTooLarge*>(&e)) return 5;
+    if (dynamic_cast<const DuplicatePoint*>(&e)) return 6;
+    if (dynamic_cast<const DuplicatePosition*>(&e)) return 7;
+    if (dynamic_cast<const PositionOutOfRange*>(&e)) return 8;
+    if (dynamic_cast<const TooFewPositions*>(&e)) return 9;
+    if (dynamic_cast<const NotEnoughSymbols*>(&e)) return 10;
+    if (dynamic_cast<const TooManyEscapes*>(&e)) return 11;
+    return 1;
+}
+
+codec::Path path_of(int p) {
+    return p == 1 ? codec::Path::Fast : p == 2 ? codec::Path::Direct : codec::Path::Auto;
+}
+
+uint32_t fetch(const uint16_t* base, const uint64_t* esc, uint64_t ne, uint64_t row, uint32_t col,
+               uint32_t L) {
+    uint16_t w = base[row * L + col];
+    if (w || !ne) return w;
+    const uint64_t key = (row << 32) | col;
+    return std::binary_search(esc, esc + ne, key) ? 65536u : 0u;
+}
+
+template <typename Fn>
+int run_parallel(uint64_t items, unsigned threads, Fn&& fn) {
+    threads = std::max(1u, threads);
+    std::atomic<uint64_t> next{0};
+    std::atomic<int> status{0};
+    auto worker = [&](unsigned w) {
+        for (;;) {
+            uint64_t t = next.fetch_add(1);
+            if (t >= items || status.load()) return;
+            try {
+                fn(w, t);
+            } catch (const std::exception& e) {
+                int expected = 0;
+                status.compare_exchange_strong(expected, status_of(e));
+                return;
+            }
+        }
+    };
+    if (threads == 1) {
+        worker(0);
+    } else {
+        std::vector<std::thread> pool;
+        for (unsigned w = 0; w < threads; ++w) pool.emplace_back(worker, w);
+        for (auto& th : pool) th.join();
+    }
+    return status.load();
+}
+
+}  // namespace
+
+extern "C" {
+
+int ref_fnt_forward(uint32_t n, const uint32_t* in, uint32_t* out) {
+    try {
+        auto v = fnt_forward(plan_for(n), std::span<const Fe>(in, n));
+        std::copy(v.begin(), v.end(), out);
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+int ref_fnt_inverse(uint32_t n, const uint32_t* in, uint32_t* out) {
+    try {
+        auto v = fnt_inverse(plan_for(n), std::span<const Fe>(in, n));
+        std::copy(v.begin(), v.end(), out);
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+int ref_encode(uint32_t k, uint32_t n, uint32_t src_len, const uint32_t* src, uint32_t* out) {
+    try {
+        auto params = codec::CodeParams::make(k, n, false);
+        auto v = codec::encode_nonsystematic(params, std::span<const Fe>(src, src_len));
+        std::copy(v.begin(), v.end(), out);
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+int ref_decode(uint32_t k, uint32_t n, uint32_t count, const uint32_t* pos, const uint32_t* val,
+               int path, uint32_t* out) {
+    try {
+        auto params = codec::CodeParams::make(k, n, false);
+        codec::Codeword rx(count);
+        for (uint32_t i = 0; i < count; ++i) rx[i] = {pos[i], val[i]};
+        auto v = codec::decode_nonsystematic(params, rx, path_of(path));
+        std::copy(v.begin(), v.end(), out);
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+// DecodePlan fields (proj/include/fntrs/interp.hpp:18-32).
+int ref_build_plan(uint32_t n, uint32_t k, const uint32_t* positions, uint32_t* a_out,
+                   uint32_t* a_len, uint32_t* aprime_inv, uint32_t* product_size,
+                   uint32_t* a_fnt) {
+    try {
+        auto plan = interp::build_plan(n, std::span<const uint32_t>(positions, k));
+        const auto& a = plan.a();
+        *a_len = static_cast<uint32_t>(a.size());
+        std::copy(a.begin(), a.end(), a_out);
+        std::copy(plan.aprime_at_x_inv.begin(), plan.aprime_at_x_inv.end(), aprime_inv);
+        *product_size = plan.product_size;
+        if (a_fnt) std::copy(plan.a_fnt.begin(), plan.a_fnt.end(), a_fnt);
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+// CLI-style batched encode over packet-major stripes. Returns the escape
+// count (sorted keys row<<32|col in out_esc) or a negative status.
+int64_t ref_encode_stripes(uint32_t k, uint32_t n, uint32_t stripes, uint32_t L,
+                           const uint16_t* src, const uint64_t* src_esc, uint64_t n_src_esc,
+                           uint16_t* out, uint64_t* out_esc, uint64_t esc_cap, unsigned threads) {
+    codec::CodeParams params;
+    try {
+        params = codec::CodeParams::make(k, n, false);
+    } catch (const std::exception& e) {
+        return -status_of(e);
+    }
+    std::mutex mu;
+    std::vector<uint64_t> escapes;
+    int st = run_parallel(uint64_t(stripes) * L, threads, [&](unsigned, uint64_t t) {
+        const uint32_t s = uint32_t(t / L), j = uint32_t(t % L);
+        std::vector<Fe> col(k);
+        for (uint32_t i = 0; i < k; ++i) col[i] = fetch(src, src_esc, n_src_esc, uint64_t(s) * k + i, j, L);
+        std::vector<Fe> enc = codec::encode_nonsystematic(params, col);
+        for (uint32_t i = 0; i < n; ++i) {
+            const uint64_t row = uint64_t(s) * n + i;
+            out[row * L + j] = enc[i] == 65536 ? 0 : uint16_t(enc[i]);
+            if (enc[i] == 65536) {
+                std::lock_guard<std::mutex> lock(mu);
+                escapes.push_back((row << 32) | j);
+            }
+        }
+    });
+    if (st) return -st;
+    if (escapes.size() > esc_cap) return -11;
+    std::sort(escapes.begin(), escapes.end());
+    std::copy(escapes.begin(), escapes.end(), out_esc);
+    return int64_t(escapes.size());
+}
+
+// CLI-style batched decode; each stripe s uses pattern stripe_pattern[s]
+// (k ascending positions), rx rows s*k+i carry the packet at position i of
+// that pattern. path: 0 Auto, 1 Fast, 2 Direct (codec.hpp:39).
+int64_t ref_decode_stripes(uint32_t k, uint32_t n, uint32_t stripes, uint32_t L,
+                           uint32_t npatterns, const uint32_t* patterns,
+                           const uint32_t* stripe_pattern, const uint16_t* rx,
+                           const uint64_t* rx_esc, uint64_t n_rx_esc, uint16_t* out,
+                           uint64_t* out_esc, uint64_t esc_cap, int path, unsigned threads) {
+    codec::CodeParams params;
+    try {
+        params = codec::CodeParams::make(k, n, false);
+    } catch (const std::exception& e) {
+        return -status_of(e);
+    }
+    for (uint32_t s = 0; s < stripes; ++s)
+        if (stripe_pattern[s] >= npatterns) return -1;
+    std::mutex mu;
+    std::vector<uint64_t> escapes;
+    const codec::Path p = path_of(path);
+    int st = run_parallel(uint64_t(stripes) * L, threads, [&](unsigned, uint64_t t) {
+        const uint32_t s = uint32_t(t / L), j = uint32_t(t % L);
+        const uint32_t* pos = patterns + uint64_t(stripe_pattern[s]) * k;
+        codec::Codeword cw(k);
+        for (uint32_t i = 0; i < k; ++i)
+            cw[i] = {pos[i], fetch(rx, rx_esc, n_rx_esc, uint64_t(s) * k + i, j, L)};
+        std::vector<Fe> dec = codec::decode_nonsystematic(params, cw, p);
+        for (uint32_t i = 0; i < k; ++i) {
+            const uint64_t row = uint64_t(s) * k + i;
+            out[row * L + j] = dec[i] == 65536 ? 0 : uint16_t(dec[i]);
+            if (dec[i] == 65536) {
+                std::lock_guard<std::mutex> lock(mu);
+                escapes.push_back((row << 32) | j);
+            }
+        }
+    });
+    if (st) return -st;
+    if (escapes.size() > esc_cap) return -11;
+    std::sort(escapes.begin(), escapes.end());
+    std::copy(escapes.begin(), escapes.end(), out_esc);
+    return int64_t(escapes.size());
+}
+
+int ref_has_avx2(void) {
+#if defined(__x86_64__)
+    return __builtin_cpu_supports("avx2") ? 1 : 0;
+#else
+    return 0;
+#endif
+}
+
+}  // extern "C"

@@ -1,0 +1,395 @@
+// capi.cu -- the extern "C" boundary (include/fntrs_gpu.h).
+//
+// Host-side responsibilities only: argument validation with the reference's
+// error classes, plan storage, kernel launches, and canonical ordering of
+// escape lists (a CUB radix sort of the few escaped symbol indices). All
+// codec arithmetic runs in the CUDA kernels; there is no CPU path.
+#include <cuda_runtime.h>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/fntrs_gpu.h"
+#include "field.cuh"
+#include "internal.h"
+
+using namespace fntrs_gpu;
+
+struct fntrs_ctx {
+    int device = 0;
+    Tables tab;
+    cudaStream_t internal = nullptr;
+    void* sort_tmp = nullptr;
+    size_t sort_tmp_bytes = 0;
+    unsigned long long* sort_alt = nullptr;
+    uint64_t sort_alt_cap = 0;
+    uint64_t launches = 0;
+    std::string err;
+};
+
+struct fntrs_plans {
+    int device = 0;
+    uint32_t k = 0, n = 0, N = 0, M = 0, kp = 0, np = 0;
+    uint32_t* pos = nullptr;
+    uint32_t* ainv = nullptr;
+    uint32_t* ahat = nullptr;
+    uint32_t ninv = 1;
+};
+
+namespace {
+
+const char* kVersion = "fntrs_b200 0.1 (sm_100a)";
+
+uint32_t next_pow2(uint32_t n) {
+    uint32_t m = 1;
+    while (m < n) m <<= 1;
+    return m;
+}
+
+int cuda_fail(fntrs_ctx* ctx, cudaError_t e, const char* where) {
+    if (ctx) ctx->err = std::string(where) + ": " + cudaGetErrorString(e);
+    return FNTRS_E_CUDA;
+}
+
+int fail(fntrs_ctx* ctx, int status, const std::string& msg) {
+    if (ctx) ctx->err = msg;
+    return status;
+}
+
+#define CK(call, where)                                   \
+    do {                                                  \
+        cudaError_t _e = (call);                          \
+        if (_e != cudaSuccess) return cuda_fail(ctx, _e, where); \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+int end_bit_for(uint64_t max_key) {
+    int b = 1;
+    while (b < 64 && (max_key >> b)) ++b;
+    return b;
+}
+
+// Escape finalisation: keys[0..cap) were pre-filled with ~0 and partially
+// overwritten by the kernel's appends; sorting the whole buffer puts the
+// real indices first, ascending (the reference's per-shard order).
+int sort_escapes(fntrs_ctx* ctx, unsigned long long* keys, uint64_t cap, uint64_t max_key,
+                 cudaStream_t st) {
+    if (cap <= 1) return FNTRS_OK;
+    if (cap > 0x7FFFFFFFull) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "escape capacity too large");
+    if (ctx->sort_alt_cap < cap) {
+        if (ctx->sort_alt) cudaFree(ctx->sort_alt);
+        ctx->sort_alt = nullptr;
+        CK(cudaMalloc(&ctx->sort_alt, cap * sizeof(unsigned long long)), "escape scratch");
+        ctx->sort_alt_cap = cap;
+    }
+    cub::DoubleBuffer<unsigned long long> db(keys, ctx->sort_alt);
+    // Keys past the real ones are all ~0; sort the full word so they stay last.
+    (void)max_key;
+    const int end_bit = 64;
+    size_t need = 0;
+    CK(cub::DeviceRadixSort::SortKeys(nullptr, need, db, int(cap), 0, end_bit, st), "escape sort size");
+    if (need > ctx->sort_tmp_bytes) {
+        if (ctx->sort_tmp) cudaFree(ctx->sort_tmp);
+        ctx->sort_tmp = nullptr;
+        CK(cudaMalloc(&ctx->sort_tmp, need), "escape sort scratch");
+        ctx->sort_tmp_bytes = need;
+    }
+    CK(cub::DeviceRadixSort::SortKeys(ctx->sort_tmp, need, db, int(cap), 0, end_bit, st), "escape sort");
+    ctx->launches += 2 * 8;  // onesweep: histogram + 8 digit passes (approximate)
+    if (db.Current() != keys)
+        CK(cudaMemcpyAsync(keys, db.Current(), cap * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st),
+           "escape copy");
+    return FNTRS_OK;
+}
+
+int prep_escapes(fntrs_ctx* ctx, uint64_t* out_esc, uint64_t esc_cap, uint64_t* n_out_esc, cudaStream_t st) {
+    if (!n_out_esc) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "n_out_esc must be a device pointer");
+    if (esc_cap && !out_esc) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "out_esc is null");
+    CK(cudaMemsetAsync(n_out_esc, 0, sizeof(uint64_t), st), "escape count reset");
+    if (esc_cap) CK(cudaMemsetAsync(out_esc, 0xFF, esc_cap * sizeof(uint64_t), st), "escape fill");
+    return FNTRS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fntrs_gpu_version(void) { return kVersion; }
+
+const char* fntrs_gpu_status_string(int s) {
+    switch (s) {
+        case FNTRS_OK: return "ok";
+        case FNTRS_E_ERROR: return "Error";
+        case FNTRS_E_ZERO_INVERSE: return "ZeroInverse";
+        case FNTRS_E_INVALID_TRANSFORM_SIZE: return "InvalidTransformSize";
+        case FNTRS_E_SIZE_MISMATCH: return "SizeMismatch";
+        case FNTRS_E_PRODUCT_TOO_LARGE: return "ProductTooLarge";
+        case FNTRS_E_DUPLICATE_POINT: return "DuplicatePoint";
+        case FNTRS_E_DUPLICATE_POSITION: return "DuplicatePosition";
+        case FNTRS_E_POSITION_OUT_OF_RANGE: return "PositionOutOfRange";
+        case FNTRS_E_TOO_FEW_POSITIONS: return "TooFewPositions";
+        case FNTRS_E_NOT_ENOUGH_SYMBOLS: return "NotEnoughSymbols";
+        case FNTRS_E_TOO_MANY_ESCAPES: return "TooManyEscapes";
+        case FNTRS_E_BAD_MAGIC: return "BadMagic";
+        case FNTRS_E_BAD_VERSION: return "BadVersion";
+        case FNTRS_E_TRUNCATED_SHARD: return "TruncatedShard";
+        case FNTRS_E_MALFORMED_ESCAPES: return "MalformedEscapes";
+        case FNTRS_E_MALFORMED_HEADER: return "MalformedHeader";
+        case FNTRS_E_LENGTH_MISMATCH: return "LengthMismatch";
+        case FNTRS_E_NOT_ENOUGH_SHARDS: return "NotEnoughShards";
+        case FNTRS_E_CUDA: return "CudaError";
+        case FNTRS_E_UNSUPPORTED: return "Unsupported";
+        case FNTRS_E_INVALID_ARGUMENT: return "InvalidArgument";
+        default: return "unknown";
+    }
+}
+
+const char* fntrs_gpu_last_error(const fntrs_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+int fntrs_gpu_device(const fntrs_ctx* ctx) { return ctx ? ctx->device : -1; }
+uint64_t fntrs_gpu_launch_count(const fntrs_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int fntrs_gpu_code_params(uint32_t k, uint32_t n, uint32_t* n_domain) {
+    if (k < 1 || k > n || n > 65536) return FNTRS_E_SIZE_MISMATCH;
+    if (n_domain) *n_domain = next_pow2(n);
+    return FNTRS_OK;
+}
+
+int fntrs_gpu_create(int device, fntrs_ctx** out) {
+    if (!out) return FNTRS_E_INVALID_ARGUMENT;
+    *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count <= 0 || device < 0 || device >= count)
+        return FNTRS_E_CUDA;
+    auto* ctx = new fntrs_ctx;
+    ctx->device = device;
+    DeviceGuard g(device);
+    cudaError_t e = cudaStreamCreateWithFlags(&ctx->internal, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = build_tables(ctx->tab, ctx->internal);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->internal);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return FNTRS_E_CUDA;
+    }
+    ctx->launches = 1;
+    *out = ctx;
+    return FNTRS_OK;
+}
+
+int fntrs_gpu_destroy(fntrs_ctx* ctx) {
+    if (!ctx) return FNTRS_OK;
+    DeviceGuard g(ctx->device);
+    cudaFree(ctx->tab.fwd);
+    cudaFree(ctx->tab.inv);
+    cudaFree(ctx->sort_tmp);
+    cudaFree(ctx->sort_alt);
+    if (ctx->internal) cudaStreamDestroy(ctx->internal);
+    delete ctx;
+    return FNTRS_OK;
+}
+
+int fntrs_gpu_encode(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t stripes, uint32_t L,
+                     const uint16_t* src, const uint64_t* src_esc, uint64_t n_src_esc, uint16_t* out,
+                     uint64_t* out_esc, uint64_t esc_cap, uint64_t* n_out_esc, void* stream) {
+    if (!ctx) return FNTRS_E_INVALID_ARGUMENT;
+    uint32_t N = 0;
+    if (fntrs_gpu_code_params(k, n, &N))
+        return fail(ctx, FNTRS_E_SIZE_MISMATCH, "code parameters need 1 <= k <= n <= 65536, got k = " +
+                                                    std::to_string(k) + ", n = " + std::to_string(n));
+    if (N > kTileMaxN) return fail(ctx, FNTRS_E_UNSUPPORTED, "n_domain > 4096 not in this build yet");
+    if (stripes && L && (!src || !out)) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "null buffer");
+    if (n_src_esc && !src_esc) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "src_esc is null");
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int rc = prep_escapes(ctx, out_esc, esc_cap, n_out_esc, st);
+    if (rc) return rc;
+    EscIn ein{reinterpret_cast<const unsigned long long*>(src_esc), n_src_esc};
+    EscOut eout{reinterpret_cast<unsigned long long*>(out_esc), reinterpret_cast<unsigned long long*>(n_out_esc),
+                esc_cap};
+    CK(launch_encode_tile(ctx->tab, k, n, N, stripes, L, src, ein, out, eout, st), "encode launch");
+    ctx->launches += 1;
+    return sort_escapes(ctx, eout.keys, esc_cap, uint64_t(stripes) * n * L, st);
+}
+
+int fntrs_gpu_plans_create(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t kp, uint32_t npatterns,
+                           const uint32_t* positions, fntrs_plans** out, void* stream) {
+    if (!ctx || !out) return FNTRS_E_INVALID_ARGUMENT;
+    *out = nullptr;
+    uint32_t N = 0;
+    if (fntrs_gpu_code_params(k, n, &N))
+        return fail(ctx, FNTRS_E_SIZE_MISMATCH, "code parameters need 1 <= k <= n <= 65536");
+    const bool full = (kp == n && n == N);
+    if (kp < k) return fail(ctx, FNTRS_E_NOT_ENOUGH_SYMBOLS, "have " + std::to_string(kp) + " symbols, need " + std::to_string(k));
+    if (kp != k && !full)
+        return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "kp must equal k (or n for complete reception)");
+    if (2ull * k > 65536ull && !full)
+        return fail(ctx, FNTRS_E_UNSUPPORTED, "2k > 65536 needs the split product (mul_low), not in this build");
+    const uint32_t M = full ? N : next_pow2(2 * k);
+    if (N > kTileMaxN || M > kTileMaxN) return fail(ctx, FNTRS_E_UNSUPPORTED, "transform sizes > 4096 not in this build yet");
+    if (npatterns && !positions) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "positions is null");
+    // validation (codec.cpp:32-48 order: range first, then duplicates)
+    std::vector<uint8_t> seen(n);
+    for (uint32_t p = 0; p < npatterns; ++p) {
+        const uint32_t* z = positions + size_t(p) * kp;
+        for (uint32_t i = 0; i < kp; ++i)
+            if (z[i] >= n)
+                return fail(ctx, FNTRS_E_POSITION_OUT_OF_RANGE, "received position " + std::to_string(z[i]) +
+                                                                   " not below n = " + std::to_string(n));
+        std::fill(seen.begin(), seen.end(), 0);
+        for (uint32_t i = 0; i < kp; ++i) {
+            if (seen[z[i]]) return fail(ctx, FNTRS_E_DUPLICATE_POSITION, "received position " + std::to_string(z[i]) + " repeats");
+            seen[z[i]] = 1;
+        }
+    }
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    auto* pl = new fntrs_plans;
+    pl->device = ctx->device;
+    pl->k = k;
+    pl->n = n;
+    pl->N = N;
+    pl->M = M;
+    pl->kp = kp;
+    pl->np = npatterns;
+    pl->ninv = cpow(N % kP, kP - 2);
+    const size_t npos = size_t(npatterns) * kp;
+    cudaError_t e = cudaSuccess;
+    if (npatterns) {
+        e = cudaMalloc(&pl->pos, npos * 4);
+        if (!e) e = cudaMalloc(&pl->ainv, npos * 4);
+        if (!e) e = cudaMalloc(&pl->ahat, size_t(npatterns) * M * 4);
+        if (!e) e = cudaMemcpyAsync(pl->pos, positions, npos * 4, cudaMemcpyHostToDevice, st);
+        if (!e && !full) {
+            e = launch_plan_build(N, M, kp, npatterns, pl->pos, pl->ainv, pl->ahat, ctx->tab, st);
+            ctx->launches += 1;
+        }
+    }
+    if (e) {
+        fntrs_gpu_plans_destroy(pl);
+        return cuda_fail(ctx, e, "plan build");
+    }
+    *out = pl;
+    return FNTRS_OK;
+}
+
+int fntrs_gpu_plans_destroy(fntrs_plans* pl) {
+    if (!pl) return FNTRS_OK;
+    DeviceGuard g(pl->device);
+    cudaFree(pl->pos);
+    cudaFree(pl->ainv);
+    cudaFree(pl->ahat);
+    delete pl;
+    return FNTRS_OK;
+}
+
+uint32_t fntrs_gpu_plans_count(const fntrs_plans* pl) { return pl ? pl->np : 0; }
+
+int fntrs_gpu_plans_export(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t pattern, uint32_t* a_coeffs,
+                           uint32_t* aprime_inv, uint32_t* product_size, uint32_t* a_fnt) {
+    if (!ctx || !pl) return FNTRS_E_INVALID_ARGUMENT;
+    if (pattern >= pl->np) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "pattern out of range");
+    if (pl->kp == pl->N && pl->kp != pl->k) return fail(ctx, FNTRS_E_UNSUPPORTED, "complete-reception plans carry no locator");
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = ctx->internal;
+    const uint32_t M = pl->M, kp = pl->kp;
+    uint32_t *acoef = nullptr, *spec = nullptr;
+    CK(cudaMalloc(&acoef, M * 4), "export alloc");
+    CK(cudaMalloc(&spec, M * 4), "export alloc");
+    // A = IFNT_M(A_hat) = -IFNT_unscaled(ahat) since ahat = -A_hat / M
+    const uint32_t* ah = pl->ahat + size_t(pattern) * M;
+    CK(launch_fnt_tile(ctx->tab, M, true, kP - 1u, 1, ah, acoef, st), "export ifnt");
+    CK(launch_fnt_tile(ctx->tab, M, false, 1u, 1, acoef, spec, st), "export fnt");
+    ctx->launches += 2;
+    std::vector<uint32_t> a(M), sp(M);
+    CK(cudaMemcpyAsync(a.data(), acoef, M * 4, cudaMemcpyDeviceToHost, st), "export copy");
+    CK(cudaMemcpyAsync(sp.data(), spec, M * 4, cudaMemcpyDeviceToHost, st), "export copy");
+    if (aprime_inv)
+        CK(cudaMemcpyAsync(aprime_inv, pl->ainv + size_t(pattern) * kp, kp * 4, cudaMemcpyDeviceToHost, st),
+           "export copy");
+    CK(cudaStreamSynchronize(st), "export sync");
+    cudaFree(acoef);
+    cudaFree(spec);
+    if (a_coeffs) std::memcpy(a_coeffs, a.data(), size_t(kp + 1 <= M ? kp + 1 : M) * 4);
+    if (product_size) *product_size = M;
+    if (a_fnt) {  // dif_forward leaves the spectrum in bit-reversed order (transform.hpp:43-48)
+        int lg = 0;
+        while ((1u << lg) < M) ++lg;
+        for (uint32_t i = 0; i < M; ++i) {
+            uint32_t r = 0;
+            for (int b = 0; b < lg; ++b) r |= ((i >> b) & 1u) << (lg - 1 - b);
+            a_fnt[i] = sp[r];
+        }
+    }
+    return FNTRS_OK;
+}
+
+int fntrs_gpu_decode(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t stripes, uint32_t L,
+                     const uint32_t* stripe_pattern, const uint16_t* rx, const uint64_t* rx_esc,
+                     uint64_t n_rx_esc, uint16_t* out, uint64_t* out_esc, uint64_t esc_cap,
+                     uint64_t* n_out_esc, void* stream) {
+    if (!ctx || !pl) return FNTRS_E_INVALID_ARGUMENT;
+    if (pl->device != ctx->device) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "plans belong to another device");
+    if (stripes && L && (!rx || !out || !stripe_pattern)) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "null buffer");
+    if (stripes && !pl->np) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "no plans");
+    if (n_rx_esc && !rx_esc) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "rx_esc is null");
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int rc = prep_escapes(ctx, out_esc, esc_cap, n_out_esc, st);
+    if (rc) return rc;
+    PlanView pv{pl->N, pl->M, pl->kp, pl->k, pl->np, pl->pos, pl->ainv, pl->ahat, pl->ninv};
+    EscIn ein{reinterpret_cast<const unsigned long long*>(rx_esc), n_rx_esc};
+    EscOut eout{reinterpret_cast<unsigned long long*>(out_esc), reinterpret_cast<unsigned long long*>(n_out_esc),
+                esc_cap};
+    CK(launch_decode_tile(ctx->tab, pv, stripes, L, stripe_pattern, rx, ein, out, eout, st), "decode launch");
+    ctx->launches += 1;
+    return sort_escapes(ctx, eout.keys, esc_cap, uint64_t(stripes) * pl->k * L, st);
+}
+
+int fntrs_gpu_fnt(fntrs_ctx* ctx, uint32_t m, int inverse, uint32_t L, const uint32_t* in, uint32_t* out,
+                  void* stream) {
+    if (!ctx) return FNTRS_E_INVALID_ARGUMENT;
+    if (m == 0 || m > 65536 || (m & (m - 1)))
+        return fail(ctx, FNTRS_E_INVALID_TRANSFORM_SIZE, "transform size must be a power of two in [1, 65536]");
+    if (m > kTileMaxN) return fail(ctx, FNTRS_E_UNSUPPORTED, "transform sizes > 4096 not in this build yet");
+    if (L && (!in || !out)) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "null buffer");
+    DeviceGuard g(ctx->device);
+    const uint32_t scale = inverse ? cpow(m % kP, kP - 2) : 1u;
+    CK(launch_fnt_tile(ctx->tab, m, inverse != 0, scale, L, in, out, static_cast<cudaStream_t>(stream)), "fnt launch");
+    ctx->launches += 1;
+    return FNTRS_OK;
+}
+
+}  // extern "C"
+
+namespace {
+__global__ void fill_symbols_kernel(uint64_t seed, uint64_t first, uint64_t count, uint16_t* out) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        uint64_t z = seed + (first + i + 1) * 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        out[i] = uint16_t(z);
+    }
+}
+}  // namespace
+
+extern "C" int fntrs_gpu_fill_symbols(uint64_t seed, uint64_t first_index, uint64_t count, uint16_t* out,
+                                      void* stream) {
+    if (!count) return FNTRS_OK;
+    if (!out) return FNTRS_E_INVALID_ARGUMENT;
+    fill_symbols_kernel<<<148 * 16, 256, 0, static_cast<cudaStream_t>(stream)>>>(seed, first_index, count, out);
+    return cudaGetLastError() == cudaSuccess ? FNTRS_OK : FNTRS_E_CUDA;
+}

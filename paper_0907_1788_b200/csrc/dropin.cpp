@@ -1,0 +1,281 @@
+// dropin.cpp -- the reference's C++ codec API (include/fntrs/codec.hpp) over
+// the C ABI (include/fntrs_gpu.h). Host work here is the reference's own
+// host logic -- argument validation, sorting the received symbols
+// (proj/src/codec.cpp:32-48), the 16-entry decode-plan LRU
+// (proj/src/interp.cpp:70-101) -- plus marshalling Fe <-> uint16 + escapes.
+// All arithmetic runs on the GPU.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <list>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "fntrs/codec.hpp"
+#include "fntrs_gpu.h"
+
+namespace fntrs {
+
+void throw_status(int status, const std::string& msg) {
+    switch (status) {
+        case FNTRS_E_ZERO_INVERSE: throw ZeroInverse(msg);
+        case FNTRS_E_INVALID_TRANSFORM_SIZE: throw InvalidTransformSize(msg);
+        case FNTRS_E_SIZE_MISMATCH: throw SizeMismatch(msg);
+        case FNTRS_E_PRODUCT_TOO_LARGE: throw ProductTooLarge(msg);
+        case FNTRS_E_DUPLICATE_POINT: throw DuplicatePoint(msg);
+        case FNTRS_E_DUPLICATE_POSITION: throw DuplicatePosition(msg);
+        case FNTRS_E_POSITION_OUT_OF_RANGE: throw PositionOutOfRange(msg);
+        case FNTRS_E_TOO_FEW_POSITIONS: throw TooFewPositions(msg);
+        case FNTRS_E_NOT_ENOUGH_SYMBOLS: throw NotEnoughSymbols(msg);
+        case FNTRS_E_TOO_MANY_ESCAPES: throw TooManyEscapes(msg);
+        case FNTRS_E_BAD_MAGIC: throw BadMagic(msg);
+        case FNTRS_E_BAD_VERSION: throw BadVersion(msg);
+        case FNTRS_E_TRUNCATED_SHARD: throw TruncatedShard(msg);
+        case FNTRS_E_MALFORMED_ESCAPES: throw MalformedEscapes(msg);
+        case FNTRS_E_MALFORMED_HEADER: throw MalformedHeader(msg);
+        case FNTRS_E_LENGTH_MISMATCH: throw LengthMismatch(msg);
+        case FNTRS_E_NOT_ENOUGH_SHARDS: throw NotEnoughShards(msg);
+        default: throw Error(msg);
+    }
+}
+
+namespace {
+
+// One shared context + scratch for the per-codeword API; calls serialise on
+// its mutex (the C ABI requires serialised calls per context).
+struct Shared {
+    std::mutex mu;
+    int device = 0;
+    fntrs_ctx* ctx = nullptr;
+    cudaStream_t stream = nullptr;
+    // device scratch
+    void* dbuf = nullptr;
+    size_t dbuf_bytes = 0;
+    // plan LRU (interp.cpp:70-101): key (n, k, kp, positions)
+    using Key = std::pair<std::vector<uint32_t>, std::vector<uint32_t>>;
+    std::list<std::pair<Key, fntrs_plans*>> lru;
+    static constexpr size_t kCapacity = 16;
+
+    ~Shared() {
+        for (auto& e : lru) fntrs_gpu_plans_destroy(e.second);
+        if (dbuf) cudaFree(dbuf);
+        if (stream) cudaStreamDestroy(stream);
+        if (ctx) fntrs_gpu_destroy(ctx);
+    }
+
+    void check(int status) {
+        if (status) throw_status(status, std::string(fntrs_gpu_status_string(status)) + ": " +
+                                             fntrs_gpu_last_error(ctx));
+    }
+
+    void ensure() {
+        if (ctx) return;
+        int rc = fntrs_gpu_create(device, &ctx);
+        if (rc) {
+            ctx = nullptr;
+            throw Error("fntrs: no usable CUDA device " + std::to_string(device) +
+                        " (the codec has no CPU fallback)");
+        }
+        cudaSetDevice(device);
+        if (cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking) != cudaSuccess)
+            throw Error("fntrs: cannot create a CUDA stream");
+    }
+
+    void* scratch(size_t bytes) {
+        if (bytes > dbuf_bytes) {
+            if (dbuf) cudaFree(dbuf);
+            dbuf = nullptr;
+            if (cudaMalloc(&dbuf, bytes) != cudaSuccess) throw Error("fntrs: device allocation failed");
+            dbuf_bytes = bytes;
+        }
+        return dbuf;
+    }
+
+    void sync() {
+        cudaError_t e = cudaStreamSynchronize(stream);
+        if (e != cudaSuccess) throw Error(std::string("fntrs: CUDA error: ") + cudaGetErrorString(e));
+    }
+
+    fntrs_plans* plan_for(uint32_t k, uint32_t n, const std::vector<uint32_t>& pos) {
+        Key key{{n, k, uint32_t(pos.size())}, pos};
+        for (auto it = lru.begin(); it != lru.end(); ++it)
+            if (it->first == key) {
+                lru.splice(lru.begin(), lru, it);
+                return lru.front().second;
+            }
+        fntrs_plans* pl = nullptr;
+        check(fntrs_gpu_plans_create(ctx, k, n, uint32_t(pos.size()), 1, pos.data(), &pl, stream));
+        lru.emplace_front(std::move(key), pl);
+        if (lru.size() > kCapacity) {
+            sync();  // the evicted plan may still be read by queued work
+            fntrs_gpu_plans_destroy(lru.back().second);
+            lru.pop_back();
+        }
+        return pl;
+    }
+};
+
+Shared& shared() {
+    static Shared s;
+    return s;
+}
+
+uint32_t next_pow2(uint32_t n) {
+    uint32_t m = 1;
+    while (m < n) m <<= 1;
+    return m;
+}
+
+// Fe values -> uint16 words + ascending escape indices (shardio.cpp:131-137).
+void split(const Fe* v, size_t count, std::vector<uint16_t>& words, std::vector<uint64_t>& esc) {
+    words.resize(count);
+    esc.clear();
+    for (size_t i = 0; i < count; ++i) {
+        if (v[i] > 65536) throw SizeMismatch("value " + std::to_string(v[i]) + " outside the field");
+        words[i] = v[i] == 65536 ? 0 : uint16_t(v[i]);
+        if (v[i] == 65536) esc.push_back(i);
+    }
+}
+
+// Runs fn(d_in_words, d_in_esc, d_out_words, d_out_esc, d_count) with the
+// host arrays staged on the device, then joins the result back into Fe.
+template <typename Fn>
+std::vector<Fe> run(Shared& S, const std::vector<uint16_t>& in_words, const std::vector<uint64_t>& in_esc,
+                    size_t out_count, Fn&& fn) {
+    const size_t cap = out_count;  // at most one escape per output symbol
+    const size_t b_in = (in_words.size() * 2 + 255) / 256 * 256;
+    const size_t b_ie = (in_esc.size() * 8 + 255) / 256 * 256 + 256;
+    const size_t b_out = (out_count * 2 + 255) / 256 * 256;
+    const size_t b_oe = (cap * 8 + 255) / 256 * 256 + 256;
+    char* base = static_cast<char*>(S.scratch(b_in + b_ie + b_out + b_oe + 256));
+    auto* d_in = reinterpret_cast<uint16_t*>(base);
+    auto* d_ie = reinterpret_cast<uint64_t*>(base + b_in);
+    auto* d_out = reinterpret_cast<uint16_t*>(base + b_in + b_ie);
+    auto* d_oe = reinterpret_cast<uint64_t*>(base + b_in + b_ie + b_out);
+    auto* d_cnt = reinterpret_cast<uint64_t*>(base + b_in + b_ie + b_out + b_oe);
+    cudaMemcpyAsync(d_in, in_words.data(), in_words.size() * 2, cudaMemcpyHostToDevice, S.stream);
+    if (!in_esc.empty())
+        cudaMemcpyAsync(d_ie, in_esc.data(), in_esc.size() * 8, cudaMemcpyHostToDevice, S.stream);
+    fn(d_in, in_esc.empty() ? nullptr : d_ie, uint64_t(in_esc.size()), d_out, d_oe, uint64_t(cap), d_cnt);
+    std::vector<uint16_t> words(out_count);
+    std::vector<uint64_t> esc(cap);
+    uint64_t ne = 0;
+    cudaMemcpyAsync(words.data(), d_out, out_count * 2, cudaMemcpyDeviceToHost, S.stream);
+    cudaMemcpyAsync(&ne, d_cnt, 8, cudaMemcpyDeviceToHost, S.stream);
+    if (cap) cudaMemcpyAsync(esc.data(), d_oe, cap * 8, cudaMemcpyDeviceToHost, S.stream);
+    S.sync();
+    if (ne > cap) throw TooManyEscapes("escape list overflow");
+    std::vector<Fe> out(words.begin(), words.end());
+    for (uint64_t e = 0; e < ne; ++e) out[esc[e]] = 65536;
+    return out;
+}
+
+}  // namespace
+
+namespace gpu {
+void set_device(int device) {
+    Shared& S = shared();
+    std::lock_guard<std::mutex> lock(S.mu);
+    if (S.ctx && S.device != device) {
+        for (auto& e : S.lru) fntrs_gpu_plans_destroy(e.second);
+        S.lru.clear();
+        if (S.dbuf) cudaFree(S.dbuf);
+        S.dbuf = nullptr;
+        S.dbuf_bytes = 0;
+        if (S.stream) cudaStreamDestroy(S.stream);
+        S.stream = nullptr;
+        fntrs_gpu_destroy(S.ctx);
+        S.ctx = nullptr;
+    }
+    S.device = device;
+}
+}  // namespace gpu
+
+namespace codec {
+
+CodeParams CodeParams::make(std::uint32_t k, std::uint32_t n, bool systematic) {
+    uint32_t nd = 0;
+    if (fntrs_gpu_code_params(k, n, &nd) != FNTRS_OK)
+        throw SizeMismatch("code parameters need 1 <= k <= n <= 65536, got k = " + std::to_string(k) +
+                           ", n = " + std::to_string(n));
+    CodeParams p;
+    p.k = k;
+    p.n = n;
+    p.n_domain = nd;
+    p.systematic = systematic;
+    return p;
+}
+
+std::vector<Fe> encode_nonsystematic(const CodeParams& params, std::span<const Fe> source) {
+    if (source.size() != params.k)
+        throw SizeMismatch("encode: got " + std::to_string(source.size()) + " source symbols for k = " +
+                           std::to_string(params.k));
+    Shared& S = shared();
+    std::lock_guard<std::mutex> lock(S.mu);
+    S.ensure();
+    std::vector<uint16_t> words;
+    std::vector<uint64_t> esc;
+    split(source.data(), source.size(), words, esc);
+    return run(S, words, esc, params.n,
+               [&](const uint16_t* din, const uint64_t* die, uint64_t nie, uint16_t* dout, uint64_t* doe,
+                   uint64_t cap, uint64_t* dcnt) {
+                   S.check(fntrs_gpu_encode(S.ctx, params.k, params.n, 1, 1, din, die, nie, dout, doe, cap,
+                                            dcnt, S.stream));
+               });
+}
+
+std::vector<Fe> decode_nonsystematic(const CodeParams& params, const Codeword& received, Path) {
+    // sorted_received (codec.cpp:32-48): range check, sort, duplicates, count
+    for (const Symbol& s : received)
+        if (s.position >= params.n)
+            throw PositionOutOfRange("received position " + std::to_string(s.position) + " not below n = " +
+                                     std::to_string(params.n));
+    Codeword sorted(received);
+    std::sort(sorted.begin(), sorted.end(), [](const Symbol& a, const Symbol& b) { return a.position < b.position; });
+    for (size_t i = 1; i < sorted.size(); ++i)
+        if (sorted[i].position == sorted[i - 1].position)
+            throw DuplicatePosition("received position " + std::to_string(sorted[i].position) + " repeats");
+    if (sorted.size() < params.k)
+        throw NotEnoughSymbols("have " + std::to_string(sorted.size()) + " symbols, need " +
+                               std::to_string(params.k));
+    const uint32_t nd = next_pow2(params.n);
+    const bool full = params.n == nd && sorted.size() == params.n;  // codec.cpp:137-144
+    const uint32_t kp = full ? params.n : params.k;                   // else the k lowest positions
+    std::vector<uint32_t> pos(kp);
+    std::vector<Fe> vals(kp);
+    for (uint32_t i = 0; i < kp; ++i) {
+        pos[i] = sorted[i].position;
+        vals[i] = sorted[i].value;
+    }
+    Shared& S = shared();
+    std::lock_guard<std::mutex> lock(S.mu);
+    S.ensure();
+    fntrs_plans* plan = S.plan_for(params.k, params.n, pos);
+    std::vector<uint16_t> words;
+    std::vector<uint64_t> esc;
+    split(vals.data(), vals.size(), words, esc);
+    // stripe_pattern: a single zero, staged in scratch after the run buffers
+    uint32_t* d_sp = nullptr;
+    if (cudaMalloc(&d_sp, 4) != cudaSuccess) throw Error("fntrs: device allocation failed");
+    cudaMemsetAsync(d_sp, 0, 4, S.stream);
+    std::vector<Fe> out;
+    try {
+        out = run(S, words, esc, params.k,
+                  [&](const uint16_t* din, const uint64_t* die, uint64_t nie, uint16_t* dout, uint64_t* doe,
+                      uint64_t cap, uint64_t* dcnt) {
+                      S.check(fntrs_gpu_decode(S.ctx, plan, 1, 1, d_sp, din, die, nie, dout, doe, cap, dcnt,
+                                               S.stream));
+                  });
+    } catch (...) {
+        cudaFree(d_sp);
+        throw;
+    }
+    cudaFree(d_sp);
+    return out;
+}
+
+}  // namespace codec
+}  // namespace fntrs

@@ -1,0 +1,69 @@
+// internal.h -- host-side declarations shared by the CUDA translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace fntrs_gpu {
+
+// Twiddle tables: tw[m + j] = r_m^j (j < m) for every m = 2^e, e <= 16, in
+// one buffer of 2^17 entries per direction (offset m). Built on the device.
+struct Tables {
+    uint32_t* fwd = nullptr;
+    uint32_t* inv = nullptr;
+};
+
+cudaError_t build_tables(Tables& t, cudaStream_t st);
+
+// Escape sink: sorted global symbol indices of values equal to 65536.
+struct EscOut {
+    unsigned long long* keys;   // capacity cap, pre-filled with ~0 by the caller
+    unsigned long long* count;  // device counter (true count, may exceed cap)
+    uint64_t cap;
+};
+
+struct EscIn {
+    const unsigned long long* keys;  // sorted ascending
+    uint64_t n;
+};
+
+// Tile geometry chosen for a transform needing `rows` shared-memory rows.
+struct TileGeom {
+    int wt;       // columns per tile (power of two, >= 2)
+    int threads;  // threads per CTA
+    size_t smem;  // dynamic shared memory bytes
+};
+TileGeom pick_tile(int rows, uint32_t L);
+
+// Small-n (N = n_domain <= kTileMaxN) batched encode of packet-major stripes.
+cudaError_t launch_encode_tile(const Tables& t, uint32_t k, uint32_t n, uint32_t N,
+                               uint32_t stripes, uint32_t L, const uint16_t* src, EscIn esc_in,
+                               uint16_t* out, EscOut esc_out, cudaStream_t st);
+
+// Per-pattern decode data (device). ahat is already scaled by -1/M.
+struct PlanView {
+    uint32_t N, M, kp, k;        // domain, product size, positions per plan, outputs
+    uint32_t npatterns;
+    const uint32_t* positions;  // [np][kp]
+    const uint32_t* ainv;       // [np][kp]
+    const uint32_t* ahat;       // [np][M]
+    uint32_t ninv;              // N^-1 (full-reception mode)
+};
+
+cudaError_t launch_decode_tile(const Tables& t, const PlanView& pv, uint32_t stripes, uint32_t L,
+                               const uint32_t* stripe_pattern, const uint16_t* rx, EscIn esc_in,
+                               uint16_t* out, EscOut esc_out, cudaStream_t st);
+
+// Generic batched transform over columns: in/out [m][L] uint32 (natural order).
+// scale multiplies every output (1/m for fnt_inverse, see launch site).
+cudaError_t launch_fnt_tile(const Tables& t, uint32_t m, bool inverse, uint32_t scale, uint32_t L,
+                            const uint32_t* in, uint32_t* out, cudaStream_t st);
+
+// Plan precompute: direct products over the erasure positions.
+cudaError_t launch_plan_build(uint32_t N, uint32_t M, uint32_t kp, uint32_t npatterns,
+                              const uint32_t* positions, uint32_t* ainv, uint32_t* ahat,
+                              const Tables& t, cudaStream_t st);
+
+constexpr uint32_t kTileMaxN = 4096;
+
+}  // namespace fntrs_gpu

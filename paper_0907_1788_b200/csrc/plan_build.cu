@@ -1,0 +1,86 @@
+// plan_build.cu -- once-per-erasure-pattern decode precompute on the GPU.
+//
+// Replaces interp::build_plan (proj/src/interp.cpp:23-68). For a pattern
+// with points x_l = r_N^(z_l), l < kp, the decoder needs
+//   aprime_inv[i] = 1 / A'(x_i) = 1 / prod_{l != i} (x_i - x_l)
+//   A_hat[j]      = A(w_j) = prod_l (w_j - x_l),  w_j = r_M^j, j < M
+// where A = prod_l (x - x_l) is the erasure-locator polynomial (the root of
+// the reference's subproduct tree, poly.cpp:216-242) and A_hat its size-M
+// transform (the reference's a_fnt, interp.cpp:59-66, in natural order).
+// Both are products of linear factors, computed here directly: one thread
+// per evaluation point, the kp points staged in shared memory and read as
+// warp broadcasts. The values are identical to the reference's (same field
+// elements; evaluation is exact), which tests/ check against the oracle.
+// The decoder consumes ahat pre-scaled by -1/M (series negation and the
+// inverse-transform scale folded in).
+#include <cuda_runtime.h>
+
+#include "field.cuh"
+#include "internal.h"
+
+namespace fntrs_gpu {
+
+namespace {
+
+constexpr int kPlanThreads = 256;
+
+__global__ void __launch_bounds__(kPlanThreads)
+plan_kernel(uint32_t N, uint32_t M, uint32_t kp, uint32_t chunks, const uint32_t* __restrict__ positions,
+            const uint32_t* __restrict__ twN, const uint32_t* __restrict__ twM, uint32_t neg_minv,
+            uint32_t* __restrict__ ainv, uint32_t* __restrict__ ahat) {
+    extern __shared__ uint32_t xs[];
+    const uint32_t pat = blockIdx.x / chunks;
+    const uint32_t chunk = blockIdx.x - pat * chunks;
+    const uint32_t* pos = positions + size_t(pat) * kp;
+    for (uint32_t l = threadIdx.x; l < kp; l += blockDim.x) xs[l] = __ldg(twN + __ldg(pos + l));
+    __syncthreads();
+
+    const uint32_t idx = chunk * blockDim.x + threadIdx.x;
+    const uint32_t npts = kp + M;
+    if (idx >= npts) return;
+    const bool self = idx < kp;
+    const uint32_t y = self ? xs[idx] : __ldg(twM + (idx - kp));
+    // four independent accumulators for ILP; values stay in [0, 2p)
+    uint32_t acc[4] = {1u, 1u, 1u, 1u};
+    uint32_t l = 0;
+    for (; l + 4 <= kp; l += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            uint32_t d = red2p(y + kP - xs[l + u]);  // y - x_l, canonical
+            if (self) d = d ? d : 1u;                // skip the l == i factor
+            acc[u] = mulw(acc[u], d);
+        }
+    }
+    for (; l < kp; ++l) {
+        uint32_t d = red2p(y + kP - xs[l]);
+        if (self) d = d ? d : 1u;
+        acc[0] = mulw(acc[0], d);
+    }
+    uint32_t prod = red2p(mulw(mulw(red2p(acc[0]), red2p(acc[1])), red2p(mulw(red2p(acc[2]), red2p(acc[3])))));
+    if (self) {
+        ainv[size_t(pat) * kp + idx] = ginv(prod);
+    } else {
+        ahat[size_t(pat) * M + (idx - kp)] = red2p(mulw(prod, neg_minv));
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_plan_build(uint32_t N, uint32_t M, uint32_t kp, uint32_t npatterns,
+                              const uint32_t* positions, uint32_t* ainv, uint32_t* ahat,
+                              const Tables& t, cudaStream_t st) {
+    if (!npatterns) return cudaSuccess;
+    const uint32_t npts = kp + M;
+    const uint32_t chunks = (npts + kPlanThreads - 1) / kPlanThreads;
+    const uint64_t blocks = uint64_t(npatterns) * chunks;
+    if (blocks > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+    const size_t smem = size_t(kp) * 4;
+    cudaError_t err = cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (err) return err;
+    const uint32_t neg_minv = kP - cpow(M % kP, kP - 2);  // -1/M
+    plan_kernel<<<unsigned(blocks), kPlanThreads, smem, st>>>(N, M, kp, chunks, positions, t.fwd + N,
+                                                               t.fwd + M, neg_minv, ainv, ahat);
+    return cudaGetLastError();
+}
+
+}  // namespace fntrs_gpu

@@ -1,0 +1,165 @@
+// tests/cpp/test_dropin.cpp -- the reference's own codec test cases, run
+// against the drop-in C++ API (include/fntrs/codec.hpp) on the GPU.
+// Cases follow /root/reference/proj/tests/test_codec.cpp (file:line in each
+// section); values are the reference's frozen golden vectors. Built by
+// `make cpptest`, run by tests/test_gpu_parity.py::test_cpp_dropin (gpu).
+#include <cstdint>
+#include <cstdio>
+#include <functional>
+#include <random>
+#include <vector>
+
+#include "fntrs/codec.hpp"
+
+using namespace fntrs;
+using namespace fntrs::codec;
+
+static int g_fail = 0, g_pass = 0;
+#define CHECK(cond)                                                        \
+    do {                                                                   \
+        if (cond) {                                                        \
+            ++g_pass;                                                      \
+        } else {                                                           \
+            ++g_fail;                                                      \
+            std::fprintf(stderr, "FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond); \
+        }                                                                  \
+    } while (0)
+
+template <typename E, typename F>
+static bool throws_as(F&& f) {
+    try {
+        f();
+    } catch (const E&) {
+        return true;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+static std::vector<Fe> random_source(uint32_t k, uint32_t seed) {
+    std::mt19937 rng(seed);
+    std::uniform_int_distribution<uint32_t> d(0, 65536);
+    std::vector<Fe> v(k);
+    for (auto& x : v) x = d(rng);
+    return v;
+}
+
+static Codeword take(const std::vector<Fe>& enc, const std::vector<uint32_t>& pos) {
+    Codeword c;
+    for (uint32_t p : pos) c.push_back({p, enc[p]});
+    return c;
+}
+
+static void for_each_subset(uint32_t n, uint32_t s, const std::function<void(const std::vector<uint32_t>&)>& fn) {
+    std::vector<uint32_t> idx(s);
+    for (uint32_t i = 0; i < s; ++i) idx[i] = i;
+    for (;;) {
+        fn(idx);
+        int i = int(s) - 1;
+        while (i >= 0 && idx[i] == n - s + uint32_t(i)) --i;
+        if (i < 0) return;
+        ++idx[i];
+        for (uint32_t j = uint32_t(i) + 1; j < s; ++j) idx[j] = idx[j - 1] + 1;
+    }
+}
+
+int main() {
+    // CodeParams (test_codec.cpp:60-70)
+    {
+        auto p = CodeParams::make(3, 6);
+        CHECK(p.k == 3 && p.n == 6 && p.n_domain == 8);
+        CHECK(CodeParams::make(16, 16).n_domain == 16);
+        CHECK(CodeParams::make(1, 65536).n_domain == 65536);
+        CHECK(throws_as<SizeMismatch>([] { CodeParams::make(0, 4); }));
+        CHECK(throws_as<SizeMismatch>([] { CodeParams::make(5, 4); }));
+        CHECK(throws_as<SizeMismatch>([] { CodeParams::make(1, 65537); }));
+    }
+    // non-systematic encode basics (test_codec.cpp:72-84)
+    {
+        auto p15 = CodeParams::make(1, 5, false);
+        CHECK(encode_nonsystematic(p15, std::vector<Fe>{77}) == (std::vector<Fe>{77, 77, 77, 77, 77}));
+        auto p24 = CodeParams::make(2, 4, false);
+        CHECK(encode_nonsystematic(p24, std::vector<Fe>{5, 7}) == (std::vector<Fe>{12, 63750, 65535, 1797}));
+        CHECK(throws_as<SizeMismatch>([&] { encode_nonsystematic(p24, std::vector<Fe>{1}); }));
+    }
+    // rate-1 code (test_codec.cpp:86-94): decode of all symbols inverts
+    {
+        auto p = CodeParams::make(8, 8, false);
+        auto src = random_source(8, 1);
+        auto enc = encode_nonsystematic(p, src);
+        CHECK(decode_nonsystematic(p, take(enc, {0, 1, 2, 3, 4, 5, 6, 7})) == src);
+        // size-8 frozen transform (test_transform.cpp:51-57): k = n = 8 encode is fnt_forward
+        CHECK(encode_nonsystematic(p, std::vector<Fe>{1, 2, 3, 4, 5, 6, 7, 8}) ==
+              (std::vector<Fe>{36, 50109, 1020, 48061, 65533, 17468, 64509, 15420}));
+    }
+    // frozen decode (test_codec.cpp:96-102)
+    {
+        auto p = CodeParams::make(2, 4, false);
+        Codeword rx{{0, 12}, {2, 65535}};
+        CHECK(decode_nonsystematic(p, rx) == (std::vector<Fe>{5, 7}));
+        CHECK(decode_nonsystematic(p, rx, Path::Fast) == (std::vector<Fe>{5, 7}));
+    }
+    // validation (test_codec.cpp:104-112)
+    {
+        auto p = CodeParams::make(2, 4, false);
+        CHECK(throws_as<NotEnoughSymbols>([&] { decode_nonsystematic(p, Codeword{{0, 1}}); }));
+        CHECK(throws_as<DuplicatePosition>([&] { decode_nonsystematic(p, Codeword{{1, 5}, {1, 6}}); }));
+        CHECK(throws_as<PositionOutOfRange>([&] { decode_nonsystematic(p, Codeword{{0, 5}, {4, 6}}); }));
+    }
+    // MDS: every erasure pattern decodes (test_codec.cpp:192-224)
+    {
+        const std::pair<uint32_t, uint32_t> cases[] = {{4, 2}, {8, 4}, {8, 5}, {16, 12}};
+        for (auto [n, k] : cases) {
+            auto p = CodeParams::make(k, n, false);
+            auto src = random_source(k, n * 31 + k);
+            auto enc = encode_nonsystematic(p, src);
+            uint64_t patterns = 0, ok = 0;
+            for (uint32_t s = k; s <= n; ++s)
+                for_each_subset(n, s, [&](const std::vector<uint32_t>& keep) {
+                    ++patterns;
+                    ok += decode_nonsystematic(p, take(enc, keep), Path::Fast) == src;
+                });
+            uint64_t expected = 0;
+            for (uint32_t s = k; s <= n; ++s) {
+                uint64_t c = 1;
+                for (uint32_t i = 0; i < s; ++i) c = c * (n - i) / (i + 1);
+                expected += c;
+            }
+            CHECK(patterns == expected);
+            CHECK(ok == patterns);
+            std::printf("MDS n=%u k=%u: %llu/%llu patterns decode\n", n, k, (unsigned long long)ok,
+                        (unsigned long long)patterns);
+        }
+    }
+    // received order is irrelevant (test_codec.cpp:226-236, non-systematic here)
+    {
+        auto p = CodeParams::make(5, 11, false);
+        auto src = random_source(5, 17);
+        auto enc = encode_nonsystematic(p, src);
+        Codeword rx = take(enc, {9, 2, 7, 4, 10, 3});
+        std::mt19937 rng(18);
+        for (int i = 0; i < 10; ++i) {
+            std::shuffle(rx.begin(), rx.end(), rng);
+            CHECK(decode_nonsystematic(p, rx) == src);
+        }
+    }
+    // k lowest positions win (test_codec.cpp:238-247)
+    {
+        auto p = CodeParams::make(3, 9, false);
+        auto src = random_source(3, 19);
+        auto enc = encode_nonsystematic(p, src);
+        auto tampered = enc;
+        tampered[8] = gf::add(tampered[8], 1);
+        CHECK(decode_nonsystematic(p, take(tampered, {1, 3, 5, 8})) == src);
+    }
+    // sources holding the top field value (test_codec.cpp:333-339, non-systematic)
+    {
+        auto p = CodeParams::make(3, 7, false);
+        std::vector<Fe> src{65536, 65536, 65536};
+        auto enc = encode_nonsystematic(p, src);
+        CHECK(decode_nonsystematic(p, take(enc, {2, 4, 6})) == src);
+    }
+    std::printf("drop-in C++ API: %d passed, %d failed\n", g_pass, g_fail);
+    return g_fail ? 1 : 0;
+}

@@ -1,0 +1,260 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle / reference.
+
+Bit-exact equality is the bar everywhere (integer arithmetic). Sizes are
+chosen so the CPU checkers finish in seconds; full-size configs are covered
+by size-independent properties (decode(encode(s)) == s, linearity).
+"""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+P = 65537
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def codec():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_0907_1788_b200 import Codec
+    return Codec(0)
+
+
+def dev_u16(a: np.ndarray):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint16).view(np.int16)).cuda()
+
+
+def host_u16(t) -> np.ndarray:
+    return t.cpu().numpy().view(np.uint16)
+
+
+def dev_esc(e: np.ndarray):
+    if e is None or len(e) == 0:
+        return None
+    return torch.from_numpy(np.ascontiguousarray(e, dtype=np.uint64).view(np.int64)).cuda()
+
+
+def source_with_escapes(S, k, L, seed, n_esc):
+    from paper_0907_1788_b200 import workload as W
+    src = W.symbols(seed, 0, S * k * L).reshape(S, k, L)
+    rng = np.random.default_rng(seed)
+    idx = np.sort(rng.choice(S * k * L, size=min(n_esc, S * k * L), replace=False)).astype(np.uint64)
+    flat = src.reshape(-1)
+    flat[idx.astype(np.int64)] = 0
+    return src, idx
+
+
+# -------------------------------------------------------------- transform ----
+@pytest.mark.parametrize("e", list(range(0, 13)))
+def test_fnt_matches_oracle(codec, oracle, e):
+    m = 1 << e
+    rng = np.random.default_rng(e)
+    for L in (1, 3, 40):
+        x = rng.integers(0, P, (m, L)).astype(np.uint32)
+        x[0, 0] = 65536
+        t = torch.from_numpy(x.view(np.int32)).cuda()
+        fw = codec.fnt(t).cpu().numpy().view(np.uint32)
+        iv = codec.fnt(t, inverse=True).cpu().numpy().view(np.uint32)
+        for c in range(L):
+            assert np.array_equal(fw[:, c], oracle.fnt(x[:, c])), (m, L, c)
+            assert np.array_equal(iv[:, c], oracle.fnt(x[:, c], True)), (m, L, c)
+
+
+# -------------------------------------------------------------- per-codeword API ----
+def test_reference_interface_golden(codec):  # proj/tests/test_codec.cpp:60-112
+    import paper_0907_1788_b200 as F
+    p = F.CodeParams.make(3, 6)
+    assert (p.k, p.n, p.n_domain) == (3, 6, 8)
+    for bad in [(0, 4), (5, 4), (1, 65537)]:
+        with pytest.raises(F.SizeMismatch):
+            F.CodeParams.make(*bad)
+    assert F.encode_nonsystematic(F.CodeParams.make(1, 5, False), [77]) == [77] * 5
+    p24 = F.CodeParams.make(2, 4, False)
+    assert F.encode_nonsystematic(p24, [5, 7]) == [12, 63750, 65535, 1797]
+    with pytest.raises(F.SizeMismatch):
+        F.encode_nonsystematic(p24, [1])
+    assert F.decode_nonsystematic(p24, [F.Symbol(0, 12), F.Symbol(2, 65535)]) == [5, 7]
+    assert F.decode_nonsystematic(p24, [F.Symbol(0, 12), F.Symbol(2, 65535)], F.Path.Fast) == [5, 7]
+    with pytest.raises(F.NotEnoughSymbols):
+        F.decode_nonsystematic(p24, [F.Symbol(0, 1)])
+    with pytest.raises(F.DuplicatePosition):
+        F.decode_nonsystematic(p24, [F.Symbol(1, 5), F.Symbol(1, 6)])
+    with pytest.raises(F.PositionOutOfRange):
+        F.decode_nonsystematic(p24, [F.Symbol(0, 5), F.Symbol(4, 6)])
+    p8 = F.CodeParams.make(8, 8, False)
+    assert F.encode_nonsystematic(p8, list(range(1, 9))) == [36, 50109, 1020, 48061, 65533, 17468, 64509, 15420]
+    src = [65536, 65536, 65536]
+    p37 = F.CodeParams.make(3, 7, False)
+    enc = F.encode_nonsystematic(p37, src)
+    assert F.decode_nonsystematic(p37, [F.Symbol(z, enc[z]) for z in (2, 4, 6)]) == src
+
+
+def test_reference_interface_mds(codec):  # test_codec.cpp:192-224
+    import itertools
+    import paper_0907_1788_b200 as F
+    rng = np.random.default_rng(9)
+    for n, k in [(4, 2), (8, 4), (8, 5)]:
+        p = F.CodeParams.make(k, n, False)
+        src = [int(x) for x in rng.integers(0, P, k)]
+        enc = F.encode_nonsystematic(p, src)
+        for s in range(k, n + 1):
+            for keep in itertools.combinations(range(n), s):
+                assert F.decode_nonsystematic(p, [F.Symbol(z, enc[z]) for z in keep]) == src, (n, k, keep)
+
+
+def test_cpp_dropin_suite():
+    exe = os.path.join(ROOT, "build", "test_dropin")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-C", ROOT, "cpptest"], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+# ---------------------------------------------------------------- batched ----
+SHAPES = [  # (k, n, L, stripes)
+    (1, 1, 8, 2), (1, 5, 3, 2), (2, 4, 16, 3), (3, 8, 5, 2), (5, 11, 7, 2), (12, 16, 32, 2),
+    (64, 128, 64, 3), (128, 256, 64, 4), (100, 256, 24, 2), (200, 256, 16, 2),
+    (512, 1024, 32, 2), (1024, 2048, 512, 1), (2048, 4096, 64, 1), (1000, 4000, 16, 1),
+]
+
+
+@pytest.mark.parametrize("k,n,L,S", SHAPES)
+def test_encode_matches_oracle(codec, oracle, k, n, L, S):
+    src, esc = source_with_escapes(S, k, L, seed=k * 7 + n, n_esc=3)
+    want, want_esc = oracle.encode_stripes(k, n, src, esc)
+    out, oe, cnt = codec.encode(k, n, dev_u16(src), dev_esc(esc))
+    from paper_0907_1788_b200 import escapes_to_numpy
+    assert np.array_equal(host_u16(out), want)
+    assert np.array_equal(escapes_to_numpy(oe, cnt), want_esc)
+
+
+def _patterns(S, n, k, seed):
+    rng = np.random.default_rng(seed)
+    pats = np.stack([np.sort(rng.choice(n, k, replace=False)) for _ in range(S)]).astype(np.uint32)
+    return pats, np.arange(S, dtype=np.uint32)
+
+
+@pytest.mark.parametrize("k,n,L,S", SHAPES)
+def test_decode_matches_oracle(codec, oracle, k, n, L, S):
+    from oracle_bind import gather_received
+    from paper_0907_1788_b200 import escapes_to_numpy
+    src, esc = source_with_escapes(S, k, L, seed=k + n, n_esc=2)
+    enc, enc_esc = oracle.encode_stripes(k, n, src, esc)
+    pats, sp = _patterns(S, n, k, seed=n)
+    # arbitrary (non-codeword) received values too: tamper with one stripe's payload
+    rx, rx_esc = gather_received(enc, enc_esc, pats, sp)
+    rx = rx.copy()
+    rx[-1, 0, 0] ^= 0x5A5A
+    rx_esc = rx_esc[rx_esc != np.uint64(((S - 1) * k) * L)]
+    want, want_esc = oracle.decode_stripes(k, n, pats, sp, rx, rx_esc)
+    plans = codec.plans(k, n, pats)
+    spd = torch.from_numpy(sp.view(np.int32)).cuda()
+    out, oe, cnt = codec.decode(plans, spd, dev_u16(rx), dev_esc(rx_esc))
+    assert np.array_equal(host_u16(out), want)
+    assert np.array_equal(escapes_to_numpy(oe, cnt), want_esc)
+
+
+@pytest.mark.parametrize("n,k", [(2, 2), (4, 2), (8, 3), (8, 5), (16, 12), (256, 128), (2048, 1024), (4096, 2048),
+                                 (1000, 300)])
+def test_plan_fields_match_oracle(codec, oracle, n, k):
+    nd = 1 << (n - 1).bit_length()
+    rng = np.random.default_rng(n + k)
+    pos = np.sort(rng.choice(n, k, replace=False)).astype(np.uint32)
+    st, a, ap, ps, af = oracle.build_plan(nd, pos)
+    plans = codec.plans(k, n, pos[None, :])
+    ga, gap, gps, gaf = plans.export(0)
+    assert gps == ps
+    assert np.array_equal(ga, a) and np.array_equal(gap, ap) and np.array_equal(gaf, af)
+
+
+def test_frozen_plan_three_positions(codec):  # test_interp.cpp:52-63
+    plans = codec.plans(3, 8, np.array([[0, 2, 5]], dtype=np.uint32))
+    a, ap, ps, af = plans.export(0)
+    inv = lambda x: pow(x, P - 2, P)
+    assert list(a) == [16, 61169, 4351, 1]
+    assert list(ap) == [inv(4337), inv(61712), inv(3600)]
+
+
+def test_complete_reception_is_inverse_transform(codec, oracle):  # codec.cpp:137-144
+    from paper_0907_1788_b200 import escapes_to_numpy
+    n, k, L = 16, 5, 8
+    rng = np.random.default_rng(11)
+    vals = rng.integers(0, 65536, (1, n, L)).astype(np.uint16)  # not a codeword
+    plans = codec.plans(k, n, np.arange(n, dtype=np.uint32)[None, :])
+    out, oe, cnt = codec.decode(plans, torch.zeros(1, dtype=torch.int32, device="cuda"), dev_u16(vals))
+    got = host_u16(out)
+    want_esc = []
+    for c in range(L):
+        want = oracle.fnt(vals[0, :, c].astype(np.uint32), inverse=True)[:k]
+        assert np.array_equal(got[0, :, c], np.where(want == 65536, 0, want))
+        want_esc += [f * L + c for f in range(k) if want[f] == 65536]
+    assert np.array_equal(escapes_to_numpy(oe, cnt), np.sort(np.array(want_esc, dtype=np.uint64)))
+
+
+def test_errors_map_to_reference_classes(codec):
+    import paper_0907_1788_b200 as F
+    with pytest.raises(F.PositionOutOfRange):
+        codec.plans(2, 4, np.array([[0, 4]], dtype=np.uint32))
+    with pytest.raises(F.DuplicatePosition):
+        codec.plans(2, 4, np.array([[1, 1]], dtype=np.uint32))
+    with pytest.raises(F.NotEnoughSymbols):
+        codec.plans(3, 4, np.array([[1, 2]], dtype=np.uint32))
+    with pytest.raises(F.SizeMismatch):
+        codec.encode(0, 4, torch.zeros((1, 0, 8), dtype=torch.int16, device="cuda"))
+
+
+# ---------------------------------------------------- configs, full size ----
+def test_config_c1_bit_exact_vs_reference(codec, oracle):
+    """C1 (n=2048, k=1024, L=512, 1 stripe) in full against the reference library."""
+    from oracle_bind import RefLib, gather_received
+    from paper_0907_1788_b200 import escapes_to_numpy, workload as W
+    cfg = W.CONFIGS["C1"]
+    src = W.symbols(W.SEED, 0, cfg.stripes * cfg.k * cfg.L).reshape(cfg.stripes, cfg.k, cfg.L)
+    chk = RefLib() if RefLib.available() else oracle
+    want, want_esc = chk.encode_stripes(cfg.k, cfg.n, src) if isinstance(chk, RefLib) else oracle.encode_stripes(cfg.k, cfg.n, src)
+    out, oe, cnt = codec.encode(cfg.k, cfg.n, dev_u16(src))
+    assert np.array_equal(host_u16(out), want)
+    assert np.array_equal(escapes_to_numpy(oe, cnt), want_esc)
+    pats, sp = W.patterns(cfg)
+    rx, rxe = gather_received(want, want_esc, pats, sp)
+    plans = codec.plans(cfg.k, cfg.n, pats)
+    dec, de, dc = codec.decode(plans, torch.from_numpy(sp.view(np.int32)).cuda(), dev_u16(rx), dev_esc(rxe))
+    assert np.array_equal(host_u16(dec), src)
+    assert escapes_to_numpy(de, dc).size == 0
+
+
+@pytest.mark.parametrize("name,stripes", [("C2", 512), ("C5", 16)])
+def test_config_roundtrip_sampled(codec, oracle, name, stripes):
+    """decode(encode(s)) == s on device for a sample of the config's stripes, plus
+    bit-exact encode against the oracle on the first two stripes."""
+    from oracle_bind import gather_received
+    from paper_0907_1788_b200 import escapes_to_numpy, workload as W
+    cfg = W.CONFIGS[name]
+    src = W.symbols(W.SEED, 0, stripes * cfg.k * cfg.L).reshape(stripes, cfg.k, cfg.L)
+    out, oe, cnt = codec.encode(cfg.k, cfg.n, dev_u16(src))
+    enc = host_u16(out)
+    enc_esc = escapes_to_numpy(oe, cnt)
+    want, want_esc = oracle.encode_stripes(cfg.k, cfg.n, src[:2])
+    assert np.array_equal(enc[:2], want)
+    assert np.array_equal(enc_esc[enc_esc < np.uint64(2 * cfg.n * cfg.L)], want_esc)
+    pats, sp = W.patterns(cfg, stripes=stripes)
+    rx, rxe = gather_received(enc, enc_esc, pats, sp)
+    plans = codec.plans(cfg.k, cfg.n, pats)
+    dec, de, dc = codec.decode(plans, torch.from_numpy(sp.view(np.int32)).cuda(), dev_u16(rx), dev_esc(rxe))
+    assert np.array_equal(host_u16(dec), src)
+
+
+def test_device_generator_matches_numpy(codec):
+    import ctypes as C
+    from paper_0907_1788_b200 import _lib, workload as W
+    t = torch.empty(100003, dtype=torch.int16, device="cuda")
+    st = _lib.load().fntrs_gpu_fill_symbols(W.SEED, 12345, t.numel(), C.c_void_p(t.data_ptr()),
+                                            C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert st == 0
+    assert np.array_equal(host_u16(t), W.symbols(W.SEED, 12345, t.numel()))
