@@ -567,14 +567,14 @@ void orc_escape_join(const uint16_t* words, uint64_t count, const uint32_t* esc,
 
 /* ---- batched stripe harness (the CLI's loop, tools/fntrs_main.cpp:122-139,
  * 222-231): packet-major uint16 stripes, codeword j = symbol j of every
- * packet. Escapes are global sorted keys (row << 32 | col), row =
+ * packet. Escapes are ascending symbol indices row * L + col, row =
  * stripe * rows_per_stripe + packet -- the same convention as the C-ABI. */
 
 static uint32_t fetch(const uint16_t* base, const uint64_t* esc, uint64_t ne, uint64_t row,
                       uint32_t col, uint32_t L) {
     uint16_t w = base[row * L + col];
     if (w || !ne) return w;
-    uint64_t key = (row << 32) | col, lo = 0, hi = ne;
+    uint64_t key = row * L + col, lo = 0, hi = ne;
     while (lo < hi) {
         uint64_t mid = (lo + hi) / 2;
         if (esc[mid] < key) lo = mid + 1; else hi = mid;
@@ -601,7 +601,7 @@ int64_t orc_encode_stripes(uint32_t k, uint32_t n, uint32_t stripes, uint32_t L,
                 out[row * L + j] = e[i] == 65536 ? 0 : (uint16_t)e[i];
                 if (e[i] == 65536) {
                     if ((uint64_t)ne >= esc_cap) { free(a); free(e); return -ORC_E_TOO_MANY_ESCAPES; }
-                    out_esc[ne++] = (row << 32) | j;
+                    out_esc[ne++] = row * L + j;
                 }
             }
         }
@@ -643,7 +643,7 @@ int64_t orc_decode_stripes(uint32_t k, uint32_t n, uint32_t stripes, uint32_t L,
                 out[row * L + j] = dec[i] == 65536 ? 0 : (uint16_t)dec[i];
                 if (dec[i] == 65536) {
                     if ((uint64_t)ne >= esc_cap) { rc = ORC_E_TOO_MANY_ESCAPES; break; }
-                    out_esc[ne++] = (row << 32) | j;
+                    out_esc[ne++] = row * L + j;
                 }
             }
         }

@@ -51,7 +51,7 @@ uint32_t fetch(const uint16_t* base, const uint64_t* esc, uint64_t ne, uint64_t 
                uint32_t L) {
     uint16_t w = base[row * L + col];
     if (w || !ne) return w;
-    const uint64_t key = (row << 32) | col;
+    const uint64_t key = row * L + col;
     return std::binary_search(esc, esc + ne, key) ? 65536u : 0u;
 }
 
@@ -151,7 +151,7 @@ int ref_build_plan(uint32_t n, uint32_t k, const uint32_t* positions, uint32_t* 
 }
 
 // CLI-style batched encode over packet-major stripes. Returns the escape
-// count (sorted keys row<<32|col in out_esc) or a negative status.
+// count (sorted symbol indices row*L+col in out_esc) or a negative status.
 int64_t ref_encode_stripes(uint32_t k, uint32_t n, uint32_t stripes, uint32_t L,
                            const uint16_t* src, const uint64_t* src_esc, uint64_t n_src_esc,
                            uint16_t* out, uint64_t* out_esc, uint64_t esc_cap, unsigned threads) {
@@ -173,7 +173,7 @@ int64_t ref_encode_stripes(uint32_t k, uint32_t n, uint32_t stripes, uint32_t L,
             out[row * L + j] = enc[i] == 65536 ? 0 : uint16_t(enc[i]);
             if (enc[i] == 65536) {
                 std::lock_guard<std::mutex> lock(mu);
-                escapes.push_back((row << 32) | j);
+                escapes.push_back(row * L + j);
             }
         }
     });
@@ -215,7 +215,7 @@ int64_t ref_decode_stripes(uint32_t k, uint32_t n, uint32_t stripes, uint32_t L,
             out[row * L + j] = dec[i] == 65536 ? 0 : uint16_t(dec[i]);
             if (dec[i] == 65536) {
                 std::lock_guard<std::mutex> lock(mu);
-                escapes.push_back((row << 32) | j);
+                escapes.push_back(row * L + j);
             }
         }
     });

@@ -117,9 +117,10 @@ __device__ __forceinline__ void load_rows(uint32_t* s, int WT, int nrows, const 
 }
 
 __device__ __forceinline__ void zero_rows(uint32_t* s, int WT, int r0, int r1) {
-    uint4* p = reinterpret_cast<uint4*>(s + size_t(r0) * WT);
-    const int n4 = (r1 - r0) * WT / 4;
-    for (int i = threadIdx.x; i < n4; i += blockDim.x) p[i] = make_uint4(0, 0, 0, 0);
+    // WT is even, so row starts are 8-byte aligned
+    uint2* p = reinterpret_cast<uint2*>(s + size_t(r0) * WT);
+    const int n2 = (r1 - r0) * WT / 2;
+    for (int i = threadIdx.x; i < n2; i += blockDim.x) p[i] = make_uint2(0, 0);
 }
 
 // Store `nout` output rows. map(f, grow, srow): global row and shared row of

@@ -116,3 +116,34 @@ def patterns(cfg: Config, seed: int = SEED, stripes: int | None = None):
             rows.append(_subset(seed, s, n, k) if c == 0 else _bursts(seed, s, n, k, 1024))
         return np.stack(rows), sp
     raise ValueError(cfg.pattern)
+
+
+# ------------------------------------------------ device-side stripe helpers ----
+def received_packets(enc, enc_esc, enc_count, pats, stripe_pattern, n: int):
+    """Gather the received packets of every stripe on the device (torch plumbing).
+
+    enc [S, n, L] int16 CUDA tensor; enc_esc/enc_count: the encoder's escape
+    list; pats [P, kp] host uint32; stripe_pattern [S] host uint32.
+    Returns (rx [S, kp, L], rx_esc int64 sorted symbol indices into rx).
+    """
+    import torch
+    S, nn, L = enc.shape
+    dev = enc.device
+    kp = pats.shape[1]
+    rows = torch.from_numpy(pats[stripe_pattern].astype(np.int64)).to(dev)           # [S, kp]
+    rx = torch.gather(enc, 1, rows[:, :, None].expand(-1, -1, L)).contiguous()
+    ne = int(enc_count.item())
+    if ne == 0:
+        return rx, None
+    keys = enc_esc[:ne]
+    row, col = keys // L, keys % L
+    s, pos = row // n, row % n
+    inv = torch.full((pats.shape[0], n), -1, dtype=torch.int64, device=dev)
+    inv.scatter_(1, torch.from_numpy(pats.astype(np.int64)).to(dev),
+                 torch.arange(kp, device=dev).expand(pats.shape[0], -1).contiguous())
+    spd = torch.from_numpy(stripe_pattern.astype(np.int64)).to(dev)
+    i = inv[spd[s], pos]
+    keep = i >= 0
+    out = (s[keep] * kp + i[keep]) * L + col[keep]
+    out, _ = torch.sort(out)
+    return rx, (out if out.numel() else None)
