@@ -134,6 +134,12 @@ int fntrs_gpu_fnt(fntrs_ctx* ctx, uint32_t m, int inverse, uint32_t L, const uin
 int fntrs_gpu_fill_symbols(uint64_t seed, uint64_t first_index, uint64_t count, uint16_t* out,
                            void* stream);
 
+/* Kernel selection: the fused v2 kernels (codec_fast.cu) serve n_domain in
+ * [32, 4096] with L a multiple of the tile width; every other shape runs the
+ * general tile kernels (codec_tile.cu). enabled = 0 forces the general
+ * kernels (used by tests to cross-check the two). Both are GPU kernels. */
+int fntrs_gpu_set_fast_path(fntrs_ctx* ctx, int enabled);
+
 /* Launch accounting: number of kernels this context has launched. */
 uint64_t fntrs_gpu_launch_count(const fntrs_ctx* ctx);
 

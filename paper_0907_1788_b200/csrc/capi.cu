@@ -21,6 +21,8 @@ using namespace fntrs_gpu;
 struct fntrs_ctx {
     int device = 0;
     Tables tab;
+    fast::FastTables ftab;
+    bool fast_enabled = true;
     cudaStream_t internal = nullptr;
     void* sort_tmp = nullptr;
     size_t sort_tmp_bytes = 0;
@@ -37,6 +39,8 @@ struct fntrs_plans {
     uint32_t* ainv = nullptr;
     uint32_t* ahat = nullptr;
     uint32_t ninv = 1;
+    uint2* rowmap = nullptr;  // fast-path tables (N == M, kp == k)
+    uint2* ahat2 = nullptr;
 };
 
 namespace {
@@ -161,6 +165,12 @@ const char* fntrs_gpu_last_error(const fntrs_ctx* ctx) { return ctx ? ctx->err.c
 int fntrs_gpu_device(const fntrs_ctx* ctx) { return ctx ? ctx->device : -1; }
 uint64_t fntrs_gpu_launch_count(const fntrs_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+int fntrs_gpu_set_fast_path(fntrs_ctx* ctx, int enabled) {
+    if (!ctx) return FNTRS_E_INVALID_ARGUMENT;
+    ctx->fast_enabled = enabled != 0;
+    return FNTRS_OK;
+}
+
 int fntrs_gpu_code_params(uint32_t k, uint32_t n, uint32_t* n_domain) {
     if (k < 1 || k > n || n > 65536) return FNTRS_E_SIZE_MISMATCH;
     if (n_domain) *n_domain = next_pow2(n);
@@ -178,6 +188,7 @@ int fntrs_gpu_create(int device, fntrs_ctx** out) {
     DeviceGuard g(device);
     cudaError_t e = cudaStreamCreateWithFlags(&ctx->internal, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = build_tables(ctx->tab, ctx->internal);
+    if (e == cudaSuccess) e = fast::build_fast_tables(ctx->ftab, ctx->internal);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->internal);
     if (e != cudaSuccess) {
         delete ctx;
@@ -193,6 +204,8 @@ int fntrs_gpu_destroy(fntrs_ctx* ctx) {
     DeviceGuard g(ctx->device);
     cudaFree(ctx->tab.fwd);
     cudaFree(ctx->tab.inv);
+    cudaFree(ctx->ftab.fwd);
+    cudaFree(ctx->ftab.inv);
     cudaFree(ctx->sort_tmp);
     cudaFree(ctx->sort_alt);
     if (ctx->internal) cudaStreamDestroy(ctx->internal);
@@ -218,7 +231,13 @@ int fntrs_gpu_encode(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t stripes, u
     EscIn ein{reinterpret_cast<const unsigned long long*>(src_esc), n_src_esc};
     EscOut eout{reinterpret_cast<unsigned long long*>(out_esc), reinterpret_cast<unsigned long long*>(n_out_esc),
                 esc_cap};
-    CK(launch_encode_tile(ctx->tab, k, n, N, stripes, L, src, ein, out, eout, st), "encode launch");
+    const int cols = fast::fast_tile_columns(N);
+    const bool fast_ok = ctx->fast_enabled && cols && L % uint32_t(cols) == 0 &&
+                         reinterpret_cast<uintptr_t>(src) % 4 == 0 && reinterpret_cast<uintptr_t>(out) % 4 == 0;
+    if (fast_ok)
+        CK(fast::launch_encode_fast(ctx->ftab, k, n, N, stripes, L, src, ein, out, eout, st), "encode launch");
+    else
+        CK(launch_encode_tile(ctx->tab, k, n, N, stripes, L, src, ein, out, eout, st), "encode launch");
     ctx->launches += 1;
     return sort_escapes(ctx, eout.keys, esc_cap, uint64_t(stripes) * n * L, st);
 }
@@ -230,14 +249,17 @@ int fntrs_gpu_plans_create(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t kp, 
     uint32_t N = 0;
     if (fntrs_gpu_code_params(k, n, &N))
         return fail(ctx, FNTRS_E_SIZE_MISMATCH, "code parameters need 1 <= k <= n <= 65536");
-    const bool full = (kp == n && n == N);
+    const bool full = (kp == n && n == N);  // complete reception: one inverse transform
     if (kp < k) return fail(ctx, FNTRS_E_NOT_ENOUGH_SYMBOLS, "have " + std::to_string(kp) + " symbols, need " + std::to_string(k));
     if (kp != k && !full)
         return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "kp must equal k (or n for complete reception)");
     if (2ull * k > 65536ull && !full)
         return fail(ctx, FNTRS_E_UNSUPPORTED, "2k > 65536 needs the split product (mul_low), not in this build");
-    const uint32_t M = full ? N : next_pow2(2 * k);
-    if (N > kTileMaxN || M > kTileMaxN) return fail(ctx, FNTRS_E_UNSUPPORTED, "transform sizes > 4096 not in this build yet");
+    const uint32_t M = 2ull * k > 65536ull ? 0u : next_pow2(2 * k);
+    // locator data: needed for decoding unless complete; kept for export when it fits
+    const bool locator = !full || (kp == k && M && M <= kTileMaxN);
+    if (N > kTileMaxN || (!full && M > kTileMaxN))
+        return fail(ctx, FNTRS_E_UNSUPPORTED, "transform sizes > 4096 not in this build yet");
     if (npatterns && !positions) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "positions is null");
     // validation (codec.cpp:32-48 order: range first, then duplicates)
     std::vector<uint8_t> seen(n);
@@ -269,11 +291,18 @@ int fntrs_gpu_plans_create(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t kp, 
     if (npatterns) {
         e = cudaMalloc(&pl->pos, npos * 4);
         if (!e) e = cudaMalloc(&pl->ainv, npos * 4);
-        if (!e) e = cudaMalloc(&pl->ahat, size_t(npatterns) * M * 4);
+        if (!e && locator) e = cudaMalloc(&pl->ahat, size_t(npatterns) * M * 4);
         if (!e) e = cudaMemcpyAsync(pl->pos, positions, npos * 4, cudaMemcpyHostToDevice, st);
-        if (!e && !full) {
+        if (!e && locator) {
             e = launch_plan_build(N, M, kp, npatterns, pl->pos, pl->ainv, pl->ahat, ctx->tab, st);
             ctx->launches += 1;
+        }
+        if (!e && !full && kp == k && M == N && fast::fast_tile_columns(N)) {
+            e = cudaMalloc(&pl->rowmap, size_t(npatterns) * N * sizeof(uint2));
+            if (!e) e = cudaMalloc(&pl->ahat2, size_t(npatterns) * N * sizeof(uint2));
+            if (!e) e = fast::launch_fast_plan_tables(N, kp, npatterns, pl->pos, pl->ainv, pl->ahat, pl->rowmap,
+                                                      pl->ahat2, st);
+            ctx->launches += 2;
         }
     }
     if (e) {
@@ -290,6 +319,8 @@ int fntrs_gpu_plans_destroy(fntrs_plans* pl) {
     cudaFree(pl->pos);
     cudaFree(pl->ainv);
     cudaFree(pl->ahat);
+    cudaFree(pl->rowmap);
+    cudaFree(pl->ahat2);
     delete pl;
     return FNTRS_OK;
 }
@@ -300,7 +331,7 @@ int fntrs_gpu_plans_export(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t patte
                            uint32_t* aprime_inv, uint32_t* product_size, uint32_t* a_fnt) {
     if (!ctx || !pl) return FNTRS_E_INVALID_ARGUMENT;
     if (pattern >= pl->np) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "pattern out of range");
-    if (pl->kp == pl->N && pl->kp != pl->k) return fail(ctx, FNTRS_E_UNSUPPORTED, "complete-reception plans carry no locator");
+    if (!pl->ahat) return fail(ctx, FNTRS_E_UNSUPPORTED, "this plan carries no locator (complete reception)");
     DeviceGuard g(ctx->device);
     cudaStream_t st = ctx->internal;
     const uint32_t M = pl->M, kp = pl->kp;
@@ -352,7 +383,15 @@ int fntrs_gpu_decode(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t stripes, ui
     EscIn ein{reinterpret_cast<const unsigned long long*>(rx_esc), n_rx_esc};
     EscOut eout{reinterpret_cast<unsigned long long*>(out_esc), reinterpret_cast<unsigned long long*>(n_out_esc),
                 esc_cap};
-    CK(launch_decode_tile(ctx->tab, pv, stripes, L, stripe_pattern, rx, ein, out, eout, st), "decode launch");
+    const int cols = fast::fast_tile_columns(pl->N);
+    const bool fast_ok = ctx->fast_enabled && pl->rowmap && cols && L % uint32_t(cols) == 0 &&
+                         reinterpret_cast<uintptr_t>(rx) % 4 == 0 && reinterpret_cast<uintptr_t>(out) % 4 == 0;
+    if (fast_ok) {
+        fast::FastPlanView fv{pl->N, pl->k, pl->rowmap, pl->ahat2};
+        CK(fast::launch_decode_fast(ctx->ftab, fv, stripes, L, stripe_pattern, rx, ein, out, eout, st), "decode launch");
+    } else {
+        CK(launch_decode_tile(ctx->tab, pv, stripes, L, stripe_pattern, rx, ein, out, eout, st), "decode launch");
+    }
     ctx->launches += 1;
     return sort_escapes(ctx, eout.keys, esc_cap, uint64_t(stripes) * pl->k * L, st);
 }

@@ -409,7 +409,7 @@ cudaError_t launch_decode_tile(const Tables& t, const PlanView& pv, uint32_t str
                                uint16_t* out, EscOut esc_out, cudaStream_t st) {
     if (!stripes || !L) return cudaSuccess;
     const int eN = log2_exact(pv.N), eM = log2_exact(pv.M);
-    const bool full = pv.kp == pv.N;
+    const bool full = pv.kp == pv.N;  // positions are distinct and < n <= N
     const int rows = int(pv.N) + ((full || pv.N == pv.M) ? 0 : int(pv.M));
     TileGeom g = pick_tile(rows, L);
     const uint32_t tps = (L + g.wt - 1) / g.wt;

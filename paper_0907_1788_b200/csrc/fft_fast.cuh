@@ -1,0 +1,239 @@
+// fft_fast.cuh -- compile-time-specialised radix-16 column-FNT engine (v2).
+//
+// Same mathematics as fft_tile.cuh (in-place mixed-radix DIF/DIT over a
+// shared-memory tile, positions in 4-bit-digit-reversed order between a DIF
+// and a DIT), but everything that v1 computed at run time is fixed at
+// compile time: the pass schedule (radix 16, then one 2/4/8 pass), the
+// thread -> butterfly mapping (shifts, no divisions), the in-register
+// twiddles, and the value bounds that let butterfly sums grow lazily across
+// stages without reductions. Passes take load / store functors, so the first
+// pass of a transform can read packet-major global memory directly and the
+// last pass can write it, and the decoder can fuse the end of one transform
+// with the start of the next in registers.
+//
+// Arithmetic (field.cuh): every value is a uint32 congruent to the field
+// element, below a compile-time bound. Multiplication by a table twiddle is
+// Shoup's (any 32-bit input, result < 2p); by a power of two (all roots of
+// order <= 32 are powers of two: r16 = 2^6, r8 = 2^12, r4 = -2^8) it is a
+// shift-and-fold on the integer ALU pipe, which keeps the FMA-heavy pipe
+// (IMAD.HI) for the table twiddles only.
+#pragma once
+#include <cstdint>
+
+#include "field.cuh"
+
+namespace fntrs_gpu {
+namespace fast {
+
+constexpr uint64_t kP64 = 65537ull;
+constexpr uint64_t ceil_p(uint64_t b) { return (b + kP64 - 1) / kP64 * kP64; }
+constexpr uint64_t umax(uint64_t a, uint64_t b) { return a > b ? a : b; }
+
+// log2 of the order of a root as a power of two of 2: the root of order L
+// (L <= 32) equals 2^(64/L * 1.5?) -- computed instead by search below.
+constexpr int pow2_exponent(uint32_t w) {
+    // smallest e in [0, 32) with 2^e == w (mod p), or -1
+    uint32_t x = 1;
+    for (int e = 0; e < 32; ++e) {
+        if (x == w) return e;
+        x = uint32_t((uint64_t(x) * 2) % kP64);
+    }
+    return -1;
+}
+
+template <int L, int J, bool INV>
+struct Tw {
+    static constexpr uint32_t w = cpow(croot(L, INV), uint32_t(J));
+    static constexpr int e2 = pow2_exponent(w);  // >= 0 for every L <= 32
+};
+
+// x * 2^E mod p, E in [0, 32), x < B. Result bound: out_bound<E, B>().
+template <int E, uint64_t B>
+struct MulPow2 {
+    static constexpr int e = E & 31;
+    static constexpr bool neg = e >= 16;  // 2^16 = -1
+    static constexpr int s = e & 15;
+    static constexpr uint64_t HB = s ? (((B - 1) >> (16 - s)) + 1) : 0;  // bound of the high part
+    static constexpr uint64_t K = s ? ceil_p(HB) : ceil_p(B);
+    static constexpr uint64_t OUT = s ? (neg ? (HB + kP64) : (65536ull + K)) : (neg ? K + 1 : B);
+    __device__ __forceinline__ static uint32_t apply(uint32_t x) {
+        if constexpr (s == 0) {
+            if constexpr (neg)
+                return uint32_t(K) - x;
+            else
+                return x;
+        } else {
+            const uint32_t xh = x >> (16 - s);
+            const uint32_t xl = (x << s) & 0xFFFFu;
+            if constexpr (neg)
+                return xh + uint32_t(kP64) - xl;  // -(xl - xh)
+            else
+                return xl + uint32_t(K) - xh;
+        }
+    }
+};
+
+#ifndef FNTRS_POW2_SHIFT
+#define FNTRS_POW2_SHIFT 1
+#endif
+
+// Multiply by the compile-time twiddle TW<L,J>; returns the new bound via OUT.
+template <int L, int J, bool INV, uint64_t B>
+struct MulTw {
+    using T = Tw<L, J, INV>;
+    static_assert(T::e2 >= 0, "in-register twiddles must be powers of two");
+    static constexpr bool shift = FNTRS_POW2_SHIFT && (B < (1ull << 31));
+    static constexpr uint64_t OUT = J == 0 ? B : (shift ? MulPow2<T::e2, B>::OUT : 2 * kP64);
+    __device__ __forceinline__ static uint32_t apply(uint32_t x) {
+        if constexpr (J == 0)
+            return x;
+        else if constexpr (shift)
+            return MulPow2<T::e2, B>::apply(x);
+        else
+            return mulw(x, T::w);
+    }
+};
+
+// ---- in-register DIF: natural in (all < BIN), v[rev(s)] = y_s out ---------
+template <int R, bool INV, int HALF, int J, uint64_t BIN>
+struct DifStage {
+    static constexpr uint64_t K = ceil_p(BIN);
+    using M = MulTw<2 * HALF, J, INV, BIN + K>;
+    static constexpr uint64_t LO = 2 * BIN;
+    static constexpr uint64_t HI = M::OUT;
+    static constexpr uint64_t out() {
+        if constexpr (J + 1 < HALF)
+            return umax(umax(LO, HI), DifStage<R, INV, HALF, J + 1, BIN>::OUT);
+        else
+            return umax(LO, HI);
+    }
+    static constexpr uint64_t OUT = out();
+    __device__ __forceinline__ static void run(uint32_t (&v)[R]) {
+#pragma unroll
+        for (int blk = 0; blk < R; blk += 2 * HALF) {
+            const uint32_t a = v[blk + J], b = v[blk + J + HALF];
+            v[blk + J] = a + b;
+            v[blk + J + HALF] = M::apply(a + uint32_t(K) - b);
+        }
+        if constexpr (J + 1 < HALF) DifStage<R, INV, HALF, J + 1, BIN>::run(v);
+    }
+};
+
+template <int R, bool INV, int HALF, uint64_t BIN>
+struct DifAll {
+    using S = DifStage<R, INV, HALF, 0, BIN>;
+    static constexpr uint64_t B1 = S::OUT;
+    static constexpr uint64_t out() {
+        if constexpr (HALF > 1)
+            return DifAll<R, INV, HALF / 2, B1>::OUT;
+        else
+            return B1;
+    }
+    static constexpr uint64_t OUT = out();
+    __device__ __forceinline__ static void run(uint32_t (&v)[R]) {
+        S::run(v);
+        if constexpr (HALF > 1) DifAll<R, INV, HALF / 2, B1>::run(v);
+    }
+};
+
+// ---- in-register DIT: v[rev(s)] in (< BIN), natural out ---------------------
+template <int R, bool INV, int HALF, int J, uint64_t BIN>
+struct DitStage {
+    using M = MulTw<2 * HALF, J, INV, BIN>;
+    static constexpr uint64_t TB = M::OUT;
+    static constexpr uint64_t K = ceil_p(TB);
+    static constexpr uint64_t OUT1 = umax(BIN + TB, BIN + K);
+    static constexpr uint64_t out() {
+        if constexpr (J + 1 < HALF)
+            return umax(OUT1, DitStage<R, INV, HALF, J + 1, BIN>::OUT);
+        else
+            return OUT1;
+    }
+    static constexpr uint64_t OUT = out();
+    __device__ __forceinline__ static void run(uint32_t (&v)[R]) {
+#pragma unroll
+        for (int blk = 0; blk < R; blk += 2 * HALF) {
+            const uint32_t a = v[blk + J];
+            const uint32_t t = M::apply(v[blk + J + HALF]);
+            v[blk + J] = a + t;
+            v[blk + J + HALF] = a + uint32_t(K) - t;
+        }
+        if constexpr (J + 1 < HALF) DitStage<R, INV, HALF, J + 1, BIN>::run(v);
+    }
+};
+
+template <int R, bool INV, int HALF, uint64_t BIN>
+struct DitAll {
+    using S = DitStage<R, INV, HALF, 0, BIN>;
+    static constexpr uint64_t B1 = S::OUT;
+    static constexpr uint64_t out() {
+        if constexpr (2 * HALF < R)
+            return DitAll<R, INV, HALF * 2, B1>::OUT;
+        else
+            return B1;
+    }
+    static constexpr uint64_t OUT = out();
+    __device__ __forceinline__ static void run(uint32_t (&v)[R]) {
+        S::run(v);
+        if constexpr (2 * HALF < R) DitAll<R, INV, HALF * 2, B1>::run(v);
+    }
+};
+
+template <int R, bool INV, uint64_t BIN>
+__device__ __forceinline__ void dif_regs(uint32_t (&v)[R]) {
+    static_assert(DifAll<R, INV, R / 2, BIN>::OUT < (1ull << 32), "lazy bound overflow");
+    DifAll<R, INV, R / 2, BIN>::run(v);
+}
+template <int R, bool INV, uint64_t BIN>
+__device__ __forceinline__ void dit_regs(uint32_t (&v)[R]) {
+    static_assert(DitAll<R, INV, 1, BIN>::OUT < (1ull << 32), "lazy bound overflow");
+    DitAll<R, INV, 1, BIN>::run(v);
+}
+template <int R, bool INV, uint64_t BIN>
+constexpr uint64_t dif_bound() { return DifAll<R, INV, R / 2, BIN>::OUT; }
+template <int R, bool INV, uint64_t BIN>
+constexpr uint64_t dit_bound() { return DitAll<R, INV, 1, BIN>::OUT; }
+
+template <int R>
+__host__ __device__ constexpr int rev(int i) {
+    int r = 0;
+    for (int b = 1, o = R >> 1; b < R; b <<= 1, o >>= 1)
+        if (i & b) r |= o;
+    return r;
+}
+
+// ---- schedule of a size-2^E transform -------------------------------------
+template <int E>
+struct Sched {
+    static constexpr int P = (E + 3) / 4;                  // number of passes
+    static constexpr int rlog(int p) { return (p < E / 4) ? 4 : (E % 4); }
+    static constexpr int llog(int p) { return E - 4 * p; }  // block length log2 of pass p (DIF order)
+    static constexpr int slog(int p) { return llog(p) - rlog(p); }
+};
+
+// frequency index of DIF output position p (4-bit digit reversal; the last
+// digit is E%4 bits wide when E%4 != 0)
+template <int E>
+__device__ __forceinline__ uint32_t perm(uint32_t p) {
+    uint32_t f = 0;
+    int sh = E, out = 0;
+#pragma unroll
+    for (int i = 0; i < E / 4; ++i) {
+        sh -= 4;
+        f |= ((p >> sh) & 15u) << out;
+        out += 4;
+    }
+    if constexpr (E % 4) f |= (p & ((1u << (E % 4)) - 1u)) << out;
+    return f;
+}
+
+// frequency of the leading digits: perm of position (b << rlast) minus the
+// last digit's contribution, i.e. perm<E>(b << RL) where RL = last radix log2.
+template <int E>
+__device__ __forceinline__ uint32_t perm_head(uint32_t b) {
+    constexpr int RL = Sched<E>::rlog(Sched<E>::P - 1);
+    return perm<E>(b << RL);
+}
+
+}  // namespace fast
+}  // namespace fntrs_gpu

@@ -66,4 +66,28 @@ cudaError_t launch_plan_build(uint32_t N, uint32_t M, uint32_t kp, uint32_t npat
 
 constexpr uint32_t kTileMaxN = 4096;
 
+// ---- v2 fast path (codec_fast.cu): 32 <= N <= 4096, L a multiple of the tile width
+namespace fast {
+struct FastTables {
+    uint2* fwd = nullptr;  // {r_m^j, 65535 r_m^j} at [m + j]
+    uint2* inv = nullptr;
+};
+struct FastPlanView {
+    uint32_t N, k;
+    const uint2* rowmap;  // [np][N] {received row or ~0, 1/A'(x_i)}
+    const uint2* ahat2;   // [np][N] {ahat_j, 65535 ahat_j}
+};
+cudaError_t build_fast_tables(FastTables& t, cudaStream_t st);
+int fast_tile_columns(uint32_t N);  // 0 when N has no fast kernel
+cudaError_t launch_encode_fast(const FastTables& t, uint32_t k, uint32_t n, uint32_t N, uint32_t stripes,
+                               uint32_t L, const uint16_t* src, EscIn ein, uint16_t* out, EscOut eout,
+                               cudaStream_t st);
+cudaError_t launch_decode_fast(const FastTables& t, const FastPlanView& pv, uint32_t stripes, uint32_t L,
+                               const uint32_t* sp, const uint16_t* rx, EscIn ein, uint16_t* out, EscOut eout,
+                               cudaStream_t st);
+cudaError_t launch_fast_plan_tables(uint32_t N, uint32_t kp, uint32_t npatterns, const uint32_t* pos,
+                                    const uint32_t* ainv, const uint32_t* ahat, uint2* rowmap, uint2* ahat2,
+                                    cudaStream_t st);
+}  // namespace fast
+
 }  // namespace fntrs_gpu

@@ -121,6 +121,9 @@ SHAPES = [  # (k, n, L, stripes)
     (1, 1, 8, 2), (1, 5, 3, 2), (2, 4, 16, 3), (3, 8, 5, 2), (5, 11, 7, 2), (12, 16, 32, 2),
     (64, 128, 64, 3), (128, 256, 64, 4), (100, 256, 24, 2), (200, 256, 16, 2),
     (512, 1024, 32, 2), (1024, 2048, 512, 1), (2048, 4096, 64, 1), (1000, 4000, 16, 1),
+    # fused v2 kernels (n_domain 32..4096, L a multiple of the tile width), incl. k != n/2
+    (16, 32, 64, 3), (100, 256, 64, 2), (50, 256, 64, 1), (300, 512, 64, 2), (1500, 4096, 16, 1),
+    (700, 2048, 32, 1), (512, 1000, 64, 1),
 ]
 
 
@@ -195,6 +198,29 @@ def test_complete_reception_is_inverse_transform(codec, oracle):  # codec.cpp:13
         assert np.array_equal(got[0, :, c], np.where(want == 65536, 0, want))
         want_esc += [f * L + c for f in range(k) if want[f] == 65536]
     assert np.array_equal(escapes_to_numpy(oe, cnt), np.sort(np.array(want_esc, dtype=np.uint64)))
+
+
+@pytest.mark.parametrize("k,n,L,S", [(128, 256, 128, 3), (1024, 2048, 64, 1), (2048, 4096, 32, 1), (300, 512, 64, 1)])
+def test_fast_kernels_match_general_kernels(codec, k, n, L, S):
+    """A/B: the fused v2 kernels and the general tile kernels agree bit for bit."""
+    from paper_0907_1788_b200 import _lib, escapes_to_numpy, workload as W
+    lib = _lib.load()
+    src, esc = source_with_escapes(S, k, L, seed=5 * k + n, n_esc=4)
+    pats, sp = _patterns(S, n, k, seed=k)
+    res = []
+    for fast in (1, 0):
+        assert lib.fntrs_gpu_set_fast_path(codec.ctx, fast) == 0
+        out, oe, cnt = codec.encode(k, n, dev_u16(src), dev_esc(esc))
+        enc_esc = escapes_to_numpy(oe, cnt)
+        rx, rxe = W.received_packets(out, torch.from_numpy(enc_esc.view(np.int64)).cuda() if enc_esc.size else oe,
+                                     cnt, pats, sp, n)
+        plans = codec.plans(k, n, pats)
+        dec, de, dc = codec.decode(plans, torch.from_numpy(sp.view(np.int32)).cuda(), rx, rxe)
+        res.append((host_u16(out), enc_esc, host_u16(dec), escapes_to_numpy(de, dc)))
+    lib.fntrs_gpu_set_fast_path(codec.ctx, 1)
+    for a, b in zip(res[0], res[1]):
+        assert np.array_equal(a, b)
+    assert np.array_equal(res[0][2], src)
 
 
 def test_errors_map_to_reference_classes(codec):
