@@ -204,8 +204,8 @@ int fntrs_gpu_destroy(fntrs_ctx* ctx) {
     DeviceGuard g(ctx->device);
     cudaFree(ctx->tab.fwd);
     cudaFree(ctx->tab.inv);
-    cudaFree(ctx->ftab.fwd);
-    cudaFree(ctx->ftab.inv);
+    cudaFree(ctx->ftab.ptab_fwd);
+    cudaFree(ctx->ftab.ptab_inv);
     cudaFree(ctx->sort_tmp);
     cudaFree(ctx->sort_alt);
     if (ctx->internal) cudaStreamDestroy(ctx->internal);
@@ -233,7 +233,7 @@ int fntrs_gpu_encode(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t stripes, u
                 esc_cap};
     const int cols = fast::fast_tile_columns(N);
     const bool fast_ok = ctx->fast_enabled && cols && L % uint32_t(cols) == 0 &&
-                         reinterpret_cast<uintptr_t>(src) % 4 == 0 && reinterpret_cast<uintptr_t>(out) % 4 == 0;
+                         reinterpret_cast<uintptr_t>(src) % 16 == 0;
     if (fast_ok)
         CK(fast::launch_encode_fast(ctx->ftab, k, n, N, stripes, L, src, ein, out, eout, st), "encode launch");
     else
@@ -333,6 +333,8 @@ int fntrs_gpu_plans_export(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t patte
     if (pattern >= pl->np) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "pattern out of range");
     if (!pl->ahat) return fail(ctx, FNTRS_E_UNSUPPORTED, "this plan carries no locator (complete reception)");
     DeviceGuard g(ctx->device);
+    // the plan was built on the caller's stream; the export runs on the context's own
+    CK(cudaDeviceSynchronize(), "export sync");
     cudaStream_t st = ctx->internal;
     const uint32_t M = pl->M, kp = pl->kp;
     uint32_t *acoef = nullptr, *spec = nullptr;
@@ -385,7 +387,7 @@ int fntrs_gpu_decode(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t stripes, ui
                 esc_cap};
     const int cols = fast::fast_tile_columns(pl->N);
     const bool fast_ok = ctx->fast_enabled && pl->rowmap && cols && L % uint32_t(cols) == 0 &&
-                         reinterpret_cast<uintptr_t>(rx) % 4 == 0 && reinterpret_cast<uintptr_t>(out) % 4 == 0;
+                         reinterpret_cast<uintptr_t>(rx) % 16 == 0;
     if (fast_ok) {
         fast::FastPlanView fv{pl->N, pl->k, pl->rowmap, pl->ahat2};
         CK(fast::launch_decode_fast(ctx->ftab, fv, stripes, L, stripe_pattern, rx, ein, out, eout, st), "decode launch");

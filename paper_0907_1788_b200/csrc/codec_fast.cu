@@ -1,28 +1,31 @@
-// codec_fast.cu -- v2 fused encode / decode kernels for 32 <= n_domain <= 4096.
+// codec_fast.cu -- fused encode / decode kernels for 32 <= n_domain <= 4096 (v3).
 //
-// One CTA = one tile (stripe, WT = 2*NPAIR adjacent codewords); one work item
-// = one radix-R butterfly for a pair of adjacent codewords (one uint32 of two
-// uint16 symbols in global memory, one uint2 in shared memory).
+// Persistent CTAs walk tiles (stripe, WT adjacent codewords). The k input
+// packets of the NEXT tile are fetched by TMA (cp.async.bulk.tensor.2d, one
+// 2-D box of <= 256 packets x WT symbols per request, completion on an
+// mbarrier) into a double-buffered uint16 staging area while the CTA runs the
+// transforms of the current tile, so HBM reads overlap the integer pipes.
+// One work item = one radix-R butterfly of one codeword (thread = codeword,
+// warp = 32 adjacent codewords, conflict-free 32-bit shared-memory rows).
 //
 // Encode  (codec::encode_nonsystematic, proj/src/codec.cpp:124-131):
-//   pass 0 reads the k source packets straight from global memory (rows >= k
-//   are the zero padding and are never loaded), the middle passes run in
-//   shared memory, the last pass writes the n output packets straight to
-//   global memory in natural order, canonical, with 65536 escapes emitted.
+//   pass 0 reads the staged source rows (the zero padding rows >= k are
+//   never touched), the middle passes run in the shared tile, the last pass
+//   writes the n output packets to global memory in natural order,
+//   canonical, with 65536 escapes emitted (proj/src/shardio.cpp:131-137).
 // Decode  (interp::interpolate, proj/src/interp.cpp:103-137, per codeword):
-//   FNT1 (DIF, fwd)  pass 0 scatters the k received packets to their
-//                    positions and scales them by 1/A'(x_i) while loading;
-//   FNT1 last pass + FNT2 first DIT pass fused in registers: the series
-//                    s'_j = F[N-1-j] is a reversal of the butterfly group,
-//                    coefficients j >= k are zeroed in registers;
-//   FNT2 last DIT pass + (. A_hat) + FNT3 first DIF pass fused in registers;
-//   FNT3 (DIF, inv)  last pass writes the k decoded packets to global memory.
-// Shared memory holds the tile between passes only; HBM traffic is the
-// algorithmic 2k B in + 2n (encode) / 2k (decode) B out per codeword.
+//   FNT1 pass 0 scatters received row i to position z_i scaled by
+//   1/A'(x_i); FNT1's last pass and FNT2's first DIT pass are fused in
+//   registers (s'_j = F[N-1-j] is a reversal of the butterfly group; j >= k
+//   zeroed); FNT2's last DIT pass, the product with A_hat and FNT3's first
+//   DIF pass are fused in registers; FNT3's last pass writes the k decoded
+//   packets.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "fft_fast.cuh"
 #include "internal.h"
+#include "tma.cuh"
 
 namespace fntrs_gpu {
 namespace fast {
@@ -32,7 +35,7 @@ namespace {
 constexpr uint64_t kSmemCap = 1ull << 20;  // bound of values kept in shared memory
 constexpr uint64_t k2P = 2 * kP64;
 
-__device__ __forceinline__ bool esc_has(const EscIn& e, unsigned long long key) {
+__device__ __noinline__ bool esc_has(const EscIn& e, unsigned long long key) {
     uint64_t lo = 0, hi = e.n;
     while (lo < hi) {
         const uint64_t mid = (lo + hi) >> 1;
@@ -44,43 +47,10 @@ __device__ __forceinline__ bool esc_has(const EscIn& e, unsigned long long key) 
     return lo < e.n && e.keys[lo] == key;
 }
 
-__device__ __forceinline__ void emit_escape(const EscOut& e, unsigned long long key) {
+__device__ __noinline__ void emit_escape(const EscOut& e, unsigned long long key) {
     const unsigned long long i = atomicAdd(e.count, 1ull);
     if (i < e.cap) e.keys[i] = key;
 }
-
-// two uint16 symbols -> two field values (escapes restored)
-__device__ __forceinline__ void unpack2(uint32_t w, const EscIn& esc, unsigned long long key0, uint32_t& x0,
-                                        uint32_t& x1) {
-    x0 = w & 0xFFFFu;
-    x1 = w >> 16;
-    if (esc.n && (x0 == 0u || x1 == 0u)) {
-        if (x0 == 0u && esc_has(esc, key0)) x0 = 65536u;
-        if (x1 == 0u && esc_has(esc, key0 + 1)) x1 = 65536u;
-    }
-}
-
-// two values < 2p -> packed canonical uint16 pair; escapes emitted
-__device__ __forceinline__ uint32_t pack2(uint32_t y0, uint32_t y1, const EscOut& esc, unsigned long long key0) {
-    y0 = red2p(y0);
-    y1 = red2p(y1);
-    if (y0 == 65536u || y1 == 65536u) {
-        if (y0 == 65536u) emit_escape(esc, key0);
-        if (y1 == 65536u) emit_escape(esc, key0 + 1);
-    }
-    return (y0 & 0xFFFFu) | (y1 << 16);
-}
-
-// Shared-memory tile [N][NPAIR] uint2 with an XOR swizzle on the pair index
-// that keeps the sub = 1 passes (rows 16b + q) free of bank conflicts.
-template <int E, int NPAIR>
-struct Tile {
-    static constexpr int SW = Sched<E>::rlog(Sched<E>::P - 1);
-    uint2* sm;
-    __device__ __forceinline__ uint2& at(uint32_t prow, int pair) const {
-        return sm[prow * NPAIR + (pair ^ int((prow >> SW) & (NPAIR - 1)))];
-    }
-};
 
 template <int N>
 constexpr int ilog2c() {
@@ -89,7 +59,6 @@ constexpr int ilog2c() {
     return e;
 }
 
-// Reduce v (bound B) so that it is below CAP.
 template <uint64_t B, uint64_t CAP>
 __device__ __forceinline__ uint32_t cap(uint32_t v) {
     if constexpr (B > CAP)
@@ -98,393 +67,504 @@ __device__ __forceinline__ uint32_t cap(uint32_t v) {
         return v;
 }
 
-// ---- generic pass -----------------------------------------------------------
+// ---- geometry ---------------------------------------------------------------
+template <int E>
+struct Geom {
+    static constexpr int N = 1 << E;
+    static constexpr int WT = N <= 256 ? 64 : (N == 512 ? 32 : (N == 1024 ? 16 : 8));
+    static constexpr int NT = N == 4096 ? 512 : 256;
+    static constexpr int RLZ = Sched<E>::rlog(Sched<E>::P - 1);
+    static constexpr int RPW = WT >= 32 ? 1 : 32 / WT;  // tile rows touched by one warp
+    // shared tile index with a row swizzle keeping the sub = 1 passes
+    // (rows R*b + q, consecutive b in one warp) on distinct banks
+    __device__ __forceinline__ static uint32_t idx(uint32_t row, uint32_t col) {
+        if constexpr (RPW > 1)
+            row ^= (row >> RLZ) & uint32_t(RPW - 1);
+        return row * WT + col;
+    }
+};
+
+// ---- generic pass (one codeword per work item) ----------------------------
 // DIF (DIT=false) or DIT pass with the geometry of DIF pass p of a size-2^E
-// transform. Loaded values must be below BIN; stored values are below OCAP
-// (>= 2p). ld(lrow, b, q, pair, x0, x1); st(lrow, b, s, pair, y0, y1).
-template <int E, int p, bool INV, bool DIT, int NPAIR, int NT, uint64_t BIN, uint64_t OCAP, class LD, class ST>
-__device__ __forceinline__ void pass(const uint2* __restrict__ tw, const LD& ld, const ST& st) {
+// transform. Loaded values must be below BIN; stored values are below OCAP.
+// twp: per-pass twiddle table, row t holds {r_len^(t s), 65535 r_len^(t s)}
+// for s < R (only read when sub > 1).
+template <int E, int p, bool INV, bool DIT, uint64_t BIN, uint64_t OCAP, class LD, class ST>
+__device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld, const ST& st) {
     using S = Sched<E>;
+    using G = Geom<E>;
     constexpr int RL = S::rlog(p), R = 1 << RL, LL = S::llog(p), SL = S::slog(p);
-    constexpr int ITEMS = (1 << (E - RL)) * NPAIR;
-    constexpr int LGP = ilog2c<NPAIR>();
+    constexpr int ITEMS = (1 << (E - RL)) * G::WT;
+    constexpr int LGW = ilog2c<G::WT>();
     static_assert(OCAP >= k2P, "");
 #pragma unroll 1
-    for (int it = threadIdx.x; it < ITEMS; it += NT) {
-        const int pair = it & (NPAIR - 1);
-        const uint32_t b = uint32_t(it) >> LGP;
+    for (int it = threadIdx.x; it < ITEMS; it += G::NT) {
+        const uint32_t col = uint32_t(it) & uint32_t(G::WT - 1);
+        const uint32_t b = uint32_t(it) >> LGW;
         const uint32_t t = b & ((1u << SL) - 1u);
         const uint32_t base = ((b >> SL) << LL) + t;
-        uint32_t v0[R], v1[R];
+        uint32_t v[R];
+        uint2 w[R];
+        if constexpr (SL > 0) {
+            const uint4* tp = twp + t * (R / 2);
+#pragma unroll
+            for (int i = 0; i < R / 2; ++i) {
+                const uint4 x = __ldg(tp + i);
+                w[2 * i] = make_uint2(x.x, x.y);
+                w[2 * i + 1] = make_uint2(x.z, x.w);
+            }
+        }
         if constexpr (!DIT) {
 #pragma unroll
-            for (int q = 0; q < R; ++q) ld(base + (uint32_t(q) << SL), b, q, pair, v0[q], v1[q]);
-            dif_regs<R, INV, BIN>(v0);
-            dif_regs<R, INV, BIN>(v1);
+            for (int q = 0; q < R; ++q) v[q] = ld(base + (uint32_t(q) << SL), b, q, col);
+            dif_regs<R, INV, BIN>(v);
             constexpr uint64_t BO = dif_bound<R, INV, BIN>();
 #pragma unroll
             for (int s = 0; s < R; ++s) {
-                uint32_t y0 = v0[rev<R>(s)], y1 = v1[rev<R>(s)];
-                if (SL > 0 && s > 0) {
-                    const uint2 w = __ldg(tw + ((t * uint32_t(s)) << (E - LL)));
-                    y0 = mulw2(y0, w.x, w.y);
-                    y1 = mulw2(y1, w.x, w.y);
-                } else {
-                    y0 = cap<BO, OCAP>(y0);
-                    y1 = cap<BO, OCAP>(y1);
-                }
-                st(base + (uint32_t(s) << SL), b, s, pair, y0, y1);
+                uint32_t y = v[rev<R>(s)];
+                if (SL > 0 && s > 0)
+                    y = mulw2(y, w[s].x, w[s].y);
+                else
+                    y = cap<BO, OCAP>(y);
+                st(base + (uint32_t(s) << SL), b, s, col, y);
             }
         } else {
             constexpr uint64_t BI = BIN > k2P ? BIN : k2P;
 #pragma unroll
             for (int s = 0; s < R; ++s) {
-                uint32_t x0, x1;
-                ld(base + (uint32_t(s) << SL), b, s, pair, x0, x1);
-                if (SL > 0 && s > 0) {
-                    const uint2 w = __ldg(tw + ((t * uint32_t(s)) << (E - LL)));
-                    x0 = mulw2(x0, w.x, w.y);
-                    x1 = mulw2(x1, w.x, w.y);
-                }
-                v0[rev<R>(s)] = x0;
-                v1[rev<R>(s)] = x1;
+                uint32_t x = ld(base + (uint32_t(s) << SL), b, s, col);
+                if (SL > 0 && s > 0) x = mulw2(x, w[s].x, w[s].y);
+                v[rev<R>(s)] = x;
             }
-            dit_regs<R, INV, BI>(v0);
-            dit_regs<R, INV, BI>(v1);
+            dit_regs<R, INV, BI>(v);
             constexpr uint64_t BO = dit_bound<R, INV, BI>();
 #pragma unroll
-            for (int q = 0; q < R; ++q)
-                st(base + (uint32_t(q) << SL), b, q, pair, cap<BO, OCAP>(v0[q]), cap<BO, OCAP>(v1[q]));
+            for (int q = 0; q < R; ++q) st(base + (uint32_t(q) << SL), b, q, col, cap<BO, OCAP>(v[q]));
         }
     }
 }
 
+// Per-pass twiddle tables for one direction: table for block length 2^LL at
+// uint2 offset 2^LL (LL <= 12): entry t*16 + s = r_len^(t s).
+__device__ __forceinline__ const uint4* pass_table(const uint2* base, int LL) {
+    return reinterpret_cast<const uint4*>(base + (1u << LL));
+}
+
+// ---- TMA staging of the k input packets of a tile ------------------------
+struct Stage {
+    uint16_t* buf[2];
+    uint64_t* bar;  // two mbarriers
+    uint32_t nbox, box_rows, bytes;
+};
+
+template <int WT>
+__device__ __forceinline__ void stage_issue(const Stage& sg, int b, const CUtensorMap* map, uint32_t c0, uint32_t row0) {
+    fence_proxy_async();
+    mbar_expect_tx(&sg.bar[b], sg.bytes);
+    for (uint32_t j = 0; j < sg.nbox; ++j)
+        tma_load_2d(sg.buf[b] + size_t(j) * sg.box_rows * WT, map, int(c0), int(row0 + j * sg.box_rows), &sg.bar[b]);
+}
+
+__device__ __forceinline__ uint32_t staged_value(const uint16_t* st, uint32_t idx, const EscIn& esc,
+                                                 unsigned long long key) {
+    const uint32_t x = st[idx];
+    if (x == 0u && esc.n && esc_has(esc, key)) return 65536u;
+    return x;
+}
+
 // ---------------------------------------------------------------------------
-template <int E, int NPAIR, int NT, bool HALFK>
-__global__ void __launch_bounds__(NT) enc_fast_kernel(const uint2* __restrict__ tw, uint32_t k, uint32_t n, uint32_t L,
-                                                      uint32_t tps, const uint16_t* __restrict__ src, EscIn esc_in,
-                                                      uint16_t* __restrict__ out, EscOut esc_out) {
-    extern __shared__ uint2 smem[];
+template <int E, bool HALFK>
+__global__ void __launch_bounds__(Geom<E>::NT) enc_fast_kernel(const __grid_constant__ CUtensorMap src_map,
+                                                               const uint2* __restrict__ ptabF, uint32_t k, uint32_t n,
+                                                               uint32_t L, uint32_t tps, uint32_t tiles, uint32_t nbox,
+                                                               uint32_t box_rows, EscIn esc_in,
+                                                               uint16_t* __restrict__ out, EscOut esc_out) {
     using S = Sched<E>;
-    constexpr int P = S::P;
-    constexpr int RL0 = S::rlog(0), RLZ = S::rlog(P - 1);
-    static_assert(P >= 2, "fast path needs at least two passes");
-    const Tile<E, NPAIR> tile{smem};
-    const uint32_t stripe = blockIdx.x / tps;
-    const uint32_t c0 = (blockIdx.x - stripe * tps) * uint32_t(2 * NPAIR);
-    const uint32_t L2 = L >> 1;
-    const uint32_t* __restrict__ srcw = reinterpret_cast<const uint32_t*>(src) + (uint64_t(stripe) * k * L + c0) / 2;
-    uint32_t* __restrict__ outw = reinterpret_cast<uint32_t*>(out) + (uint64_t(stripe) * n * L + c0) / 2;
-    const unsigned long long key_in = uint64_t(stripe) * k * L + c0;
-    const unsigned long long key_out = uint64_t(stripe) * n * L + c0;
-
-    auto ld_src = [&](uint32_t lrow, uint32_t, int q, int pair, uint32_t& x0, uint32_t& x1) {
-        if ((HALFK && q >= (1 << RL0) / 2) || (!HALFK && lrow >= k)) {
-            x0 = x1 = 0u;
-            return;
-        }
-        const uint32_t w = __ldcs(srcw + size_t(lrow) * L2 + pair);
-        unpack2(w, esc_in, key_in + uint64_t(lrow) * L + 2 * pair, x0, x1);
-    };
-    auto ld_sm = [&](uint32_t lrow, uint32_t, int, int pair, uint32_t& x0, uint32_t& x1) {
-        const uint2 v = tile.at(lrow, pair);
-        x0 = v.x;
-        x1 = v.y;
-    };
-    auto st_sm = [&](uint32_t lrow, uint32_t, int, int pair, uint32_t y0, uint32_t y1) {
-        tile.at(lrow, pair) = make_uint2(y0, y1);
-    };
-    auto st_out = [&](uint32_t, uint32_t b, int s, int pair, uint32_t y0, uint32_t y1) {
-        const uint32_t f = perm_head<E>(b) + (uint32_t(s) << (E - RLZ));
-        if (f >= n) return;
-        __stcs(outw + size_t(f) * L2 + pair, pack2(y0, y1, esc_out, key_out + uint64_t(f) * L + 2 * pair));
-    };
-
-    pass<E, 0, false, false, NPAIR, NT, kP64, kSmemCap>(tw, ld_src, st_sm);
+    using G = Geom<E>;
+    constexpr int N = 1 << E, WT = G::WT, P = S::P;
+    constexpr int RL0 = S::rlog(0), RLZ = G::RLZ;
+    static_assert(P >= 2 && P <= 3, "");
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t bars[2];
+    uint32_t* work = reinterpret_cast<uint32_t*>(smem_raw);
+    Stage sg;
+    sg.nbox = nbox;
+    sg.box_rows = box_rows;
+    sg.bytes = nbox * box_rows * WT * 2;
+    sg.buf[0] = reinterpret_cast<uint16_t*>(smem_raw + size_t(N) * WT * 4);
+    sg.buf[1] = sg.buf[0] + size_t(nbox) * box_rows * WT;
+    sg.bar = bars;
+    if (threadIdx.x == 0) {
+        tma_prefetch_desc(&src_map);
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbar_init();
+    }
     __syncthreads();
-    if constexpr (P == 3) {
-        pass<E, 1, false, false, NPAIR, NT, kSmemCap, kSmemCap>(tw, ld_sm, st_sm);
+    uint32_t tile = blockIdx.x;
+    if (threadIdx.x == 0 && tile < tiles) {
+        const uint32_t s0 = tile / tps;
+        stage_issue<WT>(sg, 0, &src_map, (tile - s0 * tps) * WT, s0 * k);
+    }
+    for (uint32_t iter = 0; tile < tiles; ++iter, tile += gridDim.x) {
+        const int bsel = iter & 1;
+        const uint32_t stripe = tile / tps;
+        const uint32_t c0 = (tile - stripe * tps) * WT;
+        const uint32_t next = tile + gridDim.x;
+        if (threadIdx.x == 0 && next < tiles) {
+            const uint32_t s1 = next / tps;
+            stage_issue<WT>(sg, bsel ^ 1, &src_map, (next - s1 * tps) * WT, s1 * k);
+        }
+        mbar_wait(&bars[bsel], (iter >> 1) & 1);
+        const uint16_t* st_in = sg.buf[bsel];
+        const unsigned long long key_in = uint64_t(stripe) * k * L + c0;
+        const unsigned long long key_out = uint64_t(stripe) * n * L + c0;
+        uint16_t* outp = out + uint64_t(stripe) * n * L + c0;
+
+        auto ld_src = [&](uint32_t lrow, uint32_t, int q, uint32_t col) -> uint32_t {
+            if ((HALFK && q >= (1 << RL0) / 2) || (!HALFK && lrow >= k)) return 0u;
+            return staged_value(st_in, lrow * WT + col, esc_in, key_in + uint64_t(lrow) * L + col);
+        };
+        auto ld_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t { return work[G::idx(lrow, col)]; };
+        auto st_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col, uint32_t y) { work[G::idx(lrow, col)] = y; };
+        auto st_out = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) {
+            const uint32_t f = perm_head<E>(b) + (uint32_t(s) << (E - RLZ));
+            if (f >= n) return;
+            y = red2p(y);
+            if (y == 65536u) emit_escape(esc_out, key_out + uint64_t(f) * L + col);
+            __stcs(outp + size_t(f) * L + col, uint16_t(y));
+        };
+
+        pass<E, 0, false, false, kP64, kSmemCap>(pass_table(ptabF, S::llog(0)), ld_src, st_sm);
+        __syncthreads();
+        if constexpr (P == 3) {
+            pass<E, 1, false, false, kSmemCap, kSmemCap>(pass_table(ptabF, S::llog(1)), ld_sm, st_sm);
+            __syncthreads();
+        }
+        pass<E, P - 1, false, false, kSmemCap, k2P>(pass_table(ptabF, S::llog(P - 1)), ld_sm, st_out);
         __syncthreads();
     }
-    pass<E, P - 1, false, false, NPAIR, NT, kSmemCap, k2P>(tw, ld_sm, st_out);
 }
 
 // ---------------------------------------------------------------------------
-template <int E, int NPAIR, int NT>
-__global__ void __launch_bounds__(NT) dec_fast_kernel(const uint2* __restrict__ twF, const uint2* __restrict__ twI,
-                                                      const uint2* __restrict__ rowmap, const uint2* __restrict__ ahat2,
-                                                      uint32_t k, uint32_t L, uint32_t tps,
-                                                      const uint32_t* __restrict__ stripe_pattern,
-                                                      const uint16_t* __restrict__ rx, EscIn esc_in,
-                                                      uint16_t* __restrict__ out, EscOut esc_out) {
-    extern __shared__ uint2 smem[];
+template <int E>
+__global__ void __launch_bounds__(Geom<E>::NT) dec_fast_kernel(const __grid_constant__ CUtensorMap rx_map,
+                                                               const uint2* __restrict__ ptabF,
+                                                               const uint2* __restrict__ ptabI,
+                                                               const uint2* __restrict__ rowmap,
+                                                               const uint2* __restrict__ ahat2, uint32_t k, uint32_t L,
+                                                               uint32_t tps, uint32_t tiles, uint32_t nbox,
+                                                               uint32_t box_rows,
+                                                               const uint32_t* __restrict__ stripe_pattern,
+                                                               EscIn esc_in, uint16_t* __restrict__ out, EscOut esc_out) {
     using S = Sched<E>;
-    constexpr int N = 1 << E;
-    constexpr int P = S::P;
-    constexpr int RLZ = S::rlog(P - 1), RZ = 1 << RLZ;
+    using G = Geom<E>;
+    constexpr int N = 1 << E, WT = G::WT, NT = G::NT, P = S::P;
+    constexpr int RLZ = G::RLZ, RZ = 1 << RLZ;
     constexpr int RL0 = S::rlog(0), R0 = 1 << RL0, SL0 = S::slog(0);
     constexpr uint32_t FLIP = uint32_t(N - 1);
-    constexpr int LGP = ilog2c<NPAIR>();
-    static_assert(P >= 2, "fast path needs at least two passes");
-    const Tile<E, NPAIR> tile{smem};
-    const uint32_t stripe = blockIdx.x / tps;
-    const uint32_t c0 = (blockIdx.x - stripe * tps) * uint32_t(2 * NPAIR);
-    const uint32_t L2 = L >> 1;
-    const uint32_t pat = __ldg(stripe_pattern + stripe);
-    const uint2* __restrict__ rm = rowmap + size_t(pat) * N;
-    const uint2* __restrict__ ah = ahat2 + size_t(pat) * N;
-    const uint32_t* __restrict__ rxw = reinterpret_cast<const uint32_t*>(rx) + (uint64_t(stripe) * k * L + c0) / 2;
-    uint32_t* __restrict__ outw = reinterpret_cast<uint32_t*>(out) + (uint64_t(stripe) * k * L + c0) / 2;
-    const unsigned long long key_in = uint64_t(stripe) * k * L + c0;
+    constexpr int LGW = ilog2c<WT>();
+    static_assert(P >= 2 && P <= 3, "");
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t bars[2];
+    uint32_t* work = reinterpret_cast<uint32_t*>(smem_raw);
+    Stage sg;
+    sg.nbox = nbox;
+    sg.box_rows = box_rows;
+    sg.bytes = nbox * box_rows * WT * 2;
+    sg.buf[0] = reinterpret_cast<uint16_t*>(smem_raw + size_t(N) * WT * 4);
+    sg.buf[1] = sg.buf[0] + size_t(nbox) * box_rows * WT;
+    sg.bar = bars;
+    if (threadIdx.x == 0) {
+        tma_prefetch_desc(&rx_map);
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    uint32_t tile = blockIdx.x;
+    if (threadIdx.x == 0 && tile < tiles) {
+        const uint32_t s0 = tile / tps;
+        stage_issue<WT>(sg, 0, &rx_map, (tile - s0 * tps) * WT, s0 * k);
+    }
+    const uint4* tF0 = pass_table(ptabF, S::llog(0));
+    const uint4* tI0 = pass_table(ptabI, S::llog(0));
+    for (uint32_t iter = 0; tile < tiles; ++iter, tile += gridDim.x) {
+        const int bsel = iter & 1;
+        const uint32_t stripe = tile / tps;
+        const uint32_t c0 = (tile - stripe * tps) * WT;
+        const uint32_t next = tile + gridDim.x;
+        if (threadIdx.x == 0 && next < tiles) {
+            const uint32_t s1 = next / tps;
+            stage_issue<WT>(sg, bsel ^ 1, &rx_map, (next - s1 * tps) * WT, s1 * k);
+        }
+        const uint32_t pat = __ldg(stripe_pattern + stripe);
+        const uint2* __restrict__ rm = rowmap + size_t(pat) * N;
+        const uint2* __restrict__ ah = ahat2 + size_t(pat) * N;
+        const unsigned long long key = uint64_t(stripe) * k * L + c0;
+        uint16_t* outp = out + uint64_t(stripe) * k * L + c0;
+        mbar_wait(&bars[bsel], (iter >> 1) & 1);
+        const uint16_t* st_in = sg.buf[bsel];
 
-    // step 4: N'[z] = v_i / A'(x_i) where z = z_i, else 0 (rowmap[z] = {i or ~0, 1/A'(x_i)})
-    auto ld_scatter = [&](uint32_t lrow, uint32_t, int, int pair, uint32_t& x0, uint32_t& x1) {
-        const uint2 m = __ldg(rm + lrow);
-        if (m.x == 0xFFFFFFFFu) {
-            x0 = x1 = 0u;
-            return;
-        }
-        const uint32_t w = __ldcs(rxw + size_t(m.x) * L2 + pair);
-        uint32_t a0, a1;
-        unpack2(w, esc_in, key_in + uint64_t(m.x) * L + 2 * pair, a0, a1);
-        const uint32_t m2 = m.y * 65535u;
-        x0 = mulw2(a0, m.y, m2);
-        x1 = mulw2(a1, m.y, m2);
-    };
-    auto ld_sm = [&](uint32_t lrow, uint32_t, int, int pair, uint32_t& x0, uint32_t& x1) {
-        const uint2 v = tile.at(lrow, pair);
-        x0 = v.x;
-        x1 = v.y;
-    };
-    auto st_sm = [&](uint32_t lrow, uint32_t, int, int pair, uint32_t y0, uint32_t y1) {
-        tile.at(lrow, pair) = make_uint2(y0, y1);
-    };
-    auto ld_smf = [&](uint32_t lrow, uint32_t, int, int pair, uint32_t& x0, uint32_t& x1) {
-        const uint2 v = tile.at(lrow ^ FLIP, pair);
-        x0 = v.x;
-        x1 = v.y;
-    };
-    auto st_smf = [&](uint32_t lrow, uint32_t, int, int pair, uint32_t y0, uint32_t y1) {
-        tile.at(lrow ^ FLIP, pair) = make_uint2(y0, y1);
-    };
-    auto st_out = [&](uint32_t, uint32_t b, int s, int pair, uint32_t y0, uint32_t y1) {
-        const uint32_t f = perm_head<E>(b) + (uint32_t(s) << (E - RLZ));
-        if (f >= k) return;
-        __stcs(outw + size_t(f) * L2 + pair, pack2(y0, y1, esc_out, key_in + uint64_t(f) * L + 2 * pair));
-    };
+        // step 4: N'[z] = v_i / A'(x_i) where z = z_i, else 0
+        auto ld_scatter = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t {
+            const uint2 m = __ldg(rm + lrow);
+            if (m.x == 0xFFFFFFFFu) return 0u;
+            const uint32_t v = staged_value(st_in, m.x * WT + col, esc_in, key + uint64_t(m.x) * L + col);
+            return mulw2(v, m.y, m.y * 65535u);
+        };
+        auto ld_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t { return work[G::idx(lrow, col)]; };
+        auto st_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col, uint32_t y) { work[G::idx(lrow, col)] = y; };
+        auto ld_smf = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t {
+            return work[G::idx(lrow ^ FLIP, col)];
+        };
+        auto st_smf = [&](uint32_t lrow, uint32_t, int, uint32_t col, uint32_t y) { work[G::idx(lrow ^ FLIP, col)] = y; };
+        auto st_out = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) {
+            const uint32_t f = perm_head<E>(b) + (uint32_t(s) << (E - RLZ));
+            if (f >= k) return;
+            y = red2p(y);
+            if (y == 65536u) emit_escape(esc_out, key + uint64_t(f) * L + col);
+            __stcs(outp + size_t(f) * L + col, uint16_t(y));
+        };
 
-    // FNT1 = FNT_N(N'), DIF, natural -> perm order (flip 0)
-    pass<E, 0, false, false, NPAIR, NT, k2P, kSmemCap>(twF, ld_scatter, st_sm);
-    __syncthreads();
-    if constexpr (P == 3) {
-        pass<E, 1, false, false, NPAIR, NT, kSmemCap, kSmemCap>(twF, ld_sm, st_sm);
+        // FNT1 = FNT_N(N'), DIF, natural -> perm order (flip 0)
+        pass<E, 0, false, false, k2P, kSmemCap>(tF0, ld_scatter, st_sm);
         __syncthreads();
-    }
-    // FNT1 last pass (sub 1, no table twiddles) + FNT2 first DIT pass on the
-    // reversed view: logical group b' = N/R - 1 - G holds s'_j = F[N-1-j].
-    {
-        constexpr int ITEMS = (N / RZ) * NPAIR;
-        constexpr uint64_t BD = dif_bound<RZ, false, kSmemCap>();
-        constexpr uint64_t BT = dit_bound<RZ, false, BD>();
-#pragma unroll 1
-        for (int it = threadIdx.x; it < ITEMS; it += NT) {
-            const int pair = it & (NPAIR - 1);
-            const uint32_t G = uint32_t(it) >> LGP;
-            uint32_t v0[RZ], v1[RZ];
-#pragma unroll
-            for (int q = 0; q < RZ; ++q) {
-                const uint2 v = tile.at((G << RLZ) + q, pair);
-                v0[q] = v.x;
-                v1[q] = v.y;
-            }
-            dif_regs<RZ, false, kSmemCap>(v0);
-            dif_regs<RZ, false, kSmemCap>(v1);
-            const uint32_t bp = uint32_t(N / RZ) - 1u - G;
-            const uint32_t fh = perm_head<E>(bp);
-            uint32_t u0[RZ], u1[RZ];
-#pragma unroll
-            for (int j = 0; j < RZ; ++j) {
-                const int sp = rev<RZ>(j);  // u[rev(s')] = x_{s'} = y_{R-1-s'}
-                const bool live = fh + (uint32_t(sp) << (E - RLZ)) < k;
-                u0[j] = live ? v0[RZ - 1 - j] : 0u;
-                u1[j] = live ? v1[RZ - 1 - j] : 0u;
-            }
-            dit_regs<RZ, false, BD>(u0);
-            dit_regs<RZ, false, BD>(u1);
-#pragma unroll
-            for (int q = 0; q < RZ; ++q)
-                tile.at((G << RLZ) + (RZ - 1 - q), pair) =
-                    make_uint2(cap<BT, kSmemCap>(u0[q]), cap<BT, kSmemCap>(u1[q]));
+        if constexpr (P == 3) {
+            pass<E, 1, false, false, kSmemCap, kSmemCap>(pass_table(ptabF, S::llog(1)), ld_sm, st_sm);
+            __syncthreads();
         }
-    }
-    __syncthreads();
-    if constexpr (P == 3) {
-        pass<E, 1, false, true, NPAIR, NT, kSmemCap, kSmemCap>(twF, ld_smf, st_smf);
-        __syncthreads();
-    }
-    // FNT2 last DIT pass + (. ahat) + FNT3 first DIF pass: rows t + q * sub0
-    {
-        constexpr int ITEMS = (N / R0) * NPAIR;
-        constexpr uint64_t BT = dit_bound<R0, false, kSmemCap>();
-        constexpr uint64_t BO = dif_bound<R0, true, k2P>();
+        // FNT1 last pass (sub 1) + FNT2 first DIT pass on the reversed view:
+        // logical group b' = N/R - 1 - G holds s'_j = F[N-1-j]; j >= k zeroed.
+        {
+            constexpr int ITEMS = (N / RZ) * WT;
+            constexpr uint64_t BD = dif_bound<RZ, false, kSmemCap>();
+            constexpr uint64_t BT = dit_bound<RZ, false, BD>();
 #pragma unroll 1
-        for (int it = threadIdx.x; it < ITEMS; it += NT) {
-            const int pair = it & (NPAIR - 1);
-            const uint32_t t = uint32_t(it) >> LGP;
-            uint32_t v0[R0], v1[R0];
+            for (int it = threadIdx.x; it < ITEMS; it += NT) {
+                const uint32_t col = uint32_t(it) & uint32_t(WT - 1);
+                const uint32_t g = uint32_t(it) >> LGW;
+                uint32_t v[RZ];
 #pragma unroll
-            for (int s = 0; s < R0; ++s) {
-                const uint2 v = tile.at((t + (uint32_t(s) << SL0)) ^ FLIP, pair);
-                uint32_t x0 = v.x, x1 = v.y;
-                if (s > 0) {
-                    const uint2 w = __ldg(twF + t * uint32_t(s));
-                    x0 = mulw2(x0, w.x, w.y);
-                    x1 = mulw2(x1, w.x, w.y);
+                for (int q = 0; q < RZ; ++q) v[q] = work[G::idx((g << RLZ) + q, col)];
+                dif_regs<RZ, false, kSmemCap>(v);
+                const uint32_t fh = perm_head<E>(uint32_t(N / RZ) - 1u - g);
+                uint32_t u[RZ];
+#pragma unroll
+                for (int j = 0; j < RZ; ++j) {  // u[rev(s')] = x_{s'} = y_{R-1-s'} = v[R-1-j]
+                    const bool live = fh + (uint32_t(rev<RZ>(j)) << (E - RLZ)) < k;
+                    u[j] = live ? v[RZ - 1 - j] : 0u;
                 }
-                v0[rev<R0>(s)] = x0;
-                v1[rev<R0>(s)] = x1;
-            }
-            dit_regs<R0, false, kSmemCap>(v0);
-            dit_regs<R0, false, kSmemCap>(v1);
-            static_assert(BT < (1ull << 32), "");
+                dit_regs<RZ, false, BD>(u);
 #pragma unroll
-            for (int q = 0; q < R0; ++q) {
-                const uint2 a = __ldg(ah + t + (uint32_t(q) << SL0));
-                v0[q] = mulw2(v0[q], a.x, a.y);
-                v1[q] = mulw2(v1[q], a.x, a.y);
-            }
-            dif_regs<R0, true, k2P>(v0);
-            dif_regs<R0, true, k2P>(v1);
-#pragma unroll
-            for (int s = 0; s < R0; ++s) {
-                uint32_t y0 = v0[rev<R0>(s)], y1 = v1[rev<R0>(s)];
-                if (s > 0) {
-                    const uint2 w = __ldg(twI + t * uint32_t(s));
-                    y0 = mulw2(y0, w.x, w.y);
-                    y1 = mulw2(y1, w.x, w.y);
-                } else {
-                    y0 = cap<BO, kSmemCap>(y0);
-                    y1 = cap<BO, kSmemCap>(y1);
-                }
-                tile.at((t + (uint32_t(s) << SL0)) ^ FLIP, pair) = make_uint2(y0, y1);
+                for (int q = 0; q < RZ; ++q) work[G::idx((g << RLZ) + (RZ - 1 - q), col)] = cap<BT, kSmemCap>(u[q]);
             }
         }
-    }
-    __syncthreads();
-    if constexpr (P == 3) {
-        pass<E, 1, true, false, NPAIR, NT, kSmemCap, kSmemCap>(twI, ld_smf, st_smf);
+        __syncthreads();
+        if constexpr (P == 3) {
+            pass<E, 1, false, true, kSmemCap, kSmemCap>(pass_table(ptabF, S::llog(1)), ld_smf, st_smf);
+            __syncthreads();
+        }
+        // FNT2 last DIT pass + (. ahat) + FNT3 first DIF pass: rows t + q * sub0
+        {
+            constexpr int ITEMS = (N / R0) * WT;
+            constexpr uint64_t BO = dif_bound<R0, true, k2P>();
+#pragma unroll 1
+            for (int it = threadIdx.x; it < ITEMS; it += NT) {
+                const uint32_t col = uint32_t(it) & uint32_t(WT - 1);
+                const uint32_t t = uint32_t(it) >> LGW;
+                uint32_t v[R0];
+                uint2 w[R0];
+                {
+                    const uint4* tp = tF0 + t * (R0 / 2);
+#pragma unroll
+                    for (int i = 0; i < R0 / 2; ++i) {
+                        const uint4 x = __ldg(tp + i);
+                        w[2 * i] = make_uint2(x.x, x.y);
+                        w[2 * i + 1] = make_uint2(x.z, x.w);
+                    }
+                }
+#pragma unroll
+                for (int s = 0; s < R0; ++s) {
+                    uint32_t x = work[G::idx((t + (uint32_t(s) << SL0)) ^ FLIP, col)];
+                    if (s > 0) x = mulw2(x, w[s].x, w[s].y);
+                    v[rev<R0>(s)] = x;
+                }
+                dit_regs<R0, false, kSmemCap>(v);
+#pragma unroll
+                for (int q = 0; q < R0; ++q) {
+                    const uint2 a = __ldg(ah + t + (uint32_t(q) << SL0));
+                    v[q] = mulw2(v[q], a.x, a.y);
+                }
+                dif_regs<R0, true, k2P>(v);
+                {
+                    const uint4* tp = tI0 + t * (R0 / 2);
+#pragma unroll
+                    for (int i = 0; i < R0 / 2; ++i) {
+                        const uint4 x = __ldg(tp + i);
+                        w[2 * i] = make_uint2(x.x, x.y);
+                        w[2 * i + 1] = make_uint2(x.z, x.w);
+                    }
+                }
+#pragma unroll
+                for (int s = 0; s < R0; ++s) {
+                    uint32_t y = v[rev<R0>(s)];
+                    if (s > 0)
+                        y = mulw2(y, w[s].x, w[s].y);
+                    else
+                        y = cap<BO, kSmemCap>(y);
+                    work[G::idx((t + (uint32_t(s) << SL0)) ^ FLIP, col)] = y;
+                }
+            }
+        }
+        __syncthreads();
+        if constexpr (P == 3) {
+            pass<E, 1, true, false, kSmemCap, kSmemCap>(pass_table(ptabI, S::llog(1)), ld_smf, st_smf);
+            __syncthreads();
+        }
+        pass<E, P - 1, true, false, kSmemCap, k2P>(pass_table(ptabI, S::llog(P - 1)), ld_smf, st_out);
         __syncthreads();
     }
-    pass<E, P - 1, true, false, NPAIR, NT, kSmemCap, k2P>(twI, ld_smf, st_out);
 }
 
-__global__ void tables2_kernel(uint2* fwd, uint2* inv) {
+// per-pass twiddle tables: [2^LL + t*16 + s] = r_(2^LL)^(t*s) for LL <= 12
+__global__ void ptab_kernel(uint2* fwd, uint2* inv) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i == 0 || i >= (1u << 17)) return;
-    const int e = 31 - __clz(i);
-    const uint32_t m = 1u << e, j = i - m;
-    const uint32_t ex = (j << (16 - e)) & 0xFFFFu;
+    if (i < 32 || i >= (1u << 13)) return;
+    const int LL = 31 - __clz(i);
+    const uint32_t j = i - (1u << LL), t = j >> 4, s = j & 15u;
+    const uint32_t ex = ((t * s) << (16 - LL)) & 0xFFFFu;  // r_len = 3^(65536/len)
     const uint32_t wf = gpow(3u, ex), wi = gpow(3u, (65536u - ex) & 0xFFFFu);
     fwd[i] = make_uint2(wf, wf * 65535u);
     inv[i] = make_uint2(wi, wi * 65535u);
 }
 
-// per-pattern decode tables for the fast kernel:
-//   rowmap[p][z] = {i, 1/A'(x_i)} if position z is received as row i, else {~0, 0}
-//   ahat2[p][j]  = {ahat_j, 65535 * ahat_j}
-__global__ void fast_plan_tables_kernel(uint32_t N, uint32_t kp, const uint32_t* __restrict__ pos,
-                                        const uint32_t* __restrict__ ainv, const uint32_t* __restrict__ ahat,
-                                        uint2* __restrict__ rowmap, uint2* __restrict__ ahat2) {
-    const uint32_t p = blockIdx.y;
-    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) {
-        rowmap[size_t(p) * N + j] = make_uint2(0xFFFFFFFFu, 0u);
-        const uint32_t a = ahat[size_t(p) * N + j];
-        ahat2[size_t(p) * N + j] = make_uint2(a, a * 65535u);
+__global__ void fast_plan_tables_kernel(uint32_t N, const uint32_t* __restrict__ ahat, uint2* __restrict__ rowmap,
+                                        uint2* __restrict__ ahat2, uint64_t total) {
+    for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < total; j += uint64_t(gridDim.x) * blockDim.x) {
+        rowmap[j] = make_uint2(0xFFFFFFFFu, 0u);
+        const uint32_t a = ahat[j];
+        ahat2[j] = make_uint2(a, a * 65535u);
     }
 }
 
 __global__ void fast_plan_scatter_kernel(uint32_t N, uint32_t kp, const uint32_t* __restrict__ pos,
-                                         const uint32_t* __restrict__ ainv, uint2* __restrict__ rowmap) {
-    const uint32_t p = blockIdx.y;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < kp; i += gridDim.x * blockDim.x)
-        rowmap[size_t(p) * N + pos[size_t(p) * kp + i]] = make_uint2(i, ainv[size_t(p) * kp + i]);
+                                         const uint32_t* __restrict__ ainv, uint2* __restrict__ rowmap, uint64_t total) {
+    for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < total; j += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t p = j / kp;
+        const uint32_t i = uint32_t(j - p * kp);
+        rowmap[p * N + pos[j]] = make_uint2(i, ainv[j]);
+    }
 }
+
+// ---- host side ----------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+// 2-D map over a packet-major uint16 buffer [rows][L], box [box_rows][wt].
+cudaError_t make_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t L, uint32_t wt, uint32_t box_rows) {
+    EncodeTiledFn fn = encode_tiled();
+    if (!fn) return cudaErrorNotSupported;
+    const cuuint64_t dims[2] = {L, rows};
+    const cuuint64_t strides[1] = {cuuint64_t(L) * 2};
+    const cuuint32_t box[2] = {wt, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+struct LaunchShape {
+    uint32_t tps, tiles, nbox, box_rows, grid;
+    size_t smem;
+};
 
 template <class K>
-cudaError_t prep(K kernel, size_t smem) {
-    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+cudaError_t shape_for(K kernel, int E, int wt, int nt, uint32_t k, uint32_t stripes, uint32_t L, LaunchShape& sh) {
+    sh.tps = L / wt;
+    const uint64_t tiles = uint64_t(stripes) * sh.tps;
+    if (tiles > 0xFFFFFFFFull) return cudaErrorInvalidConfiguration;
+    sh.tiles = uint32_t(tiles);
+    sh.box_rows = k < 256 ? k : 256;
+    sh.nbox = (k + sh.box_rows - 1) / sh.box_rows;
+    sh.smem = (size_t(1) << E) * wt * 4 + 2 * size_t(sh.nbox) * sh.box_rows * wt * 2;
+    cudaError_t err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sh.smem));
+    if (err) return err;
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if ((err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, nt, sh.smem))) return err;
+    if (per < 1) return cudaErrorInvalidConfiguration;
+    const uint64_t g = uint64_t(sms) * per;
+    sh.grid = uint32_t(g < tiles ? g : tiles);
+    return cudaSuccess;
 }
 
-// tile geometry per size: (NPAIR, NT)
 template <int E>
-struct Geom;
-template <> struct Geom<5> { static constexpr int NPAIR = 32, NT = 256; };
-template <> struct Geom<6> { static constexpr int NPAIR = 32, NT = 256; };
-template <> struct Geom<7> { static constexpr int NPAIR = 32, NT = 256; };
-template <> struct Geom<8> { static constexpr int NPAIR = 32, NT = 256; };
-template <> struct Geom<9> { static constexpr int NPAIR = 32, NT = 256; };
-template <> struct Geom<10> { static constexpr int NPAIR = 16, NT = 256; };
-template <> struct Geom<11> { static constexpr int NPAIR = 8, NT = 256; };
-template <> struct Geom<12> { static constexpr int NPAIR = 4, NT = 256; };
-
-template <int E>
-cudaError_t launch_enc(const FastTables& t, uint32_t k, uint32_t n, uint32_t stripes, uint32_t L,
-                       const uint16_t* src, EscIn ein, uint16_t* out, EscOut eout, cudaStream_t st) {
-    constexpr int NPAIR = Geom<E>::NPAIR, NT = Geom<E>::NT;
-    const uint32_t tps = L / (2 * NPAIR);
-    const uint64_t blocks = uint64_t(stripes) * tps;
-    if (blocks > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    const size_t smem = size_t(1u << E) * NPAIR * sizeof(uint2);
-    const uint2* tw = t.fwd + (1u << E);
-    cudaError_t err;
-    if (k == (1u << E) / 2) {
-        auto kern = enc_fast_kernel<E, NPAIR, NT, true>;
-        if ((err = prep(kern, smem))) return err;
-        kern<<<unsigned(blocks), NT, smem, st>>>(tw, k, n, L, tps, src, ein, out, eout);
-    } else {
-        auto kern = enc_fast_kernel<E, NPAIR, NT, false>;
-        if ((err = prep(kern, smem))) return err;
-        kern<<<unsigned(blocks), NT, smem, st>>>(tw, k, n, L, tps, src, ein, out, eout);
-    }
+cudaError_t launch_enc(const FastTables& t, uint32_t k, uint32_t n, uint32_t stripes, uint32_t L, const uint16_t* src,
+                       EscIn ein, uint16_t* out, EscOut eout, cudaStream_t st) {
+    using G = Geom<E>;
+    auto kern = (k == (1u << E) / 2) ? enc_fast_kernel<E, true> : enc_fast_kernel<E, false>;
+    LaunchShape sh;
+    cudaError_t err = shape_for(kern, E, G::WT, G::NT, k, stripes, L, sh);
+    if (err) return err;
+    if (!sh.tiles) return cudaSuccess;
+    CUtensorMap map;
+    if ((err = make_map(&map, src, uint64_t(stripes) * k, L, G::WT, sh.box_rows))) return err;
+    kern<<<sh.grid, G::NT, sh.smem, st>>>(map, t.ptab_fwd, k, n, L, sh.tps, sh.tiles, sh.nbox, sh.box_rows, ein, out, eout);
     return cudaGetLastError();
 }
 
 template <int E>
-cudaError_t launch_dec(const FastTables& t, const FastPlanView& pv, uint32_t stripes, uint32_t L,
-                       const uint32_t* sp, const uint16_t* rx, EscIn ein, uint16_t* out, EscOut eout, cudaStream_t st) {
-    constexpr int NPAIR = Geom<E>::NPAIR, NT = Geom<E>::NT;
-    const uint32_t tps = L / (2 * NPAIR);
-    const uint64_t blocks = uint64_t(stripes) * tps;
-    if (blocks > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    const size_t smem = size_t(1u << E) * NPAIR * sizeof(uint2);
-    auto kern = dec_fast_kernel<E, NPAIR, NT>;
-    cudaError_t err;
-    if ((err = prep(kern, smem))) return err;
-    kern<<<unsigned(blocks), NT, smem, st>>>(t.fwd + (1u << E), t.inv + (1u << E), pv.rowmap, pv.ahat2, pv.k, L, tps, sp,
-                                             rx, ein, out, eout);
+cudaError_t launch_dec(const FastTables& t, const FastPlanView& pv, uint32_t stripes, uint32_t L, const uint32_t* sp,
+                       const uint16_t* rx, EscIn ein, uint16_t* out, EscOut eout, cudaStream_t st) {
+    using G = Geom<E>;
+    auto kern = dec_fast_kernel<E>;
+    LaunchShape sh;
+    cudaError_t err = shape_for(kern, E, G::WT, G::NT, pv.k, stripes, L, sh);
+    if (err) return err;
+    if (!sh.tiles) return cudaSuccess;
+    CUtensorMap map;
+    if ((err = make_map(&map, rx, uint64_t(stripes) * pv.k, L, G::WT, sh.box_rows))) return err;
+    kern<<<sh.grid, G::NT, sh.smem, st>>>(map, t.ptab_fwd, t.ptab_inv, pv.rowmap, pv.ahat2, pv.k, L, sh.tps, sh.tiles,
+                                          sh.nbox, sh.box_rows, sp, ein, out, eout);
     return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t build_fast_tables(FastTables& t, cudaStream_t st) {
-    cudaError_t err = cudaMalloc(&t.fwd, sizeof(uint2) << 17);
+    cudaError_t err = cudaMalloc(&t.ptab_fwd, sizeof(uint2) << 13);
     if (err) return err;
-    if ((err = cudaMalloc(&t.inv, sizeof(uint2) << 17))) return err;
-    tables2_kernel<<<(1u << 17) / 256, 256, 0, st>>>(t.fwd, t.inv);
+    if ((err = cudaMalloc(&t.ptab_inv, sizeof(uint2) << 13))) return err;
+    ptab_kernel<<<(1u << 13) / 256, 256, 0, st>>>(t.ptab_fwd, t.ptab_inv);
     return cudaGetLastError();
 }
 
 int fast_tile_columns(uint32_t N) {
     switch (N) {
-        case 32: return 2 * Geom<5>::NPAIR;
-        case 64: return 2 * Geom<6>::NPAIR;
-        case 128: return 2 * Geom<7>::NPAIR;
-        case 256: return 2 * Geom<8>::NPAIR;
-        case 512: return 2 * Geom<9>::NPAIR;
-        case 1024: return 2 * Geom<10>::NPAIR;
-        case 2048: return 2 * Geom<11>::NPAIR;
-        case 4096: return 2 * Geom<12>::NPAIR;
+        case 32: return Geom<5>::WT;
+        case 64: return Geom<6>::WT;
+        case 128: return Geom<7>::WT;
+        case 256: return Geom<8>::WT;
+        case 512: return Geom<9>::WT;
+        case 1024: return Geom<10>::WT;
+        case 2048: return Geom<11>::WT;
+        case 4096: return Geom<12>::WT;
         default: return 0;
     }
 }
@@ -524,16 +604,9 @@ cudaError_t launch_fast_plan_tables(uint32_t N, uint32_t kp, uint32_t npatterns,
                                     const uint32_t* ainv, const uint32_t* ahat, uint2* rowmap, uint2* ahat2,
                                     cudaStream_t st) {
     if (!npatterns) return cudaSuccess;
-    for (uint32_t p0 = 0; p0 < npatterns; p0 += 65535u) {
-        const uint32_t np = npatterns - p0 < 65535u ? npatterns - p0 : 65535u;
-        dim3 g((N + 255) / 256, np);
-        fast_plan_tables_kernel<<<g, 256, 0, st>>>(N, kp, pos + size_t(p0) * kp, ainv + size_t(p0) * kp,
-                                                   ahat + size_t(p0) * N, rowmap + size_t(p0) * N,
-                                                   ahat2 + size_t(p0) * N);
-        dim3 g2((kp + 255) / 256, np);
-        fast_plan_scatter_kernel<<<g2, 256, 0, st>>>(N, kp, pos + size_t(p0) * kp, ainv + size_t(p0) * kp,
-                                                     rowmap + size_t(p0) * N);
-    }
+    const uint64_t total = uint64_t(npatterns) * N;
+    fast_plan_tables_kernel<<<148 * 8, 256, 0, st>>>(N, ahat, rowmap, ahat2, total);
+    fast_plan_scatter_kernel<<<148 * 8, 256, 0, st>>>(N, kp, pos, ainv, rowmap, uint64_t(npatterns) * kp);
     return cudaGetLastError();
 }
 

@@ -69,8 +69,8 @@ constexpr uint32_t kTileMaxN = 4096;
 // ---- v2 fast path (codec_fast.cu): 32 <= N <= 4096, L a multiple of the tile width
 namespace fast {
 struct FastTables {
-    uint2* fwd = nullptr;  // {r_m^j, 65535 r_m^j} at [m + j]
-    uint2* inv = nullptr;
+    uint2* ptab_fwd = nullptr;  // per-pass twiddles {w, 65535 w}: [2^LL + 16 t + s] = r_(2^LL)^(t s)
+    uint2* ptab_inv = nullptr;
 };
 struct FastPlanView {
     uint32_t N, k;
