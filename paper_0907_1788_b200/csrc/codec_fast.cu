@@ -68,11 +68,11 @@ __device__ __forceinline__ uint32_t cap(uint32_t v) {
 }
 
 // ---- geometry ---------------------------------------------------------------
-template <int E>
+template <int E, int WT_, int NT_>
 struct Geom {
     static constexpr int N = 1 << E;
-    static constexpr int WT = N <= 256 ? 64 : (N == 512 ? 32 : (N == 1024 ? 16 : 8));
-    static constexpr int NT = N == 4096 ? 512 : 256;
+    static constexpr int WT = WT_;
+    static constexpr int NT = NT_;
     static constexpr int RLZ = Sched<E>::rlog(Sched<E>::P - 1);
     static constexpr int RPW = WT >= 32 ? 1 : 32 / WT;  // tile rows touched by one warp
     // shared tile index with a row swizzle keeping the sub = 1 passes
@@ -84,15 +84,33 @@ struct Geom {
     }
 };
 
+// tile width / threads per size
+template <int E>
+struct Pick {
+    static constexpr int N = 1 << E;
+    static constexpr int WT = N <= 512 ? 32 : (N == 1024 ? 16 : 8);
+    static constexpr int NT = N == 4096 ? 512 : 256;
+    using G = Geom<E, WT, NT>;
+};
+
 // ---- generic pass (one codeword per work item) ----------------------------
 // DIF (DIT=false) or DIT pass with the geometry of DIF pass p of a size-2^E
 // transform. Loaded values must be below BIN; stored values are below OCAP.
 // twp: per-pass twiddle table, row t holds {r_len^(t s), 65535 r_len^(t s)}
 // for s < R (only read when sub > 1).
-template <int E, int p, bool INV, bool DIT, uint64_t BIN, uint64_t OCAP, class LD, class ST>
-__device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld, const ST& st) {
+struct NoFix {
+    template <int R>
+    __device__ __forceinline__ void operator()(uint32_t (&)[R], uint32_t, uint32_t, uint32_t) const {}
+};
+struct NoFlush {
+    __device__ __forceinline__ void operator()(uint32_t, uint32_t, uint32_t, uint32_t) const {}
+};
+
+template <int E, int p, bool INV, bool DIT, uint64_t BIN, uint64_t OCAP, class G, class LD, class ST,
+          class FIX = NoFix, class FLUSH = NoFlush>
+__device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld, const ST& st, const FIX& fix = FIX(),
+                                     const FLUSH& flush = FLUSH()) {
     using S = Sched<E>;
-    using G = Geom<E>;
     constexpr int RL = S::rlog(p), R = 1 << RL, LL = S::llog(p), SL = S::slog(p);
     constexpr int ITEMS = (1 << (E - RL)) * G::WT;
     constexpr int LGW = ilog2c<G::WT>();
@@ -114,9 +132,11 @@ __device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld
                 w[2 * i + 1] = make_uint2(x.z, x.w);
             }
         }
+        uint32_t mask = 0;
         if constexpr (!DIT) {
 #pragma unroll
             for (int q = 0; q < R; ++q) v[q] = ld(base + (uint32_t(q) << SL), b, q, col);
+            fix(v, base, b, col);
             dif_regs<R, INV, BIN>(v);
             constexpr uint64_t BO = dif_bound<R, INV, BIN>();
 #pragma unroll
@@ -126,7 +146,7 @@ __device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld
                     y = mulw2(y, w[s].x, w[s].y);
                 else
                     y = cap<BO, OCAP>(y);
-                st(base + (uint32_t(s) << SL), b, s, col, y);
+                mask |= st(base + (uint32_t(s) << SL), b, s, col, y) << s;
             }
         } else {
             constexpr uint64_t BI = BIN > k2P ? BIN : k2P;
@@ -139,8 +159,9 @@ __device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld
             dit_regs<R, INV, BI>(v);
             constexpr uint64_t BO = dit_bound<R, INV, BI>();
 #pragma unroll
-            for (int q = 0; q < R; ++q) st(base + (uint32_t(q) << SL), b, q, col, cap<BO, OCAP>(v[q]));
+            for (int q = 0; q < R; ++q) mask |= st(base + (uint32_t(q) << SL), b, q, col, cap<BO, OCAP>(v[q])) << q;
         }
+        flush(mask, base, b, col);
     }
 }
 
@@ -150,50 +171,34 @@ __device__ __forceinline__ const uint4* pass_table(const uint2* base, int LL) {
     return reinterpret_cast<const uint4*>(base + (1u << LL));
 }
 
-// ---- TMA staging of the k input packets of a tile ------------------------
-struct Stage {
-    uint16_t* buf[2];
-    uint64_t* bar;  // two mbarriers
-    uint32_t nbox, box_rows, bytes;
-};
-
-template <int WT>
-__device__ __forceinline__ void stage_issue(const Stage& sg, int b, const CUtensorMap* map, uint32_t c0, uint32_t row0) {
-    fence_proxy_async();
-    mbar_expect_tx(&sg.bar[b], sg.bytes);
-    for (uint32_t j = 0; j < sg.nbox; ++j)
-        tma_load_2d(sg.buf[b] + size_t(j) * sg.box_rows * WT, map, int(c0), int(row0 + j * sg.box_rows), &sg.bar[b]);
-}
-
-__device__ __forceinline__ uint32_t staged_value(const uint16_t* st, uint32_t idx, const EscIn& esc,
-                                                 unsigned long long key) {
-    const uint32_t x = st[idx];
-    if (x == 0u && esc.n && esc_has(esc, key)) return 65536u;
-    return x;
+// Escapes are rare (1 in 65537 symbols): loads and stores test a whole
+// butterfly group at once and only a group holding a zero word / a 65536
+// takes the slow path (one branch per group instead of one per symbol).
+template <int R>
+__device__ __forceinline__ bool any_zero(const uint32_t (&v)[R]) {
+    uint32_t m = v[0];
+#pragma unroll
+    for (int i = 1; i < R; ++i) m = min(m, v[i]);
+    return m == 0u;
 }
 
 // ---------------------------------------------------------------------------
-template <int E, bool HALFK>
-__global__ void __launch_bounds__(Geom<E>::NT) enc_fast_kernel(const __grid_constant__ CUtensorMap src_map,
-                                                               const uint2* __restrict__ ptabF, uint32_t k, uint32_t n,
-                                                               uint32_t L, uint32_t tps, uint32_t tiles, uint32_t nbox,
-                                                               uint32_t box_rows, EscIn esc_in,
-                                                               uint16_t* __restrict__ out, EscOut esc_out) {
+template <int E, class G, bool HALFK>
+__global__ void __launch_bounds__(G::NT) enc_fast_kernel(const __grid_constant__ CUtensorMap src_map,
+                                                         const uint2* __restrict__ ptabF, uint32_t k, uint32_t n,
+                                                         uint32_t L, uint32_t tps, uint32_t tiles, uint32_t nbox,
+                                                         uint32_t box_rows, EscIn esc_in, uint16_t* __restrict__ out,
+                                                         EscOut esc_out) {
     using S = Sched<E>;
-    using G = Geom<E>;
     constexpr int N = 1 << E, WT = G::WT, P = S::P;
-    constexpr int RL0 = S::rlog(0), RLZ = G::RLZ;
+    constexpr int RL0 = S::rlog(0), R0 = 1 << RL0, RLZ = G::RLZ;
     static_assert(P >= 2 && P <= 3, "");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t bars[2];
     uint32_t* work = reinterpret_cast<uint32_t*>(smem_raw);
-    Stage sg;
-    sg.nbox = nbox;
-    sg.box_rows = box_rows;
-    sg.bytes = nbox * box_rows * WT * 2;
-    sg.buf[0] = reinterpret_cast<uint16_t*>(smem_raw + size_t(N) * WT * 4);
-    sg.buf[1] = sg.buf[0] + size_t(nbox) * box_rows * WT;
-    sg.bar = bars;
+    uint16_t* stage0 = reinterpret_cast<uint16_t*>(smem_raw + size_t(N) * WT * 4);
+    const uint32_t stage_elems = nbox * box_rows * WT;
+    const uint32_t stage_bytes = stage_elems * 2;
     if (threadIdx.x == 0) {
         tma_prefetch_desc(&src_map);
         mbar_init(&bars[0], 1);
@@ -201,64 +206,83 @@ __global__ void __launch_bounds__(Geom<E>::NT) enc_fast_kernel(const __grid_cons
         fence_mbar_init();
     }
     __syncthreads();
+    auto issue = [&](uint32_t tl, int bs) {
+        const uint32_t s1 = tl / tps;
+        const uint32_t cc = (tl - s1 * tps) * WT;
+        fence_proxy_async();
+        mbar_expect_tx(&bars[bs], stage_bytes);
+        uint16_t* dst = stage0 + bs * stage_elems;
+        for (uint32_t j = 0; j < nbox; ++j)
+            tma_load_2d(dst + j * box_rows * WT, &src_map, int(cc), int(s1 * k + j * box_rows), &bars[bs]);
+    };
     uint32_t tile = blockIdx.x;
-    if (threadIdx.x == 0 && tile < tiles) {
-        const uint32_t s0 = tile / tps;
-        stage_issue<WT>(sg, 0, &src_map, (tile - s0 * tps) * WT, s0 * k);
-    }
+    if (threadIdx.x == 0 && tile < tiles) issue(tile, 0);
+    const bool esc_any = esc_in.n != 0;
     for (uint32_t iter = 0; tile < tiles; ++iter, tile += gridDim.x) {
         const int bsel = iter & 1;
         const uint32_t stripe = tile / tps;
         const uint32_t c0 = (tile - stripe * tps) * WT;
-        const uint32_t next = tile + gridDim.x;
-        if (threadIdx.x == 0 && next < tiles) {
-            const uint32_t s1 = next / tps;
-            stage_issue<WT>(sg, bsel ^ 1, &src_map, (next - s1 * tps) * WT, s1 * k);
-        }
+        if (threadIdx.x == 0 && tile + gridDim.x < tiles) issue(tile + gridDim.x, bsel ^ 1);
         mbar_wait(&bars[bsel], (iter >> 1) & 1);
-        const uint16_t* st_in = sg.buf[bsel];
+        const uint16_t* st_in = stage0 + bsel * stage_elems;
         const unsigned long long key_in = uint64_t(stripe) * k * L + c0;
         const unsigned long long key_out = uint64_t(stripe) * n * L + c0;
-        uint16_t* outp = out + uint64_t(stripe) * n * L + c0;
+        uint16_t* outp = out + key_out;
 
         auto ld_src = [&](uint32_t lrow, uint32_t, int q, uint32_t col) -> uint32_t {
-            if ((HALFK && q >= (1 << RL0) / 2) || (!HALFK && lrow >= k)) return 0u;
-            return staged_value(st_in, lrow * WT + col, esc_in, key_in + uint64_t(lrow) * L + col);
+            if ((HALFK && q >= R0 / 2) || (!HALFK && lrow >= k)) return 0u;
+            return st_in[lrow * WT + col];
+        };
+        auto fix_src = [&](uint32_t (&v)[R0], uint32_t base, uint32_t, uint32_t col) {
+            if (!esc_any) return;
+            if (!any_zero(v)) return;
+#pragma unroll 1
+            for (int q = 0; q < R0; ++q) {
+                const uint32_t lrow = base + (uint32_t(q) << S::slog(0));
+                if (v[q] == 0u && lrow < k && esc_has(esc_in, key_in + uint64_t(lrow) * L + col)) v[q] = 65536u;
+            }
         };
         auto ld_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t { return work[G::idx(lrow, col)]; };
-        auto st_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col, uint32_t y) { work[G::idx(lrow, col)] = y; };
-        auto st_out = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) {
+        auto st_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col, uint32_t y) -> uint32_t {
+            work[G::idx(lrow, col)] = y;
+            return 0u;
+        };
+        auto st_out = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) -> uint32_t {
             const uint32_t f = perm_head<E>(b) + (uint32_t(s) << (E - RLZ));
-            if (f >= n) return;
             y = red2p(y);
-            if (y == 65536u) emit_escape(esc_out, key_out + uint64_t(f) * L + col);
-            __stcs(outp + size_t(f) * L + col, uint16_t(y));
+            if (f < n) __stcs(outp + (f * L + col), uint16_t(y));
+            return (y == 65536u && f < n) ? 1u : 0u;
+        };
+        auto flush_out = [&](uint32_t mask, uint32_t, uint32_t b, uint32_t col) {
+            if (!mask) return;
+#pragma unroll 1
+            for (int s = 0; s < 16; ++s)
+                if (mask & (1u << s))
+                    emit_escape(esc_out, key_out + uint64_t(perm_head<E>(b) + (uint32_t(s) << (E - RLZ))) * L + col);
         };
 
-        pass<E, 0, false, false, kP64, kSmemCap>(pass_table(ptabF, S::llog(0)), ld_src, st_sm);
+        pass<E, 0, false, false, kP64, kSmemCap, G>(pass_table(ptabF, S::llog(0)), ld_src, st_sm, fix_src);
         __syncthreads();
         if constexpr (P == 3) {
-            pass<E, 1, false, false, kSmemCap, kSmemCap>(pass_table(ptabF, S::llog(1)), ld_sm, st_sm);
+            pass<E, 1, false, false, kSmemCap, kSmemCap, G>(pass_table(ptabF, S::llog(1)), ld_sm, st_sm);
             __syncthreads();
         }
-        pass<E, P - 1, false, false, kSmemCap, k2P>(pass_table(ptabF, S::llog(P - 1)), ld_sm, st_out);
+        pass<E, P - 1, false, false, kSmemCap, k2P, G>(pass_table(ptabF, S::llog(P - 1)), ld_sm, st_out, NoFix(),
+                                                       flush_out);
         __syncthreads();
     }
 }
 
 // ---------------------------------------------------------------------------
-template <int E>
-__global__ void __launch_bounds__(Geom<E>::NT) dec_fast_kernel(const __grid_constant__ CUtensorMap rx_map,
-                                                               const uint2* __restrict__ ptabF,
-                                                               const uint2* __restrict__ ptabI,
-                                                               const uint2* __restrict__ rowmap,
-                                                               const uint2* __restrict__ ahat2, uint32_t k, uint32_t L,
-                                                               uint32_t tps, uint32_t tiles, uint32_t nbox,
-                                                               uint32_t box_rows,
-                                                               const uint32_t* __restrict__ stripe_pattern,
-                                                               EscIn esc_in, uint16_t* __restrict__ out, EscOut esc_out) {
+template <int E, class G>
+__global__ void __launch_bounds__(G::NT) dec_fast_kernel(const __grid_constant__ CUtensorMap rx_map,
+                                                         const uint2* __restrict__ ptabF, const uint2* __restrict__ ptabI,
+                                                         const uint2* __restrict__ rowmap,
+                                                         const uint2* __restrict__ ahat2, uint32_t k, uint32_t L,
+                                                         uint32_t tps, uint32_t tiles, uint32_t nbox, uint32_t box_rows,
+                                                         const uint32_t* __restrict__ stripe_pattern, EscIn esc_in,
+                                                         uint16_t* __restrict__ out, EscOut esc_out) {
     using S = Sched<E>;
-    using G = Geom<E>;
     constexpr int N = 1 << E, WT = G::WT, NT = G::NT, P = S::P;
     constexpr int RLZ = G::RLZ, RZ = 1 << RLZ;
     constexpr int RL0 = S::rlog(0), R0 = 1 << RL0, SL0 = S::slog(0);
@@ -268,13 +292,9 @@ __global__ void __launch_bounds__(Geom<E>::NT) dec_fast_kernel(const __grid_cons
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t bars[2];
     uint32_t* work = reinterpret_cast<uint32_t*>(smem_raw);
-    Stage sg;
-    sg.nbox = nbox;
-    sg.box_rows = box_rows;
-    sg.bytes = nbox * box_rows * WT * 2;
-    sg.buf[0] = reinterpret_cast<uint16_t*>(smem_raw + size_t(N) * WT * 4);
-    sg.buf[1] = sg.buf[0] + size_t(nbox) * box_rows * WT;
-    sg.bar = bars;
+    uint16_t* stage0 = reinterpret_cast<uint16_t*>(smem_raw + size_t(N) * WT * 4);
+    const uint32_t stage_elems = nbox * box_rows * WT;
+    const uint32_t stage_bytes = stage_elems * 2;
     if (threadIdx.x == 0) {
         tma_prefetch_desc(&rx_map);
         mbar_init(&bars[0], 1);
@@ -282,60 +302,88 @@ __global__ void __launch_bounds__(Geom<E>::NT) dec_fast_kernel(const __grid_cons
         fence_mbar_init();
     }
     __syncthreads();
+    auto issue = [&](uint32_t tl, int bs) {
+        const uint32_t s1 = tl / tps;
+        const uint32_t cc = (tl - s1 * tps) * WT;
+        fence_proxy_async();
+        mbar_expect_tx(&bars[bs], stage_bytes);
+        uint16_t* dst = stage0 + bs * stage_elems;
+        for (uint32_t j = 0; j < nbox; ++j)
+            tma_load_2d(dst + j * box_rows * WT, &rx_map, int(cc), int(s1 * k + j * box_rows), &bars[bs]);
+    };
     uint32_t tile = blockIdx.x;
-    if (threadIdx.x == 0 && tile < tiles) {
-        const uint32_t s0 = tile / tps;
-        stage_issue<WT>(sg, 0, &rx_map, (tile - s0 * tps) * WT, s0 * k);
-    }
+    if (threadIdx.x == 0 && tile < tiles) issue(tile, 0);
     const uint4* tF0 = pass_table(ptabF, S::llog(0));
     const uint4* tI0 = pass_table(ptabI, S::llog(0));
+    const bool esc_any = esc_in.n != 0;
     for (uint32_t iter = 0; tile < tiles; ++iter, tile += gridDim.x) {
         const int bsel = iter & 1;
         const uint32_t stripe = tile / tps;
         const uint32_t c0 = (tile - stripe * tps) * WT;
-        const uint32_t next = tile + gridDim.x;
-        if (threadIdx.x == 0 && next < tiles) {
-            const uint32_t s1 = next / tps;
-            stage_issue<WT>(sg, bsel ^ 1, &rx_map, (next - s1 * tps) * WT, s1 * k);
-        }
+        if (threadIdx.x == 0 && tile + gridDim.x < tiles) issue(tile + gridDim.x, bsel ^ 1);
         const uint32_t pat = __ldg(stripe_pattern + stripe);
         const uint2* __restrict__ rm = rowmap + size_t(pat) * N;
         const uint2* __restrict__ ah = ahat2 + size_t(pat) * N;
         const unsigned long long key = uint64_t(stripe) * k * L + c0;
-        uint16_t* outp = out + uint64_t(stripe) * k * L + c0;
+        uint16_t* outp = out + key;
         mbar_wait(&bars[bsel], (iter >> 1) & 1);
-        const uint16_t* st_in = sg.buf[bsel];
+        const uint16_t* st_in = stage0 + bsel * stage_elems;
 
-        // step 4: N'[z] = v_i / A'(x_i) where z = z_i, else 0
+        // step 4: N'[z] = v_i / A'(x_i) where z = z_i, else 0. A received
+        // zero word may be an escaped 65536: the group fix-up re-scales it.
         auto ld_scatter = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t {
             const uint2 m = __ldg(rm + lrow);
             if (m.x == 0xFFFFFFFFu) return 0u;
-            const uint32_t v = staged_value(st_in, m.x * WT + col, esc_in, key + uint64_t(m.x) * L + col);
-            return mulw2(v, m.y, m.y * 65535u);
+            const uint32_t v = st_in[m.x * WT + col];
+            return v ? mulw2(v, m.y, m.y * 65535u) : 0u;
+        };
+        auto fix_scatter = [&](uint32_t (&v)[R0], uint32_t base, uint32_t, uint32_t col) {
+            if (!esc_any) return;
+            if (!any_zero(v)) return;
+#pragma unroll 1
+            for (int q = 0; q < R0; ++q) {
+                if (v[q] != 0u) continue;
+                const uint2 m = __ldg(rm + base + (uint32_t(q) << SL0));
+                if (m.x != 0xFFFFFFFFu && st_in[m.x * WT + col] == 0u &&
+                    esc_has(esc_in, key + uint64_t(m.x) * L + col))
+                    v[q] = mulw2(65536u, m.y, m.y * 65535u);
+            }
         };
         auto ld_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t { return work[G::idx(lrow, col)]; };
-        auto st_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col, uint32_t y) { work[G::idx(lrow, col)] = y; };
+        auto st_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col, uint32_t y) -> uint32_t {
+            work[G::idx(lrow, col)] = y;
+            return 0u;
+        };
         auto ld_smf = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t {
             return work[G::idx(lrow ^ FLIP, col)];
         };
-        auto st_smf = [&](uint32_t lrow, uint32_t, int, uint32_t col, uint32_t y) { work[G::idx(lrow ^ FLIP, col)] = y; };
-        auto st_out = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) {
+        auto st_smf = [&](uint32_t lrow, uint32_t, int, uint32_t col, uint32_t y) -> uint32_t {
+            work[G::idx(lrow ^ FLIP, col)] = y;
+            return 0u;
+        };
+        auto st_out = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) -> uint32_t {
             const uint32_t f = perm_head<E>(b) + (uint32_t(s) << (E - RLZ));
-            if (f >= k) return;
             y = red2p(y);
-            if (y == 65536u) emit_escape(esc_out, key + uint64_t(f) * L + col);
-            __stcs(outp + size_t(f) * L + col, uint16_t(y));
+            if (f < k) __stcs(outp + (f * L + col), uint16_t(y));
+            return (y == 65536u && f < k) ? 1u : 0u;
+        };
+        auto flush_out = [&](uint32_t mask, uint32_t, uint32_t b, uint32_t col) {
+            if (!mask) return;
+#pragma unroll 1
+            for (int s = 0; s < 16; ++s)
+                if (mask & (1u << s))
+                    emit_escape(esc_out, key + uint64_t(perm_head<E>(b) + (uint32_t(s) << (E - RLZ))) * L + col);
         };
 
         // FNT1 = FNT_N(N'), DIF, natural -> perm order (flip 0)
-        pass<E, 0, false, false, k2P, kSmemCap>(tF0, ld_scatter, st_sm);
+        pass<E, 0, false, false, k2P, kSmemCap, G>(tF0, ld_scatter, st_sm, fix_scatter);
         __syncthreads();
         if constexpr (P == 3) {
-            pass<E, 1, false, false, kSmemCap, kSmemCap>(pass_table(ptabF, S::llog(1)), ld_sm, st_sm);
+            pass<E, 1, false, false, kSmemCap, kSmemCap, G>(pass_table(ptabF, S::llog(1)), ld_sm, st_sm);
             __syncthreads();
         }
         // FNT1 last pass (sub 1) + FNT2 first DIT pass on the reversed view:
-        // logical group b' = N/R - 1 - G holds s'_j = F[N-1-j]; j >= k zeroed.
+        // logical group b' = N/R - 1 - g holds s'_j = F[N-1-j]; j >= k zeroed.
         {
             constexpr int ITEMS = (N / RZ) * WT;
             constexpr uint64_t BD = dif_bound<RZ, false, kSmemCap>();
@@ -362,7 +410,7 @@ __global__ void __launch_bounds__(Geom<E>::NT) dec_fast_kernel(const __grid_cons
         }
         __syncthreads();
         if constexpr (P == 3) {
-            pass<E, 1, false, true, kSmemCap, kSmemCap>(pass_table(ptabF, S::llog(1)), ld_smf, st_smf);
+            pass<E, 1, false, true, kSmemCap, kSmemCap, G>(pass_table(ptabF, S::llog(1)), ld_smf, st_smf);
             __syncthreads();
         }
         // FNT2 last DIT pass + (. ahat) + FNT3 first DIF pass: rows t + q * sub0
@@ -419,10 +467,11 @@ __global__ void __launch_bounds__(Geom<E>::NT) dec_fast_kernel(const __grid_cons
         }
         __syncthreads();
         if constexpr (P == 3) {
-            pass<E, 1, true, false, kSmemCap, kSmemCap>(pass_table(ptabI, S::llog(1)), ld_smf, st_smf);
+            pass<E, 1, true, false, kSmemCap, kSmemCap, G>(pass_table(ptabI, S::llog(1)), ld_smf, st_smf);
             __syncthreads();
         }
-        pass<E, P - 1, true, false, kSmemCap, k2P>(pass_table(ptabI, S::llog(P - 1)), ld_smf, st_out);
+        pass<E, P - 1, true, false, kSmemCap, k2P, G>(pass_table(ptabI, S::llog(P - 1)), ld_smf, st_out, NoFix(),
+                                                      flush_out);
         __syncthreads();
     }
 }
@@ -517,8 +566,8 @@ cudaError_t shape_for(K kernel, int E, int wt, int nt, uint32_t k, uint32_t stri
 template <int E>
 cudaError_t launch_enc(const FastTables& t, uint32_t k, uint32_t n, uint32_t stripes, uint32_t L, const uint16_t* src,
                        EscIn ein, uint16_t* out, EscOut eout, cudaStream_t st) {
-    using G = Geom<E>;
-    auto kern = (k == (1u << E) / 2) ? enc_fast_kernel<E, true> : enc_fast_kernel<E, false>;
+    using G = typename Pick<E>::G;
+    auto kern = (k == (1u << E) / 2) ? enc_fast_kernel<E, G, true> : enc_fast_kernel<E, G, false>;
     LaunchShape sh;
     cudaError_t err = shape_for(kern, E, G::WT, G::NT, k, stripes, L, sh);
     if (err) return err;
@@ -532,8 +581,8 @@ cudaError_t launch_enc(const FastTables& t, uint32_t k, uint32_t n, uint32_t str
 template <int E>
 cudaError_t launch_dec(const FastTables& t, const FastPlanView& pv, uint32_t stripes, uint32_t L, const uint32_t* sp,
                        const uint16_t* rx, EscIn ein, uint16_t* out, EscOut eout, cudaStream_t st) {
-    using G = Geom<E>;
-    auto kern = dec_fast_kernel<E>;
+    using G = typename Pick<E>::G;
+    auto kern = dec_fast_kernel<E, G>;
     LaunchShape sh;
     cudaError_t err = shape_for(kern, E, G::WT, G::NT, pv.k, stripes, L, sh);
     if (err) return err;
@@ -557,14 +606,14 @@ cudaError_t build_fast_tables(FastTables& t, cudaStream_t st) {
 
 int fast_tile_columns(uint32_t N) {
     switch (N) {
-        case 32: return Geom<5>::WT;
-        case 64: return Geom<6>::WT;
-        case 128: return Geom<7>::WT;
-        case 256: return Geom<8>::WT;
-        case 512: return Geom<9>::WT;
-        case 1024: return Geom<10>::WT;
-        case 2048: return Geom<11>::WT;
-        case 4096: return Geom<12>::WT;
+        case 32: return Pick<5>::WT;
+        case 64: return Pick<6>::WT;
+        case 128: return Pick<7>::WT;
+        case 256: return Pick<8>::WT;
+        case 512: return Pick<9>::WT;
+        case 1024: return Pick<10>::WT;
+        case 2048: return Pick<11>::WT;
+        case 4096: return Pick<12>::WT;
         default: return 0;
     }
 }
