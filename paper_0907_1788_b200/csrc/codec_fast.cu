@@ -35,21 +35,34 @@ namespace {
 constexpr uint64_t kSmemCap = 1ull << 20;  // bound of values kept in shared memory
 constexpr uint64_t k2P = 2 * kP64;
 
-__device__ __noinline__ bool esc_has(const EscIn& e, unsigned long long key) {
-    uint64_t lo = 0, hi = e.n;
+__device__ __noinline__ bool esc_find(const unsigned long long* keys, uint64_t n, unsigned long long key) {
+    uint64_t lo = 0, hi = n;
     while (lo < hi) {
         const uint64_t mid = (lo + hi) >> 1;
-        if (e.keys[mid] < key)
+        if (keys[mid] < key)
             lo = mid + 1;
         else
             hi = mid;
     }
-    return lo < e.n && e.keys[lo] == key;
+    return lo < n && keys[lo] == key;
+}
+__device__ __forceinline__ bool esc_has(const EscIn& e, unsigned long long key) { return esc_find(e.keys, e.n, key); }
+
+__device__ __noinline__ void esc_append(unsigned long long* keys, unsigned long long* count, uint64_t cap,
+                                        unsigned long long key) {
+    const unsigned long long i = atomicAdd(count, 1ull);
+    if (i < cap) keys[i] = key;
+}
+__device__ __forceinline__ void emit_escape(const EscOut& e, unsigned long long key) {
+    esc_append(e.keys, e.count, e.cap, key);
 }
 
-__device__ __noinline__ void emit_escape(const EscOut& e, unsigned long long key) {
-    const unsigned long long i = atomicAdd(e.count, 1ull);
-    if (i < e.cap) e.keys[i] = key;
+// opaque copy: keeps the per-tile base pointer in a register so per-symbol
+// addresses are one 32-bit offset away (no 64-bit re-association)
+template <class T>
+__device__ __forceinline__ T* launder(T* p) {
+    asm("mov.b64 %0, %0;" : "+l"(p));
+    return p;
 }
 
 template <int N>
@@ -183,7 +196,7 @@ __device__ __forceinline__ bool any_zero(const uint32_t (&v)[R]) {
 }
 
 // ---------------------------------------------------------------------------
-template <int E, class G, bool HALFK>
+template <int E, class G, bool HALFK, bool PUNCT>
 __global__ void __launch_bounds__(G::NT) enc_fast_kernel(const __grid_constant__ CUtensorMap src_map,
                                                          const uint2* __restrict__ ptabF, uint32_t k, uint32_t n,
                                                          uint32_t L, uint32_t tps, uint32_t tiles, uint32_t nbox,
@@ -227,7 +240,7 @@ __global__ void __launch_bounds__(G::NT) enc_fast_kernel(const __grid_constant__
         const uint16_t* st_in = stage0 + bsel * stage_elems;
         const unsigned long long key_in = uint64_t(stripe) * k * L + c0;
         const unsigned long long key_out = uint64_t(stripe) * n * L + c0;
-        uint16_t* outp = out + key_out;
+        uint16_t* outp = launder(out + key_out);
 
         auto ld_src = [&](uint32_t lrow, uint32_t, int q, uint32_t col) -> uint32_t {
             if ((HALFK && q >= R0 / 2) || (!HALFK && lrow >= k)) return 0u;
@@ -236,7 +249,7 @@ __global__ void __launch_bounds__(G::NT) enc_fast_kernel(const __grid_constant__
         auto fix_src = [&](uint32_t (&v)[R0], uint32_t base, uint32_t, uint32_t col) {
             if (!esc_any) return;
             if (!any_zero(v)) return;
-#pragma unroll 1
+#pragma unroll
             for (int q = 0; q < R0; ++q) {
                 const uint32_t lrow = base + (uint32_t(q) << S::slog(0));
                 if (v[q] == 0u && lrow < k && esc_has(esc_in, key_in + uint64_t(lrow) * L + col)) v[q] = 65536u;
@@ -250,8 +263,8 @@ __global__ void __launch_bounds__(G::NT) enc_fast_kernel(const __grid_constant__
         auto st_out = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) -> uint32_t {
             const uint32_t f = perm_head<E>(b) + (uint32_t(s) << (E - RLZ));
             y = red2p(y);
-            if (f < n) __stcs(outp + (f * L + col), uint16_t(y));
-            return (y == 65536u && f < n) ? 1u : 0u;
+            if (!PUNCT || f < n) __stcs(outp + (f * L + col), uint16_t(y));
+            return (y == 65536u && (!PUNCT || f < n)) ? 1u : 0u;
         };
         auto flush_out = [&](uint32_t mask, uint32_t, uint32_t b, uint32_t col) {
             if (!mask) return;
@@ -274,7 +287,7 @@ __global__ void __launch_bounds__(G::NT) enc_fast_kernel(const __grid_constant__
 }
 
 // ---------------------------------------------------------------------------
-template <int E, class G>
+template <int E, class G, bool HALFK>
 __global__ void __launch_bounds__(G::NT) dec_fast_kernel(const __grid_constant__ CUtensorMap rx_map,
                                                          const uint2* __restrict__ ptabF, const uint2* __restrict__ ptabI,
                                                          const uint2* __restrict__ rowmap,
@@ -325,7 +338,7 @@ __global__ void __launch_bounds__(G::NT) dec_fast_kernel(const __grid_constant__
         const uint2* __restrict__ rm = rowmap + size_t(pat) * N;
         const uint2* __restrict__ ah = ahat2 + size_t(pat) * N;
         const unsigned long long key = uint64_t(stripe) * k * L + c0;
-        uint16_t* outp = out + key;
+        uint16_t* outp = launder(out + key);
         mbar_wait(&bars[bsel], (iter >> 1) & 1);
         const uint16_t* st_in = stage0 + bsel * stage_elems;
 
@@ -340,7 +353,7 @@ __global__ void __launch_bounds__(G::NT) dec_fast_kernel(const __grid_constant__
         auto fix_scatter = [&](uint32_t (&v)[R0], uint32_t base, uint32_t, uint32_t col) {
             if (!esc_any) return;
             if (!any_zero(v)) return;
-#pragma unroll 1
+#pragma unroll
             for (int q = 0; q < R0; ++q) {
                 if (v[q] != 0u) continue;
                 const uint2 m = __ldg(rm + base + (uint32_t(q) << SL0));
@@ -363,9 +376,11 @@ __global__ void __launch_bounds__(G::NT) dec_fast_kernel(const __grid_constant__
         };
         auto st_out = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) -> uint32_t {
             const uint32_t f = perm_head<E>(b) + (uint32_t(s) << (E - RLZ));
+            // k = N/2: kept iff s < R/2 (compile time after unrolling)
+            const bool keep = HALFK ? (s < RZ / 2) : (f < k);
             y = red2p(y);
-            if (f < k) __stcs(outp + (f * L + col), uint16_t(y));
-            return (y == 65536u && f < k) ? 1u : 0u;
+            if (keep) __stcs(outp + (f * L + col), uint16_t(y));
+            return (y == 65536u && keep) ? 1u : 0u;
         };
         auto flush_out = [&](uint32_t mask, uint32_t, uint32_t b, uint32_t col) {
             if (!mask) return;
@@ -400,7 +415,8 @@ __global__ void __launch_bounds__(G::NT) dec_fast_kernel(const __grid_constant__
                 uint32_t u[RZ];
 #pragma unroll
                 for (int j = 0; j < RZ; ++j) {  // u[rev(s')] = x_{s'} = y_{R-1-s'} = v[R-1-j]
-                    const bool live = fh + (uint32_t(rev<RZ>(j)) << (E - RLZ)) < k;
+                    // k = N/2: live iff rev(j) < R/2, i.e. j even (compile time)
+                    const bool live = HALFK ? ((j & 1) == 0) : (fh + (uint32_t(rev<RZ>(j)) << (E - RLZ)) < k);
                     u[j] = live ? v[RZ - 1 - j] : 0u;
                 }
                 dit_regs<RZ, false, BD>(u);
@@ -567,7 +583,9 @@ template <int E>
 cudaError_t launch_enc(const FastTables& t, uint32_t k, uint32_t n, uint32_t stripes, uint32_t L, const uint16_t* src,
                        EscIn ein, uint16_t* out, EscOut eout, cudaStream_t st) {
     using G = typename Pick<E>::G;
-    auto kern = (k == (1u << E) / 2) ? enc_fast_kernel<E, G, true> : enc_fast_kernel<E, G, false>;
+    const bool half = k == (1u << E) / 2, punct = n < (1u << E);
+    auto kern = half ? (punct ? enc_fast_kernel<E, G, true, true> : enc_fast_kernel<E, G, true, false>)
+                     : (punct ? enc_fast_kernel<E, G, false, true> : enc_fast_kernel<E, G, false, false>);
     LaunchShape sh;
     cudaError_t err = shape_for(kern, E, G::WT, G::NT, k, stripes, L, sh);
     if (err) return err;
@@ -582,7 +600,7 @@ template <int E>
 cudaError_t launch_dec(const FastTables& t, const FastPlanView& pv, uint32_t stripes, uint32_t L, const uint32_t* sp,
                        const uint16_t* rx, EscIn ein, uint16_t* out, EscOut eout, cudaStream_t st) {
     using G = typename Pick<E>::G;
-    auto kern = dec_fast_kernel<E, G>;
+    auto kern = pv.k == (1u << E) / 2 ? dec_fast_kernel<E, G, true> : dec_fast_kernel<E, G, false>;
     LaunchShape sh;
     cudaError_t err = shape_for(kern, E, G::WT, G::NT, pv.k, stripes, L, sh);
     if (err) return err;
