@@ -1,0 +1,495 @@
+#!/usr/bin/env python3
+"""Benchmark: batched non-systematic FNT Reed-Solomon codec over GF(65537).
+
+Metric (BASELINE.json): encode & decode GB/s of source data per GPU, with the
+HBM-roofline fraction. One STEP is one pass of the hot path over the whole
+workload resident in HBM: build the decode plans of every erasure pattern,
+encode every stripe, decode every stripe from its received packets.
+value = source bytes of the workload (all ranks) / step time.
+
+Default workload: configs[1] of BASELINE.json ("C2": n=256, k=128, 65536
+stripes of 128 x 4 KiB source packets = 32 GiB of source per GPU), which is
+the configuration the metric is quoted on and fits one B200. Multi-GPU runs
+(torchrun, one rank per GPU) are weak scaling: every rank codes its own
+stripes of the same shape (seeded per rank); no collective on the data path,
+NCCL is used only for the barrier and the max-over-ranks of the step time.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2]
+  python bench.py --impl reference ...   # the reference's own CPU codec
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_0907_1788_b200 import workload as W  # noqa: E402
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback, only if MEASURED_PEAKS.json is absent
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_FILE) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------- clocks ----
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, nm in enumerate(names):
+                if len(r) > 3 + i and r[3 + i].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ------------------------------------------------------ CPU reference ----
+def reference_lib():
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_bind import RefLib  # checker / baseline only
+    if not RefLib.available():
+        return None
+    return RefLib()
+
+
+def cpu_reference_sample(cfg, seed, stripes, threads):
+    """Time the reference library (oracle/_ref, the unmodified reference codec)
+    on `stripes` stripes of the config, the way the reference CLI runs it
+    (per-codeword encode/decode_nonsystematic, Path::Auto, threads over
+    codewords). Returns (enc_s, dec_s, source_bytes)."""
+    ref = reference_lib()
+    if ref is None:
+        raise RuntimeError("reference library oracle/_ref not built")
+    from oracle_bind import gather_received
+    src = W.symbols(seed, 0, stripes * cfg.k * cfg.L).reshape(stripes, cfg.k, cfg.L)
+    pats, sp = W.patterns(cfg, seed=seed, stripes=stripes)
+    t0 = time.perf_counter()
+    enc, esc = ref.encode_stripes(cfg.k, cfg.n, src, threads=threads)
+    t1 = time.perf_counter()
+    rx, rxe = gather_received(enc, esc, pats, sp)
+    t2 = time.perf_counter()
+    dec, _ = ref.decode_stripes(cfg.k, cfg.n, pats, sp, rx, rxe, path=0, threads=threads)
+    t3 = time.perf_counter()
+    if not np.array_equal(dec, src):
+        raise RuntimeError("reference decode mismatch")
+    return t1 - t0, t3 - t2, src.nbytes
+
+
+def pick_cpu_sample(cfg, threads, budget_s):
+    """Stripes (and codewords) so the reference run takes ~budget_s."""
+    # calibrate on one stripe
+    e, d, b = cpu_reference_sample(cfg, W.SEED, 1, threads)
+    per = max(e + d, 1e-4)
+    return max(1, min(cfg.stripes, int(budget_s / per))), per
+
+
+# ------------------------------------------------------------ GPU arm ----
+def run_gpu(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_0907_1788_b200 import Codec, _lib, default_escape_capacity
+
+    dev = torch.device(f"cuda:{local_rank}")
+    torch.cuda.set_device(dev)
+    cfg = W.CONFIGS[args.config]
+    S = args.stripes or cfg.stripes
+    if args.scaling == "strong":
+        per = (S + world - 1) // world
+        lo, hi = rank * per, min(S, (rank + 1) * per)
+        S_rank = max(0, hi - lo)
+    else:
+        S_rank = S
+    seed = W.SEED + 1000003 * rank
+    k, n, L = cfg.k, cfg.n, cfg.L
+    lib = _lib.load()
+    codec = Codec(local_rank)
+    stream = torch.cuda.current_stream(dev)
+    chunk = max(1, min(S_rank, args.chunk))
+    nchunks = (S_rank + chunk - 1) // chunk
+
+    # ---- workload resident in HBM (untimed setup)
+    src = torch.empty((S_rank, k, L), dtype=torch.int16, device=dev)
+    st = lib.fntrs_gpu_fill_symbols(seed, 0, src.numel(), C.c_void_p(src.data_ptr()), C.c_void_p(stream.cuda_stream))
+    assert st == 0
+    enc = torch.empty((S_rank, n, L), dtype=torch.int16, device=dev)
+    esc_cap = default_escape_capacity(chunk * n * L)
+    enc_esc = [torch.empty(esc_cap, dtype=torch.int64, device=dev) for _ in range(nchunks)]
+    enc_cnt = torch.zeros(nchunks, dtype=torch.int64, device=dev)
+    dec_cap = default_escape_capacity(chunk * k * L)
+    dec_esc = torch.empty(dec_cap, dtype=torch.int64, device=dev)
+    dec_cnt = torch.zeros(nchunks, dtype=torch.int64, device=dev)
+    dec = torch.empty((chunk, k, L), dtype=torch.int16, device=dev)
+
+    def encode_chunk(c):
+        a, b = c * chunk, min(S_rank, (c + 1) * chunk)
+        codec.encode(k, n, src[a:b], out=enc[a:b], esc_out=enc_esc[c], esc_cap=esc_cap, count=enc_cnt[c:c + 1])
+
+    for c in range(nchunks):
+        encode_chunk(c)
+    pats, sp = W.patterns(cfg, seed=seed, stripes=S_rank)
+    rx = torch.empty((S_rank, k, L), dtype=torch.int16, device=dev)
+    rx_esc = []
+    for c in range(nchunks):
+        a, b = c * chunk, min(S_rank, (c + 1) * chunk)
+        sub_sp = sp[a:b]
+        r, e = W.received_packets(enc[a:b], enc_esc[c], enc_cnt[c:c + 1], pats, sub_sp, n)
+        rx[a:b].copy_(r)
+        del r
+        rx_esc.append(e)
+    sp_dev = torch.from_numpy(sp.astype(np.int32)).to(dev)
+    pats_pinned = torch.from_numpy(pats.astype(np.int32)).pin_memory()
+    torch.cuda.synchronize(dev)
+
+    plans_box = {}
+
+    def build_plans():
+        if "p" in plans_box:
+            plans_box["p"].close()
+        plans_box["p"] = codec.plans(k, n, pats_pinned)
+
+    dec_events = []
+
+    def decode_chunk(c, timed=False):
+        a, b = c * chunk, min(S_rank, (c + 1) * chunk)
+        if timed:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        codec.decode(plans_box["p"], sp_dev[a:b], rx[a:b], rx_esc[c], out=dec[: b - a], esc_out=dec_esc,
+                     esc_cap=dec_cap, count=dec_cnt[c:c + 1])
+        if timed:
+            e1.record(stream)
+            dec_events.append((e0, e1))
+
+    enc_events = []
+
+    def step(timed=False, verify=False):
+        ok = True
+        t = {}
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record(stream)
+        build_plans()
+        ev[1].record(stream)
+        for c in range(nchunks):
+            if timed:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            encode_chunk(c)
+            if timed:
+                e1.record(stream)
+                enc_events.append((e0, e1))
+        ev[2].record(stream)
+        for c in range(nchunks):
+            decode_chunk(c, timed)
+            if verify:
+                a, b = c * chunk, min(S_rank, (c + 1) * chunk)
+                ok &= bool(torch.equal(dec[: b - a], src[a:b]))
+        ev[3].record(stream)
+        return ok, ev
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # warm-up (the first also verifies decode(encode(s)) == s on every stripe)
+    ok_all = True
+    for w in range(args.warmup):
+        ok, _ = step(verify=(w == 0))
+        ok_all &= ok
+    torch.cuda.synchronize(dev)
+    if not ok_all:
+        raise RuntimeError("decode(encode(s)) != s during warm-up")
+
+    launches0 = codec.launches
+    phase_ms = np.zeros(3)
+    barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local_rank) as clocks:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        evs = []
+        for _ in range(args.steps):
+            _, ev = step(timed=True)
+            evs.append(ev)
+        t_end.record(stream)
+        torch.cuda.synchronize(dev)
+    barrier()
+    gpu_launches = codec.launches - launches0
+    total_ms = t_start.elapsed_time(t_end)
+    for ev in evs:
+        phase_ms += [ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])]
+    phase_ms /= args.steps
+    dec_launch_ms = float(np.mean([a.elapsed_time(b) for a, b in dec_events]))
+    enc_launch_ms = float(np.mean([a.elapsed_time(b) for a, b in enc_events]))
+    if world > 1:
+        tt = torch.tensor([total_ms, *phase_ms, dec_launch_ms, enc_launch_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms, phase_ms, dec_launch_ms, enc_launch_ms = float(tt[0]), tt[1:4].cpu().numpy(), float(tt[4]), float(tt[5])
+
+    ms_per_step = total_ms / args.steps
+    src_bytes_rank = 2 * k * L * S_rank
+    src_bytes_all = src_bytes_rank * (world if args.scaling == "weak" else 1)
+    if args.scaling == "strong":
+        src_bytes_all = 2 * k * L * S
+    value = src_bytes_all / (ms_per_step * 1e-3) / 1e9
+
+    # roofline of the dominant kernel (decode), per launch = one chunk
+    peak, peak_src = hbm_peak()
+    rows = chunk
+    dec_bytes = 2 * (2 * k * L * rows)          # read 2k + write 2k per codeword
+    enc_bytes = 2 * k * L * rows + 2 * n * L * rows  # read 2k + write 2n
+    dec_achieved = dec_bytes / (dec_launch_ms * 1e-3) / 1e9
+    enc_achieved = enc_bytes / (enc_launch_ms * 1e-3) / 1e9
+    result = {
+        "metric": "encode & decode GB/s of source data per GPU (1/2/4/8 B200), % of HBM roofline",
+        "value": round(value, 3),
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_per_step, 3),
+        "higher_is_better": True,
+        "scaling": args.scaling,
+        "vs_baseline": None,
+        "dtype": "u32 (GF(65537) in 32-bit lanes; uint16 packets)",
+        "data": "synthetic (seeded splitmix64 uint16 source, seeded erasure patterns per BASELINE config)",
+        "config": {
+            "workload": f"{cfg.name}: n={n} k={k} L={L} stripes/GPU={S_rank} patterns/GPU={len(pats)} "
+                        f"({cfg.pattern}); step = plans + encode + decode of all stripes",
+            "n": n, "k": k, "L": L, "stripes_per_gpu": S_rank, "source_bytes_per_gpu": src_bytes_rank,
+            "chunk_stripes": chunk, "l2_policy": "inputs (%.1f GiB/GPU) far larger than L2" % (src_bytes_rank / 2**30),
+            "parallelism": f"stripes{'/rank' if args.scaling == 'weak' else ' sharded'} x {world} GPU",
+        },
+        "phases_ms": {"plans": round(float(phase_ms[0]), 3), "encode": round(float(phase_ms[1]), 3),
+                      "decode": round(float(phase_ms[2]), 3)},
+        "encode_gbs": round(src_bytes_rank / (phase_ms[1] * 1e-3) / 1e9, 2),
+        "decode_gbs": round(src_bytes_rank / (phase_ms[2] * 1e-3) / 1e9, 2),
+        "decode_with_plans_gbs": round(src_bytes_rank / ((phase_ms[2] + phase_ms[0]) * 1e-3) / 1e9, 2),
+        "roofline": {
+            "bound": "hbm", "kernel": "dec_fast_kernel (fused decode, one launch per chunk)",
+            "achieved": round(dec_achieved, 2), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+            "frac": round(dec_achieved / peak, 4), "traffic": args.traffic,
+            "algorithmic_bytes_per_launch": dec_bytes, "avg_launch_ms": round(dec_launch_ms, 4),
+        },
+        "roofline_encode": {
+            "bound": "hbm", "kernel": "enc_fast_kernel", "achieved": round(enc_achieved, 2), "peak": peak,
+            "unit": "GB/s", "frac": round(enc_achieved / peak, 4), "algorithmic_bytes_per_launch": enc_bytes,
+            "avg_launch_ms": round(enc_launch_ms, 4),
+        },
+        "gpu_launches": int(gpu_launches),
+        "clocks": clocks.summary(),
+    }
+    del rx, enc
+    torch.cuda.empty_cache()
+    if args.e2e_stripes:
+        result["e2e"] = run_e2e(args, codec, cfg, dev, stream, seed, world)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(cfg, args.cpu_seconds)
+    return result
+
+
+def run_e2e(args, codec, cfg, dev, stream, seed, world):
+    """Same metric through the public API with pinned HOST buffers: every step
+    copies the source and received packets host->device and the encoded and
+    decoded packets (plus escape counts) device->host inside the timed region."""
+    import torch
+    import torch.distributed as dist
+    k, n, L = cfg.k, cfg.n, cfg.L
+    S = min(args.e2e_stripes, cfg.stripes)
+    src_h = torch.from_numpy(W.symbols(seed + 7, 0, S * k * L).view(np.int16).reshape(S, k, L)).pin_memory()
+    pats, sp = W.patterns(cfg, seed=seed + 7, stripes=S)
+    # received packets prepared once on the host (the erasure channel, not the codec)
+    d_src = src_h.to(dev)
+    enc0, e0, c0 = codec.encode(k, n, d_src)
+    rx0, rxe0 = W.received_packets(enc0, e0, c0, pats, sp, n)
+    rx_h = rx0.cpu().pin_memory()
+    rxe_h = rxe0.cpu().pin_memory() if rxe0 is not None else None
+    del enc0, rx0, d_src
+    enc_h = torch.empty((S, n, L), dtype=torch.int16).pin_memory()
+    dec_h = torch.empty((S, k, L), dtype=torch.int16).pin_memory()
+    cnt_h = torch.zeros(2, dtype=torch.int64).pin_memory()
+    d_src = torch.empty((S, k, L), dtype=torch.int16, device=dev)
+    d_rx = torch.empty_like(d_src)
+    d_enc = torch.empty((S, n, L), dtype=torch.int16, device=dev)
+    d_dec = torch.empty_like(d_src)
+    sp_d = torch.from_numpy(sp.astype(np.int32)).to(dev)
+    h2d = d_src.numel() * 2 + d_rx.numel() * 2 + (rxe_h.numel() * 8 if rxe_h is not None else 0) + sp.nbytes
+    d2h = enc_h.numel() * 2 + dec_h.numel() * 2 + 16
+
+    def step():
+        d_src.copy_(src_h, non_blocking=True)
+        _, _, ce = codec.encode(k, n, d_src, out=d_enc)
+        enc_h.copy_(d_enc, non_blocking=True)
+        d_rx.copy_(rx_h, non_blocking=True)
+        rxe = rxe_h.to(dev, non_blocking=True) if rxe_h is not None else None
+        plans = codec.plans(k, n, pats)
+        _, _, cd = codec.decode(plans, sp_d, d_rx, rxe, out=d_dec)
+        dec_h.copy_(d_dec, non_blocking=True)
+        cnt_h[0:1].copy_(ce, non_blocking=True)
+        cnt_h[1:2].copy_(cd, non_blocking=True)
+        return plans
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    torch.cuda.synchronize(dev)
+    assert torch.equal(dec_h, src_h), "e2e decode mismatch"
+    if world > 1:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = max(1, args.steps)
+    keep = []
+    a.record(stream)
+    for _ in range(steps):
+        keep.append(step())
+    b.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = a.elapsed_time(b) / steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    total_src = 2 * k * L * S * world
+    return {"value": round(total_src / (ms * 1e-3) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ms, 3),
+            "sample": f"{S} stripes/GPU of {cfg.name} via Codec.encode/plans/decode (C ABI) from pinned host memory"}
+
+
+def cpu_baseline(cfg, budget_s):
+    threads = os.cpu_count() or 1
+    try:
+        stripes, per = pick_cpu_sample(cfg, threads, budget_s)
+        e, d, b = cpu_reference_sample(cfg, W.SEED + 99, stripes, threads)
+    except Exception as ex:  # reported, never fatal for the GPU arm
+        return {"value": None, "error": str(ex)[:200]}
+    return {"value": round(b / (e + d) / 1e9, 6), "unit": "GB/s", "cores": threads, "kind": "reference",
+            "encode_gbs": round(b / e / 1e9, 6), "decode_gbs": round(b / d / 1e9, 6),
+            "sample": f"{stripes} stripes of {cfg.name} (encode + Path::Auto decode incl. plan build), "
+                      f"{threads} threads over codewords, AVX2 path, oracle/_ref = unmodified reference library"}
+
+
+# ----------------------------------------------------- reference arm ----
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    cfg = W.CONFIGS[args.config]
+    threads = os.cpu_count() or 1
+    ref = reference_lib()
+    if ref is None:
+        return {"impl": "reference", "unavailable": "reference library (oracle/_ref) not built"}
+    stripes, per = pick_cpu_sample(cfg, threads, args.ref_step_seconds)
+    times = []
+    for i in range(args.warmup + args.steps):
+        e, d, b = cpu_reference_sample(cfg, W.SEED + i, stripes, threads)
+        if i >= args.warmup:
+            times.append(e + d)
+    ms = 1e3 * float(np.mean(times))
+    value = 2 * cfg.k * cfg.L * stripes / (ms * 1e-3) / 1e9
+    return {
+        "impl": "reference",
+        "metric": "encode & decode GB/s of source data per GPU (1/2/4/8 B200), % of HBM roofline",
+        "value": round(value, 6), "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+        "dtype": "u32 (GF(65537))", "data": "synthetic (same generator and erasure classes)",
+        "config": {"workload": f"{cfg.name}: n={cfg.n} k={cfg.k} L={cfg.L}; step = encode + decode "
+                               f"(incl. plan build) of a {stripes}-stripe sample", "stripes_per_step": stripes},
+        "cpu_baseline": {"value": round(value, 6), "unit": "GB/s", "cores": threads, "kind": "reference",
+                         "sample": f"{stripes} stripes per step, {threads} threads, Path::Auto"},
+        "e2e": {"value": round(value, 6), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C2", choices=sorted(W.CONFIGS))
+    ap.add_argument("--stripes", type=int, default=0, help="override stripes per GPU (default: the config's)")
+    ap.add_argument("--chunk", type=int, default=8192, help="stripes per kernel launch")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--e2e-stripes", type=int, default=4096)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-step-seconds", type=float, default=6.0)
+    ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes per decode launch (profiles/)")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    res = run_gpu(args, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -100,6 +100,9 @@ int fntrs_gpu_encode(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t stripes, u
 int fntrs_gpu_plans_create(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t kp,
                            uint32_t npatterns, const uint32_t* positions, fntrs_plans** out,
                            void* stream);
+/* Plan buffers are stream-ordered allocations on the creation stream and are
+ * released in that stream's order (work queued before destroy may still use
+ * them). Use pinned host positions for a fully asynchronous create. */
 int fntrs_gpu_plans_destroy(fntrs_plans* plans);
 uint32_t fntrs_gpu_plans_count(const fntrs_plans* plans);
 

@@ -187,15 +187,22 @@ class Codec:
         return out, esc_out, count
 
     # -- plans ------------------------------------------------------------
-    def plans(self, k: int, n: int, positions: np.ndarray, stream=None) -> Plans:
-        """positions: host [P, kp] uint32 received positions per pattern."""
-        pos = np.ascontiguousarray(positions, dtype=np.uint32)
-        if pos.ndim == 1:
-            pos = pos[None, :]
-        P, kp = pos.shape
+    def plans(self, k: int, n: int, positions, stream=None) -> Plans:
+        """positions: host [P, kp] uint32 received positions per pattern (a numpy
+        array, or a pinned CPU torch tensor for a fully asynchronous upload)."""
+        if hasattr(positions, "data_ptr"):
+            pos_t = positions if positions.dim() == 2 else positions[None, :]
+            P, kp = pos_t.shape
+            ptr, keep = pos_t.data_ptr(), pos_t
+        else:
+            pos = np.ascontiguousarray(positions, dtype=np.uint32)
+            if pos.ndim == 1:
+                pos = pos[None, :]
+            P, kp = pos.shape
+            ptr, keep = pos.ctypes.data, pos
         h = C.c_void_p()
-        st = _lib.load().fntrs_gpu_plans_create(self.ctx, k, n, kp, P, pos.ctypes.data, C.byref(h),
-                                                _stream_ptr(stream))
+        st = _lib.load().fntrs_gpu_plans_create(self.ctx, k, n, kp, P, ptr, C.byref(h), _stream_ptr(stream))
+        del keep
         self._check(st)
         return Plans(self, h, k, n, kp, P)
 

@@ -34,6 +34,7 @@ struct fntrs_ctx {
 
 struct fntrs_plans {
     int device = 0;
+    cudaStream_t stream = nullptr;  // buffers are stream-ordered allocations on this stream
     uint32_t k = 0, n = 0, N = 0, M = 0, kp = 0, np = 0;
     uint32_t* pos = nullptr;
     uint32_t* ainv = nullptr;
@@ -288,18 +289,19 @@ int fntrs_gpu_plans_create(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t kp, 
     pl->ninv = cpow(N % kP, kP - 2);
     const size_t npos = size_t(npatterns) * kp;
     cudaError_t e = cudaSuccess;
+    pl->stream = st;
     if (npatterns) {
-        e = cudaMalloc(&pl->pos, npos * 4);
-        if (!e) e = cudaMalloc(&pl->ainv, npos * 4);
-        if (!e && locator) e = cudaMalloc(&pl->ahat, size_t(npatterns) * M * 4);
+        e = cudaMallocAsync(&pl->pos, npos * 4, st);
+        if (!e) e = cudaMallocAsync(&pl->ainv, npos * 4, st);
+        if (!e && locator) e = cudaMallocAsync(&pl->ahat, size_t(npatterns) * M * 4, st);
         if (!e) e = cudaMemcpyAsync(pl->pos, positions, npos * 4, cudaMemcpyHostToDevice, st);
         if (!e && locator) {
             e = launch_plan_build(N, M, kp, npatterns, pl->pos, pl->ainv, pl->ahat, ctx->tab, st);
             ctx->launches += 1;
         }
         if (!e && !full && kp == k && M == N && fast::fast_tile_columns(N)) {
-            e = cudaMalloc(&pl->rowmap, size_t(npatterns) * N * sizeof(uint2));
-            if (!e) e = cudaMalloc(&pl->ahat2, size_t(npatterns) * N * sizeof(uint2));
+            e = cudaMallocAsync(&pl->rowmap, size_t(npatterns) * N * sizeof(uint2), st);
+            if (!e) e = cudaMallocAsync(&pl->ahat2, size_t(npatterns) * N * sizeof(uint2), st);
             if (!e) e = fast::launch_fast_plan_tables(N, kp, npatterns, pl->pos, pl->ainv, pl->ahat, pl->rowmap,
                                                       pl->ahat2, st);
             ctx->launches += 2;
@@ -316,11 +318,10 @@ int fntrs_gpu_plans_create(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t kp, 
 int fntrs_gpu_plans_destroy(fntrs_plans* pl) {
     if (!pl) return FNTRS_OK;
     DeviceGuard g(pl->device);
-    cudaFree(pl->pos);
-    cudaFree(pl->ainv);
-    cudaFree(pl->ahat);
-    cudaFree(pl->rowmap);
-    cudaFree(pl->ahat2);
+    // stream-ordered release: work already queued on the plan's stream may
+    // still read the buffers; callers using other streams must order them
+    for (void* p : {(void*)pl->pos, (void*)pl->ainv, (void*)pl->ahat, (void*)pl->rowmap, (void*)pl->ahat2})
+        if (p) cudaFreeAsync(p, pl->stream);
     delete pl;
     return FNTRS_OK;
 }
