@@ -35,6 +35,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 from paper_0907_1788_b200 import workload as W  # noqa: E402
+from paper_0907_1788_b200.sharding import max_over_ranks, rank_seed, rank_stripes  # noqa: E402
 
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback, only if MEASURED_PEAKS.json is absent
@@ -146,13 +147,9 @@ def run_gpu(args, rank, world, local_rank):
     torch.cuda.set_device(dev)
     cfg = W.CONFIGS[args.config]
     S = args.stripes or cfg.stripes
-    if args.scaling == "strong":
-        per = (S + world - 1) // world
-        lo, hi = rank * per, min(S, (rank + 1) * per)
-        S_rank = max(0, hi - lo)
-    else:
-        S_rank = S
-    seed = W.SEED + 1000003 * rank
+    lo, hi = rank_stripes(S, rank, world, args.scaling)
+    S_rank = hi - lo
+    seed = rank_seed(W.SEED, rank) if args.scaling == "weak" else W.SEED
     k, n, L = cfg.k, cfg.n, cfg.L
     lib = _lib.load()
     codec = Codec(local_rank)
@@ -162,7 +159,8 @@ def run_gpu(args, rank, world, local_rank):
 
     # ---- workload resident in HBM (untimed setup)
     src = torch.empty((S_rank, k, L), dtype=torch.int16, device=dev)
-    st = lib.fntrs_gpu_fill_symbols(seed, 0, src.numel(), C.c_void_p(src.data_ptr()), C.c_void_p(stream.cuda_stream))
+    st = lib.fntrs_gpu_fill_symbols(seed, lo * k * L, src.numel(), C.c_void_p(src.data_ptr()),
+                                    C.c_void_p(stream.cuda_stream))
     assert st == 0
     enc = torch.empty((S_rank, n, L), dtype=torch.int16, device=dev)
     esc_cap = default_escape_capacity(chunk * n * L)
@@ -179,7 +177,12 @@ def run_gpu(args, rank, world, local_rank):
 
     for c in range(nchunks):
         encode_chunk(c)
-    pats, sp = W.patterns(cfg, seed=seed, stripes=S_rank)
+    if lo == 0:
+        pats, sp = W.patterns(cfg, seed=seed, stripes=S_rank)
+    else:  # strong scaling: this rank's slice of the global stripes and the patterns they use
+        pats_all, sp_all = W.patterns(cfg, seed=seed, stripes=S)
+        used, sp = np.unique(sp_all[lo:hi], return_inverse=True)
+        pats, sp = pats_all[used], sp.astype(np.uint32)
     rx = torch.empty((S_rank, k, L), dtype=torch.int16, device=dev)
     rx_esc = []
     for c in range(nchunks):
@@ -274,10 +277,8 @@ def run_gpu(args, rank, world, local_rank):
     phase_ms /= args.steps
     dec_launch_ms = float(np.mean([a.elapsed_time(b) for a, b in dec_events]))
     enc_launch_ms = float(np.mean([a.elapsed_time(b) for a, b in enc_events]))
-    if world > 1:
-        tt = torch.tensor([total_ms, *phase_ms, dec_launch_ms, enc_launch_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms, phase_ms, dec_launch_ms, enc_launch_ms = float(tt[0]), tt[1:4].cpu().numpy(), float(tt[4]), float(tt[5])
+    mx = max_over_ranks([total_ms, *phase_ms, dec_launch_ms, enc_launch_ms], device=dev)
+    total_ms, phase_ms, dec_launch_ms, enc_launch_ms = mx[0], np.array(mx[1:4]), mx[4], mx[5]
 
     ms_per_step = total_ms / args.steps
     src_bytes_rank = 2 * k * L * S_rank

@@ -1,0 +1,67 @@
+"""Multi-rank host logic of the stripe sharding (gloo, world size 2, CPU)."""
+import os
+import socket
+
+import pytest
+
+from paper_0907_1788_b200.sharding import max_over_ranks, rank_seed, rank_stripes
+
+
+def test_strong_ranges_partition_exactly():
+    for total in (0, 1, 7, 2048, 65536):
+        for world in (1, 2, 3, 4, 8):
+            covered = []
+            for r in range(world):
+                lo, hi = rank_stripes(total, r, world, "strong")
+                assert 0 <= lo <= hi <= total
+                covered.extend(range(lo, hi))
+            assert covered == list(range(total))
+            sizes = [rank_stripes(total, r, world, "strong")[1] - rank_stripes(total, r, world, "strong")[0]
+                     for r in range(world)]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_weak_ranges_and_seeds():
+    assert all(rank_stripes(65536, r, 8, "weak") == (0, 65536) for r in range(8))
+    assert len({rank_seed(5, r) for r in range(8)}) == 8
+    with pytest.raises(ValueError):
+        rank_stripes(10, 2, 2)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lo, hi = rank_stripes(2048, rank, world, "strong")
+        # per-rank "times": the max over ranks must come back on every rank
+        got = max_over_ranks([10.0 + rank, 100.0 - rank, float(hi - lo)])
+        dist.barrier()
+        q.put((rank, lo, hi, got))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_max_over_ranks():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [(r[1], r[2]) for r in res] == [(0, 1024), (1024, 2048)]
+    for r in res:
+        assert r[3] == [11.0, 100.0, 1024.0]
