@@ -81,8 +81,9 @@ __device__ __forceinline__ uint32_t cap(uint32_t v) {
 }
 
 // ---- geometry ---------------------------------------------------------------
-template <int E, int WT_, int NT_>
+template <int E, int WT_, int NT_, int MINB_ = 1>
 struct Geom {
+    static constexpr int MINB = MINB_;
     static constexpr int N = 1 << E;
     static constexpr int WT = WT_;
     static constexpr int NT = NT_;
@@ -103,7 +104,9 @@ struct Pick {
     static constexpr int N = 1 << E;
     static constexpr int WT = N <= 512 ? 32 : (N == 1024 ? 16 : 8);
     static constexpr int NT = N == 4096 ? 512 : 256;
-    using G = Geom<E, WT, NT>;
+    // blocks per SM the register budget should allow (shared memory permits 4 at N <= 512)
+    static constexpr int MINB = N <= 512 ? 4 : (N <= 2048 ? 2 : 1);
+    using G = Geom<E, WT, NT, MINB>;
 };
 
 // ---- generic pass (one codeword per work item) ----------------------------
@@ -135,16 +138,7 @@ __device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld
         const uint32_t t = b & ((1u << SL) - 1u);
         const uint32_t base = ((b >> SL) << LL) + t;
         uint32_t v[R];
-        uint2 w[R];
-        if constexpr (SL > 0) {
-            const uint4* tp = twp + t * (R / 2);
-#pragma unroll
-            for (int i = 0; i < R / 2; ++i) {
-                const uint4 x = __ldg(tp + i);
-                w[2 * i] = make_uint2(x.x, x.y);
-                w[2 * i + 1] = make_uint2(x.z, x.w);
-            }
-        }
+        const uint2* tp = reinterpret_cast<const uint2*>(twp) + t * R;  // row t: r_len^(t s), s < R
         uint32_t mask = 0;
         if constexpr (!DIT) {
 #pragma unroll
@@ -155,10 +149,12 @@ __device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld
 #pragma unroll
             for (int s = 0; s < R; ++s) {
                 uint32_t y = v[rev<R>(s)];
-                if (SL > 0 && s > 0)
-                    y = mulw2(y, w[s].x, w[s].y);
-                else
+                if (SL > 0 && s > 0) {
+                    const uint2 w = __ldg(tp + s);
+                    y = mulw2(y, w.x, w.y);
+                } else {
                     y = cap<BO, OCAP>(y);
+                }
                 mask |= st(base + (uint32_t(s) << SL), b, s, col, y) << s;
             }
         } else {
@@ -166,7 +162,10 @@ __device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld
 #pragma unroll
             for (int s = 0; s < R; ++s) {
                 uint32_t x = ld(base + (uint32_t(s) << SL), b, s, col);
-                if (SL > 0 && s > 0) x = mulw2(x, w[s].x, w[s].y);
+                if (SL > 0 && s > 0) {
+                    const uint2 w = __ldg(tp + s);
+                    x = mulw2(x, w.x, w.y);
+                }
                 v[rev<R>(s)] = x;
             }
             dit_regs<R, INV, BI>(v);
@@ -197,7 +196,7 @@ __device__ __forceinline__ bool any_zero(const uint32_t (&v)[R]) {
 
 // ---------------------------------------------------------------------------
 template <int E, class G, bool HALFK, bool PUNCT>
-__global__ void __launch_bounds__(G::NT) enc_fast_kernel(const __grid_constant__ CUtensorMap src_map,
+__global__ void __launch_bounds__(G::NT, G::MINB) enc_fast_kernel(const __grid_constant__ CUtensorMap src_map,
                                                          const uint2* __restrict__ ptabF, uint32_t k, uint32_t n,
                                                          uint32_t L, uint32_t tps, uint32_t tiles, uint32_t nbox,
                                                          uint32_t box_rows, EscIn esc_in, uint16_t* __restrict__ out,
@@ -288,7 +287,7 @@ __global__ void __launch_bounds__(G::NT) enc_fast_kernel(const __grid_constant__
 
 // ---------------------------------------------------------------------------
 template <int E, class G, bool HALFK>
-__global__ void __launch_bounds__(G::NT) dec_fast_kernel(const __grid_constant__ CUtensorMap rx_map,
+__global__ void __launch_bounds__(G::NT, G::MINB) dec_fast_kernel(const __grid_constant__ CUtensorMap rx_map,
                                                          const uint2* __restrict__ ptabF, const uint2* __restrict__ ptabI,
                                                          const uint2* __restrict__ rowmap,
                                                          const uint2* __restrict__ ahat2, uint32_t k, uint32_t L,
@@ -345,10 +344,9 @@ __global__ void __launch_bounds__(G::NT) dec_fast_kernel(const __grid_constant__
         // step 4: N'[z] = v_i / A'(x_i) where z = z_i, else 0. A received
         // zero word may be an escaped 65536: the group fix-up re-scales it.
         auto ld_scatter = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t {
-            const uint2 m = __ldg(rm + lrow);
-            if (m.x == 0xFFFFFFFFu) return 0u;
-            const uint32_t v = st_in[m.x * WT + col];
-            return v ? mulw2(v, m.y, m.y * 65535u) : 0u;
+            const uint2 m = __ldg(rm + lrow);  // erased: {~0, 0} -> reads row 0, scales by 0
+            const uint32_t row = m.x == 0xFFFFFFFFu ? 0u : m.x;
+            return mulw2(uint32_t(st_in[row * WT + col]), m.y, m.y * 65535u);
         };
         auto fix_scatter = [&](uint32_t (&v)[R0], uint32_t base, uint32_t, uint32_t col) {
             if (!esc_any) return;
@@ -438,20 +436,15 @@ __global__ void __launch_bounds__(G::NT) dec_fast_kernel(const __grid_constant__
                 const uint32_t col = uint32_t(it) & uint32_t(WT - 1);
                 const uint32_t t = uint32_t(it) >> LGW;
                 uint32_t v[R0];
-                uint2 w[R0];
-                {
-                    const uint4* tp = tF0 + t * (R0 / 2);
-#pragma unroll
-                    for (int i = 0; i < R0 / 2; ++i) {
-                        const uint4 x = __ldg(tp + i);
-                        w[2 * i] = make_uint2(x.x, x.y);
-                        w[2 * i + 1] = make_uint2(x.z, x.w);
-                    }
-                }
+                const uint2* tpf = reinterpret_cast<const uint2*>(tF0) + t * R0;
+                const uint2* tpi = reinterpret_cast<const uint2*>(tI0) + t * R0;
 #pragma unroll
                 for (int s = 0; s < R0; ++s) {
                     uint32_t x = work[G::idx((t + (uint32_t(s) << SL0)) ^ FLIP, col)];
-                    if (s > 0) x = mulw2(x, w[s].x, w[s].y);
+                    if (s > 0) {
+                        const uint2 w = __ldg(tpf + s);
+                        x = mulw2(x, w.x, w.y);
+                    }
                     v[rev<R0>(s)] = x;
                 }
                 dit_regs<R0, false, kSmemCap>(v);
@@ -461,22 +454,15 @@ __global__ void __launch_bounds__(G::NT) dec_fast_kernel(const __grid_constant__
                     v[q] = mulw2(v[q], a.x, a.y);
                 }
                 dif_regs<R0, true, k2P>(v);
-                {
-                    const uint4* tp = tI0 + t * (R0 / 2);
-#pragma unroll
-                    for (int i = 0; i < R0 / 2; ++i) {
-                        const uint4 x = __ldg(tp + i);
-                        w[2 * i] = make_uint2(x.x, x.y);
-                        w[2 * i + 1] = make_uint2(x.z, x.w);
-                    }
-                }
 #pragma unroll
                 for (int s = 0; s < R0; ++s) {
                     uint32_t y = v[rev<R0>(s)];
-                    if (s > 0)
-                        y = mulw2(y, w[s].x, w[s].y);
-                    else
+                    if (s > 0) {
+                        const uint2 w = __ldg(tpi + s);
+                        y = mulw2(y, w.x, w.y);
+                    } else {
                         y = cap<BO, kSmemCap>(y);
+                    }
                     work[G::idx((t + (uint32_t(s) << SL0)) ^ FLIP, col)] = y;
                 }
             }
