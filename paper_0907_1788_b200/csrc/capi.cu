@@ -8,6 +8,7 @@
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -30,6 +31,8 @@ struct fntrs_ctx {
     uint64_t sort_alt_cap = 0;
     uint64_t launches = 0;
     std::string err;
+    uint32_t* scratch[2] = {nullptr, nullptr};  // four-step intermediates (stream-ordered)
+    size_t scratch_bytes = 0;
 };
 
 struct fntrs_plans {
@@ -120,6 +123,22 @@ int sort_escapes(fntrs_ctx* ctx, unsigned long long* keys, uint64_t cap, uint64_
     return FNTRS_OK;
 }
 
+constexpr size_t kScratchCap = size_t(2) << 30;  // per four-step intermediate buffer
+
+// Two stream-ordered scratch buffers of at least `bytes` each.
+int ensure_scratch(fntrs_ctx* ctx, size_t bytes, cudaStream_t st) {
+    if (ctx->scratch_bytes >= bytes) return FNTRS_OK;
+    for (auto& p : ctx->scratch)
+        if (p) {
+            cudaFreeAsync(p, st);
+            p = nullptr;
+        }
+    ctx->scratch_bytes = 0;
+    for (auto& p : ctx->scratch) CK(cudaMallocAsync(&p, bytes, st), "scratch alloc");
+    ctx->scratch_bytes = bytes;
+    return FNTRS_OK;
+}
+
 int prep_escapes(fntrs_ctx* ctx, uint64_t* out_esc, uint64_t esc_cap, uint64_t* n_out_esc, cudaStream_t st) {
     if (!n_out_esc) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "n_out_esc must be a device pointer");
     if (esc_cap && !out_esc) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "out_esc is null");
@@ -190,6 +209,7 @@ int fntrs_gpu_create(int device, fntrs_ctx** out) {
     cudaError_t e = cudaStreamCreateWithFlags(&ctx->internal, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = build_tables(ctx->tab, ctx->internal);
     if (e == cudaSuccess) e = fast::build_fast_tables(ctx->ftab, ctx->internal);
+    if (e == cudaSuccess) e = fast::build_large_tables(ctx->ftab, ctx->internal);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->internal);
     if (e != cudaSuccess) {
         delete ctx;
@@ -207,6 +227,11 @@ int fntrs_gpu_destroy(fntrs_ctx* ctx) {
     cudaFree(ctx->tab.inv);
     cudaFree(ctx->ftab.ptab_fwd);
     cudaFree(ctx->ftab.ptab_inv);
+    cudaFree(ctx->ftab.big_fwd);
+    cudaFree(ctx->ftab.big_inv);
+    cudaDeviceSynchronize();
+    cudaFree(ctx->scratch[0]);
+    cudaFree(ctx->scratch[1]);
     cudaFree(ctx->sort_tmp);
     cudaFree(ctx->sort_alt);
     if (ctx->internal) cudaStreamDestroy(ctx->internal);
@@ -222,7 +247,9 @@ int fntrs_gpu_encode(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t stripes, u
     if (fntrs_gpu_code_params(k, n, &N))
         return fail(ctx, FNTRS_E_SIZE_MISMATCH, "code parameters need 1 <= k <= n <= 65536, got k = " +
                                                     std::to_string(k) + ", n = " + std::to_string(n));
-    if (N > kTileMaxN) return fail(ctx, FNTRS_E_UNSUPPORTED, "n_domain > 4096 not in this build yet");
+    const bool large = fast::large_supported(N);
+    if (N > kTileMaxN && !(large && L % fast::large_tile_columns() == 0))
+        return fail(ctx, FNTRS_E_UNSUPPORTED, "n_domain > 4096 needs L to be a multiple of 64 in this build");
     if (stripes && L && (!src || !out)) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "null buffer");
     if (n_src_esc && !src_esc) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "src_esc is null");
     DeviceGuard g(ctx->device);
@@ -235,6 +262,17 @@ int fntrs_gpu_encode(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t stripes, u
     const int cols = fast::fast_tile_columns(N);
     const bool fast_ok = ctx->fast_enabled && cols && L % uint32_t(cols) == 0 &&
                          reinterpret_cast<uintptr_t>(src) % 16 == 0;
+    if (large) {
+        if (stripes && L) {
+            const uint32_t batch = std::min(stripes, fast::large_batch(N, L, kScratchCap));
+            rc = ensure_scratch(ctx, size_t(batch) * N * L * 4, st);
+            if (rc) return rc;
+            CK(fast::launch_encode_large(ctx->ftab, k, n, N, stripes, L, src, ein, out, eout, ctx->scratch[0], batch, st),
+               "encode launch");
+            ctx->launches += 2 * ((stripes + batch - 1) / batch);
+        }
+        return sort_escapes(ctx, eout.keys, esc_cap, uint64_t(stripes) * n * L, st);
+    }
     if (fast_ok)
         CK(fast::launch_encode_fast(ctx->ftab, k, n, N, stripes, L, src, ein, out, eout, st), "encode launch");
     else
@@ -259,8 +297,10 @@ int fntrs_gpu_plans_create(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t kp, 
     const uint32_t M = 2ull * k > 65536ull ? 0u : next_pow2(2 * k);
     // locator data: needed for decoding unless complete; kept for export when it fits
     const bool locator = !full || (kp == k && M && M <= kTileMaxN);
-    if (N > kTileMaxN || (!full && M > kTileMaxN))
-        return fail(ctx, FNTRS_E_UNSUPPORTED, "transform sizes > 4096 not in this build yet");
+    const bool large = fast::large_supported(N) && !full && kp == k && M == N;
+    if (!large && (N > kTileMaxN || (!full && M > kTileMaxN)))
+        return fail(ctx, FNTRS_E_UNSUPPORTED,
+                    "transform sizes > 4096 need k in (n_domain/4, n_domain/2] in this build");
     if (npatterns && !positions) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "positions is null");
     // validation (codec.cpp:32-48 order: range first, then duplicates)
     std::vector<uint8_t> seen(n);
@@ -299,7 +339,7 @@ int fntrs_gpu_plans_create(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t kp, 
             e = launch_plan_build(N, M, kp, npatterns, pl->pos, pl->ainv, pl->ahat, ctx->tab, st);
             ctx->launches += 1;
         }
-        if (!e && !full && kp == k && M == N && fast::fast_tile_columns(N)) {
+        if (!e && !full && kp == k && M == N && (fast::fast_tile_columns(N) || large)) {
             e = cudaMallocAsync(&pl->rowmap, size_t(npatterns) * N * sizeof(uint2), st);
             if (!e) e = cudaMallocAsync(&pl->ahat2, size_t(npatterns) * N * sizeof(uint2), st);
             if (!e) e = fast::launch_fast_plan_tables(N, kp, npatterns, pl->pos, pl->ainv, pl->ahat, pl->rowmap,
@@ -389,7 +429,20 @@ int fntrs_gpu_decode(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t stripes, ui
     const int cols = fast::fast_tile_columns(pl->N);
     const bool fast_ok = ctx->fast_enabled && pl->rowmap && cols && L % uint32_t(cols) == 0 &&
                          reinterpret_cast<uintptr_t>(rx) % 16 == 0;
-    if (fast_ok) {
+    if (fast::large_supported(pl->N) && pl->rowmap) {
+        if (L % fast::large_tile_columns())
+            return fail(ctx, FNTRS_E_UNSUPPORTED, "n_domain > 4096 needs L to be a multiple of 64 in this build");
+        if (stripes && L) {
+            const uint32_t batch = std::min(stripes, fast::large_batch(pl->N, L, kScratchCap));
+            rc = ensure_scratch(ctx, size_t(batch) * pl->N * L * 4, st);
+            if (rc) return rc;
+            fast::FastPlanView fv{pl->N, pl->k, pl->rowmap, pl->ahat2};
+            CK(fast::launch_decode_large(ctx->ftab, fv, stripes, L, stripe_pattern, rx, ein, out, eout, ctx->scratch[0],
+                                         ctx->scratch[1], batch, st),
+               "decode launch");
+            ctx->launches += 4 * ((stripes + batch - 1) / batch);
+        }
+    } else if (fast_ok) {
         fast::FastPlanView fv{pl->N, pl->k, pl->rowmap, pl->ahat2};
         CK(fast::launch_decode_fast(ctx->ftab, fv, stripes, L, stripe_pattern, rx, ein, out, eout, st), "decode launch");
     } else {

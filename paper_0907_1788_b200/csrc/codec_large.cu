@@ -1,0 +1,450 @@
+// codec_large.cu -- encode / decode for 8192 <= n_domain <= 65536 (four-step).
+//
+// A size-N transform (N = N1*N2, N1 = 2^E1 >= N2 = 2^E2, both <= 256) is
+//   X[m1 + N1 m2] = sum_i2 r_N2^(i2 m2) * [ r_N^(i2 m1) * sum_i1 x[i1 N2 + i2] r_N1^(i1 m1) ]
+// i.e. N2 transforms of size N1 over stride-N2 rows ("pass A"), a twiddle,
+// then N1 transforms of size N2 over contiguous rows ("pass B"). Each CTA
+// owns one inner index and 64 adjacent codewords, so every pass is a
+// shared-memory tile [size][64] run by the same radix-16 engine as the
+// fused kernels, with loads / stores going straight to HBM.
+//
+// Encode = pass A (zero padding never read) + pass B (natural-order packets).
+// Decode (interp::interpolate, proj/src/interp.cpp:103-137) = 3 transforms
+// in 4 kernels; the transform boundaries are fused inside CTAs:
+//   D1  FNT1 pass A, scatter-loading received packets scaled by 1/A'(x_i)
+//   D2  FNT1 pass B + reversal/truncation s'_j = F[N-1-j] + FNT2 pass A
+//       (the coset F[m1 + N1 m2], m2 < N2 is exactly s' on i1' = N1-1-m1)
+//   D3  FNT2 pass B + (. A_hat) + FNT3 pass A (both on the coset q2 mod N2)
+//   D4  FNT3 pass B, writing the k decoded packets.
+// Intermediates (uint32, < 2p) go through a stripe-batched HBM scratch.
+#include <cuda_runtime.h>
+
+#include "fft_pass.cuh"
+
+namespace fntrs_gpu {
+namespace fast {
+
+namespace {
+
+constexpr int kLW = 64;   // codewords per CTA
+constexpr int kLNT = 256;  // threads per CTA
+
+template <int E>
+using LG = Geom<E, kLW, kLNT, (1 << E) <= 128 ? 4 : 2>;
+
+struct BlockIdx {
+    uint32_t sb, g, c0;
+};
+
+__device__ __forceinline__ BlockIdx block_index(uint32_t tps, uint32_t ng) {
+    const uint32_t tile = blockIdx.x;
+    const uint32_t ct = tile % tps;
+    const uint32_t rest = tile / tps;
+    return {rest / ng, rest % ng, ct * kLW};
+}
+
+// ---------------------------------------------------------------- encode ----
+template <int E1, int E2, bool HALFK>
+__global__ void __launch_bounds__(kLNT, LG<E1>::MINB)
+enc_a_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, uint32_t k, uint32_t L, uint32_t tps,
+             uint32_t stripe0, const uint16_t* __restrict__ src, EscIn esc_in, uint32_t* __restrict__ Y) {
+    using G = LG<E1>;
+    using S = Sched<E1>;
+    constexpr uint32_t N1 = 1u << E1, N2 = 1u << E2, N = N1 * N2;
+    constexpr int R0 = 1 << S::rlog(0), RLZ = G::RLZ;
+    extern __shared__ __align__(128) uint32_t work[];
+    const BlockIdx bi = block_index(tps, N2);
+    const uint32_t i2 = bi.g, stripe = stripe0 + bi.sb;
+    const unsigned long long key_in = uint64_t(stripe) * k * L + bi.c0;
+    const uint16_t* srcp = launder(src + key_in);
+    uint32_t* yp = launder(Y + (uint64_t(bi.sb) * N) * L + bi.c0);
+    const bool esc_any = esc_in.n != 0;
+
+    auto ld = [&](uint32_t i1, uint32_t, int q, uint32_t col) -> uint32_t {
+        const uint32_t row = i1 * N2 + i2;
+        if ((HALFK && q >= R0 / 2) || (!HALFK && row >= k)) return 0u;
+        return srcp[row * L + col];
+    };
+    auto fix = [&](uint32_t (&v)[R0], uint32_t base, uint32_t, uint32_t col) {
+        if (!esc_any || !any_zero(v)) return;
+#pragma unroll
+        for (int q = 0; q < R0; ++q) {
+            const uint32_t row = (base + (uint32_t(q) << S::slog(0))) * N2 + i2;
+            if (v[q] == 0u && row < k && esc_has(esc_in, key_in + uint64_t(row) * L + col)) v[q] = 65536u;
+        }
+    };
+    auto st_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col, uint32_t y) -> uint32_t {
+        work[G::idx(lrow, col)] = y;
+        return 0u;
+    };
+    auto ld_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t { return work[G::idx(lrow, col)]; };
+    auto st_y = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) -> uint32_t {
+        const uint32_t m1 = perm_head<E1>(b) + (uint32_t(s) << (E1 - RLZ));
+        const uint2 w = __ldg(bigF + N + ((i2 * m1) & (N - 1)));
+        yp[(m1 * N2 + i2) * L + col] = mulw2(y, w.x, w.y);
+        return 0u;
+    };
+    pass<E1, 0, false, false, kP64, kSmemCap, G>(pass_table(ptab, S::llog(0)), ld, st_sm, fix);
+    __syncthreads();
+    pass<E1, 1, false, false, kSmemCap, kSmemCap, G>(pass_table(ptab, S::llog(1)), ld_sm, st_y);
+}
+
+template <int E1, int E2, bool PUNCT>
+__global__ void __launch_bounds__(kLNT, LG<E2>::MINB)
+enc_b_kernel(const uint2* __restrict__ ptab, uint32_t n, uint32_t L, uint32_t tps, uint32_t stripe0,
+             const uint32_t* __restrict__ Y, uint16_t* __restrict__ out, EscOut esc_out) {
+    using G = LG<E2>;
+    using S = Sched<E2>;
+    constexpr uint32_t N1 = 1u << E1, N2 = 1u << E2, N = N1 * N2;
+    constexpr int RLZ = G::RLZ;
+    extern __shared__ __align__(128) uint32_t work[];
+    const BlockIdx bi = block_index(tps, N1);
+    const uint32_t m1 = bi.g, stripe = stripe0 + bi.sb;
+    const uint32_t* yp = launder(Y + (uint64_t(bi.sb) * N + m1 * N2) * L + bi.c0);
+    const unsigned long long key_out = uint64_t(stripe) * n * L + bi.c0;
+    uint16_t* outp = launder(out + key_out);
+
+    auto ld = [&](uint32_t i2, uint32_t, int, uint32_t col) -> uint32_t { return yp[i2 * L + col]; };
+    auto st_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col, uint32_t y) -> uint32_t {
+        work[G::idx(lrow, col)] = y;
+        return 0u;
+    };
+    auto ld_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t { return work[G::idx(lrow, col)]; };
+    auto st_out = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) -> uint32_t {
+        const uint32_t row = m1 + N1 * (perm_head<E2>(b) + (uint32_t(s) << (E2 - RLZ)));
+        y = red2p(y);
+        const bool keep = !PUNCT || row < n;
+        if (keep) __stcs(outp + (row * L + col), uint16_t(y));
+        return (y == 65536u && keep) ? 1u : 0u;
+    };
+    auto flush = [&](uint32_t mask, uint32_t, uint32_t b, uint32_t col) {
+        if (!mask) return;
+#pragma unroll 1
+        for (int s = 0; s < 16; ++s)
+            if (mask & (1u << s))
+                emit_escape(esc_out,
+                            key_out + uint64_t(m1 + N1 * (perm_head<E2>(b) + (uint32_t(s) << (E2 - RLZ)))) * L + col);
+    };
+    pass<E2, 0, false, false, k2P, kSmemCap, G>(pass_table(ptab, S::llog(0)), ld, st_sm);
+    __syncthreads();
+    pass<E2, 1, false, false, kSmemCap, k2P, G>(pass_table(ptab, S::llog(1)), ld_sm, st_out, NoFix(), flush);
+}
+
+// ---------------------------------------------------------------- decode ----
+template <int E1, int E2>
+__global__ void __launch_bounds__(kLNT, LG<E1>::MINB)
+dec_1_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, const uint2* __restrict__ rowmap,
+             uint32_t k, uint32_t L, uint32_t tps, uint32_t stripe0, const uint32_t* __restrict__ stripe_pattern,
+             const uint16_t* __restrict__ rx, EscIn esc_in, uint32_t* __restrict__ Y) {
+    using G = LG<E1>;
+    using S = Sched<E1>;
+    constexpr uint32_t N1 = 1u << E1, N2 = 1u << E2, N = N1 * N2;
+    constexpr int R0 = 1 << S::rlog(0), RLZ = G::RLZ;
+    extern __shared__ __align__(128) uint32_t work[];
+    const BlockIdx bi = block_index(tps, N2);
+    const uint32_t i2 = bi.g, stripe = stripe0 + bi.sb;
+    const uint2* __restrict__ rm = rowmap + size_t(__ldg(stripe_pattern + stripe)) * N;
+    const unsigned long long key = uint64_t(stripe) * k * L + bi.c0;
+    const uint16_t* rxp = launder(rx + key);
+    uint32_t* yp = launder(Y + (uint64_t(bi.sb) * N) * L + bi.c0);
+    const bool esc_any = esc_in.n != 0;
+
+    auto ld = [&](uint32_t i1, uint32_t, int, uint32_t col) -> uint32_t {
+        const uint2 m = __ldg(rm + i1 * N2 + i2);  // erased: {~0, 0}
+        const uint32_t row = m.x == 0xFFFFFFFFu ? 0u : m.x;
+        return mulw2(uint32_t(rxp[row * L + col]), m.y, m.y * 65535u);
+    };
+    auto fix = [&](uint32_t (&v)[R0], uint32_t base, uint32_t, uint32_t col) {
+        if (!esc_any || !any_zero(v)) return;
+#pragma unroll
+        for (int q = 0; q < R0; ++q) {
+            if (v[q] != 0u) continue;
+            const uint2 m = __ldg(rm + (base + (uint32_t(q) << S::slog(0))) * N2 + i2);
+            if (m.x != 0xFFFFFFFFu && rxp[m.x * L + col] == 0u && esc_has(esc_in, key + uint64_t(m.x) * L + col))
+                v[q] = mulw2(65536u, m.y, m.y * 65535u);
+        }
+    };
+    auto st_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col, uint32_t y) -> uint32_t {
+        work[G::idx(lrow, col)] = y;
+        return 0u;
+    };
+    auto ld_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t { return work[G::idx(lrow, col)]; };
+    auto st_y = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) -> uint32_t {
+        const uint32_t m1 = perm_head<E1>(b) + (uint32_t(s) << (E1 - RLZ));
+        const uint2 w = __ldg(bigF + N + ((i2 * m1) & (N - 1)));
+        yp[(m1 * N2 + i2) * L + col] = mulw2(y, w.x, w.y);
+        return 0u;
+    };
+    pass<E1, 0, false, false, k2P, kSmemCap, G>(pass_table(ptab, S::llog(0)), ld, st_sm, fix);
+    __syncthreads();
+    pass<E1, 1, false, false, kSmemCap, kSmemCap, G>(pass_table(ptab, S::llog(1)), ld_sm, st_y);
+}
+
+template <int E1, int E2, bool HALFK>
+__global__ void __launch_bounds__(kLNT, LG<E2>::MINB)
+dec_2_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, uint32_t k, uint32_t L, uint32_t tps,
+             const uint32_t* __restrict__ Y1, uint32_t* __restrict__ Y2) {
+    using G = LG<E2>;
+    using S = Sched<E2>;
+    constexpr uint32_t N1 = 1u << E1, N2 = 1u << E2, N = N1 * N2;
+    constexpr int RLZ = G::RLZ, RZ = 1 << RLZ;
+    constexpr uint32_t FLIP = N2 - 1;
+    constexpr int LGW = ilog2c<kLW>();
+    extern __shared__ __align__(128) uint32_t work[];
+    const BlockIdx bi = block_index(tps, N1);
+    const uint32_t m1 = bi.g, i1p = N1 - 1 - m1;
+    const uint32_t* y1 = launder(Y1 + (uint64_t(bi.sb) * N + m1 * N2) * L + bi.c0);
+    uint32_t* y2 = launder(Y2 + (uint64_t(bi.sb) * N) * L + bi.c0);
+
+    auto ld = [&](uint32_t i2, uint32_t, int, uint32_t col) -> uint32_t { return y1[i2 * L + col]; };
+    auto st_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col, uint32_t y) -> uint32_t {
+        work[G::idx(lrow, col)] = y;
+        return 0u;
+    };
+    auto ld_smf = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t {
+        return work[G::idx(lrow ^ FLIP, col)];
+    };
+    auto st_y2 = [&](uint32_t q2, uint32_t, int, uint32_t col, uint32_t y) -> uint32_t {
+        const uint2 w = __ldg(bigF + N + ((i1p * q2) & (N - 1)));
+        y2[(q2 * N1 + i1p) * L + col] = mulw2(y, w.x, w.y);
+        return 0u;
+    };
+    // FNT1 pass B, first radix pass
+    pass<E2, 0, false, false, k2P, kSmemCap, G>(pass_table(ptab, S::llog(0)), ld, st_sm);
+    __syncthreads();
+    // FNT1 pass B last radix pass + FNT2 pass A first DIT pass (reversed view over i2' = N2-1-m2,
+    // s'_{i1' + N1 i2'} zeroed when i1' + N1 i2' >= k)
+    {
+        constexpr int ITEMS = (int(N2) / RZ) * kLW;
+        constexpr uint64_t BD = dif_bound<RZ, false, kSmemCap>();
+        constexpr uint64_t BT = dit_bound<RZ, false, BD>();
+#pragma unroll 1
+        for (int it = threadIdx.x; it < ITEMS; it += kLNT) {
+            const uint32_t col = uint32_t(it) & uint32_t(kLW - 1);
+            const uint32_t g = uint32_t(it) >> LGW;
+            uint32_t v[RZ];
+#pragma unroll
+            for (int q = 0; q < RZ; ++q) v[q] = work[G::idx((g << RLZ) + q, col)];
+            dif_regs<RZ, false, kSmemCap>(v);
+            const uint32_t fh = perm_head<E2>(N2 / RZ - 1u - g);
+            uint32_t u[RZ];
+#pragma unroll
+            for (int j = 0; j < RZ; ++j) {
+                const uint32_t i2p = fh + (uint32_t(rev<RZ>(j)) << (E2 - RLZ));
+                const bool live = HALFK ? ((j & 1) == 0) : (i1p + N1 * i2p < k);
+                u[j] = live ? v[RZ - 1 - j] : 0u;
+            }
+            dit_regs<RZ, false, BD>(u);
+#pragma unroll
+            for (int q = 0; q < RZ; ++q) work[G::idx((g << RLZ) + (RZ - 1 - q), col)] = cap<BT, kSmemCap>(u[q]);
+        }
+    }
+    __syncthreads();
+    // FNT2 pass A last DIT pass -> natural q2, four-step twiddle r_N^(i1' q2)
+    pass<E2, 0, false, true, kSmemCap, kSmemCap, G>(pass_table(ptab, S::llog(0)), ld_smf, st_y2);
+}
+
+template <int E1, int E2>
+__global__ void __launch_bounds__(kLNT, LG<E1>::MINB)
+dec_3_kernel(const uint2* __restrict__ ptabF, const uint2* __restrict__ ptabI, const uint2* __restrict__ bigI,
+             const uint2* __restrict__ ahat2, uint32_t L, uint32_t tps, uint32_t stripe0,
+             const uint32_t* __restrict__ stripe_pattern, const uint32_t* __restrict__ Y2, uint32_t* __restrict__ Y3) {
+    using G = LG<E1>;
+    using S = Sched<E1>;
+    constexpr uint32_t N1 = 1u << E1, N2 = 1u << E2, N = N1 * N2;
+    constexpr int RLZ = G::RLZ, RZ = 1 << RLZ;
+    constexpr int LGW = ilog2c<kLW>();
+    extern __shared__ __align__(128) uint32_t work[];
+    const BlockIdx bi = block_index(tps, N2);
+    const uint32_t q2 = bi.g, stripe = stripe0 + bi.sb;
+    const uint2* __restrict__ ah = ahat2 + size_t(__ldg(stripe_pattern + stripe)) * N;
+    const uint32_t* y2 = launder(Y2 + (uint64_t(bi.sb) * N + q2 * N1) * L + bi.c0);
+    uint32_t* y3 = launder(Y3 + (uint64_t(bi.sb) * N) * L + bi.c0);
+
+    auto ld = [&](uint32_t i1p, uint32_t, int, uint32_t col) -> uint32_t { return y2[i1p * L + col]; };
+    auto st_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col, uint32_t y) -> uint32_t {
+        work[G::idx(lrow, col)] = y;
+        return 0u;
+    };
+    auto ld_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t { return work[G::idx(lrow, col)]; };
+    auto st_y3 = [&](uint32_t t1, uint32_t, int, uint32_t col, uint32_t y) -> uint32_t {
+        const uint2 w = __ldg(bigI + N + ((q2 * t1) & (N - 1)));
+        y3[(t1 * N2 + q2) * L + col] = mulw2(y, w.x, w.y);
+        return 0u;
+    };
+    // FNT2 pass B, first radix pass
+    pass<E1, 0, false, false, k2P, kSmemCap, G>(pass_table(ptabF, S::llog(0)), ld, st_sm);
+    __syncthreads();
+    // FNT2 pass B last radix pass + (. ahat at q2 + N2 q1) + FNT3 pass A first DIT pass (inverse)
+    {
+        constexpr int ITEMS = (int(N1) / RZ) * kLW;
+        constexpr uint64_t BT = dit_bound<RZ, true, k2P>();
+#pragma unroll 1
+        for (int it = threadIdx.x; it < ITEMS; it += kLNT) {
+            const uint32_t col = uint32_t(it) & uint32_t(kLW - 1);
+            const uint32_t g = uint32_t(it) >> LGW;
+            uint32_t v[RZ];
+#pragma unroll
+            for (int q = 0; q < RZ; ++q) v[q] = work[G::idx((g << RLZ) + q, col)];
+            dif_regs<RZ, false, kSmemCap>(v);  // v[rev(s)] = X2 at q1 = fh + s * N1/RZ
+            const uint32_t fh = perm_head<E1>(g);
+#pragma unroll
+            for (int s = 0; s < RZ; ++s) {
+                const uint32_t q1 = fh + (uint32_t(s) << (E1 - RLZ));
+                const uint2 a = __ldg(ah + q2 + N2 * q1);
+                v[rev<RZ>(s)] = mulw2(v[rev<RZ>(s)], a.x, a.y);  // DIT input order: u[rev(s)] = x_s
+            }
+            dit_regs<RZ, true, k2P>(v);
+#pragma unroll
+            for (int q = 0; q < RZ; ++q) work[G::idx((g << RLZ) + q, col)] = cap<BT, kSmemCap>(v[q]);
+        }
+    }
+    __syncthreads();
+    // FNT3 pass A last DIT pass (inverse) -> natural t1, twiddle r_N^(-q2 t1)
+    pass<E1, 0, true, true, kSmemCap, kSmemCap, G>(pass_table(ptabI, S::llog(0)), ld_sm, st_y3);
+}
+
+template <int E1, int E2, bool HALFK>
+__global__ void __launch_bounds__(kLNT, LG<E2>::MINB)
+dec_4_kernel(const uint2* __restrict__ ptabI, uint32_t k, uint32_t L, uint32_t tps, uint32_t stripe0,
+             const uint32_t* __restrict__ Y3, uint16_t* __restrict__ out, EscOut esc_out) {
+    using G = LG<E2>;
+    using S = Sched<E2>;
+    constexpr uint32_t N1 = 1u << E1, N2 = 1u << E2, N = N1 * N2;
+    constexpr int RLZ = G::RLZ, RZ = 1 << RLZ;
+    extern __shared__ __align__(128) uint32_t work[];
+    const BlockIdx bi = block_index(tps, N1);
+    const uint32_t t1 = bi.g, stripe = stripe0 + bi.sb;
+    const uint32_t* y3 = launder(Y3 + (uint64_t(bi.sb) * N + t1 * N2) * L + bi.c0);
+    const unsigned long long key = uint64_t(stripe) * k * L + bi.c0;
+    uint16_t* outp = launder(out + key);
+
+    auto ld = [&](uint32_t i2, uint32_t, int, uint32_t col) -> uint32_t { return y3[i2 * L + col]; };
+    auto st_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col, uint32_t y) -> uint32_t {
+        work[G::idx(lrow, col)] = y;
+        return 0u;
+    };
+    auto ld_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t { return work[G::idx(lrow, col)]; };
+    auto st_out = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) -> uint32_t {
+        const uint32_t row = t1 + N1 * (perm_head<E2>(b) + (uint32_t(s) << (E2 - RLZ)));
+        const bool keep = HALFK ? (s < RZ / 2) : (row < k);
+        y = red2p(y);
+        if (keep) __stcs(outp + (row * L + col), uint16_t(y));
+        return (y == 65536u && keep) ? 1u : 0u;
+    };
+    auto flush = [&](uint32_t mask, uint32_t, uint32_t b, uint32_t col) {
+        if (!mask) return;
+#pragma unroll 1
+        for (int s = 0; s < 16; ++s)
+            if (mask & (1u << s))
+                emit_escape(esc_out, key + uint64_t(t1 + N1 * (perm_head<E2>(b) + (uint32_t(s) << (E2 - RLZ)))) * L + col);
+    };
+    pass<E2, 0, true, false, k2P, kSmemCap, G>(pass_table(ptabI, S::llog(0)), ld, st_sm);
+    __syncthreads();
+    pass<E2, 1, true, false, kSmemCap, k2P, G>(pass_table(ptabI, S::llog(1)), ld_sm, st_out, NoFix(), flush);
+}
+
+template <class K>
+cudaError_t prep(K kernel, size_t smem) {
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+}
+
+template <int E1, int E2>
+cudaError_t run_encode(const FastTables& t, uint32_t k, uint32_t n, uint32_t stripes, uint32_t L, const uint16_t* src,
+                       EscIn ein, uint16_t* out, EscOut eout, uint32_t* Y, uint32_t batch, cudaStream_t st) {
+    constexpr uint32_t N1 = 1u << E1, N2 = 1u << E2, N = N1 * N2;
+    const uint32_t tps = L / kLW;
+    const size_t smA = size_t(N1) * kLW * 4, smB = size_t(N2) * kLW * 4;
+    const bool half = k == N / 2, punct = n < N;
+    auto ka = half ? enc_a_kernel<E1, E2, true> : enc_a_kernel<E1, E2, false>;
+    auto kb = punct ? enc_b_kernel<E1, E2, true> : enc_b_kernel<E1, E2, false>;
+    cudaError_t err;
+    if ((err = prep(ka, smA)) || (err = prep(kb, smB))) return err;
+    for (uint32_t s0 = 0; s0 < stripes; s0 += batch) {
+        const uint32_t sb = stripes - s0 < batch ? stripes - s0 : batch;
+        ka<<<sb * N2 * tps, kLNT, smA, st>>>(t.ptab_fwd, t.big_fwd, k, L, tps, s0, src, ein, Y);
+        kb<<<sb * N1 * tps, kLNT, smB, st>>>(t.ptab_fwd, n, L, tps, s0, Y, out, eout);
+    }
+    return cudaGetLastError();
+}
+
+template <int E1, int E2>
+cudaError_t run_decode(const FastTables& t, const FastPlanView& pv, uint32_t stripes, uint32_t L, const uint32_t* sp,
+                       const uint16_t* rx, EscIn ein, uint16_t* out, EscOut eout, uint32_t* YA, uint32_t* YB,
+                       uint32_t batch, cudaStream_t st) {
+    constexpr uint32_t N1 = 1u << E1, N2 = 1u << E2, N = N1 * N2;
+    const uint32_t tps = L / kLW;
+    const size_t sm1 = size_t(N1) * kLW * 4, sm2 = size_t(N2) * kLW * 4;
+    const bool half = pv.k == N / 2;
+    auto k1 = dec_1_kernel<E1, E2>;
+    auto k2 = half ? dec_2_kernel<E1, E2, true> : dec_2_kernel<E1, E2, false>;
+    auto k3 = dec_3_kernel<E1, E2>;
+    auto k4 = half ? dec_4_kernel<E1, E2, true> : dec_4_kernel<E1, E2, false>;
+    cudaError_t err;
+    if ((err = prep(k1, sm1)) || (err = prep(k2, sm2)) || (err = prep(k3, sm1)) || (err = prep(k4, sm2))) return err;
+    for (uint32_t s0 = 0; s0 < stripes; s0 += batch) {
+        const uint32_t sb = stripes - s0 < batch ? stripes - s0 : batch;
+        k1<<<sb * N2 * tps, kLNT, sm1, st>>>(t.ptab_fwd, t.big_fwd, pv.rowmap, pv.k, L, tps, s0, sp, rx, ein, YA);
+        k2<<<sb * N1 * tps, kLNT, sm2, st>>>(t.ptab_fwd, t.big_fwd, pv.k, L, tps, YA, YB);
+        k3<<<sb * N2 * tps, kLNT, sm1, st>>>(t.ptab_fwd, t.ptab_inv, t.big_inv, pv.ahat2, L, tps, s0, sp, YB, YA);
+        k4<<<sb * N1 * tps, kLNT, sm2, st>>>(t.ptab_inv, pv.k, L, tps, s0, YA, out, eout);
+    }
+    return cudaGetLastError();
+}
+
+__global__ void big_tables_kernel(uint2* fwd, uint2* inv) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0 || i >= (1u << 17)) return;
+    const int e = 31 - __clz(i);
+    const uint32_t j = i - (1u << e);
+    const uint32_t ex = (j << (16 - e)) & 0xFFFFu;
+    const uint32_t wf = gpow(3u, ex), wi = gpow(3u, (65536u - ex) & 0xFFFFu);
+    fwd[i] = make_uint2(wf, wf * 65535u);
+    inv[i] = make_uint2(wi, wi * 65535u);
+}
+
+}  // namespace
+
+cudaError_t build_large_tables(FastTables& t, cudaStream_t st) {
+    cudaError_t err = cudaMalloc(&t.big_fwd, sizeof(uint2) << 17);
+    if (err) return err;
+    if ((err = cudaMalloc(&t.big_inv, sizeof(uint2) << 17))) return err;
+    big_tables_kernel<<<(1u << 17) / 256, 256, 0, st>>>(t.big_fwd, t.big_inv);
+    return cudaGetLastError();
+}
+
+int large_supported(uint32_t N) { return N >= 8192 && N <= 65536 && (N & (N - 1)) == 0; }
+uint32_t large_tile_columns() { return kLW; }
+
+uint32_t large_batch(uint32_t N, uint32_t L, size_t scratch_bytes) {
+    const size_t per = size_t(N) * L * 4;
+    const size_t b = scratch_bytes / per;
+    return b < 1 ? 1u : (b > 0xFFFFu ? 0xFFFFu : uint32_t(b));
+}
+
+cudaError_t launch_encode_large(const FastTables& t, uint32_t k, uint32_t n, uint32_t N, uint32_t stripes, uint32_t L,
+                                const uint16_t* src, EscIn ein, uint16_t* out, EscOut eout, uint32_t* Y,
+                                uint32_t batch, cudaStream_t st) {
+    switch (N) {
+        case 8192: return run_encode<7, 6>(t, k, n, stripes, L, src, ein, out, eout, Y, batch, st);
+        case 16384: return run_encode<7, 7>(t, k, n, stripes, L, src, ein, out, eout, Y, batch, st);
+        case 32768: return run_encode<8, 7>(t, k, n, stripes, L, src, ein, out, eout, Y, batch, st);
+        case 65536: return run_encode<8, 8>(t, k, n, stripes, L, src, ein, out, eout, Y, batch, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_decode_large(const FastTables& t, const FastPlanView& pv, uint32_t stripes, uint32_t L,
+                                const uint32_t* sp, const uint16_t* rx, EscIn ein, uint16_t* out, EscOut eout,
+                                uint32_t* YA, uint32_t* YB, uint32_t batch, cudaStream_t st) {
+    switch (pv.N) {
+        case 8192: return run_decode<7, 6>(t, pv, stripes, L, sp, rx, ein, out, eout, YA, YB, batch, st);
+        case 16384: return run_decode<7, 7>(t, pv, stripes, L, sp, rx, ein, out, eout, YA, YB, batch, st);
+        case 32768: return run_decode<8, 7>(t, pv, stripes, L, sp, rx, ein, out, eout, YA, YB, batch, st);
+        case 65536: return run_decode<8, 8>(t, pv, stripes, L, sp, rx, ein, out, eout, YA, YB, batch, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace fast
+}  // namespace fntrs_gpu

@@ -1,0 +1,179 @@
+// fft_pass.cuh -- shared device building blocks of the fused codec kernels:
+// escape helpers, tile geometry, and the generic radix pass over a shared
+// tile with load / store functors (see codec_fast.cu for the design).
+#pragma once
+#include <cstdint>
+
+#include "fft_fast.cuh"
+#include "internal.h"
+
+namespace fntrs_gpu {
+namespace fast {
+namespace {
+
+constexpr uint64_t kSmemCap = 1ull << 20;  // bound of values kept in shared memory
+constexpr uint64_t k2P = 2 * kP64;
+
+__device__ __noinline__ bool esc_find(const unsigned long long* keys, uint64_t n, unsigned long long key) {
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (keys[mid] < key)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo < n && keys[lo] == key;
+}
+__device__ __forceinline__ bool esc_has(const EscIn& e, unsigned long long key) { return esc_find(e.keys, e.n, key); }
+
+__device__ __noinline__ void esc_append(unsigned long long* keys, unsigned long long* count, uint64_t cap,
+                                        unsigned long long key) {
+    const unsigned long long i = atomicAdd(count, 1ull);
+    if (i < cap) keys[i] = key;
+}
+__device__ __forceinline__ void emit_escape(const EscOut& e, unsigned long long key) {
+    esc_append(e.keys, e.count, e.cap, key);
+}
+
+// opaque copy: keeps the per-tile base pointer in a register so per-symbol
+// addresses are one 32-bit offset away (no 64-bit re-association)
+template <class T>
+__device__ __forceinline__ T* launder(T* p) {
+    asm("mov.b64 %0, %0;" : "+l"(p));
+    return p;
+}
+
+template <int N>
+constexpr int ilog2c() {
+    int e = 0;
+    while ((1 << e) < N) ++e;
+    return e;
+}
+
+template <uint64_t B, uint64_t CAP>
+__device__ __forceinline__ uint32_t cap(uint32_t v) {
+    if constexpr (B > CAP)
+        return red(v);
+    else
+        return v;
+}
+
+// ---- geometry ---------------------------------------------------------------
+template <int E, int WT_, int NT_, int MINB_ = 1>
+struct Geom {
+    static constexpr int MINB = MINB_;
+    static constexpr int N = 1 << E;
+    static constexpr int WT = WT_;
+    static constexpr int NT = NT_;
+    static constexpr int RLZ = Sched<E>::rlog(Sched<E>::P - 1);
+    static constexpr int RPW = WT >= 32 ? 1 : 32 / WT;  // tile rows touched by one warp
+    // shared tile index with a row swizzle keeping the sub = 1 passes
+    // (rows R*b + q, consecutive b in one warp) on distinct banks
+    __device__ __forceinline__ static uint32_t idx(uint32_t row, uint32_t col) {
+        if constexpr (RPW > 1)
+            row ^= (row >> RLZ) & uint32_t(RPW - 1);
+        return row * WT + col;
+    }
+};
+
+// tile width / threads per size
+template <int E>
+struct Pick {
+    static constexpr int N = 1 << E;
+    static constexpr int WT = N <= 512 ? 32 : (N == 1024 ? 16 : 8);
+    static constexpr int NT = N == 4096 ? 512 : 256;
+    // blocks per SM the register budget should allow (shared memory permits 4 at N <= 512)
+    static constexpr int MINB = N <= 512 ? 4 : (N <= 2048 ? 2 : 1);
+    using G = Geom<E, WT, NT, MINB>;
+};
+
+// ---- generic pass (one codeword per work item) ----------------------------
+// DIF (DIT=false) or DIT pass with the geometry of DIF pass p of a size-2^E
+// transform. Loaded values must be below BIN; stored values are below OCAP.
+// twp: per-pass twiddle table, row t holds {r_len^(t s), 65535 r_len^(t s)}
+// for s < R (only read when sub > 1).
+struct NoFix {
+    template <int R>
+    __device__ __forceinline__ void operator()(uint32_t (&)[R], uint32_t, uint32_t, uint32_t) const {}
+};
+struct NoFlush {
+    __device__ __forceinline__ void operator()(uint32_t, uint32_t, uint32_t, uint32_t) const {}
+};
+
+template <int E, int p, bool INV, bool DIT, uint64_t BIN, uint64_t OCAP, class G, class LD, class ST,
+          class FIX = NoFix, class FLUSH = NoFlush>
+__device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld, const ST& st, const FIX& fix = FIX(),
+                                     const FLUSH& flush = FLUSH()) {
+    using S = Sched<E>;
+    constexpr int RL = S::rlog(p), R = 1 << RL, LL = S::llog(p), SL = S::slog(p);
+    constexpr int ITEMS = (1 << (E - RL)) * G::WT;
+    constexpr int LGW = ilog2c<G::WT>();
+    static_assert(OCAP >= k2P, "");
+#pragma unroll 1
+    for (int it = threadIdx.x; it < ITEMS; it += G::NT) {
+        const uint32_t col = uint32_t(it) & uint32_t(G::WT - 1);
+        const uint32_t b = uint32_t(it) >> LGW;
+        const uint32_t t = b & ((1u << SL) - 1u);
+        const uint32_t base = ((b >> SL) << LL) + t;
+        uint32_t v[R];
+        const uint2* tp = reinterpret_cast<const uint2*>(twp) + t * R;  // row t: r_len^(t s), s < R
+        uint32_t mask = 0;
+        if constexpr (!DIT) {
+#pragma unroll
+            for (int q = 0; q < R; ++q) v[q] = ld(base + (uint32_t(q) << SL), b, q, col);
+            fix(v, base, b, col);
+            dif_regs<R, INV, BIN>(v);
+            constexpr uint64_t BO = dif_bound<R, INV, BIN>();
+#pragma unroll
+            for (int s = 0; s < R; ++s) {
+                uint32_t y = v[rev<R>(s)];
+                if (SL > 0 && s > 0) {
+                    const uint2 w = __ldg(tp + s);
+                    y = mulw2(y, w.x, w.y);
+                } else {
+                    y = cap<BO, OCAP>(y);
+                }
+                mask |= st(base + (uint32_t(s) << SL), b, s, col, y) << s;
+            }
+        } else {
+            constexpr uint64_t BI = BIN > k2P ? BIN : k2P;
+#pragma unroll
+            for (int s = 0; s < R; ++s) {
+                uint32_t x = ld(base + (uint32_t(s) << SL), b, s, col);
+                if (SL > 0 && s > 0) {
+                    const uint2 w = __ldg(tp + s);
+                    x = mulw2(x, w.x, w.y);
+                }
+                v[rev<R>(s)] = x;
+            }
+            dit_regs<R, INV, BI>(v);
+            constexpr uint64_t BO = dit_bound<R, INV, BI>();
+#pragma unroll
+            for (int q = 0; q < R; ++q) mask |= st(base + (uint32_t(q) << SL), b, q, col, cap<BO, OCAP>(v[q])) << q;
+        }
+        flush(mask, base, b, col);
+    }
+}
+
+// Per-pass twiddle tables for one direction: table for block length 2^LL at
+// uint2 offset 2^LL (LL <= 12): entry t*16 + s = r_len^(t s).
+__device__ __forceinline__ const uint4* pass_table(const uint2* base, int LL) {
+    return reinterpret_cast<const uint4*>(base + (1u << LL));
+}
+
+// Escapes are rare (1 in 65537 symbols): loads and stores test a whole
+// butterfly group at once and only a group holding a zero word / a 65536
+// takes the slow path (one branch per group instead of one per symbol).
+template <int R>
+__device__ __forceinline__ bool any_zero(const uint32_t (&v)[R]) {
+    uint32_t m = v[0];
+#pragma unroll
+    for (int i = 1; i < R; ++i) m = min(m, v[i]);
+    return m == 0u;
+}
+
+
+}  // namespace
+}  // namespace fast
+}  // namespace fntrs_gpu

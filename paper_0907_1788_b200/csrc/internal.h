@@ -71,6 +71,8 @@ namespace fast {
 struct FastTables {
     uint2* ptab_fwd = nullptr;  // per-pass twiddles {w, 65535 w}: [2^LL + 16 t + s] = r_(2^LL)^(t s)
     uint2* ptab_inv = nullptr;
+    uint2* big_fwd = nullptr;   // {r_m^j, 65535 r_m^j} at [m + j], m <= 65536 (four-step twiddles)
+    uint2* big_inv = nullptr;
 };
 struct FastPlanView {
     uint32_t N, k;
@@ -88,6 +90,18 @@ cudaError_t launch_decode_fast(const FastTables& t, const FastPlanView& pv, uint
 cudaError_t launch_fast_plan_tables(uint32_t N, uint32_t kp, uint32_t npatterns, const uint32_t* pos,
                                     const uint32_t* ainv, const uint32_t* ahat, uint2* rowmap, uint2* ahat2,
                                     cudaStream_t st);
+
+// ---- four-step path (codec_large.cu): 8192 <= N <= 65536, L a multiple of 64
+cudaError_t build_large_tables(FastTables& t, cudaStream_t st);
+int large_supported(uint32_t N);
+uint32_t large_tile_columns();
+uint32_t large_batch(uint32_t N, uint32_t L, size_t scratch_bytes);  // stripes per scratch buffer
+cudaError_t launch_encode_large(const FastTables& t, uint32_t k, uint32_t n, uint32_t N, uint32_t stripes, uint32_t L,
+                                const uint16_t* src, EscIn ein, uint16_t* out, EscOut eout, uint32_t* Y,
+                                uint32_t batch, cudaStream_t st);
+cudaError_t launch_decode_large(const FastTables& t, const FastPlanView& pv, uint32_t stripes, uint32_t L,
+                                const uint32_t* sp, const uint16_t* rx, EscIn ein, uint16_t* out, EscOut eout,
+                                uint32_t* YA, uint32_t* YB, uint32_t batch, cudaStream_t st);
 }  // namespace fast
 
 }  // namespace fntrs_gpu

@@ -124,6 +124,9 @@ SHAPES = [  # (k, n, L, stripes)
     # fused v2 kernels (n_domain 32..4096, L a multiple of the tile width), incl. k != n/2
     (16, 32, 64, 3), (100, 256, 64, 2), (50, 256, 64, 1), (300, 512, 64, 2), (1500, 4096, 16, 1),
     (700, 2048, 32, 1), (512, 1000, 64, 1),
+    # four-step kernels (n_domain 8192..65536, L a multiple of 64)
+    (4096, 8192, 64, 2), (8192, 16384, 64, 2), (16384, 32768, 64, 1), (32768, 65536, 64, 1),
+    (5000, 12000, 64, 1), (3000, 8192, 128, 1),
 ]
 
 
