@@ -258,7 +258,7 @@ def test_config_c1_bit_exact_vs_reference(codec, oracle):
     assert escapes_to_numpy(de, dc).size == 0
 
 
-@pytest.mark.parametrize("name,stripes", [("C2", 512), ("C5", 16)])
+@pytest.mark.parametrize("name,stripes", [("C2", 512), ("C5", 16), ("C3", 1), ("C4", 6)])
 def test_config_roundtrip_sampled(codec, oracle, name, stripes):
     """decode(encode(s)) == s on device for a sample of the config's stripes, plus
     bit-exact encode against the oracle on the first two stripes."""
@@ -269,14 +269,27 @@ def test_config_roundtrip_sampled(codec, oracle, name, stripes):
     out, oe, cnt = codec.encode(cfg.k, cfg.n, dev_u16(src))
     enc = host_u16(out)
     enc_esc = escapes_to_numpy(oe, cnt)
-    want, want_esc = oracle.encode_stripes(cfg.k, cfg.n, src[:2])
-    assert np.array_equal(enc[:2], want)
-    assert np.array_equal(enc_esc[enc_esc < np.uint64(2 * cfg.n * cfg.L)], want_esc)
+    # bit-exact against the oracle on the first stripe(s), a column sample for the long codes
+    ns = min(2, stripes)
+    cols = slice(0, cfg.L) if cfg.n <= 4096 else slice(0, 64)
+    sub = np.ascontiguousarray(src[:ns, :, cols])
+    want, want_esc = oracle.encode_stripes(cfg.k, cfg.n, sub)
+    assert np.array_equal(enc[:ns, :, cols], want)
+    Lc = sub.shape[2]
+    got_esc = [e for e in enc_esc if e < ns * cfg.n * cfg.L and (e % cfg.L) < Lc]
+    want_esc_full = [int(e // Lc) * cfg.L + int(e % Lc) for e in want_esc]
+    assert [int(e) for e in got_esc] == want_esc_full
     pats, sp = W.patterns(cfg, stripes=stripes)
     rx, rxe = gather_received(enc, enc_esc, pats, sp)
     plans = codec.plans(cfg.k, cfg.n, pats)
     dec, de, dc = codec.decode(plans, torch.from_numpy(sp.view(np.int32)).cuda(), dev_u16(rx), dev_esc(rxe))
-    assert np.array_equal(host_u16(dec), src)
+    got = host_u16(dec)
+    assert np.array_equal(got, src)
+    # decode bit-exact against the oracle on a column sample of the first stripe, from the same input
+    rx0 = np.ascontiguousarray(rx[:1, :, :16])
+    e0 = [int(e // cfg.L) * 16 + int(e % cfg.L) for e in rxe if e < cfg.k * cfg.L and e % cfg.L < 16]
+    want_dec, _ = oracle.decode_stripes(cfg.k, cfg.n, pats, sp[:1], rx0, np.array(e0, dtype=np.uint64))
+    assert np.array_equal(got[:1, :, :16], want_dec)
 
 
 def test_device_generator_matches_numpy(codec):
