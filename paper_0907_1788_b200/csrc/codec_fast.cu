@@ -141,9 +141,17 @@ __global__ void __launch_bounds__(G::NT, G::MINB) dec_fast_kernel(const __grid_c
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t bars[2];
     uint32_t* work = reinterpret_cast<uint32_t*>(smem_raw);
-    uint16_t* stage0 = reinterpret_cast<uint16_t*>(smem_raw + size_t(N) * WT * 4);
+    // [guard | stage 0 | guard | stage 1]: each guard is the WT-symbol row just
+    // below its stage (an erased position's row index ~0 wraps onto it) and
+    // holds ones, so raw received words can be tested for zero unmasked.
     const uint32_t stage_elems = nbox * box_rows * WT;
     const uint32_t stage_bytes = stage_elems * 2;
+    uint16_t* stage0 = reinterpret_cast<uint16_t*>(smem_raw + size_t(N) * WT * 4 + kGuardBytes);
+    const uint32_t stage_stride = stage_elems + kGuardBytes / 2;
+    for (uint32_t i = threadIdx.x; i < uint32_t(WT); i += NT) {
+        stage0[i - WT] = 1;
+        stage0[stage_stride + i - WT] = 1;
+    }
     if (threadIdx.x == 0) {
         tma_prefetch_desc(&rx_map);
         mbar_init(&bars[0], 1);
@@ -156,7 +164,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) dec_fast_kernel(const __grid_c
         const uint32_t cc = (tl - s1 * tps) * WT;
         fence_proxy_async();
         mbar_expect_tx(&bars[bs], stage_bytes);
-        uint16_t* dst = stage0 + bs * stage_elems;
+        uint16_t* dst = stage0 + bs * stage_stride;
         for (uint32_t j = 0; j < nbox; ++j)
             tma_load_2d(dst + j * box_rows * WT, &rx_map, int(cc), int(s1 * k + j * box_rows), &bars[bs]);
     };
@@ -176,18 +184,22 @@ __global__ void __launch_bounds__(G::NT, G::MINB) dec_fast_kernel(const __grid_c
         const unsigned long long key = uint64_t(stripe) * k * L + c0;
         uint16_t* outp = launder(out + key);
         mbar_wait(&bars[bsel], (iter >> 1) & 1);
-        const uint16_t* st_in = stage0 + bsel * stage_elems;
+        const uint16_t* st_in = stage0 + bsel * stage_stride;
 
-        // step 4: N'[z] = v_i / A'(x_i) where z = z_i, else 0. A received
-        // zero word may be an escaped 65536: the group fix-up re-scales it.
+        // step 4: N'[z] = v_i / A'(x_i) where z = z_i, else 0 (rowmap {~0, 0}:
+        // reads the guard row of ones, scales by 0). A received zero word may
+        // be an escaped 65536: the group fix-up re-scales it.
+        uint32_t zmin = 0xFFFFFFFFu;
         auto ld_scatter = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t {
-            const uint2 m = __ldg(rm + lrow);  // erased: {~0, 0} -> reads row 0, scales by 0
-            const uint32_t row = m.x == 0xFFFFFFFFu ? 0u : m.x;
-            return mulw2(uint32_t(st_in[row * WT + col]), m.y, m.y * 65535u);
+            const uint2 m = __ldg(rm + lrow);
+            const uint32_t raw = st_in[int(m.x * uint32_t(WT) + col)];
+            zmin = min(zmin, raw);
+            return mulw2(raw, m.y, m.y * 65535u);
         };
         auto fix_scatter = [&](uint32_t (&v)[R0], uint32_t base, uint32_t, uint32_t col) {
-            if (!esc_any) return;
-            if (!any_zero(v)) return;
+            const bool any = zmin == 0u;
+            zmin = 0xFFFFFFFFu;
+            if (!esc_any || !any) return;
 #pragma unroll
             for (int q = 0; q < R0; ++q) {
                 if (v[q] != 0u) continue;
@@ -382,14 +394,15 @@ struct LaunchShape {
 };
 
 template <class K>
-cudaError_t shape_for(K kernel, int E, int wt, int nt, uint32_t k, uint32_t stripes, uint32_t L, LaunchShape& sh) {
+cudaError_t shape_for(K kernel, int E, int wt, int nt, uint32_t k, uint32_t stripes, uint32_t L, LaunchShape& sh,
+                      size_t extra = 0) {
     sh.tps = L / wt;
     const uint64_t tiles = uint64_t(stripes) * sh.tps;
     if (tiles > 0xFFFFFFFFull) return cudaErrorInvalidConfiguration;
     sh.tiles = uint32_t(tiles);
     sh.box_rows = k < 256 ? k : 256;
     sh.nbox = (k + sh.box_rows - 1) / sh.box_rows;
-    sh.smem = (size_t(1) << E) * wt * 4 + 2 * size_t(sh.nbox) * sh.box_rows * wt * 2;
+    sh.smem = (size_t(1) << E) * wt * 4 + 2 * size_t(sh.nbox) * sh.box_rows * wt * 2 + extra;
     cudaError_t err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sh.smem));
     if (err) return err;
     int dev = 0, sms = 0, per = 0;
@@ -425,7 +438,7 @@ cudaError_t launch_dec(const FastTables& t, const FastPlanView& pv, uint32_t str
     using G = typename Pick<E>::G;
     auto kern = pv.k == (1u << E) / 2 ? dec_fast_kernel<E, G, true> : dec_fast_kernel<E, G, false>;
     LaunchShape sh;
-    cudaError_t err = shape_for(kern, E, G::WT, G::NT, pv.k, stripes, L, sh);
+    cudaError_t err = shape_for(kern, E, G::WT, G::NT, pv.k, stripes, L, sh, 2 * kGuardBytes);
     if (err) return err;
     if (!sh.tiles) return cudaSuccess;
     CUtensorMap map;

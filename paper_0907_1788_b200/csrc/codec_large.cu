@@ -149,13 +149,18 @@ dec_1_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, con
     uint32_t* yp = launder(Y + (uint64_t(bi.sb) * N) * L + bi.c0);
     const bool esc_any = esc_in.n != 0;
 
+    uint32_t zflag = 0;  // a received (non-erased) zero word in this butterfly group
     auto ld = [&](uint32_t i1, uint32_t, int, uint32_t col) -> uint32_t {
         const uint2 m = __ldg(rm + i1 * N2 + i2);  // erased: {~0, 0}
         const uint32_t row = m.x == 0xFFFFFFFFu ? 0u : m.x;
-        return mulw2(uint32_t(rxp[row * L + col]), m.y, m.y * 65535u);
+        const uint32_t raw = rxp[row * L + col];
+        zflag |= (raw == 0u) & (m.y != 0u);
+        return mulw2(raw, m.y, m.y * 65535u);
     };
     auto fix = [&](uint32_t (&v)[R0], uint32_t base, uint32_t, uint32_t col) {
-        if (!esc_any || !any_zero(v)) return;
+        const uint32_t any = zflag;
+        zflag = 0;
+        if (!esc_any || !any) return;
 #pragma unroll
         for (int q = 0; q < R0; ++q) {
             if (v[q] != 0u) continue;

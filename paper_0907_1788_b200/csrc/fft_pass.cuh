@@ -13,6 +13,7 @@ namespace {
 
 constexpr uint64_t kSmemCap = 1ull << 20;  // bound of values kept in shared memory
 constexpr uint64_t k2P = 2 * kP64;
+constexpr uint32_t kGuardBytes = 128;  // guard row slot below each decode stage buffer
 
 __device__ __noinline__ bool esc_find(const unsigned long long* keys, uint64_t n, unsigned long long key) {
     uint64_t lo = 0, hi = n;
