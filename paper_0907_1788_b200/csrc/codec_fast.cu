@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) enc_fast_kernel(const __grid_c
         };
         auto st_out = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) -> uint32_t {
             const uint32_t f = perm_head<E>(b) + (uint32_t(s) << (E - RLZ));
-            y = red2p(y);
+            y = canon_s2p(y);
             if (!PUNCT || f < n) __stcs(outp + (f * L + col), uint16_t(y));
             return (y == 65536u && (!PUNCT || f < n)) ? 1u : 0u;
         };
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) dec_fast_kernel(const __grid_c
             const uint2 m = __ldg(rm + lrow);
             const uint32_t raw = st_in[int(m.x * uint32_t(WT) + col)];
             zmin = min(zmin, raw);
-            return mulw2(raw, m.y, m.y * 65535u);
+            return mulws(raw, m.y, m.y * 65535u);
         };
         auto fix_scatter = [&](uint32_t (&v)[R0], uint32_t base, uint32_t, uint32_t col) {
             const bool any = zmin == 0u;
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) dec_fast_kernel(const __grid_c
                 const uint2 m = __ldg(rm + base + (uint32_t(q) << SL0));
                 if (m.x != 0xFFFFFFFFu && st_in[m.x * WT + col] == 0u &&
                     esc_has(esc_in, key + uint64_t(m.x) * L + col))
-                    v[q] = mulw2(65536u, m.y, m.y * 65535u);
+                    v[q] = mulws(65536u, m.y, m.y * 65535u);
             }
         };
         auto ld_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t { return work[G::idx(lrow, col)]; };
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) dec_fast_kernel(const __grid_c
             const uint32_t f = perm_head<E>(b) + (uint32_t(s) << (E - RLZ));
             // k = N/2: kept iff s < R/2 (compile time after unrolling)
             const bool keep = HALFK ? (s < RZ / 2) : (f < k);
-            y = red2p(y);
+            y = canon_s2p(y);
             if (keep) __stcs(outp + (f * L + col), uint16_t(y));
             return (y == 65536u && keep) ? 1u : 0u;
         };
@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) dec_fast_kernel(const __grid_c
                     uint32_t x = work[G::idx((t + (uint32_t(s) << SL0)) ^ FLIP, col)];
                     if (s > 0) {
                         const uint2 w = __ldg(tpf + s);
-                        x = mulw2(x, w.x, w.y);
+                        x = mulws(x, w.x, w.y);
                     }
                     v[rev<R0>(s)] = x;
                 }
@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) dec_fast_kernel(const __grid_c
 #pragma unroll
                 for (int q = 0; q < R0; ++q) {
                     const uint2 a = __ldg(ah + t + (uint32_t(q) << SL0));
-                    v[q] = mulw2(v[q], a.x, a.y);
+                    v[q] = mulws(v[q], a.x, a.y);
                 }
                 dif_regs<R0, true, k2P>(v);
 #pragma unroll
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) dec_fast_kernel(const __grid_c
                     uint32_t y = v[rev<R0>(s)];
                     if (s > 0) {
                         const uint2 w = __ldg(tpi + s);
-                        y = mulw2(y, w.x, w.y);
+                        y = mulws(y, w.x, w.y);
                     } else {
                         y = cap<BO, kSmemCap>(y);
                     }
@@ -334,17 +334,17 @@ __global__ void ptab_kernel(uint2* fwd, uint2* inv) {
     const int LL = 31 - __clz(i);
     const uint32_t j = i - (1u << LL), t = j >> 4, s = j & 15u;
     const uint32_t ex = ((t * s) << (16 - LL)) & 0xFFFFu;  // r_len = 3^(65536/len)
-    const uint32_t wf = gpow(3u, ex), wi = gpow(3u, (65536u - ex) & 0xFFFFu);
-    fwd[i] = make_uint2(wf, wf * 65535u);
-    inv[i] = make_uint2(wi, wi * 65535u);
+    const int32_t wf = balanced(gpow(3u, ex)), wi = balanced(gpow(3u, (65536u - ex) & 0xFFFFu));
+    fwd[i] = make_uint2(uint32_t(wf), uint32_t(wf * 65535));
+    inv[i] = make_uint2(uint32_t(wi), uint32_t(wi * 65535));
 }
 
 __global__ void fast_plan_tables_kernel(uint32_t N, const uint32_t* __restrict__ ahat, uint2* __restrict__ rowmap,
                                         uint2* __restrict__ ahat2, uint64_t total) {
     for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < total; j += uint64_t(gridDim.x) * blockDim.x) {
         rowmap[j] = make_uint2(0xFFFFFFFFu, 0u);
-        const uint32_t a = ahat[j];
-        ahat2[j] = make_uint2(a, a * 65535u);
+        const int32_t a = balanced(ahat[j]);  // signed Shoup pair
+        ahat2[j] = make_uint2(uint32_t(a), uint32_t(a * 65535));
     }
 }
 
@@ -353,7 +353,7 @@ __global__ void fast_plan_scatter_kernel(uint32_t N, uint32_t kp, const uint32_t
     for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < total; j += uint64_t(gridDim.x) * blockDim.x) {
         const uint64_t p = j / kp;
         const uint32_t i = uint32_t(j - p * kp);
-        rowmap[p * N + pos[j]] = make_uint2(i, ainv[j]);
+        rowmap[p * N + pos[j]] = make_uint2(i, uint32_t(balanced(ainv[j])));
     }
 }
 

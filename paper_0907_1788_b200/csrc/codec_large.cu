@@ -81,7 +81,7 @@ enc_a_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, uin
     auto st_y = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) -> uint32_t {
         const uint32_t m1 = perm_head<E1>(b) + (uint32_t(s) << (E1 - RLZ));
         const uint2 w = __ldg(bigF + N + ((i2 * m1) & (N - 1)));
-        yp[(m1 * N2 + i2) * L + col] = mulw2(y, w.x, w.y);
+        yp[(m1 * N2 + i2) * L + col] = mulws(y, w.x, w.y);
         return 0u;
     };
     pass<E1, 0, false, false, kP64, kSmemCap, G>(pass_table(ptab, S::llog(0)), ld, st_sm, fix);
@@ -112,7 +112,7 @@ enc_b_kernel(const uint2* __restrict__ ptab, uint32_t n, uint32_t L, uint32_t tp
     auto ld_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t { return work[G::idx(lrow, col)]; };
     auto st_out = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) -> uint32_t {
         const uint32_t row = m1 + N1 * (perm_head<E2>(b) + (uint32_t(s) << (E2 - RLZ)));
-        y = red2p(y);
+        y = canon_s2p(y);
         const bool keep = !PUNCT || row < n;
         if (keep) __stcs(outp + (row * L + col), uint16_t(y));
         return (y == 65536u && keep) ? 1u : 0u;
@@ -155,7 +155,7 @@ dec_1_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, con
         const uint32_t row = m.x == 0xFFFFFFFFu ? 0u : m.x;
         const uint32_t raw = rxp[row * L + col];
         zflag |= (raw == 0u) & (m.y != 0u);
-        return mulw2(raw, m.y, m.y * 65535u);
+        return mulws(raw, m.y, m.y * 65535u);
     };
     auto fix = [&](uint32_t (&v)[R0], uint32_t base, uint32_t, uint32_t col) {
         const uint32_t any = zflag;
@@ -166,7 +166,7 @@ dec_1_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, con
             if (v[q] != 0u) continue;
             const uint2 m = __ldg(rm + (base + (uint32_t(q) << S::slog(0))) * N2 + i2);
             if (m.x != 0xFFFFFFFFu && rxp[m.x * L + col] == 0u && esc_has(esc_in, key + uint64_t(m.x) * L + col))
-                v[q] = mulw2(65536u, m.y, m.y * 65535u);
+                v[q] = mulws(65536u, m.y, m.y * 65535u);
         }
     };
     auto st_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col, uint32_t y) -> uint32_t {
@@ -177,7 +177,7 @@ dec_1_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, con
     auto st_y = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) -> uint32_t {
         const uint32_t m1 = perm_head<E1>(b) + (uint32_t(s) << (E1 - RLZ));
         const uint2 w = __ldg(bigF + N + ((i2 * m1) & (N - 1)));
-        yp[(m1 * N2 + i2) * L + col] = mulw2(y, w.x, w.y);
+        yp[(m1 * N2 + i2) * L + col] = mulws(y, w.x, w.y);
         return 0u;
     };
     pass<E1, 0, false, false, k2P, kSmemCap, G>(pass_table(ptab, S::llog(0)), ld, st_sm, fix);
@@ -211,7 +211,7 @@ dec_2_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, uin
     };
     auto st_y2 = [&](uint32_t q2, uint32_t, int, uint32_t col, uint32_t y) -> uint32_t {
         const uint2 w = __ldg(bigF + N + ((i1p * q2) & (N - 1)));
-        y2[(q2 * N1 + i1p) * L + col] = mulw2(y, w.x, w.y);
+        y2[(q2 * N1 + i1p) * L + col] = mulws(y, w.x, w.y);
         return 0u;
     };
     // FNT1 pass B, first radix pass
@@ -274,7 +274,7 @@ dec_3_kernel(const uint2* __restrict__ ptabF, const uint2* __restrict__ ptabI, c
     auto ld_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t { return work[G::idx(lrow, col)]; };
     auto st_y3 = [&](uint32_t t1, uint32_t, int, uint32_t col, uint32_t y) -> uint32_t {
         const uint2 w = __ldg(bigI + N + ((q2 * t1) & (N - 1)));
-        y3[(t1 * N2 + q2) * L + col] = mulw2(y, w.x, w.y);
+        y3[(t1 * N2 + q2) * L + col] = mulws(y, w.x, w.y);
         return 0u;
     };
     // FNT2 pass B, first radix pass
@@ -297,7 +297,7 @@ dec_3_kernel(const uint2* __restrict__ ptabF, const uint2* __restrict__ ptabI, c
             for (int s = 0; s < RZ; ++s) {
                 const uint32_t q1 = fh + (uint32_t(s) << (E1 - RLZ));
                 const uint2 a = __ldg(ah + q2 + N2 * q1);
-                v[rev<RZ>(s)] = mulw2(v[rev<RZ>(s)], a.x, a.y);  // DIT input order: u[rev(s)] = x_s
+                v[rev<RZ>(s)] = mulws(v[rev<RZ>(s)], a.x, a.y);  // DIT input order: u[rev(s)] = x_s
             }
             dit_regs<RZ, true, k2P>(v);
 #pragma unroll
@@ -333,7 +333,7 @@ dec_4_kernel(const uint2* __restrict__ ptabI, uint32_t k, uint32_t L, uint32_t t
     auto st_out = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) -> uint32_t {
         const uint32_t row = t1 + N1 * (perm_head<E2>(b) + (uint32_t(s) << (E2 - RLZ)));
         const bool keep = HALFK ? (s < RZ / 2) : (row < k);
-        y = red2p(y);
+        y = canon_s2p(y);
         if (keep) __stcs(outp + (row * L + col), uint16_t(y));
         return (y == 65536u && keep) ? 1u : 0u;
     };
@@ -403,9 +403,9 @@ __global__ void big_tables_kernel(uint2* fwd, uint2* inv) {
     const int e = 31 - __clz(i);
     const uint32_t j = i - (1u << e);
     const uint32_t ex = (j << (16 - e)) & 0xFFFFu;
-    const uint32_t wf = gpow(3u, ex), wi = gpow(3u, (65536u - ex) & 0xFFFFu);
-    fwd[i] = make_uint2(wf, wf * 65535u);
-    inv[i] = make_uint2(wi, wi * 65535u);
+    const int32_t wf = balanced(gpow(3u, ex)), wi = balanced(gpow(3u, (65536u - ex) & 0xFFFFu));
+    fwd[i] = make_uint2(uint32_t(wf), uint32_t(wf * 65535));
+    inv[i] = make_uint2(uint32_t(wi), uint32_t(wi * 65535));
 }
 
 }  // namespace

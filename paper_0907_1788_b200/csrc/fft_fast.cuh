@@ -11,12 +11,11 @@
 // last pass can write it, and the decoder can fuse the end of one transform
 // with the start of the next in registers.
 //
-// Arithmetic (field.cuh): every value is a uint32 congruent to the field
-// element, below a compile-time bound. Multiplication by a table twiddle is
-// Shoup's (any 32-bit input, result < 2p); by a power of two (all roots of
-// order <= 32 are powers of two: r16 = 2^6, r8 = 2^12, r4 = -2^8) it is a
-// shift-and-fold on the integer ALU pipe, which keeps the FMA-heavy pipe
-// (IMAD.HI) for the table twiddles only.
+// Arithmetic: signed lazy values (|v| below a compile-time bound, see
+// below). Multiplication by a table twiddle is Shoup's with a balanced
+// twiddle (result in (-p, 2p)); by a power of two (all roots of order <= 32
+// are powers of two: r16 = 2^6, r8 = 2^12, r4 = -2^8) it is an exact
+// shift-and-fold of three instructions.
 #pragma once
 #include <cstdint>
 
@@ -47,28 +46,31 @@ struct Tw {
     static constexpr int e2 = pow2_exponent(w);  // >= 0 for every L <= 32
 };
 
-// x * 2^E mod p, E in [0, 32), x < B. Result bound: out_bound<E, B>().
+// Signed lazy representation: every value is an int32 (kept in uint32
+// registers) congruent to the field element, with |v| < B for a bound B
+// tracked at compile time (static_assert B < 2^31). Butterfly differences need
+// no offsets, and multiplication by a power of two is three instructions:
+//   x * 2^s == (x mod 2^(16-s)) * 2^s - floor(x / 2^(16-s))       (2^16 == -1)
+//           == (x << s) - xh * 65537   exactly, xh = x >> (16-s) (arithmetic),
+// i.e. SHF + IMAD.SHL + IMAD (one ALU, two FMA-pipe instructions).
+
+// balanced representative of a canonical residue: (-p/2, p/2]
+__host__ __device__ constexpr int32_t balanced(uint32_t w) { return w > 32768u ? int32_t(w) - 65537 : int32_t(w); }
+
+// x * 2^E mod p, E in [0, 32), |x| < B.
 template <int E, uint64_t B>
 struct MulPow2 {
     static constexpr int e = E & 31;
     static constexpr bool neg = e >= 16;  // 2^16 = -1
     static constexpr int s = e & 15;
-    static constexpr uint64_t HB = s ? (((B - 1) >> (16 - s)) + 1) : 0;  // bound of the high part
-    static constexpr uint64_t K = s ? ceil_p(HB) : ceil_p(B);
-    static constexpr uint64_t OUT = s ? (neg ? (HB + kP64) : (65536ull + K)) : (neg ? K + 1 : B);
+    static constexpr uint64_t OUT = s ? (65536ull + (B >> (16 - s)) + 2) : B;
     __device__ __forceinline__ static uint32_t apply(uint32_t x) {
         if constexpr (s == 0) {
-            if constexpr (neg)
-                return uint32_t(K) - x;
-            else
-                return x;
+            return neg ? 0u - x : x;
         } else {
-            const uint32_t xh = x >> (16 - s);
-            const uint32_t xl = (x << s) & 0xFFFFu;
-            if constexpr (neg)
-                return xh + uint32_t(kP64) - xl;  // -(xl - xh)
-            else
-                return xl + uint32_t(K) - xh;
+            const uint32_t xh = uint32_t(int32_t(x) >> (16 - s));
+            const uint32_t xs = x << s;
+            return neg ? xh * 65537u - xs : xs - xh * 65537u;
         }
     }
 };
@@ -77,12 +79,29 @@ struct MulPow2 {
 #define FNTRS_POW2_SHIFT 1
 #endif
 
-// Multiply by the compile-time twiddle TW<L,J>; returns the new bound via OUT.
+// signed Shoup product by a balanced twiddle w (w2 = 65535 w): (-p, 2p)
+__device__ __forceinline__ uint32_t mulws(uint32_t x, uint32_t w, uint32_t w2) {
+    const uint32_t q = uint32_t(__mulhi(int32_t(x), int32_t(w2)));
+    return x * w - q * kP;
+}
+// signed reduction: (-p, 2p)
+__device__ __forceinline__ uint32_t reds(uint32_t x) {
+    const uint32_t q = uint32_t(__mulhi(int32_t(x), 65535));
+    return x - q * kP;
+}
+// |x| < 2p -> canonical [0, p)
+__device__ __forceinline__ uint32_t canon_s2p(uint32_t x) {
+    uint32_t r = x + 2 * kP;   // [0, 4p)
+    r = min(r, r - 2 * kP);    // [0, 2p)
+    return min(r, r - kP);
+}
+
+// Multiply by the compile-time twiddle TW<L,J>; OUT is the new bound.
 template <int L, int J, bool INV, uint64_t B>
 struct MulTw {
     using T = Tw<L, J, INV>;
     static_assert(T::e2 >= 0, "in-register twiddles must be powers of two");
-    static constexpr bool shift = FNTRS_POW2_SHIFT && (B < (1ull << 31));
+    static constexpr bool shift = FNTRS_POW2_SHIFT;
     static constexpr uint64_t OUT = J == 0 ? B : (shift ? MulPow2<T::e2, B>::OUT : 2 * kP64);
     __device__ __forceinline__ static uint32_t apply(uint32_t x) {
         if constexpr (J == 0)
@@ -90,15 +109,14 @@ struct MulTw {
         else if constexpr (shift)
             return MulPow2<T::e2, B>::apply(x);
         else
-            return mulw(x, T::w);
+            return mulws(x, uint32_t(balanced(T::w)), uint32_t(balanced(T::w) * 65535));
     }
 };
 
-// ---- in-register DIF: natural in (all < BIN), v[rev(s)] = y_s out ---------
+// ---- in-register DIF: natural in (|v| < BIN), v[rev(s)] = y_s out -----------
 template <int R, bool INV, int HALF, int J, uint64_t BIN>
 struct DifStage {
-    static constexpr uint64_t K = ceil_p(BIN);
-    using M = MulTw<2 * HALF, J, INV, BIN + K>;
+    using M = MulTw<2 * HALF, J, INV, 2 * BIN>;
     static constexpr uint64_t LO = 2 * BIN;
     static constexpr uint64_t HI = M::OUT;
     static constexpr uint64_t out() {
@@ -113,7 +131,7 @@ struct DifStage {
         for (int blk = 0; blk < R; blk += 2 * HALF) {
             const uint32_t a = v[blk + J], b = v[blk + J + HALF];
             v[blk + J] = a + b;
-            v[blk + J + HALF] = M::apply(a + uint32_t(K) - b);
+            v[blk + J + HALF] = M::apply(a - b);
         }
         if constexpr (J + 1 < HALF) DifStage<R, INV, HALF, J + 1, BIN>::run(v);
     }
@@ -136,13 +154,11 @@ struct DifAll {
     }
 };
 
-// ---- in-register DIT: v[rev(s)] in (< BIN), natural out ---------------------
+// ---- in-register DIT: v[rev(s)] in (|v| < BIN), natural out -----------------
 template <int R, bool INV, int HALF, int J, uint64_t BIN>
 struct DitStage {
     using M = MulTw<2 * HALF, J, INV, BIN>;
-    static constexpr uint64_t TB = M::OUT;
-    static constexpr uint64_t K = ceil_p(TB);
-    static constexpr uint64_t OUT1 = umax(BIN + TB, BIN + K);
+    static constexpr uint64_t OUT1 = BIN + M::OUT;
     static constexpr uint64_t out() {
         if constexpr (J + 1 < HALF)
             return umax(OUT1, DitStage<R, INV, HALF, J + 1, BIN>::OUT);
@@ -156,7 +172,7 @@ struct DitStage {
             const uint32_t a = v[blk + J];
             const uint32_t t = M::apply(v[blk + J + HALF]);
             v[blk + J] = a + t;
-            v[blk + J + HALF] = a + uint32_t(K) - t;
+            v[blk + J + HALF] = a - t;
         }
         if constexpr (J + 1 < HALF) DitStage<R, INV, HALF, J + 1, BIN>::run(v);
     }
@@ -181,12 +197,12 @@ struct DitAll {
 
 template <int R, bool INV, uint64_t BIN>
 __device__ __forceinline__ void dif_regs(uint32_t (&v)[R]) {
-    static_assert(DifAll<R, INV, R / 2, BIN>::OUT < (1ull << 32), "lazy bound overflow");
+    static_assert(DifAll<R, INV, R / 2, BIN>::OUT < (1ull << 31), "lazy bound overflow");
     DifAll<R, INV, R / 2, BIN>::run(v);
 }
 template <int R, bool INV, uint64_t BIN>
 __device__ __forceinline__ void dit_regs(uint32_t (&v)[R]) {
-    static_assert(DitAll<R, INV, 1, BIN>::OUT < (1ull << 32), "lazy bound overflow");
+    static_assert(DitAll<R, INV, 1, BIN>::OUT < (1ull << 31), "lazy bound overflow");
     DitAll<R, INV, 1, BIN>::run(v);
 }
 template <int R, bool INV, uint64_t BIN>

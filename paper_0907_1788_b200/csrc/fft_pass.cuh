@@ -55,7 +55,7 @@ constexpr int ilog2c() {
 template <uint64_t B, uint64_t CAP>
 __device__ __forceinline__ uint32_t cap(uint32_t v) {
     if constexpr (B > CAP)
-        return red(v);
+        return reds(v);
     else
         return v;
 }
@@ -131,7 +131,7 @@ __device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld
                 uint32_t y = v[rev<R>(s)];
                 if (SL > 0 && s > 0) {
                     const uint2 w = __ldg(tp + s);
-                    y = mulw2(y, w.x, w.y);
+                    y = mulws(y, w.x, w.y);
                 } else {
                     y = cap<BO, OCAP>(y);
                 }
@@ -144,7 +144,7 @@ __device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld
                 uint32_t x = ld(base + (uint32_t(s) << SL), b, s, col);
                 if (SL > 0 && s > 0) {
                     const uint2 w = __ldg(tp + s);
-                    x = mulw2(x, w.x, w.y);
+                    x = mulws(x, w.x, w.y);
                 }
                 v[rev<R>(s)] = x;
             }
