@@ -98,7 +98,6 @@ __global__ void __launch_bounds__(G::NT, G::MINB) enc_fast_kernel(const __grid_c
         };
         auto st_out = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) -> uint32_t {
             const uint32_t f = perm_head<E>(b) + (uint32_t(s) << (E - RLZ));
-            y = canon_s2p(y);
             if (!PUNCT || f < n) __stcs(outp + (f * L + col), uint16_t(y));
             return (y == 65536u && (!PUNCT || f < n)) ? 1u : 0u;
         };
@@ -116,7 +115,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) enc_fast_kernel(const __grid_c
             pass<E, 1, false, false, kSmemCap, kSmemCap, G>(pass_table(ptabF, S::llog(1)), ld_sm, st_sm);
             __syncthreads();
         }
-        pass<E, P - 1, false, false, kSmemCap, k2P, G>(pass_table(ptabF, S::llog(P - 1)), ld_sm, st_out, NoFix(),
+        pass<E, P - 1, false, false, kSmemCap, kCanon, G>(pass_table(ptabF, S::llog(P - 1)), ld_sm, st_out, NoFix(),
                                                        flush_out);
         __syncthreads();
     }
@@ -225,7 +224,6 @@ __global__ void __launch_bounds__(G::NT, G::MINB) dec_fast_kernel(const __grid_c
             const uint32_t f = perm_head<E>(b) + (uint32_t(s) << (E - RLZ));
             // k = N/2: kept iff s < R/2 (compile time after unrolling)
             const bool keep = HALFK ? (s < RZ / 2) : (f < k);
-            y = canon_s2p(y);
             if (keep) __stcs(outp + (f * L + col), uint16_t(y));
             return (y == 65536u && keep) ? 1u : 0u;
         };
@@ -321,7 +319,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) dec_fast_kernel(const __grid_c
             pass<E, 1, true, false, kSmemCap, kSmemCap, G>(pass_table(ptabI, S::llog(1)), ld_smf, st_smf);
             __syncthreads();
         }
-        pass<E, P - 1, true, false, kSmemCap, k2P, G>(pass_table(ptabI, S::llog(P - 1)), ld_smf, st_out, NoFix(),
+        pass<E, P - 1, true, false, kSmemCap, kCanon, G>(pass_table(ptabI, S::llog(P - 1)), ld_smf, st_out, NoFix(),
                                                       flush_out);
         __syncthreads();
     }

@@ -112,7 +112,6 @@ enc_b_kernel(const uint2* __restrict__ ptab, uint32_t n, uint32_t L, uint32_t tp
     auto ld_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t { return work[G::idx(lrow, col)]; };
     auto st_out = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) -> uint32_t {
         const uint32_t row = m1 + N1 * (perm_head<E2>(b) + (uint32_t(s) << (E2 - RLZ)));
-        y = canon_s2p(y);
         const bool keep = !PUNCT || row < n;
         if (keep) __stcs(outp + (row * L + col), uint16_t(y));
         return (y == 65536u && keep) ? 1u : 0u;
@@ -127,7 +126,7 @@ enc_b_kernel(const uint2* __restrict__ ptab, uint32_t n, uint32_t L, uint32_t tp
     };
     pass<E2, 0, false, false, k2P, kSmemCap, G>(pass_table(ptab, S::llog(0)), ld, st_sm);
     __syncthreads();
-    pass<E2, 1, false, false, kSmemCap, k2P, G>(pass_table(ptab, S::llog(1)), ld_sm, st_out, NoFix(), flush);
+    pass<E2, 1, false, false, kSmemCap, kCanon, G>(pass_table(ptab, S::llog(1)), ld_sm, st_out, NoFix(), flush);
 }
 
 // ---------------------------------------------------------------- decode ----
@@ -333,7 +332,6 @@ dec_4_kernel(const uint2* __restrict__ ptabI, uint32_t k, uint32_t L, uint32_t t
     auto st_out = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) -> uint32_t {
         const uint32_t row = t1 + N1 * (perm_head<E2>(b) + (uint32_t(s) << (E2 - RLZ)));
         const bool keep = HALFK ? (s < RZ / 2) : (row < k);
-        y = canon_s2p(y);
         if (keep) __stcs(outp + (row * L + col), uint16_t(y));
         return (y == 65536u && keep) ? 1u : 0u;
     };
@@ -346,7 +344,7 @@ dec_4_kernel(const uint2* __restrict__ ptabI, uint32_t k, uint32_t L, uint32_t t
     };
     pass<E2, 0, true, false, k2P, kSmemCap, G>(pass_table(ptabI, S::llog(0)), ld, st_sm);
     __syncthreads();
-    pass<E2, 1, true, false, kSmemCap, k2P, G>(pass_table(ptabI, S::llog(1)), ld_sm, st_out, NoFix(), flush);
+    pass<E2, 1, true, false, kSmemCap, kCanon, G>(pass_table(ptabI, S::llog(1)), ld_sm, st_out, NoFix(), flush);
 }
 
 template <class K>

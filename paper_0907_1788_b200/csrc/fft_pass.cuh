@@ -52,8 +52,25 @@ constexpr int ilog2c() {
     return e;
 }
 
+// |v| < B -> canonical [0, p), cheapest route for the bound
+template <uint64_t B>
+__device__ __forceinline__ uint32_t canon_b(uint32_t v) {
+    if constexpr (B <= k2P) {
+        return canon_s2p(v);
+    } else {
+        static_assert(2 * ceil_p(B) < (1ull << 32), "");
+        return red2p(red(v + uint32_t(ceil_p(B))));  // [0, 2K) -> [0, 2p) -> [0, p)
+    }
+}
+
+// stored-value cap meaning "store canonical [0, p)"
+constexpr uint64_t kCanon = 1;
+
 template <uint64_t B, uint64_t CAP>
 __device__ __forceinline__ uint32_t cap(uint32_t v) {
+    if constexpr (CAP == kCanon)
+        return canon_b<B>(v);
+    else
     if constexpr (B > CAP)
         return reds(v);
     else
@@ -110,7 +127,7 @@ __device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld
     constexpr int RL = S::rlog(p), R = 1 << RL, LL = S::llog(p), SL = S::slog(p);
     constexpr int ITEMS = (1 << (E - RL)) * G::WT;
     constexpr int LGW = ilog2c<G::WT>();
-    static_assert(OCAP >= k2P, "");
+    static_assert(OCAP >= k2P || OCAP == kCanon, "");
 #pragma unroll 1
     for (int it = threadIdx.x; it < ITEMS; it += G::NT) {
         const uint32_t col = uint32_t(it) & uint32_t(G::WT - 1);
@@ -132,6 +149,7 @@ __device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld
                 if (SL > 0 && s > 0) {
                     const uint2 w = __ldg(tp + s);
                     y = mulws(y, w.x, w.y);
+                    if constexpr (OCAP == kCanon) y = canon_s2p(y);
                 } else {
                     y = cap<BO, OCAP>(y);
                 }
