@@ -397,11 +397,7 @@ def run_e2e(args, codec, cfg, dev, stream, seed, world):
         keep.append(step())
     b.record(stream)
     torch.cuda.synchronize(dev)
-    ms = a.elapsed_time(b) / steps
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t[0])
+    ms = max_over_ranks([a.elapsed_time(b) / steps], device=dev)[0]
     total_src = 2 * k * L * S * world
     return {"value": round(total_src / (ms * 1e-3) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ms, 3),
@@ -467,6 +463,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-step-seconds", type=float, default=6.0)
     ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes per decode launch (profiles/)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo = test mode for several ranks on fewer GPUs (host-side barrier/max only)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -482,8 +480,15 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        ndev = torch.cuda.device_count()
+        if args.dist_backend == "gloo":
+            # test mode: ranks may share GPUs; the barrier / max-over-ranks run on the host
+            local_rank = local_rank % max(1, ndev)
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
     res = run_gpu(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(res), flush=True)

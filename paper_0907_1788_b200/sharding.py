@@ -39,6 +39,8 @@ def max_over_ranks(values, device=None):
     vals = [float(v) for v in values]
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return vals
+    if dist.get_backend() == "gloo":
+        device = "cpu"
     t = torch.tensor(vals, dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return [float(x) for x in t.cpu()]
