@@ -9,6 +9,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cstdio>
 #include <algorithm>
+#include <map>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -33,6 +34,8 @@ struct fntrs_ctx {
     std::string err;
     uint32_t* scratch[2] = {nullptr, nullptr};  // four-step intermediates (stream-ordered)
     size_t scratch_bytes = 0;
+    fast::LogTables ltab;
+    std::map<std::pair<uint32_t, uint32_t>, uint32_t*> digit_spectra;  // (N, w) -> Dh [N][D]
 };
 
 struct fntrs_plans {
@@ -147,6 +150,11 @@ int prep_escapes(fntrs_ctx* ctx, uint64_t* out_esc, uint64_t esc_cap, uint64_t* 
     return FNTRS_OK;
 }
 
+__global__ void negate_scale_kernel(const uint32_t* in, uint32_t* out, uint32_t n, uint32_t s) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = gmul(in[i], s);
+}
+
 }  // namespace
 
 extern "C" {
@@ -210,6 +218,7 @@ int fntrs_gpu_create(int device, fntrs_ctx** out) {
     if (e == cudaSuccess) e = build_tables(ctx->tab, ctx->internal);
     if (e == cudaSuccess) e = fast::build_fast_tables(ctx->ftab, ctx->internal);
     if (e == cudaSuccess) e = fast::build_large_tables(ctx->ftab, ctx->internal);
+    if (e == cudaSuccess) e = fast::build_log_tables(ctx->ltab, ctx->internal);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->internal);
     if (e != cudaSuccess) {
         delete ctx;
@@ -232,6 +241,9 @@ int fntrs_gpu_destroy(fntrs_ctx* ctx) {
     cudaDeviceSynchronize();
     cudaFree(ctx->scratch[0]);
     cudaFree(ctx->scratch[1]);
+    cudaFree(ctx->ltab.exp3);
+    cudaFree(ctx->ltab.log3);
+    for (auto& kv : ctx->digit_spectra) cudaFree(kv.second);
     cudaFree(ctx->sort_tmp);
     cudaFree(ctx->sort_alt);
     if (ctx->internal) cudaStreamDestroy(ctx->internal);
@@ -335,16 +347,35 @@ int fntrs_gpu_plans_create(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t kp, 
         if (!e) e = cudaMallocAsync(&pl->ainv, npos * 4, st);
         if (!e && locator) e = cudaMallocAsync(&pl->ahat, size_t(npatterns) * M * 4, st);
         if (!e) e = cudaMemcpyAsync(pl->pos, positions, npos * 4, cudaMemcpyHostToDevice, st);
-        if (!e && locator) {
-            e = launch_plan_build(N, M, kp, npatterns, pl->pos, pl->ainv, pl->ahat, ctx->tab, st);
-            ctx->launches += 1;
-        }
-        if (!e && !full && kp == k && M == N && (fast::fast_tile_columns(N) || large)) {
+        const bool fastplan = !full && kp == k && M == N && (fast::fast_tile_columns(N) || large);
+        if (!e && fastplan) {
+            // log-domain convolution plan (plan_fast.cu): ainv, ahat, rowmap, ahat2 at once
             e = cudaMallocAsync(&pl->rowmap, size_t(npatterns) * N * sizeof(uint2), st);
             if (!e) e = cudaMallocAsync(&pl->ahat2, size_t(npatterns) * N * sizeof(uint2), st);
-            if (!e) e = fast::launch_fast_plan_tables(N, kp, npatterns, pl->pos, pl->ainv, pl->ahat, pl->rowmap,
-                                                      pl->ahat2, st);
-            ctx->launches += 2;
+            const uint32_t w = fast::plan_digit_width(k), D = (16 + w - 1) / w;
+            uint32_t* Dh = nullptr;
+            auto it = ctx->digit_spectra.find({N, w});
+            if (!e && it == ctx->digit_spectra.end()) {
+                uint32_t* tmp = nullptr;
+                e = cudaMalloc(&Dh, size_t(N) * D * 4);
+                if (!e) e = cudaMallocAsync(&tmp, size_t(N) * D * 4 + 256, st);
+                if (!e) e = fast::build_digit_spectra(ctx->ftab, ctx->tab, ctx->ltab, N, w, Dh, tmp, st);
+                if (tmp) cudaFreeAsync(tmp, st);
+                if (!e) ctx->digit_spectra[{N, w}] = Dh;
+                ctx->launches += 2;
+            } else if (!e) {
+                Dh = it->second;
+            }
+            uint32_t* scratch = nullptr;
+            if (!e) e = cudaMallocAsync(&scratch, fast::plan_fast_scratch_words(N, k, npatterns) * 4, st);
+            if (!e)
+                e = fast::launch_plan_fast(ctx->ftab, ctx->tab, ctx->ltab, N, k, npatterns, pl->pos, Dh, scratch,
+                                           pl->ainv, pl->ahat, pl->rowmap, pl->ahat2, st);
+            if (scratch) cudaFreeAsync(scratch, st);
+            ctx->launches += 8;
+        } else if (!e && locator) {
+            e = launch_plan_build(N, M, kp, npatterns, pl->pos, pl->ainv, pl->ahat, ctx->tab, st);
+            ctx->launches += 1;
         }
     }
     if (e) {
@@ -383,8 +414,16 @@ int fntrs_gpu_plans_export(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t patte
     CK(cudaMalloc(&spec, M * 4), "export alloc");
     // A = IFNT_M(A_hat) = -IFNT_unscaled(ahat) since ahat = -A_hat / M
     const uint32_t* ah = pl->ahat + size_t(pattern) * M;
-    CK(launch_fnt_tile(ctx->tab, M, true, kP - 1u, 1, ah, acoef, st), "export ifnt");
-    CK(launch_fnt_tile(ctx->tab, M, false, 1u, 1, acoef, spec, st), "export fnt");
+    if (M <= kTileMaxN) {
+        CK(launch_fnt_tile(ctx->tab, M, true, kP - 1u, 1, ah, acoef, st), "export ifnt");
+        CK(launch_fnt_tile(ctx->tab, M, false, 1u, 1, acoef, spec, st), "export fnt");
+    } else {  // A = IFNT_M(-M ahat): scale the inverse by -M * (1/M) = -1 via a forward-then-negate pair
+        int rc = ensure_scratch(ctx, size_t(M) * 4, st);
+        if (rc) return rc;
+        CK(fast::launch_fnt_cols(ctx->ftab, M, true, 1, ah, ctx->scratch[0], spec, st), "export ifnt");
+        negate_scale_kernel<<<(M + 255) / 256, 256, 0, st>>>(spec, acoef, M, kP - (M % kP));  // * (-M)
+        CK(fast::launch_fnt_cols(ctx->ftab, M, false, 1, acoef, ctx->scratch[0], spec, st), "export fnt");
+    }
     ctx->launches += 2;
     std::vector<uint32_t> a(M), sp(M);
     CK(cudaMemcpyAsync(a.data(), acoef, M * 4, cudaMemcpyDeviceToHost, st), "export copy");
@@ -457,9 +496,16 @@ int fntrs_gpu_fnt(fntrs_ctx* ctx, uint32_t m, int inverse, uint32_t L, const uin
     if (!ctx) return FNTRS_E_INVALID_ARGUMENT;
     if (m == 0 || m > 65536 || (m & (m - 1)))
         return fail(ctx, FNTRS_E_INVALID_TRANSFORM_SIZE, "transform size must be a power of two in [1, 65536]");
-    if (m > kTileMaxN) return fail(ctx, FNTRS_E_UNSUPPORTED, "transform sizes > 4096 not in this build yet");
     if (L && (!in || !out)) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "null buffer");
     DeviceGuard g(ctx->device);
+    if (m > kTileMaxN) {  // column-batched four-step kernels (plan_fast.cu)
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        int rc = ensure_scratch(ctx, size_t(m) * L * 4, st);
+        if (rc) return rc;
+        CK(fast::launch_fnt_cols(ctx->ftab, m, inverse != 0, L, in, ctx->scratch[0], out, st), "fnt launch");
+        ctx->launches += 2;
+        return FNTRS_OK;
+    }
     const uint32_t scale = inverse ? cpow(m % kP, kP - 2) : 1u;
     CK(launch_fnt_tile(ctx->tab, m, inverse != 0, scale, L, in, out, static_cast<cudaStream_t>(stream)), "fnt launch");
     ctx->launches += 1;

@@ -102,6 +102,24 @@ cudaError_t launch_encode_large(const FastTables& t, uint32_t k, uint32_t n, uin
 cudaError_t launch_decode_large(const FastTables& t, const FastPlanView& pv, uint32_t stripes, uint32_t L,
                                 const uint32_t* sp, const uint16_t* rx, EscIn ein, uint16_t* out, EscOut eout,
                                 uint32_t* YA, uint32_t* YB, uint32_t batch, cudaStream_t st);
+
+// ---- log-domain plans and column transforms (plan_fast.cu)
+struct LogTables {
+    uint32_t* exp3 = nullptr;  // 3^e, e < 65536
+    uint16_t* log3 = nullptr;  // log_3(x) at [x - 1], x in [1, 65536]
+};
+cudaError_t build_log_tables(LogTables& lt, cudaStream_t st);
+uint32_t plan_digit_width(uint32_t k);
+// digit spectra Dh [N][D] (D = ceil(16 / w)); scratch: N*D words when N >= 8192
+cudaError_t build_digit_spectra(const FastTables& t, const Tables& tab, const LogTables& lt, uint32_t N, uint32_t w,
+                                uint32_t* Dh, uint32_t* scratch, cudaStream_t st);
+size_t plan_fast_scratch_words(uint32_t N, uint32_t k, uint32_t P);
+cudaError_t launch_plan_fast(const FastTables& t, const Tables& tab, const LogTables& lt, uint32_t N, uint32_t k,
+                             uint32_t P, const uint32_t* pos, const uint32_t* Dh, uint32_t* scratch, uint32_t* ainv,
+                             uint32_t* ahat, uint2* rowmap, uint2* ahat2, cudaStream_t st);
+// natural-order column transforms [N][C] of any N <= 65536 (scratch N*C words when N >= 8192)
+cudaError_t launch_fnt_cols(const FastTables& t, uint32_t N, bool inverse, uint32_t C, const uint32_t* in,
+                            uint32_t* scratch, uint32_t* out, cudaStream_t st);
 }  // namespace fast
 
 }  // namespace fntrs_gpu

@@ -167,7 +167,7 @@ def test_decode_matches_oracle(codec, oracle, k, n, L, S):
 
 
 @pytest.mark.parametrize("n,k", [(2, 2), (4, 2), (8, 3), (8, 5), (16, 12), (256, 128), (2048, 1024), (4096, 2048),
-                                 (1000, 300)])
+                                 (1000, 300), (200, 100), (64, 17), (16384, 8192), (12000, 5000)])
 def test_plan_fields_match_oracle(codec, oracle, n, k):
     nd = 1 << (n - 1).bit_length()
     rng = np.random.default_rng(n + k)
@@ -177,6 +177,19 @@ def test_plan_fields_match_oracle(codec, oracle, n, k):
     ga, gap, gps, gaf = plans.export(0)
     assert gps == ps
     assert np.array_equal(ga, a) and np.array_equal(gap, ap) and np.array_equal(gaf, af)
+
+
+@pytest.mark.parametrize("m", [1 << e for e in range(13, 17)])
+def test_fnt_large_matches_oracle(codec, oracle, m):
+    rng = np.random.default_rng(m)
+    L = 3
+    x = rng.integers(0, P, (m, L)).astype(np.uint32)
+    t = torch.from_numpy(x.view(np.int32)).cuda()
+    fw = codec.fnt(t).cpu().numpy().view(np.uint32)
+    iv = codec.fnt(t, inverse=True).cpu().numpy().view(np.uint32)
+    for c in range(L):
+        assert np.array_equal(fw[:, c], oracle.fnt(x[:, c]))
+        assert np.array_equal(iv[:, c], oracle.fnt(x[:, c], True))
 
 
 def test_frozen_plan_three_positions(codec):  # test_interp.cpp:52-63
