@@ -215,6 +215,13 @@ int fntrs_gpu_create(int device, fntrs_ctx** out) {
     ctx->device = device;
     DeviceGuard g(device);
     cudaError_t e = cudaStreamCreateWithFlags(&ctx->internal, cudaStreamNonBlocking);
+    {  // keep stream-ordered allocations (plans, scratch) cached across calls
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t threshold = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+        }
+    }
     if (e == cudaSuccess) e = build_tables(ctx->tab, ctx->internal);
     if (e == cudaSuccess) e = fast::build_fast_tables(ctx->ftab, ctx->internal);
     if (e == cudaSuccess) e = fast::build_large_tables(ctx->ftab, ctx->internal);

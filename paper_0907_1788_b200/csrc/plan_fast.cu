@@ -242,50 +242,63 @@ __global__ void indicator_kernel(uint32_t N, uint32_t k, uint32_t P, const uint3
     }
 }
 
-__device__ __forceinline__ uint32_t conv_at(const uint32_t* __restrict__ Y, uint32_t PD, uint32_t j, uint32_t p,
-                                            uint32_t D, uint32_t w) {
-    uint32_t c = 0;
-    const uint32_t* y = Y + size_t(j) * PD + size_t(p) * D;
-    for (uint32_t b = 0; b < D; ++b) c += __ldg(y + b) << (w * b);
-    return c & 0xFFFFu;
+// conv[p][j] = (sum_b Y[j][p*D + b] << (w b)) mod 2^16, transposing [N][P*D] -> [P][N]
+// through a 32x32 shared tile so both sides are coalesced.
+__global__ void conv_combine_kernel(uint32_t N, uint32_t P, uint32_t D, uint32_t w, const uint32_t* __restrict__ Y,
+                                    uint32_t* __restrict__ conv) {
+    __shared__ uint32_t tile[32][33];
+    const uint32_t p0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+    const uint32_t tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+    for (uint32_t r = ty; r < 32; r += 8) {
+        const uint32_t j = j0 + r, p = p0 + tx;
+        uint32_t c = 0;
+        if (j < N && p < P) {
+            const uint32_t* y = Y + size_t(j) * P * D + size_t(p) * D;
+            for (uint32_t b = 0; b < D; ++b) c += __ldg(y + b) << (w * b);
+        }
+        tile[r][tx] = c & 0xFFFFu;
+    }
+    __syncthreads();
+    for (uint32_t r = ty; r < 32; r += 8) {
+        const uint32_t p = p0 + r, j = j0 + tx;
+        if (j < N && p < P) conv[size_t(p) * N + j] = tile[tx][r];
+    }
 }
 
 // ainv[p][i], rowmap[p][z_i] = {i, balanced 1/A'(x_i)}
-__global__ void plan_ainv_kernel(uint32_t N, uint32_t k, uint32_t P, uint32_t D, uint32_t w,
-                                 const uint32_t* __restrict__ pos, const uint32_t* __restrict__ S,
-                                 const uint32_t* __restrict__ Y, const uint32_t* __restrict__ exp3,
-                                 uint32_t* __restrict__ ainv, uint2* __restrict__ rowmap) {
+__global__ void plan_ainv_kernel(uint32_t N, uint32_t k, uint32_t P, const uint32_t* __restrict__ pos,
+                                 const uint32_t* __restrict__ S, const uint32_t* __restrict__ conv,
+                                 const uint32_t* __restrict__ exp3, uint32_t* __restrict__ ainv,
+                                 uint2* __restrict__ rowmap) {
     const uint64_t total = uint64_t(P) * k;
     const uint32_t sc = 65536u / N;
     for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < total; t += uint64_t(gridDim.x) * blockDim.x) {
         const uint32_t p = uint32_t(t / k), i = uint32_t(t - uint64_t(p) * k);
         const uint32_t z = pos[t];
-        const uint32_t e = (sc * ((S[p] + N - z) & (N - 1)) + conv_at(Y, P * D, z, p, D, w)) & 0xFFFFu;
+        const uint32_t e = (sc * ((S[p] + N - z) & (N - 1)) + __ldg(conv + size_t(p) * N + z)) & 0xFFFFu;
         const uint32_t inv = __ldg(exp3 + ((65536u - e) & 0xFFFFu));
         ainv[t] = inv;
-        if (rowmap) rowmap[size_t(p) * N + z] = make_uint2(i, uint32_t(balanced(inv)));
+        rowmap[size_t(p) * N + z] = make_uint2(i, uint32_t(balanced(inv)));
     }
 }
 
 // ahat[p][j] = -A(r^j)/N (0 on received positions), ahat2 = signed Shoup pairs
-__global__ void plan_ahat_kernel(uint32_t N, uint32_t P, uint32_t D, uint32_t w, const uint32_t* __restrict__ S,
-                                 const uint32_t* __restrict__ Xind, const uint32_t* __restrict__ Y,
+__global__ void plan_ahat_kernel(uint32_t N, uint32_t P, const uint32_t* __restrict__ S,
+                                 const uint32_t* __restrict__ conv, const uint2* __restrict__ rowmap,
                                  const uint32_t* __restrict__ exp3, uint32_t neg_ninv, uint32_t* __restrict__ ahat,
                                  uint2* __restrict__ ahat2) {
     const uint64_t total = uint64_t(P) * N;
     const uint32_t sc = 65536u / N;
     for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < total; t += uint64_t(gridDim.x) * blockDim.x) {
-        const uint32_t p = uint32_t(t / N), j = uint32_t(t - uint64_t(p) * N);
+        const uint32_t p = uint32_t(t / N);
         uint32_t a = 0;
-        if (!Xind[size_t(j) * P + p]) {
-            const uint32_t e = (sc * S[p] + conv_at(Y, P * D, j, p, D, w)) & 0xFFFFu;
+        if (rowmap[t].x == 0xFFFFFFFFu) {
+            const uint32_t e = (sc * S[p] + conv[t]) & 0xFFFFu;
             a = red2p(mulw(__ldg(exp3 + e), neg_ninv));
         }
         ahat[t] = a;
-        if (ahat2) {
-            const int32_t ab = balanced(a);
-            ahat2[t] = make_uint2(uint32_t(ab), uint32_t(ab * 65535));
-        }
+        const int32_t ab = balanced(a);
+        ahat2[t] = make_uint2(uint32_t(ab), uint32_t(ab * 65535));
     }
 }
 
@@ -327,8 +340,8 @@ cudaError_t build_digit_spectra(const FastTables& t, const Tables& tab, const Lo
 
 size_t plan_fast_scratch_words(uint32_t N, uint32_t k, uint32_t P) {
     const uint32_t D = (16 + plan_digit_width(k) - 1) / plan_digit_width(k);
-    // X (N*P) + spectrum (N*P) + Y (N*P*D) + four-step intermediate (N*P*D)
-    return size_t(N) * P * (2 + 2 * size_t(D)) + 64 + P;
+    // X (N*P) + spectrum (N*P) + Y (N*P*D) + four-step intermediate (N*P*D) + conv (N*P)
+    return size_t(N) * P * (3 + 2 * size_t(D)) + 64 + P;
 }
 
 cudaError_t launch_plan_fast(const FastTables& t, const Tables& tab, const LogTables& lt, uint32_t N, uint32_t k,
@@ -341,15 +354,17 @@ cudaError_t launch_plan_fast(const FastTables& t, const Tables& tab, const LogTa
     uint32_t* Y = Xhat + size_t(N) * P;         // [N][P*D]
     uint32_t* tmp = Y + size_t(N) * P * D;      // four-step intermediate
     uint32_t* S = tmp + size_t(N) * P * D;      // [P]
+    uint32_t* conv = S + P + 32;                // [P][N]
     cudaError_t err = cudaMemsetAsync(Xind, 0, sizeof(uint32_t) * N * size_t(P), st);
     if (err) return err;
     indicator_kernel<<<P, 256, 0, st>>>(N, k, P, pos, Xind, S);
     if ((err = run_cols<false>(t, N, LdPlain{Xind, P}, P, 1u, tmp, Xhat, st))) return err;
     const uint32_t ninv = cpow(N % kP, kP - 2);
     if ((err = run_cols<true>(t, N, LdSpectrumProduct{Xhat, Dh, P, D}, P * D, ninv, tmp, Y, st))) return err;
-    if (rowmap) fill_rowmap_kernel<<<148 * 8, 256, 0, st>>>(rowmap, uint64_t(P) * N);  // erased: {~0, 0}
-    plan_ainv_kernel<<<148 * 8, 256, 0, st>>>(N, k, P, D, w, pos, S, Y, lt.exp3, ainv, rowmap);
-    plan_ahat_kernel<<<148 * 8, 256, 0, st>>>(N, P, D, w, S, Xind, Y, lt.exp3, kP - ninv, ahat, ahat2);
+    conv_combine_kernel<<<dim3((P + 31) / 32, (N + 31) / 32), dim3(32, 8), 0, st>>>(N, P, D, w, Y, conv);
+    fill_rowmap_kernel<<<148 * 8, 256, 0, st>>>(rowmap, uint64_t(P) * N);  // erased: {~0, 0}
+    plan_ainv_kernel<<<148 * 8, 256, 0, st>>>(N, k, P, pos, S, conv, lt.exp3, ainv, rowmap);
+    plan_ahat_kernel<<<148 * 8, 256, 0, st>>>(N, P, S, conv, rowmap, lt.exp3, kP - ninv, ahat, ahat2);
     return cudaGetLastError();
 }
 
