@@ -343,44 +343,46 @@ def run_gpu(args, rank, world, local_rank):
 
 
 def run_e2e(args, codec, cfg, dev, stream, seed, world):
-    """Same metric through the public API with pinned HOST buffers: every step
-    copies the source and received packets host->device and the encoded and
-    decoded packets (plus escape counts) device->host inside the timed region."""
+    """Same metric through the public API with pinned HOST buffers
+    (paper_0907_1788_b200.pipeline.HostPipeline over the Codec / C-ABI calls):
+    every step copies the source and the received packets (and their escape
+    list) host->device and the encoded and decoded packets (and escape lists)
+    device->host inside the timed region; chunks overlap H2D, kernels and D2H
+    on three streams."""
     import torch
-    import torch.distributed as dist
+    from paper_0907_1788_b200.pipeline import HostPipeline, escape_ranges
     k, n, L = cfg.k, cfg.n, cfg.L
     S = min(args.e2e_stripes, cfg.stripes)
+    chunk = max(1, min(S, args.e2e_chunk))
     src_h = torch.from_numpy(W.symbols(seed + 7, 0, S * k * L).view(np.int16).reshape(S, k, L)).pin_memory()
     pats, sp = W.patterns(cfg, seed=seed + 7, stripes=S)
-    # received packets prepared once on the host (the erasure channel, not the codec)
+    pats_h = torch.from_numpy(pats.astype(np.int32)).pin_memory()
+    # received packets prepared once (the erasure channel, not the codec)
     d_src = src_h.to(dev)
     enc0, e0, c0 = codec.encode(k, n, d_src)
     rx0, rxe0 = W.received_packets(enc0, e0, c0, pats, sp, n)
     rx_h = rx0.cpu().pin_memory()
-    rxe_h = rxe0.cpu().pin_memory() if rxe0 is not None else None
+    rxe_np = rxe0.cpu().numpy().view(np.uint64) if rxe0 is not None else np.zeros(0, np.uint64)
+    rxe_h = torch.from_numpy(rxe_np.view(np.int64)).pin_memory() if rxe_np.size else None
     del enc0, rx0, d_src
+    nch = (S + chunk - 1) // chunk
+    ranges = escape_ranges(rxe_np, S, chunk, k, L)
+    pipe = HostPipeline(codec, k, n, L, chunk)
     enc_h = torch.empty((S, n, L), dtype=torch.int16).pin_memory()
     dec_h = torch.empty((S, k, L), dtype=torch.int16).pin_memory()
-    cnt_h = torch.zeros(2, dtype=torch.int64).pin_memory()
-    d_src = torch.empty((S, k, L), dtype=torch.int16, device=dev)
-    d_rx = torch.empty_like(d_src)
-    d_enc = torch.empty((S, n, L), dtype=torch.int16, device=dev)
-    d_dec = torch.empty_like(d_src)
+    enc_esc_h = torch.empty((nch, pipe.cap_e), dtype=torch.int64).pin_memory()
+    dec_esc_h = torch.empty((nch, pipe.cap_e), dtype=torch.int64).pin_memory()
+    cnt_h = torch.zeros(2 * nch, dtype=torch.int64).pin_memory()
     sp_d = torch.from_numpy(sp.astype(np.int32)).to(dev)
-    h2d = d_src.numel() * 2 + d_rx.numel() * 2 + (rxe_h.numel() * 8 if rxe_h is not None else 0) + sp.nbytes
-    d2h = enc_h.numel() * 2 + dec_h.numel() * 2 + 16
+    h2d = src_h.numel() * 2 + rx_h.numel() * 2 + (rxe_h.numel() * 8 if rxe_h is not None else 0) + pats_h.numel() * 4
+    d2h = enc_h.numel() * 2 + dec_h.numel() * 2 + enc_esc_h.numel() * 8 + dec_esc_h.numel() * 8 + cnt_h.numel() * 8
 
     def step():
-        d_src.copy_(src_h, non_blocking=True)
-        _, _, ce = codec.encode(k, n, d_src, out=d_enc)
-        enc_h.copy_(d_enc, non_blocking=True)
-        d_rx.copy_(rx_h, non_blocking=True)
-        rxe = rxe_h.to(dev, non_blocking=True) if rxe_h is not None else None
-        plans = codec.plans(k, n, pats)
-        _, _, cd = codec.decode(plans, sp_d, d_rx, rxe, out=d_dec)
-        dec_h.copy_(d_dec, non_blocking=True)
-        cnt_h[0:1].copy_(ce, non_blocking=True)
-        cnt_h[1:2].copy_(cd, non_blocking=True)
+        pipe.encode_host(src_h, enc_h, enc_esc_h, cnt_h[:nch])
+        rxe_d = rxe_h.to(dev, non_blocking=True) if rxe_h is not None else None
+        plans = codec.plans(k, n, pats_h)
+        pipe.decode_host(plans, sp_d, rx_h, rxe_d, dec_h, dec_esc_h, cnt_h[nch:], ranges)
+        pipe.join()
         return plans
 
     for _ in range(max(1, args.warmup)):
@@ -388,6 +390,7 @@ def run_e2e(args, codec, cfg, dev, stream, seed, world):
     torch.cuda.synchronize(dev)
     assert torch.equal(dec_h, src_h), "e2e decode mismatch"
     if world > 1:
+        import torch.distributed as dist
         dist.barrier()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     steps = max(1, args.steps)
@@ -401,7 +404,8 @@ def run_e2e(args, codec, cfg, dev, stream, seed, world):
     total_src = 2 * k * L * S * world
     return {"value": round(total_src / (ms * 1e-3) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ms, 3),
-            "sample": f"{S} stripes/GPU of {cfg.name} via Codec.encode/plans/decode (C ABI) from pinned host memory"}
+            "sample": f"{S} stripes/GPU of {cfg.name} from pinned host memory via HostPipeline "
+                      f"(Codec.encode/plans/decode C-ABI calls, {chunk}-stripe chunks on 3 streams)"}
 
 
 def cpu_baseline(cfg, budget_s):
@@ -459,6 +463,7 @@ def main():
     ap.add_argument("--chunk", type=int, default=8192, help="stripes per kernel launch")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--e2e-stripes", type=int, default=4096)
+    ap.add_argument("--e2e-chunk", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-step-seconds", type=float, default=6.0)
