@@ -26,14 +26,8 @@ struct fntrs_ctx {
     fast::FastTables ftab;
     bool fast_enabled = true;
     cudaStream_t internal = nullptr;
-    void* sort_tmp = nullptr;
-    size_t sort_tmp_bytes = 0;
-    unsigned long long* sort_alt = nullptr;
-    uint64_t sort_alt_cap = 0;
     uint64_t launches = 0;
     std::string err;
-    uint32_t* scratch[2] = {nullptr, nullptr};  // four-step intermediates (stream-ordered)
-    size_t scratch_bytes = 0;
     fast::LogTables ltab;
     std::map<std::pair<uint32_t, uint32_t>, uint32_t*> digit_spectra;  // (N, w) -> Dh [N][D]
 };
@@ -100,46 +94,40 @@ int sort_escapes(fntrs_ctx* ctx, unsigned long long* keys, uint64_t cap, uint64_
                  cudaStream_t st) {
     if (cap <= 1) return FNTRS_OK;
     if (cap > 0x7FFFFFFFull) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "escape capacity too large");
-    if (ctx->sort_alt_cap < cap) {
-        if (ctx->sort_alt) cudaFree(ctx->sort_alt);
-        ctx->sort_alt = nullptr;
-        CK(cudaMalloc(&ctx->sort_alt, cap * sizeof(unsigned long long)), "escape scratch");
-        ctx->sort_alt_cap = cap;
-    }
-    cub::DoubleBuffer<unsigned long long> db(keys, ctx->sort_alt);
-    // Keys past the real ones are all ~0; sort the full word so they stay last.
+    // per-call, stream-ordered scratch: calls on different streams never share it
     (void)max_key;
-    const int end_bit = 64;
+    unsigned long long* alt = nullptr;
+    void* tmp = nullptr;
     size_t need = 0;
-    CK(cub::DeviceRadixSort::SortKeys(nullptr, need, db, int(cap), 0, end_bit, st), "escape sort size");
-    if (need > ctx->sort_tmp_bytes) {
-        if (ctx->sort_tmp) cudaFree(ctx->sort_tmp);
-        ctx->sort_tmp = nullptr;
-        CK(cudaMalloc(&ctx->sort_tmp, need), "escape sort scratch");
-        ctx->sort_tmp_bytes = need;
-    }
-    CK(cub::DeviceRadixSort::SortKeys(ctx->sort_tmp, need, db, int(cap), 0, end_bit, st), "escape sort");
+    CK(cudaMallocAsync(&alt, cap * sizeof(unsigned long long), st), "escape scratch");
+    cub::DoubleBuffer<unsigned long long> db(keys, alt);
+    // Keys past the real ones are all ~0; sort the full word so they stay last.
+    CK(cub::DeviceRadixSort::SortKeys(nullptr, need, db, int(cap), 0, 64, st), "escape sort size");
+    CK(cudaMallocAsync(&tmp, need, st), "escape sort scratch");
+    CK(cub::DeviceRadixSort::SortKeys(tmp, need, db, int(cap), 0, 64, st), "escape sort");
     ctx->launches += 2 * 8;  // onesweep: histogram + 8 digit passes (approximate)
     if (db.Current() != keys)
         CK(cudaMemcpyAsync(keys, db.Current(), cap * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st),
            "escape copy");
+    cudaFreeAsync(tmp, st);
+    cudaFreeAsync(alt, st);
     return FNTRS_OK;
 }
 
 constexpr size_t kScratchCap = size_t(2) << 30;  // per four-step intermediate buffer
 
-// Two stream-ordered scratch buffers of at least `bytes` each.
-int ensure_scratch(fntrs_ctx* ctx, size_t bytes, cudaStream_t st) {
-    if (ctx->scratch_bytes >= bytes) return FNTRS_OK;
-    for (auto& p : ctx->scratch)
-        if (p) {
-            cudaFreeAsync(p, st);
-            p = nullptr;
-        }
-    ctx->scratch_bytes = 0;
-    for (auto& p : ctx->scratch) CK(cudaMallocAsync(&p, bytes, st), "scratch alloc");
-    ctx->scratch_bytes = bytes;
+// Per-call stream-ordered scratch (released in stream order by release_scratch),
+// so concurrent calls on different streams never share intermediates.
+struct Scratch {
+    uint32_t* p[2] = {nullptr, nullptr};
+};
+int get_scratch(fntrs_ctx* ctx, Scratch& s, size_t bytes, int count, cudaStream_t st) {
+    for (int i = 0; i < count; ++i) CK(cudaMallocAsync(&s.p[i], bytes, st), "scratch alloc");
     return FNTRS_OK;
+}
+void release_scratch(Scratch& s, cudaStream_t st) {
+    for (auto& q : s.p)
+        if (q) cudaFreeAsync(q, st);
 }
 
 int prep_escapes(fntrs_ctx* ctx, uint64_t* out_esc, uint64_t esc_cap, uint64_t* n_out_esc, cudaStream_t st) {
@@ -246,13 +234,9 @@ int fntrs_gpu_destroy(fntrs_ctx* ctx) {
     cudaFree(ctx->ftab.big_fwd);
     cudaFree(ctx->ftab.big_inv);
     cudaDeviceSynchronize();
-    cudaFree(ctx->scratch[0]);
-    cudaFree(ctx->scratch[1]);
     cudaFree(ctx->ltab.exp3);
     cudaFree(ctx->ltab.log3);
     for (auto& kv : ctx->digit_spectra) cudaFree(kv.second);
-    cudaFree(ctx->sort_tmp);
-    cudaFree(ctx->sort_alt);
     if (ctx->internal) cudaStreamDestroy(ctx->internal);
     delete ctx;
     return FNTRS_OK;
@@ -284,10 +268,12 @@ int fntrs_gpu_encode(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t stripes, u
     if (large) {
         if (stripes && L) {
             const uint32_t batch = std::min(stripes, fast::large_batch(N, L, kScratchCap));
-            rc = ensure_scratch(ctx, size_t(batch) * N * L * 4, st);
+            Scratch sc;
+            rc = get_scratch(ctx, sc, size_t(batch) * N * L * 4, 1, st);
             if (rc) return rc;
-            CK(fast::launch_encode_large(ctx->ftab, k, n, N, stripes, L, src, ein, out, eout, ctx->scratch[0], batch, st),
-               "encode launch");
+            cudaError_t le = fast::launch_encode_large(ctx->ftab, k, n, N, stripes, L, src, ein, out, eout, sc.p[0], batch, st);
+            release_scratch(sc, st);
+            CK(le, "encode launch");
             ctx->launches += 2 * ((stripes + batch - 1) / batch);
         }
         return sort_escapes(ctx, eout.keys, esc_cap, uint64_t(stripes) * n * L, st);
@@ -425,11 +411,13 @@ int fntrs_gpu_plans_export(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t patte
         CK(launch_fnt_tile(ctx->tab, M, true, kP - 1u, 1, ah, acoef, st), "export ifnt");
         CK(launch_fnt_tile(ctx->tab, M, false, 1u, 1, acoef, spec, st), "export fnt");
     } else {  // A = IFNT_M(-M ahat): scale the inverse by -M * (1/M) = -1 via a forward-then-negate pair
-        int rc = ensure_scratch(ctx, size_t(M) * 4, st);
+        Scratch sc;
+        int rc = get_scratch(ctx, sc, size_t(M) * 4 + 256, 1, st);
         if (rc) return rc;
-        CK(fast::launch_fnt_cols(ctx->ftab, M, true, 1, ah, ctx->scratch[0], spec, st), "export ifnt");
+        CK(fast::launch_fnt_cols(ctx->ftab, M, true, 1, ah, sc.p[0], spec, st), "export ifnt");
         negate_scale_kernel<<<(M + 255) / 256, 256, 0, st>>>(spec, acoef, M, kP - (M % kP));  // * (-M)
-        CK(fast::launch_fnt_cols(ctx->ftab, M, false, 1, acoef, ctx->scratch[0], spec, st), "export fnt");
+        CK(fast::launch_fnt_cols(ctx->ftab, M, false, 1, acoef, sc.p[0], spec, st), "export fnt");
+        release_scratch(sc, st);
     }
     ctx->launches += 2;
     std::vector<uint32_t> a(M), sp(M);
@@ -480,12 +468,14 @@ int fntrs_gpu_decode(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t stripes, ui
             return fail(ctx, FNTRS_E_UNSUPPORTED, "n_domain > 4096 needs L to be a multiple of 64 in this build");
         if (stripes && L) {
             const uint32_t batch = std::min(stripes, fast::large_batch(pl->N, L, kScratchCap));
-            rc = ensure_scratch(ctx, size_t(batch) * pl->N * L * 4, st);
+            Scratch sc;
+            rc = get_scratch(ctx, sc, size_t(batch) * pl->N * L * 4, 2, st);
             if (rc) return rc;
             fast::FastPlanView fv{pl->N, pl->k, pl->rowmap, pl->ahat2};
-            CK(fast::launch_decode_large(ctx->ftab, fv, stripes, L, stripe_pattern, rx, ein, out, eout, ctx->scratch[0],
-                                         ctx->scratch[1], batch, st),
-               "decode launch");
+            cudaError_t le = fast::launch_decode_large(ctx->ftab, fv, stripes, L, stripe_pattern, rx, ein, out, eout,
+                                                       sc.p[0], sc.p[1], batch, st);
+            release_scratch(sc, st);
+            CK(le, "decode launch");
             ctx->launches += 4 * ((stripes + batch - 1) / batch);
         }
     } else if (fast_ok) {
@@ -507,9 +497,12 @@ int fntrs_gpu_fnt(fntrs_ctx* ctx, uint32_t m, int inverse, uint32_t L, const uin
     DeviceGuard g(ctx->device);
     if (m > kTileMaxN) {  // column-batched four-step kernels (plan_fast.cu)
         cudaStream_t st = static_cast<cudaStream_t>(stream);
-        int rc = ensure_scratch(ctx, size_t(m) * L * 4, st);
+        Scratch sc;
+        int rc = get_scratch(ctx, sc, size_t(m) * L * 4 + 256, 1, st);
         if (rc) return rc;
-        CK(fast::launch_fnt_cols(ctx->ftab, m, inverse != 0, L, in, ctx->scratch[0], out, st), "fnt launch");
+        cudaError_t le = fast::launch_fnt_cols(ctx->ftab, m, inverse != 0, L, in, sc.p[0], out, st);
+        release_scratch(sc, st);
+        CK(le, "fnt launch");
         ctx->launches += 2;
         return FNTRS_OK;
     }
