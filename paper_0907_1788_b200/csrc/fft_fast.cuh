@@ -195,20 +195,159 @@ struct DitAll {
     }
 };
 
+// ---- direct R-point DFTs, natural order in and out ---------------------------
+// y[s] = sum_q x[q] w_R^(qs), w_R = root of order R (inverse root when INV).
+// R = 16 is 4 x 4 (Cooley-Tukey): four 4-point DFTs over stride-4 inputs, the
+// nine non-trivial twiddles w16^(q2 s1) (powers of two), four 4-point DFTs.
+// A 4-point DFT with three-input adds:
+//   B = x1+x3, Y0 = x0+x2+B, Y2 = x0+x2-B, D = w4 (x1-x3), Y1 = x0-x2+D, Y3 = x0-x2-D
+// is 6 adds + 1 shift-multiply (vs 8 + 1 as two radix-2 stages).
+template <int R>
+__host__ __device__ constexpr int rev(int i);
+
+template <bool INV, uint64_t B>
+struct Dft4 {
+    static constexpr int E4 = INV ? 8 : 24;  // w4 = 2^24 = -2^8; w4^-1 = 2^8
+    using M = MulPow2<E4, 2 * B>;
+    static constexpr uint64_t OUT = umax(4 * B, 2 * B + M::OUT);
+    __device__ __forceinline__ static void run(uint32_t x0, uint32_t x1, uint32_t x2, uint32_t x3, uint32_t& y0,
+                                               uint32_t& y1, uint32_t& y2, uint32_t& y3) {
+        const uint32_t b = x1 + x3;
+        const uint32_t d = M::apply(x1 - x3);
+        y0 = x0 + x2 + b;
+        y2 = x0 + x2 - b;
+        y1 = x0 - x2 + d;
+        y3 = x0 - x2 - d;
+    }
+};
+
+template <int R, bool INV, uint64_t B>
+struct Dft;
+
+template <bool INV, uint64_t B>
+struct Dft<1, INV, B> {
+    static constexpr uint64_t OUT = B;
+    __device__ __forceinline__ static void run(const uint32_t (&)[1], uint32_t (&y)[1]) {}
+};
+
+template <bool INV, uint64_t B>
+struct Dft<2, INV, B> {
+    static constexpr uint64_t OUT = 2 * B;
+    __device__ __forceinline__ static void run(const uint32_t (&x)[2], uint32_t (&y)[2]) {
+        y[0] = x[0] + x[1];
+        y[1] = x[0] - x[1];
+    }
+};
+
+template <bool INV, uint64_t B>
+struct Dft<4, INV, B> {
+    static constexpr uint64_t OUT = Dft4<INV, B>::OUT;
+    __device__ __forceinline__ static void run(const uint32_t (&x)[4], uint32_t (&y)[4]) {
+        Dft4<INV, B>::run(x[0], x[1], x[2], x[3], y[0], y[1], y[2], y[3]);
+    }
+};
+
+// twiddle w_R^(e) applied to a value of bound B (R <= 32: powers of two)
+template <int R, int EXP, bool INV, uint64_t B>
+struct TwR {
+    static constexpr int e2 = Tw<R, (EXP % R + R) % R, INV>::e2;
+    using M = MulPow2<e2, B>;
+    static constexpr bool trivial = (EXP % R) == 0;
+    static constexpr uint64_t OUT = trivial ? B : M::OUT;
+    __device__ __forceinline__ static uint32_t apply(uint32_t x) {
+        if constexpr (trivial)
+            return x;
+        else
+            return M::apply(x);
+    }
+};
+
+// R = 8: 2 x 4 (q = 2 q1 + q2, s = s1 + 4 s2): DFT4 over q1 for each q2,
+// twiddle w8^(q2 s1), DFT2 over q2.
+template <bool INV, uint64_t B>
+struct Dft<8, INV, B> {
+    static constexpr uint64_t B1 = Dft4<INV, B>::OUT;
+    static constexpr uint64_t BT = umax(umax(TwR<8, 1, INV, B1>::OUT, TwR<8, 2, INV, B1>::OUT), TwR<8, 3, INV, B1>::OUT);
+    static constexpr uint64_t OUT = 2 * umax(B1, BT);
+    __device__ __forceinline__ static void run(const uint32_t (&x)[8], uint32_t (&y)[8]) {
+        uint32_t z0[4], z1[4];
+        Dft4<INV, B>::run(x[0], x[2], x[4], x[6], z0[0], z0[1], z0[2], z0[3]);
+        Dft4<INV, B>::run(x[1], x[3], x[5], x[7], z1[0], z1[1], z1[2], z1[3]);
+        z1[1] = TwR<8, 1, INV, B1>::apply(z1[1]);
+        z1[2] = TwR<8, 2, INV, B1>::apply(z1[2]);
+        z1[3] = TwR<8, 3, INV, B1>::apply(z1[3]);
+#pragma unroll
+        for (int s1 = 0; s1 < 4; ++s1) {
+            y[s1] = z0[s1] + z1[s1];
+            y[s1 + 4] = z0[s1] - z1[s1];
+        }
+    }
+};
+
+template <bool INV, uint64_t B, int Q2, int S1>
+struct Tw16 {
+    using T = TwR<16, Q2 * S1, INV, Dft4<INV, B>::OUT>;
+};
+
+template <bool INV, uint64_t B>
+struct Dft<16, INV, B> {
+    static constexpr uint64_t B1 = Dft4<INV, B>::OUT;
+    static constexpr uint64_t tw_bound() {
+        uint64_t m = B1;
+        m = umax(m, TwR<16, 1, INV, B1>::OUT);
+        m = umax(m, TwR<16, 2, INV, B1>::OUT);
+        m = umax(m, TwR<16, 3, INV, B1>::OUT);
+        m = umax(m, TwR<16, 4, INV, B1>::OUT);
+        m = umax(m, TwR<16, 6, INV, B1>::OUT);
+        m = umax(m, TwR<16, 9, INV, B1>::OUT);
+        return m;
+    }
+    static constexpr uint64_t BT = tw_bound();
+    static constexpr uint64_t OUT = Dft4<INV, BT>::OUT;
+    template <int Q2, int S1>
+    __device__ __forceinline__ static uint32_t tw(uint32_t x) {
+        return TwR<16, Q2 * S1, INV, B1>::apply(x);
+    }
+    __device__ __forceinline__ static void run(const uint32_t (&x)[16], uint32_t (&y)[16]) {
+        uint32_t z[4][4];  // z[q2][s1]
+#pragma unroll
+        for (int q2 = 0; q2 < 4; ++q2) Dft4<INV, B>::run(x[q2], x[q2 + 4], x[q2 + 8], x[q2 + 12], z[q2][0], z[q2][1], z[q2][2], z[q2][3]);
+        z[1][1] = tw<1, 1>(z[1][1]);
+        z[1][2] = tw<1, 2>(z[1][2]);
+        z[1][3] = tw<1, 3>(z[1][3]);
+        z[2][1] = tw<2, 1>(z[2][1]);
+        z[2][2] = tw<2, 2>(z[2][2]);
+        z[2][3] = tw<2, 3>(z[2][3]);
+        z[3][1] = tw<3, 1>(z[3][1]);
+        z[3][2] = tw<3, 2>(z[3][2]);
+        z[3][3] = tw<3, 3>(z[3][3]);
+#pragma unroll
+        for (int s1 = 0; s1 < 4; ++s1)
+            Dft4<INV, BT>::run(z[0][s1], z[1][s1], z[2][s1], z[3][s1], y[s1], y[s1 + 4], y[s1 + 8], y[s1 + 12]);
+    }
+};
+
+// DIF placement: natural in, v[rev(s)] = y_s out. DIT placement: v[rev(s)] in, natural out.
 template <int R, bool INV, uint64_t BIN>
 __device__ __forceinline__ void dif_regs(uint32_t (&v)[R]) {
-    static_assert(DifAll<R, INV, R / 2, BIN>::OUT < (1ull << 31), "lazy bound overflow");
-    DifAll<R, INV, R / 2, BIN>::run(v);
+    static_assert(Dft<R, INV, BIN>::OUT < (1ull << 31), "lazy bound overflow");
+    uint32_t y[R];
+    Dft<R, INV, BIN>::run(v, y);
+#pragma unroll
+    for (int s = 0; s < R; ++s) v[rev<R>(s)] = y[s];
 }
 template <int R, bool INV, uint64_t BIN>
 __device__ __forceinline__ void dit_regs(uint32_t (&v)[R]) {
-    static_assert(DitAll<R, INV, 1, BIN>::OUT < (1ull << 31), "lazy bound overflow");
-    DitAll<R, INV, 1, BIN>::run(v);
+    static_assert(Dft<R, INV, BIN>::OUT < (1ull << 31), "lazy bound overflow");
+    uint32_t x[R];
+#pragma unroll
+    for (int s = 0; s < R; ++s) x[s] = v[rev<R>(s)];
+    Dft<R, INV, BIN>::run(x, v);
 }
 template <int R, bool INV, uint64_t BIN>
-constexpr uint64_t dif_bound() { return DifAll<R, INV, R / 2, BIN>::OUT; }
+constexpr uint64_t dif_bound() { return Dft<R, INV, BIN>::OUT; }
 template <int R, bool INV, uint64_t BIN>
-constexpr uint64_t dit_bound() { return DitAll<R, INV, 1, BIN>::OUT; }
+constexpr uint64_t dit_bound() { return Dft<R, INV, BIN>::OUT; }
 
 template <int R>
 __host__ __device__ constexpr int rev(int i) {
