@@ -283,29 +283,32 @@ __global__ void __launch_bounds__(G::NT, G::MINB) dec_fast_kernel(const __grid_c
                 const uint32_t col = uint32_t(it) & uint32_t(WT - 1);
                 const uint32_t t = uint32_t(it) >> LGW;
                 uint32_t v[R0];
-                const uint2* tpf = reinterpret_cast<const uint2*>(tF0) + t * R0;
-                const uint2* tpi = reinterpret_cast<const uint2*>(tI0) + t * R0;
+                const uint4* tpf = tF0 + t * (R0 / 2);
+                const uint4* tpi = tI0 + t * (R0 / 2);
+                uint4 w4 = make_uint4(0, 0, 0, 0);
 #pragma unroll
                 for (int s = 0; s < R0; ++s) {
                     uint32_t x = work[G::idx((t + (uint32_t(s) << SL0)) ^ FLIP, col)];
                     if (s > 0) {
-                        const uint2 w = __ldg(tpf + s);
+                        const uint2 w = tw_at(tpf, s, w4);
                         x = mulws(x, w.x, w.y);
                     }
                     v[rev<R0>(s)] = x;
                 }
                 dit_regs<R0, false, kSmemCap>(v);
+                const uint4* ahq = reinterpret_cast<const uint4*>(ah) + t * (R0 / 2);  // ahat2_slot order
 #pragma unroll
-                for (int q = 0; q < R0; ++q) {
-                    const uint2 a = __ldg(ah + t + (uint32_t(q) << SL0));
+                for (int q = 0; q < R0; q += 2) {
+                    const uint4 a = __ldg(ahq + q / 2);
                     v[q] = mulws(v[q], a.x, a.y);
+                    v[q + 1] = mulws(v[q + 1], a.z, a.w);
                 }
                 dif_regs<R0, true, k2P>(v);
 #pragma unroll
                 for (int s = 0; s < R0; ++s) {
                     uint32_t y = v[rev<R0>(s)];
                     if (s > 0) {
-                        const uint2 w = __ldg(tpi + s);
+                        const uint2 w = tw_at(tpi, s, w4);
                         y = mulws(y, w.x, w.y);
                     } else {
                         y = cap<BO, kSmemCap>(y);
@@ -342,7 +345,7 @@ __global__ void fast_plan_tables_kernel(uint32_t N, const uint32_t* __restrict__
     for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < total; j += uint64_t(gridDim.x) * blockDim.x) {
         rowmap[j] = make_uint2(0xFFFFFFFFu, 0u);
         const int32_t a = balanced(ahat[j]);  // signed Shoup pair
-        ahat2[j] = make_uint2(uint32_t(a), uint32_t(a * 65535));
+        ahat2[(j & ~uint64_t(N - 1)) | ahat2_slot(N, uint32_t(j) & (N - 1))] = make_uint2(uint32_t(a), uint32_t(a * 65535));
     }
 }
 

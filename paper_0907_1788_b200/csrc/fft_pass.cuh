@@ -119,6 +119,13 @@ struct NoFlush {
     __device__ __forceinline__ void operator()(uint32_t, uint32_t, uint32_t, uint32_t) const {}
 };
 
+// twiddle s of a row stored as uint4 pairs; s is a compile-time constant after
+// unrolling, so each pair is loaded once (on its first use, s = 1 or s even)
+__device__ __forceinline__ uint2 tw_at(const uint4* __restrict__ tq, int s, uint4& w4) {
+    if (s == 1 || (s & 1) == 0) w4 = __ldg(tq + (s >> 1));
+    return (s & 1) ? make_uint2(w4.z, w4.w) : make_uint2(w4.x, w4.y);
+}
+
 template <int E, int p, bool INV, bool DIT, uint64_t BIN, uint64_t OCAP, class G, class LD, class ST,
           class FIX = NoFix, class FLUSH = NoFlush>
 __device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld, const ST& st, const FIX& fix = FIX(),
@@ -135,8 +142,9 @@ __device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld
         const uint32_t t = b & ((1u << SL) - 1u);
         const uint32_t base = ((b >> SL) << LL) + t;
         uint32_t v[R];
-        const uint2* tp = reinterpret_cast<const uint2*>(twp) + t * R;  // row t: r_len^(t s), s < R
+        const uint4* tq = twp + t * (R / 2);  // row t: r_len^(t s), s < R, two per uint4
         uint32_t mask = 0;
+        uint4 w4 = make_uint4(0, 0, 0, 0);
         if constexpr (!DIT) {
 #pragma unroll
             for (int q = 0; q < R; ++q) v[q] = ld(base + (uint32_t(q) << SL), b, q, col);
@@ -147,7 +155,7 @@ __device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld
             for (int s = 0; s < R; ++s) {
                 uint32_t y = v[rev<R>(s)];
                 if (SL > 0 && s > 0) {
-                    const uint2 w = __ldg(tp + s);
+                    const uint2 w = tw_at(tq, s, w4);
                     y = mulws(y, w.x, w.y);
                     if constexpr (OCAP == kCanon) y = canon_s2p(y);
                 } else {
@@ -161,7 +169,7 @@ __device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld
             for (int s = 0; s < R; ++s) {
                 uint32_t x = ld(base + (uint32_t(s) << SL), b, s, col);
                 if (SL > 0 && s > 0) {
-                    const uint2 w = __ldg(tp + s);
+                    const uint2 w = tw_at(tq, s, w4);
                     x = mulws(x, w.x, w.y);
                 }
                 v[rev<R>(s)] = x;

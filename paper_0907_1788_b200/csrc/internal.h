@@ -77,8 +77,17 @@ struct FastTables {
 struct FastPlanView {
     uint32_t N, k;
     const uint2* rowmap;  // [np][N] {received row or ~0, 1/A'(x_i)}
-    const uint2* ahat2;   // [np][N] {ahat_j, 65535 ahat_j}
+    const uint2* ahat2;   // [np][N] {ahat_j, 65535 ahat_j} at slot ahat2_slot(N, j)
 };
+// Storage slot of ahat2 entry j (0 <= j < N, N a power of two). For the fused
+// N <= 4096 decode kernel the table is kept in first-pass order, j = t + q 2^(E-4)
+// -> t*16 + q, so each thread's 16 multipliers are two-per-uint4 contiguous;
+// the four-step kernels (N >= 8192) read it in natural order.
+__host__ __device__ inline uint32_t ahat2_slot(uint32_t N, uint32_t j) {
+    if (N < 16 || N > 4096) return j;
+    const uint32_t sl0 = uint32_t(31 - __builtin_clz(N)) - 4u;
+    return ((j & ((1u << sl0) - 1u)) << 4) | (j >> sl0);
+}
 cudaError_t build_fast_tables(FastTables& t, cudaStream_t st);
 int fast_tile_columns(uint32_t N);  // 0 when N has no fast kernel
 cudaError_t launch_encode_fast(const FastTables& t, uint32_t k, uint32_t n, uint32_t N, uint32_t stripes,

@@ -298,7 +298,7 @@ __global__ void plan_ahat_kernel(uint32_t N, uint32_t P, const uint32_t* __restr
         }
         ahat[t] = a;
         const int32_t ab = balanced(a);
-        ahat2[t] = make_uint2(uint32_t(ab), uint32_t(ab * 65535));
+        ahat2[size_t(p) * N + ahat2_slot(N, uint32_t(t - uint64_t(p) * N))] = make_uint2(uint32_t(ab), uint32_t(ab * 65535));
     }
 }
 
