@@ -214,10 +214,10 @@ __global__ void __launch_bounds__(G::NT, G::MINB) dec_fast_kernel(const __grid_c
             return 0u;
         };
         auto ld_smf = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t {
-            return work[G::idx(lrow ^ FLIP, col)];
+            return work[G::template idx_flip<FLIP + 1>(lrow, col)];
         };
         auto st_smf = [&](uint32_t lrow, uint32_t, int, uint32_t col, uint32_t y) -> uint32_t {
-            work[G::idx(lrow ^ FLIP, col)] = y;
+            work[G::template idx_flip<FLIP + 1>(lrow, col)] = y;
             return 0u;
         };
         auto st_out = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) -> uint32_t {
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) dec_fast_kernel(const __grid_c
                 uint4 w4 = make_uint4(0, 0, 0, 0);
 #pragma unroll
                 for (int s = 0; s < R0; ++s) {
-                    uint32_t x = work[G::idx((t + (uint32_t(s) << SL0)) ^ FLIP, col)];
+                    uint32_t x = work[G::template idx_flip<FLIP + 1>(t + (uint32_t(s) << SL0), col)];
                     if (s > 0) {
                         const uint2 w = tw_at(tpf, s, w4);
                         x = mulws(x, w.x, w.y);
@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) dec_fast_kernel(const __grid_c
                     } else {
                         y = cap<BO, kSmemCap>(y);
                     }
-                    work[G::idx((t + (uint32_t(s) << SL0)) ^ FLIP, col)] = y;
+                    work[G::template idx_flip<FLIP + 1>(t + (uint32_t(s) << SL0), col)] = y;
                 }
             }
         }

@@ -206,7 +206,7 @@ dec_2_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, uin
         return 0u;
     };
     auto ld_smf = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t {
-        return work[G::idx(lrow ^ FLIP, col)];
+        return work[G::template idx_flip<FLIP + 1>(lrow, col)];
     };
     auto st_y2 = [&](uint32_t q2, uint32_t, int, uint32_t col, uint32_t y) -> uint32_t {
         const uint2 w = __ldg(bigF + N + ((i1p * q2) & (N - 1)));

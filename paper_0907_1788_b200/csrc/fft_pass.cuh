@@ -93,6 +93,16 @@ struct Geom {
             row ^= (row >> RLZ) & uint32_t(RPW - 1);
         return row * WT + col;
     }
+    // index of row (N2 - 1 - row) for row < N2 (N2 a power of two): the reversed
+    // view. Unswizzled, the subtraction form lets a compile-time row offset fold
+    // into the shared-memory immediate; swizzled, XOR is cheaper.
+    template <uint32_t N2>
+    __device__ __forceinline__ static uint32_t idx_flip(uint32_t row, uint32_t col) {
+        if constexpr (RPW > 1)
+            return idx(row ^ (N2 - 1u), col);
+        else
+            return idx((N2 - 1u) - row, col);
+    }
 };
 
 // tile width / threads per size
