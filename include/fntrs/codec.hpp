@@ -9,8 +9,10 @@
 // fntrs_gpu_decode over stripes x codewords). There is no CPU fallback: a
 // call without a usable CUDA device throws fntrs::Error.
 //
-// Not in this header (outside the accelerated path):
-// the systematic and quadratic "direct" variants.
+// Also the systematic pair (codec.hpp:56-65 of the reference), through
+// fntrs_gpu_encode_systematic / fntrs_gpu_decode_systematic. Not in this
+// header: the quadratic "direct" encoder variants (encode_systematic_direct,
+// encode_systematic_intermediate_direct), CPU cross-checks in the reference.
 #pragma once
 
 #include <cstdint>
@@ -54,6 +56,16 @@ std::vector<Fe> encode_nonsystematic(const CodeParams& params, std::span<const F
 // transform). Throws NotEnoughSymbols, DuplicatePosition, PositionOutOfRange.
 std::vector<Fe> decode_nonsystematic(const CodeParams& params, const Codeword& received,
                                      Path path = Path::Auto);
+
+// Systematic: outputs 0..k-1 are the source, k..n-1 the parity (interpolate
+// at positions 0..k-1, then the punctured forward transform).
+std::vector<Fe> encode_systematic(const CodeParams& params, std::span<const Fe> source,
+                                  Path path = Path::Auto);
+
+// The k source symbols from any >= k received symbols of a systematic codeword
+// (the k lowest positions are used). Same exceptions as decode_nonsystematic.
+std::vector<Fe> decode_systematic(const CodeParams& params, const Codeword& received,
+                                  Path path = Path::Auto);
 
 }  // namespace fntrs::codec
 

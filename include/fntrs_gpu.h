@@ -125,6 +125,29 @@ int fntrs_gpu_decode(fntrs_ctx* ctx, const fntrs_plans* plans, uint32_t stripes,
                      uint64_t n_rx_esc, uint16_t* out, uint64_t* out_esc, uint64_t esc_cap,
                      uint64_t* n_out_esc, void* stream);
 
+/* Batched systematic codec (proj/src/codec.cpp:151-196); symbols 0..k-1 of
+ * every codeword are the source itself.
+ *   encode_systematic: P = interpolate(positions 0..k-1, source)
+ *     (codec.cpp:156-159), out = FNT_{n_domain}(P) truncated to n
+ *     (transform_of_padded, codec.cpp:75-82). Buffers as in fntrs_gpu_encode.
+ *   decode_systematic: P = interpolate(the plan's k positions, rx)
+ *     (interpolate_selected, codec.cpp:85-94), out = FNT_{n_domain}(P)
+ *     truncated to k. Plans/buffers as in fntrs_gpu_decode; out [stripes][k][L].
+ *     Stripes whose pattern is 0..k-1 reproduce rx exactly, which is the
+ *     reference's systematic_prefix_present copy (codec.cpp:167-171).
+ * Both run the interpolation kernels into a stream-ordered intermediate and
+ * then the forward transform kernels; the intermediate's escape count is read
+ * back once, so each call synchronises `stream` once. rate 1 (k == n) encode
+ * is a device copy. */
+int fntrs_gpu_encode_systematic(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t stripes, uint32_t L,
+                                const uint16_t* src, const uint64_t* src_esc, uint64_t n_src_esc,
+                                uint16_t* out, uint64_t* out_esc, uint64_t esc_cap, uint64_t* n_out_esc,
+                                void* stream);
+int fntrs_gpu_decode_systematic(fntrs_ctx* ctx, const fntrs_plans* plans, uint32_t stripes, uint32_t L,
+                                const uint32_t* stripe_pattern, const uint16_t* rx, const uint64_t* rx_esc,
+                                uint64_t n_rx_esc, uint16_t* out, uint64_t* out_esc, uint64_t esc_cap,
+                                uint64_t* n_out_esc, void* stream);
+
 /* fnt_forward / fnt_inverse (proj/src/transform.cpp:302-323) over the columns
  * of a DEVICE [m][L] uint32 array of canonical values; natural order. */
 int fntrs_gpu_fnt(fntrs_ctx* ctx, uint32_t m, int inverse, uint32_t L, const uint32_t* in,

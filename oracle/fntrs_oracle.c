@@ -541,6 +541,81 @@ int orc_decode(uint32_t k, uint32_t n, uint32_t count, const uint32_t* pos, cons
     return rc;
 }
 
+/* ---- systematic codec: proj/src/codec.cpp:151-196 ---------------------------
+ * encode: P = interpolate(positions 0..k-1, source) (codec.cpp:156-159), then
+ * transform_of_padded(P, n_domain, n) (codec.cpp:75-82): symbols 0..k-1 of the
+ * result are the source itself. */
+int orc_encode_systematic(uint32_t k, uint32_t n, const uint32_t* src, uint32_t* out) {
+    uint32_t nd;
+    int rc = orc_code_params(k, n, &nd);
+    if (rc) return rc;
+    uint32_t* pos = (uint32_t*)malloc(sizeof(uint32_t) * k);
+    uint32_t* buf = (uint32_t*)calloc(nd, sizeof(uint32_t));
+    for (uint32_t i = 0; i < k; ++i) pos[i] = i;
+    rc = orc_decode(k, n, k, pos, src, buf); /* the unique degree < k interpolant */
+    if (!rc) {
+        orc_fnt_forward(nd, buf, buf);
+        memcpy(out, buf, sizeof(uint32_t) * n);
+    }
+    free(pos);
+    free(buf);
+    return rc;
+}
+
+/* decode (codec.cpp:163-196): validate and sort like sorted_received; when the
+ * k lowest received positions are exactly 0..k-1 the values are the source
+ * (systematic_prefix_present, codec.cpp:51-55,167-171); otherwise interpolate
+ * the k lowest (interpolate_selected, codec.cpp:85-94) and evaluate the
+ * interpolant at r^0..r^(k-1) (transform_of_padded(P, n_domain, k)). */
+int orc_decode_systematic(uint32_t k, uint32_t n, uint32_t count, const uint32_t* pos, const uint32_t* val,
+                          uint32_t* out) {
+    uint32_t nd;
+    int rc = orc_code_params(k, n, &nd);
+    if (rc) return rc;
+    for (uint32_t i = 0; i < count; ++i)
+        if (pos[i] >= n) return ORC_E_POSITION_OUT_OF_RANGE;
+    sym_t* s = (sym_t*)malloc(sizeof(sym_t) * (count ? count : 1));
+    for (uint32_t i = 0; i < count; ++i) {
+        s[i].pos = pos[i];
+        s[i].val = val[i];
+    }
+    qsort(s, count, sizeof(sym_t), cmp_sym);
+    for (uint32_t i = 1; i < count; ++i)
+        if (s[i].pos == s[i - 1].pos) {
+            free(s);
+            return ORC_E_DUPLICATE_POSITION;
+        }
+    if (count < k) {
+        free(s);
+        return ORC_E_NOT_ENOUGH_SYMBOLS;
+    }
+    int prefix = 1;
+    for (uint32_t i = 0; i < k; ++i)
+        if (s[i].pos != i) prefix = 0;
+    if (prefix) {
+        for (uint32_t i = 0; i < k; ++i) out[i] = s[i].val;
+        free(s);
+        return ORC_OK;
+    }
+    uint32_t* zp = (uint32_t*)malloc(sizeof(uint32_t) * k);
+    uint32_t* vs = (uint32_t*)malloc(sizeof(uint32_t) * k);
+    uint32_t* buf = (uint32_t*)calloc(nd, sizeof(uint32_t));
+    for (uint32_t i = 0; i < k; ++i) {
+        zp[i] = s[i].pos;
+        vs[i] = s[i].val;
+    }
+    free(s);
+    rc = orc_decode(k, n, k, zp, vs, buf);
+    if (!rc) {
+        orc_fnt_forward(nd, buf, buf);
+        memcpy(out, buf, sizeof(uint32_t) * k);
+    }
+    free(zp);
+    free(vs);
+    free(buf);
+    return rc;
+}
+
 /* ---- shardio escape rule: proj/src/shardio.cpp:131-137,153-154,203-208 -
  * 65536 is written as 0x0000 and its index appended (ascending) to the
  * escape list; reading restores 65536 at the listed indices. Returns the

@@ -54,6 +54,9 @@ int orc_code_params(uint32_t k, uint32_t n, uint32_t* n_domain);
 int orc_encode(uint32_t k, uint32_t n, const uint32_t* src, uint32_t* out);
 int orc_decode(uint32_t k, uint32_t n, uint32_t count, const uint32_t* pos, const uint32_t* val,
                uint32_t* out);
+int orc_encode_systematic(uint32_t k, uint32_t n, const uint32_t* src, uint32_t* out);
+int orc_decode_systematic(uint32_t k, uint32_t n, uint32_t count, const uint32_t* pos, const uint32_t* val,
+                          uint32_t* out);
 
 int64_t orc_escape_split(const uint32_t* v, uint64_t count, uint16_t* words, uint32_t* esc);
 void orc_escape_join(const uint16_t* words, uint64_t count, const uint32_t* esc, uint64_t ne,

@@ -132,6 +132,33 @@ int ref_decode(uint32_t k, uint32_t n, uint32_t count, const uint32_t* pos, cons
     }
 }
 
+// Systematic codec (proj/src/codec.cpp:151-196), reference-default path selection.
+int ref_encode_systematic(uint32_t k, uint32_t n, uint32_t src_len, const uint32_t* src, int path,
+                          uint32_t* out) {
+    try {
+        auto params = codec::CodeParams::make(k, n, true);
+        auto v = codec::encode_systematic(params, std::span<const Fe>(src, src_len), path_of(path));
+        std::copy(v.begin(), v.end(), out);
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+int ref_decode_systematic(uint32_t k, uint32_t n, uint32_t count, const uint32_t* pos, const uint32_t* val,
+                          int path, uint32_t* out) {
+    try {
+        auto params = codec::CodeParams::make(k, n, true);
+        codec::Codeword rx(count);
+        for (uint32_t i = 0; i < count; ++i) rx[i] = {pos[i], val[i]};
+        auto v = codec::decode_systematic(params, rx, path_of(path));
+        std::copy(v.begin(), v.end(), out);
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
 // DecodePlan fields (proj/include/fntrs/interp.hpp:18-32).
 int ref_build_plan(uint32_t n, uint32_t k, const uint32_t* positions, uint32_t* a_out,
                    uint32_t* a_len, uint32_t* aprime_inv, uint32_t* product_size,

@@ -7,7 +7,8 @@ include/fntrs_gpu.h); this package is the Python host mirror of the
 reference interface plus the batched API. See DESIGN.md.
 """
 from .codec import (  # noqa: F401
-    Codec, CodeParams, Path, Plans, Symbol, decode_nonsystematic, encode_nonsystematic,
+    Codec, CodeParams, Path, Plans, Symbol, decode_nonsystematic, decode_systematic, encode_nonsystematic,
+    encode_systematic,
     Error, ZeroInverse, InvalidTransformSize, SizeMismatch, ProductTooLarge, DuplicatePoint,
     DuplicatePosition, PositionOutOfRange, TooFewPositions, NotEnoughSymbols, TooManyEscapes,
     UnsupportedShape, default_escape_capacity, escapes_to_numpy,

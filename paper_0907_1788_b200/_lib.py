@@ -33,6 +33,8 @@ SIGNATURES = [
     ("fntrs_gpu_plans_count", _u32, [_vp]),
     ("fntrs_gpu_plans_export", _int, [_vp, _vp, _u32, _vp, _vp, _pu32, _vp]),
     ("fntrs_gpu_decode", _int, [_vp, _vp, _u32, _u32, _vp, _vp, _vp, _u64, _vp, _vp, _u64, _vp, _vp]),
+    ("fntrs_gpu_encode_systematic", _int, [_vp, _u32, _u32, _u32, _u32, _vp, _vp, _u64, _vp, _vp, _u64, _vp, _vp]),
+    ("fntrs_gpu_decode_systematic", _int, [_vp, _vp, _u32, _u32, _vp, _vp, _vp, _u64, _vp, _vp, _u64, _vp, _vp]),
     ("fntrs_gpu_fnt", _int, [_vp, _u32, _int, _u32, _vp, _vp, _vp]),
     ("fntrs_gpu_launch_count", _u64, [_vp]),
     ("fntrs_gpu_set_fast_path", _int, [_vp, _int]),

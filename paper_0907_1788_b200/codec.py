@@ -165,7 +165,7 @@ class Codec:
 
     # -- encode -----------------------------------------------------------
     def encode(self, k: int, n: int, src, src_esc=None, out=None, esc_out=None, esc_cap: int | None = None,
-               count=None, stream=None):
+               count=None, stream=None, systematic: bool = False):
         """src: int16 CUDA tensor [S, k, L] (uint16 bits). Returns (out [S, n, L], esc, count)."""
         torch = _torch()
         S, kk, L = src.shape
@@ -181,10 +181,17 @@ class Codec:
         if count is None:
             count = self._counts[0:1]
         ne = 0 if src_esc is None else src_esc.numel()
-        st = _lib.load().fntrs_gpu_encode(self.ctx, k, n, S, L, _ptr(src), _ptr(src_esc) if ne else None, ne,
-                                          _ptr(out), _ptr(esc_out), esc_cap, _ptr(count), _stream_ptr(stream))
+        fn = _lib.load().fntrs_gpu_encode_systematic if systematic else _lib.load().fntrs_gpu_encode
+        st = fn(self.ctx, k, n, S, L, _ptr(src), _ptr(src_esc) if ne else None, ne,
+                _ptr(out), _ptr(esc_out), esc_cap, _ptr(count), _stream_ptr(stream))
         self._check(st)
         return out, esc_out, count
+
+    def encode_systematic(self, k: int, n: int, src, src_esc=None, out=None, esc_out=None,
+                          esc_cap: int | None = None, count=None, stream=None):
+        """codec::encode_systematic batched (codec.cpp:151-161): rows 0..k-1 of every
+        output stripe are the source; rows k..n-1 the parity. Synchronises `stream` once."""
+        return self.encode(k, n, src, src_esc, out, esc_out, esc_cap, count, stream, systematic=True)
 
     # -- plans ------------------------------------------------------------
     def plans(self, k: int, n: int, positions, stream=None) -> Plans:
@@ -208,7 +215,7 @@ class Codec:
 
     # -- decode -----------------------------------------------------------
     def decode(self, plans: Plans, stripe_pattern, rx, rx_esc=None, out=None, esc_out=None,
-               esc_cap: int | None = None, count=None, stream=None):
+               esc_cap: int | None = None, count=None, stream=None, systematic: bool = False):
         """rx: int16 CUDA tensor [S, kp, L]; stripe_pattern: int32 CUDA tensor [S]."""
         torch = _torch()
         S, kp, L = rx.shape
@@ -223,11 +230,19 @@ class Codec:
         if count is None:
             count = self._counts[1:2]
         ne = 0 if rx_esc is None else rx_esc.numel()
-        st = _lib.load().fntrs_gpu_decode(self.ctx, plans.handle, S, L, _ptr(stripe_pattern), _ptr(rx),
-                                          _ptr(rx_esc) if ne else None, ne, _ptr(out), _ptr(esc_out), esc_cap,
-                                          _ptr(count), _stream_ptr(stream))
+        fn = _lib.load().fntrs_gpu_decode_systematic if systematic else _lib.load().fntrs_gpu_decode
+        st = fn(self.ctx, plans.handle, S, L, _ptr(stripe_pattern), _ptr(rx), _ptr(rx_esc) if ne else None, ne,
+                _ptr(out), _ptr(esc_out), esc_cap, _ptr(count), _stream_ptr(stream))
         self._check(st)
         return out, esc_out, count
+
+    def decode_systematic(self, plans: Plans, stripe_pattern, rx, rx_esc=None, out=None, esc_out=None,
+                          esc_cap: int | None = None, count=None, stream=None):
+        """codec::decode_systematic batched (codec.cpp:163-196): the source rows
+        0..k-1 of every stripe, rebuilt from the packets the plan names.
+        Synchronises `stream` once."""
+        return self.decode(plans, stripe_pattern, rx, rx_esc, out, esc_out, esc_cap, count, stream,
+                           systematic=True)
 
     # -- transform --------------------------------------------------------
     def fnt(self, x, inverse: bool = False, stream=None):
@@ -314,6 +329,10 @@ def _join(words: np.ndarray, esc: np.ndarray) -> list[int]:
 
 def encode_nonsystematic(params: CodeParams, source) -> list[int]:
     """codec::encode_nonsystematic (codec.cpp:124-131): output j is s(r^j), j < n."""
+    return _encode_one(params, source, systematic=False)
+
+
+def _encode_one(params: CodeParams, source, systematic: bool) -> list[int]:
     torch = _torch()
     src = list(source)
     if len(src) != params.k:
@@ -324,13 +343,12 @@ def encode_nonsystematic(params: CodeParams, source) -> list[int]:
         dev = f"cuda:{c.device}"
         t = torch.from_numpy(words.view(np.int16).reshape(1, params.k, 1)).to(dev)
         te = torch.from_numpy(esc).to(dev) if esc.size else None
-        out, oe, cnt = c.encode(params.k, params.n, t, te, esc_cap=params.n)
+        out, oe, cnt = c.encode(params.k, params.n, t, te, esc_cap=params.n, systematic=systematic)
         return _join(out.cpu().numpy().reshape(-1).view(np.uint16), escapes_to_numpy(oe, cnt))
 
 
-def decode_nonsystematic(params: CodeParams, received, path: Path = Path.Auto) -> list[int]:
-    """codec::decode_nonsystematic (codec.cpp:133-149) with sorted_received (:32-48)."""
-    torch = _torch()
+def _sorted_received(params: CodeParams, received) -> list[tuple[int, int]]:
+    """sorted_received (codec.cpp:32-48): range check, sort, duplicates, count."""
     rx = [(int(s.position), int(s.value)) for s in received]
     for p, _ in rx:
         if p >= params.n:
@@ -341,8 +359,30 @@ def decode_nonsystematic(params: CodeParams, received, path: Path = Path.Auto) -
             raise DuplicatePosition(f"received position {rx[i][0]} repeats")
     if len(rx) < params.k:
         raise NotEnoughSymbols(f"have {len(rx)} symbols, need {params.k}")
+    return rx
+
+
+def decode_nonsystematic(params: CodeParams, received, path: Path = Path.Auto) -> list[int]:
+    """codec::decode_nonsystematic (codec.cpp:133-149) with sorted_received (:32-48)."""
+    rx = _sorted_received(params, received)
     full = params.n == params.n_domain and len(rx) == params.n
-    kp = params.n if full else params.k
+    return _decode_one(params, rx, params.n if full else params.k, systematic=False)
+
+
+def decode_systematic(params: CodeParams, received, path: Path = Path.Auto) -> list[int]:
+    """codec::decode_systematic (codec.cpp:163-196): interpolate the k lowest
+    received symbols and evaluate at positions 0..k-1. When those k lowest are
+    0..k-1 the kernels reproduce them exactly (the reference's verbatim copy)."""
+    return _decode_one(params, _sorted_received(params, received), params.k, systematic=True)
+
+
+def encode_systematic(params: CodeParams, source, path: Path = Path.Auto) -> list[int]:
+    """codec::encode_systematic (codec.cpp:151-161): outputs 0..k-1 are the source."""
+    return _encode_one(params, source, systematic=True)
+
+
+def _decode_one(params: CodeParams, rx, kp: int, systematic: bool) -> list[int]:
+    torch = _torch()
     pos = np.array([p for p, _ in rx[:kp]], dtype=np.uint32)
     vals = [v for _, v in rx[:kp]]
     c = _shared_codec()
@@ -362,5 +402,5 @@ def decode_nonsystematic(params: CodeParams, received, path: Path = Path.Auto) -
         t = torch.from_numpy(words.view(np.int16).reshape(1, kp, 1)).to(dev)
         te = torch.from_numpy(esc).to(dev) if esc.size else None
         sp = torch.zeros(1, dtype=torch.int32, device=dev)
-        out, oe, cnt = c.decode(plan, sp, t, te, esc_cap=params.k)
+        out, oe, cnt = c.decode(plan, sp, t, te, esc_cap=params.k, systematic=systematic)
         return _join(out.cpu().numpy().reshape(-1).view(np.uint16), escapes_to_numpy(oe, cnt))

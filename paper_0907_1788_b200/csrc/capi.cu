@@ -30,6 +30,7 @@ struct fntrs_ctx {
     std::string err;
     fast::LogTables ltab;
     std::map<std::pair<uint32_t, uint32_t>, uint32_t*> digit_spectra;  // (N, w) -> Dh [N][D]
+    std::map<std::pair<uint32_t, uint32_t>, fntrs_plans*> sys_plans;    // (k, n) -> plan of positions 0..k-1
 };
 
 struct fntrs_plans {
@@ -143,6 +144,12 @@ __global__ void negate_scale_kernel(const uint32_t* in, uint32_t* out, uint32_t 
     if (i < n) out[i] = gmul(in[i], s);
 }
 
+int encode_impl(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t N, uint32_t stripes, uint32_t L,
+                const uint16_t* src, const uint64_t* src_esc, uint64_t n_src_esc, uint16_t* out,
+                uint64_t* out_esc, uint64_t esc_cap, uint64_t* n_out_esc, void* stream);
+
+__global__ void set_u64_kernel(uint64_t* p, uint64_t v) { *p = v; }
+
 }  // namespace
 
 extern "C" {
@@ -237,6 +244,7 @@ int fntrs_gpu_destroy(fntrs_ctx* ctx) {
     cudaFree(ctx->ltab.exp3);
     cudaFree(ctx->ltab.log3);
     for (auto& kv : ctx->digit_spectra) cudaFree(kv.second);
+    for (auto& kv : ctx->sys_plans) fntrs_gpu_plans_destroy(kv.second);
     if (ctx->internal) cudaStreamDestroy(ctx->internal);
     delete ctx;
     return FNTRS_OK;
@@ -250,6 +258,17 @@ int fntrs_gpu_encode(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t stripes, u
     if (fntrs_gpu_code_params(k, n, &N))
         return fail(ctx, FNTRS_E_SIZE_MISMATCH, "code parameters need 1 <= k <= n <= 65536, got k = " +
                                                     std::to_string(k) + ", n = " + std::to_string(n));
+    return encode_impl(ctx, k, n, N, stripes, L, src, src_esc, n_src_esc, out, out_esc, esc_cap, n_out_esc, stream);
+}
+
+}  // extern "C"
+
+namespace {
+// FNT_N of k source symbols per codeword, first n outputs (n <= N): the
+// kernels behind fntrs_gpu_encode, with the transform size given explicitly.
+int encode_impl(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t N, uint32_t stripes, uint32_t L,
+                const uint16_t* src, const uint64_t* src_esc, uint64_t n_src_esc, uint16_t* out,
+                uint64_t* out_esc, uint64_t esc_cap, uint64_t* n_out_esc, void* stream) {
     const bool large = fast::large_supported(N);
     if (N > kTileMaxN && !(large && L % fast::large_tile_columns() == 0))
         return fail(ctx, FNTRS_E_UNSUPPORTED, "n_domain > 4096 needs L to be a multiple of 64 in this build");
@@ -285,6 +304,9 @@ int fntrs_gpu_encode(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t stripes, u
     ctx->launches += 1;
     return sort_escapes(ctx, eout.keys, esc_cap, uint64_t(stripes) * n * L, st);
 }
+}  // namespace
+
+extern "C" {
 
 int fntrs_gpu_plans_create(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t kp, uint32_t npatterns,
                            const uint32_t* positions, fntrs_plans** out, void* stream) {
@@ -486,6 +508,123 @@ int fntrs_gpu_decode(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t stripes, ui
     }
     ctx->launches += 1;
     return sort_escapes(ctx, eout.keys, esc_cap, uint64_t(stripes) * pl->k * L, st);
+}
+
+}  // extern "C"
+
+namespace {
+// Interpolation stage of the systematic codec: P = interpolate(plan, rx) into a
+// stream-ordered [stripes][k][L] intermediate with its sorted escape list. The
+// escape count is read back (one stream synchronisation) so the list can never
+// silently overflow; a second pass runs with the exact capacity if it did.
+struct Interp {
+    uint16_t* coef = nullptr;
+    uint64_t* esc = nullptr;
+    uint64_t* cnt = nullptr;
+    uint64_t n_esc = 0;
+    void release(cudaStream_t st) {
+        for (void* p : {(void*)coef, (void*)esc, (void*)cnt})
+            if (p) cudaFreeAsync(p, st);
+    }
+};
+int interpolate_stage(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t stripes, uint32_t L, const uint32_t* sp,
+                      const uint16_t* rx, const uint64_t* rx_esc, uint64_t n_rx_esc, cudaStream_t st, Interp& it) {
+    const uint64_t syms = uint64_t(stripes) * pl->k * L;
+    uint64_t cap = syms / 4096 + 4096;
+    CK(cudaMallocAsync(&it.coef, std::max<uint64_t>(syms, 1) * 2, st), "systematic intermediate");
+    CK(cudaMallocAsync(&it.cnt, sizeof(uint64_t), st), "systematic intermediate");
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        CK(cudaMallocAsync(&it.esc, cap * sizeof(uint64_t), st), "systematic intermediate");
+        int rc = fntrs_gpu_decode(ctx, pl, stripes, L, sp, rx, rx_esc, n_rx_esc, it.coef, it.esc, cap, it.cnt, st);
+        if (rc) return rc;
+        uint64_t got = 0;
+        CK(cudaMemcpyAsync(&got, it.cnt, sizeof(uint64_t), cudaMemcpyDeviceToHost, st), "escape count");
+        CK(cudaStreamSynchronize(st), "escape count");
+        if (got <= cap) {
+            it.n_esc = got;
+            return FNTRS_OK;
+        }
+        cudaFreeAsync(it.esc, st);
+        it.esc = nullptr;
+        cap = got;
+    }
+    return fail(ctx, FNTRS_E_TOO_MANY_ESCAPES, "systematic intermediate escape list overflowed");
+}
+}  // namespace
+
+extern "C" {
+
+int fntrs_gpu_encode_systematic(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t stripes, uint32_t L,
+                                const uint16_t* src, const uint64_t* src_esc, uint64_t n_src_esc,
+                                uint16_t* out, uint64_t* out_esc, uint64_t esc_cap, uint64_t* n_out_esc,
+                                void* stream) {
+    if (!ctx) return FNTRS_E_INVALID_ARGUMENT;
+    uint32_t N = 0;
+    if (fntrs_gpu_code_params(k, n, &N))
+        return fail(ctx, FNTRS_E_SIZE_MISMATCH, "code parameters need 1 <= k <= n <= 65536, got k = " +
+                                                    std::to_string(k) + ", n = " + std::to_string(n));
+    if (stripes && L && (!src || !out)) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "null buffer");
+    if (n_src_esc && !src_esc) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "src_esc is null");
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (k == n) {  // no parity: the codeword is the source
+        int rc = prep_escapes(ctx, out_esc, esc_cap, n_out_esc, st);
+        if (rc) return rc;
+        const uint64_t bytes = uint64_t(stripes) * k * L * 2;
+        if (bytes) CK(cudaMemcpyAsync(out, src, bytes, cudaMemcpyDeviceToDevice, st), "systematic copy");
+        const uint64_t keep = std::min(n_src_esc, esc_cap);
+        if (keep) CK(cudaMemcpyAsync(out_esc, src_esc, keep * 8, cudaMemcpyDeviceToDevice, st), "systematic copy");
+        set_u64_kernel<<<1, 1, 0, st>>>(n_out_esc, n_src_esc);
+        CK(cudaGetLastError(), "systematic copy");
+        ctx->launches += 1;
+        return FNTRS_OK;
+    }
+    fntrs_plans* pl = nullptr;
+    auto found = ctx->sys_plans.find({k, n});
+    if (found != ctx->sys_plans.end()) {
+        pl = found->second;
+    } else {
+        std::vector<uint32_t> pos(k);
+        for (uint32_t i = 0; i < k; ++i) pos[i] = i;
+        int rc = fntrs_gpu_plans_create(ctx, k, n, k, 1, pos.data(), &pl, stream);
+        if (rc) return rc;
+        CK(cudaStreamSynchronize(st), "systematic plan");  // later calls may use other streams
+        ctx->sys_plans[{k, n}] = pl;
+    }
+    if (!stripes || !L) {
+        int rc = prep_escapes(ctx, out_esc, esc_cap, n_out_esc, st);
+        return rc;
+    }
+    uint32_t* sp = nullptr;
+    CK(cudaMallocAsync(&sp, size_t(stripes) * 4, st), "systematic pattern map");
+    CK(cudaMemsetAsync(sp, 0, size_t(stripes) * 4, st), "systematic pattern map");
+    Interp it;
+    int rc = interpolate_stage(ctx, pl, stripes, L, sp, src, src_esc, n_src_esc, st, it);
+    if (!rc) rc = encode_impl(ctx, k, n, N, stripes, L, it.coef, it.esc, it.n_esc, out, out_esc, esc_cap, n_out_esc, stream);
+    it.release(st);
+    cudaFreeAsync(sp, st);
+    return rc;
+}
+
+int fntrs_gpu_decode_systematic(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t stripes, uint32_t L,
+                                const uint32_t* stripe_pattern, const uint16_t* rx, const uint64_t* rx_esc,
+                                uint64_t n_rx_esc, uint16_t* out, uint64_t* out_esc, uint64_t esc_cap,
+                                uint64_t* n_out_esc, void* stream) {
+    if (!ctx || !pl) return FNTRS_E_INVALID_ARGUMENT;
+    if (pl->device != ctx->device) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "plans belong to another device");
+    if (stripes && L && (!rx || !out || !stripe_pattern)) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "null buffer");
+    if (stripes && !pl->np) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "no plans");
+    if (n_rx_esc && !rx_esc) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "rx_esc is null");
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (!stripes || !L) return prep_escapes(ctx, out_esc, esc_cap, n_out_esc, st);
+    Interp it;
+    int rc = interpolate_stage(ctx, pl, stripes, L, stripe_pattern, rx, rx_esc, n_rx_esc, st, it);
+    if (!rc)
+        rc = encode_impl(ctx, pl->k, pl->k, pl->N, stripes, L, it.coef, it.esc, it.n_esc, out, out_esc, esc_cap,
+                         n_out_esc, stream);
+    it.release(st);
+    return rc;
 }
 
 int fntrs_gpu_fnt(fntrs_ctx* ctx, uint32_t m, int inverse, uint32_t L, const uint32_t* in, uint32_t* out,

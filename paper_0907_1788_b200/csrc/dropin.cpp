@@ -209,7 +209,8 @@ CodeParams CodeParams::make(std::uint32_t k, std::uint32_t n, bool systematic) {
     return p;
 }
 
-std::vector<Fe> encode_nonsystematic(const CodeParams& params, std::span<const Fe> source) {
+namespace {
+std::vector<Fe> encode_one(const CodeParams& params, std::span<const Fe> source, bool systematic) {
     if (source.size() != params.k)
         throw SizeMismatch("encode: got " + std::to_string(source.size()) + " source symbols for k = " +
                            std::to_string(params.k));
@@ -219,16 +220,16 @@ std::vector<Fe> encode_nonsystematic(const CodeParams& params, std::span<const F
     std::vector<uint16_t> words;
     std::vector<uint64_t> esc;
     split(source.data(), source.size(), words, esc);
+    auto fn = systematic ? fntrs_gpu_encode_systematic : fntrs_gpu_encode;
     return run(S, words, esc, params.n,
                [&](const uint16_t* din, const uint64_t* die, uint64_t nie, uint16_t* dout, uint64_t* doe,
                    uint64_t cap, uint64_t* dcnt) {
-                   S.check(fntrs_gpu_encode(S.ctx, params.k, params.n, 1, 1, din, die, nie, dout, doe, cap,
-                                            dcnt, S.stream));
+                   S.check(fn(S.ctx, params.k, params.n, 1, 1, din, die, nie, dout, doe, cap, dcnt, S.stream));
                });
 }
 
-std::vector<Fe> decode_nonsystematic(const CodeParams& params, const Codeword& received, Path) {
-    // sorted_received (codec.cpp:32-48): range check, sort, duplicates, count
+// sorted_received (codec.cpp:32-48): range check, sort, duplicates, count
+Codeword sorted_received(const CodeParams& params, const Codeword& received) {
     for (const Symbol& s : received)
         if (s.position >= params.n)
             throw PositionOutOfRange("received position " + std::to_string(s.position) + " not below n = " +
@@ -241,9 +242,11 @@ std::vector<Fe> decode_nonsystematic(const CodeParams& params, const Codeword& r
     if (sorted.size() < params.k)
         throw NotEnoughSymbols("have " + std::to_string(sorted.size()) + " symbols, need " +
                                std::to_string(params.k));
-    const uint32_t nd = next_pow2(params.n);
-    const bool full = params.n == nd && sorted.size() == params.n;  // codec.cpp:137-144
-    const uint32_t kp = full ? params.n : params.k;                   // else the k lowest positions
+    return sorted;
+}
+
+// Decode one codeword from the kp lowest received symbols.
+std::vector<Fe> decode_one(const CodeParams& params, const Codeword& sorted, uint32_t kp, bool systematic) {
     std::vector<uint32_t> pos(kp);
     std::vector<Fe> vals(kp);
     for (uint32_t i = 0; i < kp; ++i) {
@@ -257,17 +260,16 @@ std::vector<Fe> decode_nonsystematic(const CodeParams& params, const Codeword& r
     std::vector<uint16_t> words;
     std::vector<uint64_t> esc;
     split(vals.data(), vals.size(), words, esc);
-    // stripe_pattern: a single zero, staged in scratch after the run buffers
-    uint32_t* d_sp = nullptr;
+    uint32_t* d_sp = nullptr;  // stripe_pattern: a single zero
     if (cudaMalloc(&d_sp, 4) != cudaSuccess) throw Error("fntrs: device allocation failed");
     cudaMemsetAsync(d_sp, 0, 4, S.stream);
+    auto fn = systematic ? fntrs_gpu_decode_systematic : fntrs_gpu_decode;
     std::vector<Fe> out;
     try {
         out = run(S, words, esc, params.k,
                   [&](const uint16_t* din, const uint64_t* die, uint64_t nie, uint16_t* dout, uint64_t* doe,
                       uint64_t cap, uint64_t* dcnt) {
-                      S.check(fntrs_gpu_decode(S.ctx, plan, 1, 1, d_sp, din, die, nie, dout, doe, cap, dcnt,
-                                               S.stream));
+                      S.check(fn(S.ctx, plan, 1, 1, d_sp, din, die, nie, dout, doe, cap, dcnt, S.stream));
                   });
     } catch (...) {
         cudaFree(d_sp);
@@ -275,6 +277,27 @@ std::vector<Fe> decode_nonsystematic(const CodeParams& params, const Codeword& r
     }
     cudaFree(d_sp);
     return out;
+}
+}  // namespace
+
+std::vector<Fe> encode_nonsystematic(const CodeParams& params, std::span<const Fe> source) {
+    return encode_one(params, source, false);
+}
+
+std::vector<Fe> decode_nonsystematic(const CodeParams& params, const Codeword& received, Path) {
+    Codeword sorted = sorted_received(params, received);
+    const bool full = params.n == next_pow2(params.n) && sorted.size() == params.n;  // codec.cpp:137-144
+    return decode_one(params, sorted, full ? params.n : params.k, false);  // else the k lowest positions
+}
+
+std::vector<Fe> encode_systematic(const CodeParams& params, std::span<const Fe> source, Path) {
+    return encode_one(params, source, true);
+}
+
+std::vector<Fe> decode_systematic(const CodeParams& params, const Codeword& received, Path) {
+    // interpolate the k lowest, evaluate at 0..k-1; when those are 0..k-1 the
+    // result is the received values themselves (systematic_prefix_present)
+    return decode_one(params, sorted_received(params, received), params.k, true);
 }
 
 }  // namespace codec

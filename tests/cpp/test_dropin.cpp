@@ -3,6 +3,7 @@
 // Cases follow /root/reference/proj/tests/test_codec.cpp (file:line in each
 // section); values are the reference's frozen golden vectors. Built by
 // `make cpptest`, run by tests/test_gpu_parity.py::test_cpp_dropin (gpu).
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 #include <functional>
@@ -159,6 +160,56 @@ int main() {
         std::vector<Fe> src{65536, 65536, 65536};
         auto enc = encode_nonsystematic(p, src);
         CHECK(decode_nonsystematic(p, take(enc, {2, 4, 6})) == src);
+    }
+    // systematic encode carries the source verbatim (test_codec.cpp:112-124)
+    {
+        const std::pair<uint32_t, uint32_t> cases[] = {{1, 6}, {2, 4}, {4, 8}, {5, 13}, {300, 700}};
+        for (auto [k, n] : cases) {
+            auto params = CodeParams::make(k, n);
+            auto src = random_source(k, 100 + k);
+            for (Path path : {Path::Fast, Path::Direct}) {
+                auto enc = encode_systematic(params, src, path);
+                CHECK(enc.size() == n);
+                CHECK(std::equal(src.begin(), src.end(), enc.begin()));
+            }
+        }
+    }
+    // systematic encode frozen examples (test_codec.cpp:126-136)
+    {
+        CHECK(encode_systematic(CodeParams::make(2, 4), std::vector<Fe>{5, 7}) ==
+              (std::vector<Fe>{5, 7, 65032, 65030}));
+        CHECK(encode_systematic(CodeParams::make(4, 8), std::vector<Fe>{100, 200, 300, 400}) ==
+              (std::vector<Fe>{100, 200, 300, 400, 33256, 17912, 53593, 3200}));
+        CHECK(encode_systematic(CodeParams::make(1, 6), std::vector<Fe>{9}) == std::vector<Fe>(6, 9));
+    }
+    // systematic decode shortcuts and reconstructions (test_codec.cpp:164-190)
+    {
+        auto params = CodeParams::make(4, 8);
+        std::vector<Fe> src{100, 200, 300, 400};
+        auto enc = encode_systematic(params, src);
+        CHECK(decode_systematic(params, take(enc, {0, 1, 2, 3, 6})) == src);
+        CHECK(decode_systematic(params, take(enc, {2, 3, 4, 5, 6, 7}), Path::Fast) == src);
+        CHECK(decode_systematic(params, take(enc, {2, 3, 4, 5, 6, 7}), Path::Direct) == src);
+        CHECK(throws_as<NotEnoughSymbols>([&] { decode_systematic(params, take(enc, {1, 2, 3})); }));
+        CHECK(throws_as<DuplicatePosition>([&] {
+            decode_systematic(params, Codeword{{1, 5}, {1, 5}, {2, 6}, {3, 7}});
+        }));
+    }
+    // systematic MDS over every k-subset, and the top field value (test_codec.cpp:192-224,333-339)
+    {
+        auto p = CodeParams::make(4, 8);
+        auto src = random_source(4, 23);
+        auto enc = encode_systematic(p, src);
+        uint64_t ok = 0, pats = 0;
+        for_each_subset(8, 4, [&](const std::vector<uint32_t>& keep) {
+            ++pats;
+            ok += decode_systematic(p, take(enc, keep)) == src;
+        });
+        CHECK(ok == pats && pats == 70);
+        auto p3 = CodeParams::make(3, 7);
+        std::vector<Fe> top{65536, 65536, 65536};
+        auto enc3 = encode_systematic(p3, top);
+        CHECK(decode_systematic(p3, take(enc3, {2, 4, 6})) == top);
     }
     std::printf("drop-in C++ API: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail ? 1 : 0;

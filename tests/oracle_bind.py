@@ -64,6 +64,8 @@ class Oracle:
         L.orc_code_params.argtypes = [u32, u32, C.POINTER(u32)]
         L.orc_encode.argtypes = [u32, u32, u32p, u32p]
         L.orc_decode.argtypes = [u32, u32, u32, u32p, u32p, u32p]
+        L.orc_encode_systematic.argtypes = [u32, u32, u32p, u32p]
+        L.orc_decode_systematic.argtypes = [u32, u32, u32, u32p, u32p, u32p]
         L.orc_escape_split.restype = i64
         L.orc_escape_split.argtypes = [u32p, u64, u16p, u32p]
         L.orc_encode_stripes.restype = i64
@@ -135,6 +137,17 @@ class Oracle:
         st = self.lib.orc_decode(k, n, pos.size, pos, val, out)
         return st, out
 
+    def encode_systematic(self, k, n, src):
+        out = np.zeros(n, dtype=np.uint32)
+        st = self.lib.orc_encode_systematic(k, n, _a32(src), out)
+        return st, out
+
+    def decode_systematic(self, k, n, pos, val):
+        pos, val = _a32(pos), _a32(val)
+        out = np.zeros(k, dtype=np.uint32)
+        st = self.lib.orc_decode_systematic(k, n, pos.size, pos, val, out)
+        return st, out
+
     def encode_stripes(self, k, n, src, src_esc=None):
         S, kk, L = src.shape
         src = np.ascontiguousarray(src, dtype=np.uint16)
@@ -180,6 +193,8 @@ class RefLib:
         L.ref_fnt_inverse.argtypes = [u32, u32p, u32p]
         L.ref_encode.argtypes = [u32, u32, u32, u32p, u32p]
         L.ref_decode.argtypes = [u32, u32, u32, u32p, u32p, i32, u32p]
+        L.ref_encode_systematic.argtypes = [u32, u32, u32, u32p, i32, u32p]
+        L.ref_decode_systematic.argtypes = [u32, u32, u32, u32p, u32p, i32, u32p]
         L.ref_build_plan.argtypes = [u32, u32, u32p, u32p, C.POINTER(u32), u32p, C.POINTER(u32), C.c_void_p]
         L.ref_encode_stripes.restype = i64
         L.ref_encode_stripes.argtypes = [u32, u32, u32, u32, u16p, C.c_void_p, u64, u16p, u64p, u64, uns]
@@ -204,6 +219,18 @@ class RefLib:
         pos, val = _a32(pos), _a32(val)
         out = np.zeros(max(k, 1), dtype=np.uint32)
         st = self.lib.ref_decode(k, n, pos.size, pos, val, path, out)
+        return st, out
+
+    def encode_systematic(self, k, n, src, path=0):
+        src = _a32(src)
+        out = np.zeros(max(n, 1), dtype=np.uint32)
+        st = self.lib.ref_encode_systematic(k, n, src.size, src, path, out)
+        return st, out
+
+    def decode_systematic(self, k, n, pos, val, path=0):
+        pos, val = _a32(pos), _a32(val)
+        out = np.zeros(max(k, 1), dtype=np.uint32)
+        st = self.lib.ref_decode_systematic(k, n, pos.size, pos, val, path, out)
         return st, out
 
     def build_plan(self, n, positions):

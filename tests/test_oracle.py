@@ -189,6 +189,47 @@ def test_batched_stripes_roundtrip(oracle):
     assert np.array_equal(dec, src) and desc.size == 0
 
 
+# ------------------------------------------------------- systematic ----
+def test_systematic_golden(oracle):  # proj/tests/test_codec.cpp:112-136,164-190
+    assert list(oracle.encode_systematic(2, 4, [5, 7])[1]) == [5, 7, 65032, 65030]
+    assert list(oracle.encode_systematic(4, 8, [100, 200, 300, 400])[1]) == [
+        100, 200, 300, 400, 33256, 17912, 53593, 3200]
+    assert list(oracle.encode_systematic(1, 6, [9])[1]) == [9] * 6
+    rng = np.random.default_rng(100)
+    for k, n in [(1, 6), (2, 4), (4, 8), (5, 13), (300, 700)]:
+        src = rng.integers(0, P, k).astype(np.uint32)
+        st, enc = oracle.encode_systematic(k, n, src)
+        assert st == 0 and enc.size == n and np.array_equal(enc[:k], src)
+    src = np.array([100, 200, 300, 400], dtype=np.uint32)
+    enc = oracle.encode_systematic(4, 8, src)[1]
+    for keep in ([0, 1, 2, 3, 6], [2, 3, 4, 5, 6, 7]):
+        keep = np.array(keep, dtype=np.uint32)
+        st, got = oracle.decode_systematic(4, 8, keep, enc[keep])
+        assert st == 0 and np.array_equal(got, src)
+    assert oracle.encode_systematic(3, 2, [1, 2, 3])[0] == 4  # SizeMismatch
+    assert oracle.decode_systematic(2, 4, [0], [1])[0] == 10  # NotEnoughSymbols
+
+
+def test_systematic_matches_reference_library(oracle, ref):  # codec.cpp:151-196
+    rng = np.random.default_rng(17)
+    for _ in range(60):
+        n = int(rng.integers(1, 300))
+        k = int(rng.integers(1, n + 1))
+        src = rng.integers(0, P, k).astype(np.uint32)
+        so, eo = oracle.encode_systematic(k, n, src)
+        sr, er = ref.encode_systematic(k, n, src)
+        assert so == sr == 0 and np.array_equal(eo, er[:n]), (k, n)
+        cnt = int(rng.integers(k, n + 1))
+        pos = rng.choice(n, cnt, replace=False).astype(np.uint32)
+        vals = rng.integers(0, P, cnt).astype(np.uint32)  # arbitrary values: k-lowest rule and prefix shortcut
+        do, dr = oracle.decode_systematic(k, n, pos, vals), ref.decode_systematic(k, n, pos, vals)
+        assert do[0] == dr[0] == 0 and np.array_equal(do[1], dr[1][:k]), (k, n)
+        got = oracle.decode_systematic(k, n, pos, eo[pos])[1]
+        assert np.array_equal(got, src)
+    for args in [(2, 4, [0], [1]), (2, 4, [1, 1], [5, 6]), (2, 4, [0, 4], [5, 6])]:
+        assert oracle.decode_systematic(*args)[0] == ref.decode_systematic(*args)[0]
+
+
 # -------------------------------------------------- oracle vs reference ----
 def test_oracle_matches_reference_library(oracle, ref):
     rng = np.random.default_rng(5)
