@@ -41,6 +41,26 @@ PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback, only if MEASURED_PEAKS.json is absent
 
 
+def profiled_traffic(cfg, chunk, systematic):
+    """DRAM bytes (read + write) of one decode launch from the committed ncu
+    --set full capture (profiles/r01_ncu_full_raw.csv: dec_fast_kernel<8>, one
+    8192-stripe C2 chunk), when this run's launch has that exact shape."""
+    if systematic or cfg.name != "C2" or chunk != 8192:
+        return None
+    try:
+        import csv
+        rows = list(csv.reader(open(os.path.join(ROOT, "profiles", "r01_ncu_full_raw.csv"))))
+        h, u, v = rows[0], rows[1], rows[2]
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        tot = 0.0
+        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = h.index(m)
+            tot += float(v[i]) * scale[u[i]]
+        return int(tot)
+    except Exception:
+        return None
+
+
 def hbm_peak():
     try:
         with open(PEAKS_FILE) as f:
@@ -105,15 +125,20 @@ def reference_lib():
     return RefLib()
 
 
+SYSTEMATIC = False  # --codec systematic
+
+
 def cpu_reference_sample(cfg, seed, stripes, threads):
     """Time the reference library (oracle/_ref, the unmodified reference codec)
     on `stripes` stripes of the config, the way the reference CLI runs it
-    (per-codeword encode/decode_nonsystematic, Path::Auto, threads over
-    codewords). Returns (enc_s, dec_s, source_bytes)."""
+    (per-codeword encode/decode_nonsystematic -- or the systematic pair with
+    --codec systematic -- Path::Auto, threads over codewords).
+    Returns (enc_s, dec_s, source_bytes)."""
     ref = reference_lib()
     if ref is None:
         raise RuntimeError("reference library oracle/_ref not built")
     from oracle_bind import gather_received
+    ref.set_systematic(SYSTEMATIC)
     src = W.symbols(seed, 0, stripes * cfg.k * cfg.L).reshape(stripes, cfg.k, cfg.L)
     pats, sp = W.patterns(cfg, seed=seed, stripes=stripes)
     t0 = time.perf_counter()
@@ -173,7 +198,8 @@ def run_gpu(args, rank, world, local_rank):
 
     def encode_chunk(c):
         a, b = c * chunk, min(S_rank, (c + 1) * chunk)
-        codec.encode(k, n, src[a:b], out=enc[a:b], esc_out=enc_esc[c], esc_cap=esc_cap, count=enc_cnt[c:c + 1])
+        codec.encode(k, n, src[a:b], out=enc[a:b], esc_out=enc_esc[c], esc_cap=esc_cap, count=enc_cnt[c:c + 1],
+                     systematic=SYSTEMATIC)
 
     for c in range(nchunks):
         encode_chunk(c)
@@ -211,7 +237,7 @@ def run_gpu(args, rank, world, local_rank):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
         codec.decode(plans_box["p"], sp_dev[a:b], rx[a:b], rx_esc[c], out=dec[: b - a], esc_out=dec_esc,
-                     esc_cap=dec_cap, count=dec_cnt[c:c + 1])
+                     esc_cap=dec_cap, count=dec_cnt[c:c + 1], systematic=SYSTEMATIC)
         if timed:
             e1.record(stream)
             dec_events.append((e0, e1))
@@ -296,6 +322,7 @@ def run_gpu(args, rank, world, local_rank):
     enc_achieved = enc_bytes / (enc_launch_ms * 1e-3) / 1e9
     result = {
         "metric": "encode & decode GB/s of source data per GPU (1/2/4/8 B200), % of HBM roofline",
+        "codec": "systematic" if SYSTEMATIC else "non-systematic",
         "value": round(value, 3),
         "unit": "GB/s",
         "n_gpus": world,
@@ -320,9 +347,14 @@ def run_gpu(args, rank, world, local_rank):
         "decode_gbs": round(src_bytes_rank / (phase_ms[2] * 1e-3) / 1e9, 2),
         "decode_with_plans_gbs": round(src_bytes_rank / ((phase_ms[2] + phase_ms[0]) * 1e-3) / 1e9, 2),
         "roofline": {
-            "bound": "hbm", "kernel": "dec_fast_kernel (fused decode, one launch per chunk)",
+            "bound": "hbm",
+            "kernel": ("decode_systematic call per chunk (interpolation kernel + transform kernel)" if SYSTEMATIC
+                       else "dec_fast_kernel (fused decode, one launch per chunk)"),
             "achieved": round(dec_achieved, 2), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
-            "frac": round(dec_achieved / peak, 4), "traffic": args.traffic,
+            "frac": round(dec_achieved / peak, 4),
+            "traffic": args.traffic if args.traffic is not None else profiled_traffic(cfg, chunk, SYSTEMATIC),
+            "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum per launch "
+                              "(profiles/r01_ncu_full_raw.csv)",
             "algorithmic_bytes_per_launch": dec_bytes, "avg_launch_ms": round(dec_launch_ms, 4),
         },
         "roofline_encode": {
@@ -359,7 +391,7 @@ def run_e2e(args, codec, cfg, dev, stream, seed, world):
     pats_h = torch.from_numpy(pats.astype(np.int32)).pin_memory()
     # received packets prepared once (the erasure channel, not the codec)
     d_src = src_h.to(dev)
-    enc0, e0, c0 = codec.encode(k, n, d_src)
+    enc0, e0, c0 = codec.encode(k, n, d_src, systematic=SYSTEMATIC)
     rx0, rxe0 = W.received_packets(enc0, e0, c0, pats, sp, n)
     rx_h = rx0.cpu().pin_memory()
     rxe_np = rxe0.cpu().numpy().view(np.uint64) if rxe0 is not None else np.zeros(0, np.uint64)
@@ -367,7 +399,7 @@ def run_e2e(args, codec, cfg, dev, stream, seed, world):
     del enc0, rx0, d_src
     nch = (S + chunk - 1) // chunk
     ranges = escape_ranges(rxe_np, S, chunk, k, L)
-    pipe = HostPipeline(codec, k, n, L, chunk)
+    pipe = HostPipeline(codec, k, n, L, chunk, systematic=SYSTEMATIC)
     enc_h = torch.empty((S, n, L), dtype=torch.int16).pin_memory()
     dec_h = torch.empty((S, k, L), dtype=torch.int16).pin_memory()
     enc_esc_h = torch.empty((nch, pipe.cap_e), dtype=torch.int64).pin_memory()
@@ -441,6 +473,7 @@ def run_reference(args, rank, world):
     return {
         "impl": "reference",
         "metric": "encode & decode GB/s of source data per GPU (1/2/4/8 B200), % of HBM roofline",
+        "codec": "systematic" if SYSTEMATIC else "non-systematic",
         "value": round(value, 6), "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "u32 (GF(65537))", "data": "synthetic (same generator and erasure classes)",
@@ -470,9 +503,13 @@ def main():
     ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes per decode launch (profiles/)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo = test mode for several ranks on fewer GPUs (host-side barrier/max only)")
+    ap.add_argument("--codec", default="nonsystematic", choices=["nonsystematic", "systematic"],
+                    help="headline: non-systematic (BASELINE north_star); systematic = the SURVEY 8(f) next row")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    global SYSTEMATIC
+    SYSTEMATIC = args.codec == "systematic"
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -177,6 +177,12 @@ int ref_build_plan(uint32_t n, uint32_t k, const uint32_t* positions, uint32_t* 
     }
 }
 
+// Which codec the batched stripe loops run: 0 non-systematic (default), 1 the
+// systematic pair (encode_systematic / decode_systematic, the CLI default mode,
+// proj/tools/fntrs_main.cpp:413).
+static std::atomic<int> g_systematic{0};
+void ref_set_systematic(int on) { g_systematic = on; }
+
 // CLI-style batched encode over packet-major stripes. Returns the escape
 // count (sorted symbol indices row*L+col in out_esc) or a negative status.
 int64_t ref_encode_stripes(uint32_t k, uint32_t n, uint32_t stripes, uint32_t L,
@@ -190,11 +196,12 @@ int64_t ref_encode_stripes(uint32_t k, uint32_t n, uint32_t stripes, uint32_t L,
     }
     std::mutex mu;
     std::vector<uint64_t> escapes;
+    const bool sys = g_systematic.load() != 0;
     int st = run_parallel(uint64_t(stripes) * L, threads, [&](unsigned, uint64_t t) {
         const uint32_t s = uint32_t(t / L), j = uint32_t(t % L);
         std::vector<Fe> col(k);
         for (uint32_t i = 0; i < k; ++i) col[i] = fetch(src, src_esc, n_src_esc, uint64_t(s) * k + i, j, L);
-        std::vector<Fe> enc = codec::encode_nonsystematic(params, col);
+        std::vector<Fe> enc = sys ? codec::encode_systematic(params, col) : codec::encode_nonsystematic(params, col);
         for (uint32_t i = 0; i < n; ++i) {
             const uint64_t row = uint64_t(s) * n + i;
             out[row * L + j] = enc[i] == 65536 ? 0 : uint16_t(enc[i]);
@@ -230,13 +237,14 @@ int64_t ref_decode_stripes(uint32_t k, uint32_t n, uint32_t stripes, uint32_t L,
     std::mutex mu;
     std::vector<uint64_t> escapes;
     const codec::Path p = path_of(path);
+    const bool sys = g_systematic.load() != 0;
     int st = run_parallel(uint64_t(stripes) * L, threads, [&](unsigned, uint64_t t) {
         const uint32_t s = uint32_t(t / L), j = uint32_t(t % L);
         const uint32_t* pos = patterns + uint64_t(stripe_pattern[s]) * k;
         codec::Codeword cw(k);
         for (uint32_t i = 0; i < k; ++i)
             cw[i] = {pos[i], fetch(rx, rx_esc, n_rx_esc, uint64_t(s) * k + i, j, L)};
-        std::vector<Fe> dec = codec::decode_nonsystematic(params, cw, p);
+        std::vector<Fe> dec = sys ? codec::decode_systematic(params, cw, p) : codec::decode_nonsystematic(params, cw, p);
         for (uint32_t i = 0; i < k; ++i) {
             const uint64_t row = uint64_t(s) * k + i;
             out[row * L + j] = dec[i] == 65536 ? 0 : uint16_t(dec[i]);

@@ -19,9 +19,10 @@ from .codec import Codec, Plans, default_escape_capacity
 
 
 class HostPipeline:
-    def __init__(self, codec: Codec, k: int, n: int, L: int, max_chunk_stripes: int, nstreams: int = 3):
+    def __init__(self, codec: Codec, k: int, n: int, L: int, max_chunk_stripes: int, nstreams: int = 3,
+                 systematic: bool = False):
         import torch
-        self.torch, self.codec = torch, codec
+        self.torch, self.codec, self.systematic = torch, codec, systematic
         self.k, self.n, self.L = k, n, L
         self.chunk = max(1, max_chunk_stripes)
         dev = torch.device(f"cuda:{codec.device}")
@@ -52,7 +53,7 @@ class HostPipeline:
                 d_in, d_enc = self.d_in[i][: b - a], self.d_enc[i][: b - a]
                 d_in.copy_(src_h[a:b], non_blocking=True)
                 self.codec.encode(self.k, self.n, d_in, out=d_enc, esc_out=self.d_esc[i], esc_cap=self.cap_e,
-                                  count=self.d_cnt[i], stream=st)
+                                  count=self.d_cnt[i], stream=st, systematic=self.systematic)
                 enc_h[a:b].copy_(d_enc, non_blocking=True)
                 esc_h[c].copy_(self.d_esc[i], non_blocking=True)
                 counts_h[c:c + 1].copy_(self.d_cnt[i], non_blocking=True)
@@ -78,7 +79,7 @@ class HostPipeline:
                     if hi > lo:
                         esc = rx_esc_dev[lo:hi] - a * self.k * self.L
                 self.codec.decode(plans, stripe_pattern_dev[a:b], d_rx, esc, out=d_dec, esc_out=self.d_esc[i],
-                                  esc_cap=self.cap_e, count=self.d_cnt[i], stream=st)
+                                  esc_cap=self.cap_e, count=self.d_cnt[i], stream=st, systematic=self.systematic)
                 dec_h[a:b].copy_(d_dec, non_blocking=True)
                 esc_h[c].copy_(self.d_esc[i], non_blocking=True)
                 counts_h[c:c + 1].copy_(self.d_cnt[i], non_blocking=True)

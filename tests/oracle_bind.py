@@ -202,6 +202,12 @@ class RefLib:
         L.ref_decode_stripes.argtypes = [u32, u32, u32, u32, u32, u32p, u32p, u16p, C.c_void_p, u64, u16p,
                                          u64p, u64, i32, uns]
         L.ref_has_avx2.restype = i32
+        L.ref_set_systematic.argtypes = [i32]
+        L.ref_set_systematic.restype = None
+
+    def set_systematic(self, on: bool):
+        """Batched stripe loops run encode/decode_systematic instead of the non-systematic pair."""
+        self.lib.ref_set_systematic(int(bool(on)))
 
     def fnt(self, a, inverse=False):
         a = _a32(a)
