@@ -122,8 +122,16 @@ __global__ void __launch_bounds__(G::NT, G::MINB) enc_fast_kernel(const __grid_c
 }
 
 // ---------------------------------------------------------------------------
+// Decode occupancy: the staged input is read only by the first pass, so one
+// stage buffer suffices (the next tile's TMA load is issued right after that
+// pass's barrier) and at N <= 256 five CTAs fit per SM.
+template <int E>
+struct DecOcc {
+    static constexpr int MINB = (E <= 8) ? 5 : Pick<E>::MINB;
+};
+
 template <int E, class G, bool HALFK>
-__global__ void __launch_bounds__(G::NT, G::MINB) dec_fast_kernel(const __grid_constant__ CUtensorMap rx_map,
+__global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const __grid_constant__ CUtensorMap rx_map,
                                                          const uint2* __restrict__ ptabF, const uint2* __restrict__ ptabI,
                                                          const uint2* __restrict__ rowmap,
                                                          const uint2* __restrict__ ahat2, uint32_t k, uint32_t L,
@@ -140,21 +148,17 @@ __global__ void __launch_bounds__(G::NT, G::MINB) dec_fast_kernel(const __grid_c
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t bars[2];
     uint32_t* work = reinterpret_cast<uint32_t*>(smem_raw);
-    // [guard | stage 0 | guard | stage 1]: each guard is the WT-symbol row just
-    // below its stage (an erased position's row index ~0 wraps onto it) and
-    // holds ones, so raw received words can be tested for zero unmasked.
+    // [guard | stage]: the guard is the WT-symbol row just below the stage (an
+    // erased position's row index ~0 wraps onto it) and holds ones, so raw
+    // received words can be tested for zero unmasked.
     const uint32_t stage_elems = nbox * box_rows * WT;
     const uint32_t stage_bytes = stage_elems * 2;
     uint16_t* stage0 = reinterpret_cast<uint16_t*>(smem_raw + size_t(N) * WT * 4 + kGuardBytes);
-    const uint32_t stage_stride = stage_elems + kGuardBytes / 2;
-    for (uint32_t i = threadIdx.x; i < uint32_t(WT); i += NT) {
-        stage0[i - WT] = 1;
-        stage0[stage_stride + i - WT] = 1;
-    }
+    constexpr uint32_t stage_stride = 0;  // single stage
+    for (uint32_t i = threadIdx.x; i < uint32_t(WT); i += NT) stage0[i - WT] = 1;
     if (threadIdx.x == 0) {
         tma_prefetch_desc(&rx_map);
         mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -173,17 +177,15 @@ __global__ void __launch_bounds__(G::NT, G::MINB) dec_fast_kernel(const __grid_c
     const uint4* tI0 = pass_table(ptabI, S::llog(0));
     const bool esc_any = esc_in.n != 0;
     for (uint32_t iter = 0; tile < tiles; ++iter, tile += gridDim.x) {
-        const int bsel = iter & 1;
         const uint32_t stripe = tile / tps;
         const uint32_t c0 = (tile - stripe * tps) * WT;
-        if (threadIdx.x == 0 && tile + gridDim.x < tiles) issue(tile + gridDim.x, bsel ^ 1);
         const uint32_t pat = __ldg(stripe_pattern + stripe);
         const uint2* __restrict__ rm = rowmap + size_t(pat) * N;
         const uint2* __restrict__ ah = ahat2 + size_t(pat) * N;
         const unsigned long long key = uint64_t(stripe) * k * L + c0;
         uint16_t* outp = launder(out + key);
-        mbar_wait(&bars[bsel], (iter >> 1) & 1);
-        const uint16_t* st_in = stage0 + bsel * stage_stride;
+        mbar_wait(&bars[0], iter & 1);
+        const uint16_t* st_in = stage0;
 
         // step 4: N'[z] = v_i / A'(x_i) where z = z_i, else 0 (rowmap {~0, 0}:
         // reads the guard row of ones, scales by 0). A received zero word may
@@ -238,6 +240,8 @@ __global__ void __launch_bounds__(G::NT, G::MINB) dec_fast_kernel(const __grid_c
         // FNT1 = FNT_N(N'), DIF, natural -> perm order (flip 0)
         pass<E, 0, false, false, k2P, kSmemCap, G>(tF0, ld_scatter, st_sm, fix_scatter);
         __syncthreads();
+        // the stage is consumed: stream the next tile's packets in behind the remaining passes
+        if (threadIdx.x == 0 && tile + gridDim.x < tiles) issue(tile + gridDim.x, 0);
         if constexpr (P == 3) {
             pass<E, 1, false, false, kSmemCap, kSmemCap, G>(pass_table(ptabF, S::llog(1)), ld_sm, st_sm);
             __syncthreads();
@@ -396,14 +400,14 @@ struct LaunchShape {
 
 template <class K>
 cudaError_t shape_for(K kernel, int E, int wt, int nt, uint32_t k, uint32_t stripes, uint32_t L, LaunchShape& sh,
-                      size_t extra = 0) {
+                      size_t extra = 0, int stages = 2) {
     sh.tps = L / wt;
     const uint64_t tiles = uint64_t(stripes) * sh.tps;
     if (tiles > 0xFFFFFFFFull) return cudaErrorInvalidConfiguration;
     sh.tiles = uint32_t(tiles);
     sh.box_rows = k < 256 ? k : 256;
     sh.nbox = (k + sh.box_rows - 1) / sh.box_rows;
-    sh.smem = (size_t(1) << E) * wt * 4 + 2 * size_t(sh.nbox) * sh.box_rows * wt * 2 + extra;
+    sh.smem = (size_t(1) << E) * wt * 4 + size_t(stages) * sh.nbox * sh.box_rows * wt * 2 + extra;
     cudaError_t err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sh.smem));
     if (err) return err;
     int dev = 0, sms = 0, per = 0;
@@ -439,7 +443,7 @@ cudaError_t launch_dec(const FastTables& t, const FastPlanView& pv, uint32_t str
     using G = typename Pick<E>::G;
     auto kern = pv.k == (1u << E) / 2 ? dec_fast_kernel<E, G, true> : dec_fast_kernel<E, G, false>;
     LaunchShape sh;
-    cudaError_t err = shape_for(kern, E, G::WT, G::NT, pv.k, stripes, L, sh, 2 * kGuardBytes);
+    cudaError_t err = shape_for(kern, E, G::WT, G::NT, pv.k, stripes, L, sh, kGuardBytes, 1);
     if (err) return err;
     if (!sh.tiles) return cudaSuccess;
     CUtensorMap map;
