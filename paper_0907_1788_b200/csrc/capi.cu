@@ -41,8 +41,10 @@ struct fntrs_plans {
     uint32_t* ainv = nullptr;
     uint32_t* ahat = nullptr;
     uint32_t ninv = 1;
-    uint2* rowmap = nullptr;  // fast-path tables (N == M, kp == k)
+    uint2* rowmap = nullptr;  // fast-path tables (N == M, kp == k), and the general column path
     uint2* ahat2 = nullptr;
+    bool cols = false;        // served by the general column path (codec_cols.cu)
+    bool full = false;        // complete reception
 };
 
 namespace {
@@ -120,7 +122,7 @@ constexpr size_t kScratchCap = size_t(2) << 30;  // per four-step intermediate b
 // Per-call stream-ordered scratch (released in stream order by release_scratch),
 // so concurrent calls on different streams never share intermediates.
 struct Scratch {
-    uint32_t* p[2] = {nullptr, nullptr};
+    uint32_t* p[3] = {nullptr, nullptr, nullptr};
 };
 int get_scratch(fntrs_ctx* ctx, Scratch& s, size_t bytes, int count, cudaStream_t st) {
     for (int i = 0; i < count; ++i) CK(cudaMallocAsync(&s.p[i], bytes, st), "scratch alloc");
@@ -269,9 +271,7 @@ namespace {
 int encode_impl(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t N, uint32_t stripes, uint32_t L,
                 const uint16_t* src, const uint64_t* src_esc, uint64_t n_src_esc, uint16_t* out,
                 uint64_t* out_esc, uint64_t esc_cap, uint64_t* n_out_esc, void* stream) {
-    const bool large = fast::large_supported(N);
-    if (N > kTileMaxN && !(large && L % fast::large_tile_columns() == 0))
-        return fail(ctx, FNTRS_E_UNSUPPORTED, "n_domain > 4096 needs L to be a multiple of 64 in this build");
+    const bool large = fast::large_supported(N) && L % fast::large_tile_columns() == 0;
     if (stripes && L && (!src || !out)) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "null buffer");
     if (n_src_esc && !src_esc) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "src_esc is null");
     DeviceGuard g(ctx->device);
@@ -284,6 +284,20 @@ int encode_impl(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t N, uint32_t str
     const int cols = fast::fast_tile_columns(N);
     const bool fast_ok = ctx->fast_enabled && cols && L % uint32_t(cols) == 0 &&
                          reinterpret_cast<uintptr_t>(src) % 16 == 0;
+    if (N > kTileMaxN && !large) {  // general column path (codec_cols.cu)
+        if (stripes && L) {
+            const uint64_t cap = std::min<uint64_t>(uint64_t(stripes) * L, fast::cols_batch_columns(N, kScratchCap));
+            Scratch sc;
+            rc = get_scratch(ctx, sc, size_t(N) * cap * 4, 2, st);
+            if (rc) return rc;
+            cudaError_t le = fast::launch_encode_cols(ctx->ftab, k, n, N, stripes, L, src, ein, out, eout, sc.p[0],
+                                                      sc.p[1], cap, st);
+            release_scratch(sc, st);
+            CK(le, "encode launch");
+            ctx->launches += 3 * ((uint64_t(stripes) * L + cap - 1) / cap);
+        }
+        return sort_escapes(ctx, eout.keys, esc_cap, uint64_t(stripes) * n * L, st);
+    }
     if (large) {
         if (stripes && L) {
             const uint32_t batch = std::min(stripes, fast::large_batch(N, L, kScratchCap));
@@ -325,9 +339,8 @@ int fntrs_gpu_plans_create(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t kp, 
     // locator data: needed for decoding unless complete; kept for export when it fits
     const bool locator = !full || (kp == k && M && M <= kTileMaxN);
     const bool large = fast::large_supported(N) && !full && kp == k && M == N;
-    if (!large && (N > kTileMaxN || (!full && M > kTileMaxN)))
-        return fail(ctx, FNTRS_E_UNSUPPORTED,
-                    "transform sizes > 4096 need k in (n_domain/4, n_domain/2] in this build");
+    // shapes neither the fused nor the tile kernels take: the general column path
+    const bool cols = !large && (N > kTileMaxN || (!full && M > kTileMaxN));
     if (npatterns && !positions) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "positions is null");
     // validation (codec.cpp:32-48 order: range first, then duplicates)
     std::vector<uint8_t> seen(n);
@@ -353,6 +366,8 @@ int fntrs_gpu_plans_create(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t kp, 
     pl->M = M;
     pl->kp = kp;
     pl->np = npatterns;
+    pl->cols = cols;
+    pl->full = full;
     pl->ninv = cpow(N % kP, kP - 2);
     const size_t npos = size_t(npatterns) * kp;
     cudaError_t e = cudaSuccess;
@@ -391,6 +406,11 @@ int fntrs_gpu_plans_create(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t kp, 
         } else if (!e && locator) {
             e = launch_plan_build(N, M, kp, npatterns, pl->pos, pl->ainv, pl->ahat, ctx->tab, st);
             ctx->launches += 1;
+        }
+        if (!e && cols) {  // received-row map for the column path's scatter loader
+            e = cudaMallocAsync(&pl->rowmap, size_t(npatterns) * N * sizeof(uint2), st);
+            if (!e) e = fast::build_cols_rowmap(N, kp, npatterns, pl->pos, full ? nullptr : pl->ainv, pl->rowmap, st);
+            ctx->launches += 2;
         }
     }
     if (e) {
@@ -482,12 +502,25 @@ int fntrs_gpu_decode(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t stripes, ui
     EscIn ein{reinterpret_cast<const unsigned long long*>(rx_esc), n_rx_esc};
     EscOut eout{reinterpret_cast<unsigned long long*>(out_esc), reinterpret_cast<unsigned long long*>(n_out_esc),
                 esc_cap};
-    const int cols = fast::fast_tile_columns(pl->N);
-    const bool fast_ok = ctx->fast_enabled && pl->rowmap && cols && L % uint32_t(cols) == 0 &&
+    const int tcols = fast::fast_tile_columns(pl->N);
+    const bool fast_ok = ctx->fast_enabled && !pl->cols && pl->rowmap && tcols && L % uint32_t(tcols) == 0 &&
                          reinterpret_cast<uintptr_t>(rx) % 16 == 0;
-    if (fast::large_supported(pl->N) && pl->rowmap) {
-        if (L % fast::large_tile_columns())
-            return fail(ctx, FNTRS_E_UNSUPPORTED, "n_domain > 4096 needs L to be a multiple of 64 in this build");
+    const bool large_plan = !pl->cols && fast::large_supported(pl->N) && pl->rowmap;
+    if (pl->cols || (large_plan && L % fast::large_tile_columns())) {  // general column path
+        if (stripes && L) {
+            const uint32_t D = std::max(pl->N, pl->M);
+            const uint64_t cap = std::min<uint64_t>(uint64_t(stripes) * L, fast::cols_batch_columns(D, kScratchCap));
+            Scratch sc;
+            rc = get_scratch(ctx, sc, size_t(D) * cap * 4, 3, st);
+            if (rc) return rc;
+            fast::ColsPlanView cv{pl->N, pl->full ? pl->N : pl->M, pl->k, pl->kp, pl->full, pl->rowmap, pl->ahat};
+            cudaError_t le = fast::launch_decode_cols(ctx->ftab, cv, stripes, L, stripe_pattern, rx, ein, out, eout,
+                                                      sc.p[0], sc.p[1], sc.p[2], cap, st);
+            release_scratch(sc, st);
+            CK(le, "decode launch");
+            ctx->launches += 7 * ((uint64_t(stripes) * L + cap - 1) / cap);
+        }
+    } else if (large_plan) {
         if (stripes && L) {
             const uint32_t batch = std::min(stripes, fast::large_batch(pl->N, L, kScratchCap));
             Scratch sc;

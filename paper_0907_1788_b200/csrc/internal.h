@@ -129,6 +129,27 @@ cudaError_t launch_plan_fast(const FastTables& t, const Tables& tab, const LogTa
 // natural-order column transforms [N][C] of any N <= 65536 (scratch N*C words when N >= 8192)
 cudaError_t launch_fnt_cols(const FastTables& t, uint32_t N, bool inverse, uint32_t C, const uint32_t* in,
                             uint32_t* scratch, uint32_t* out, cudaStream_t st);
+
+// ---- general path (codec_cols.cu): column transforms through HBM, any shape
+// with n_domain, M <= 65536
+struct ColsPlanView {
+    uint32_t N, M, k, kp;
+    bool full;             // complete reception: one inverse transform
+    const uint2* rowmap;   // [np][N] {received row or ~0, balanced 1/A'(x_i) (1 when full)}
+    const uint32_t* ahat;  // [np][M] -A_hat / M (unused when full)
+};
+// columns per batch so one [max(N, M)][C] uint32 buffer stays within cap_bytes
+uint64_t cols_batch_columns(uint32_t D, size_t cap_bytes);
+cudaError_t build_cols_rowmap(uint32_t N, uint32_t kp, uint32_t P, const uint32_t* pos, const uint32_t* ainv,
+                              uint2* rowmap, cudaStream_t st);
+// A, T: [N][cap_cols] uint32 scratch each
+cudaError_t launch_encode_cols(const FastTables& t, uint32_t k, uint32_t n, uint32_t N, uint32_t stripes, uint32_t L,
+                               const uint16_t* src, EscIn ein, uint16_t* out, EscOut eout, uint32_t* A, uint32_t* T,
+                               uint64_t cap_cols, cudaStream_t st);
+// A, B, T: [max(N, M)][cap_cols] uint32 scratch each
+cudaError_t launch_decode_cols(const FastTables& t, const ColsPlanView& pv, uint32_t stripes, uint32_t L,
+                               const uint32_t* sp, const uint16_t* rx, EscIn ein, uint16_t* out, EscOut eout,
+                               uint32_t* A, uint32_t* B, uint32_t* T, uint64_t cap_cols, cudaStream_t st);
 }  // namespace fast
 
 }  // namespace fntrs_gpu

@@ -127,6 +127,9 @@ SHAPES = [  # (k, n, L, stripes)
     # four-step kernels (n_domain 8192..65536, L a multiple of 64)
     (4096, 8192, 64, 2), (8192, 16384, 64, 2), (16384, 32768, 64, 1), (32768, 65536, 64, 1),
     (5000, 12000, 64, 1), (3000, 8192, 128, 1),
+    # general column path (codec_cols.cu): product size M != n_domain above 4096, any L
+    (3000, 4096, 16, 1), (2000, 16384, 8, 1), (1000, 8192, 10, 2), (4096, 8192, 40, 1), (5000, 9000, 8, 1),
+    (20000, 32768, 8, 1), (40, 10000, 16, 1),
 ]
 
 
@@ -207,6 +210,23 @@ def test_complete_reception_is_inverse_transform(codec, oracle):  # codec.cpp:13
     vals = rng.integers(0, 65536, (1, n, L)).astype(np.uint16)  # not a codeword
     plans = codec.plans(k, n, np.arange(n, dtype=np.uint32)[None, :])
     out, oe, cnt = codec.decode(plans, torch.zeros(1, dtype=torch.int32, device="cuda"), dev_u16(vals))
+    got = host_u16(out)
+    want_esc = []
+    for c in range(L):
+        want = oracle.fnt(vals[0, :, c].astype(np.uint32), inverse=True)[:k]
+        assert np.array_equal(got[0, :, c], np.where(want == 65536, 0, want))
+        want_esc += [f * L + c for f in range(k) if want[f] == 65536]
+    assert np.array_equal(escapes_to_numpy(oe, cnt), np.sort(np.array(want_esc, dtype=np.uint64)))
+
+
+def test_complete_reception_large_domain(codec, oracle):  # codec.cpp:137-144 at n_domain 8192 (column path)
+    from paper_0907_1788_b200 import escapes_to_numpy
+    n, k, L = 8192, 100, 3
+    rng = np.random.default_rng(12)
+    vals = rng.integers(0, 65536, (1, n, L)).astype(np.uint16)  # not a codeword
+    perm = rng.permutation(n).astype(np.uint32)  # positions in any order
+    plans = codec.plans(k, n, perm[None, :])
+    out, oe, cnt = codec.decode(plans, torch.zeros(1, dtype=torch.int32, device="cuda"), dev_u16(vals[:, perm, :]))
     got = host_u16(out)
     want_esc = []
     for c in range(L):
