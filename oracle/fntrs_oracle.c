@@ -384,16 +384,56 @@ int orc_build_plan(uint32_t n, uint32_t k, const uint32_t* positions, uint32_t* 
     return ORC_OK;
 }
 
+/* mul_low (poly.cpp:139-169): the first `count` coefficients of a*b. When
+ * the truncated product fits one transform it is one orc_poly_mul; otherwise
+ * both operands split at h = ceil(count/2) and high*high (degrees >= 2h) is
+ * dropped: out = lo*lo + x^h (mul_low(alo, bhi) + mul_low(ahi, blo)).
+ * Writes exactly `count` coefficients (zero-padded). */
+static int mul_low(const uint32_t* a, uint32_t la, const uint32_t* b, uint32_t lb, uint32_t count, uint32_t* out) {
+    memset(out, 0, sizeof(uint32_t) * count);
+    uint32_t at = la < count ? la : count, bt = lb < count ? lb : count;
+    if (!at || !bt) return ORC_OK;
+    uint32_t len = at + bt - 1;
+    if (len <= 65536) {
+        uint32_t* full = (uint32_t*)malloc(sizeof(uint32_t) * len);
+        int rc = orc_poly_mul(a, at, b, bt, full);
+        if (!rc) memcpy(out, full, sizeof(uint32_t) * (len < count ? len : count));
+        free(full);
+        return rc;
+    }
+    uint32_t h = (count + 1) / 2;
+    uint32_t alo = at < h ? at : h, blo = bt < h ? bt : h;
+    uint32_t* lo = (uint32_t*)malloc(sizeof(uint32_t) * (alo + blo - 1));
+    int rc = orc_poly_mul(a, alo, b, blo, lo);
+    if (!rc) {
+        uint32_t ll = alo + blo - 1;
+        memcpy(out, lo, sizeof(uint32_t) * (ll < count ? ll : count));
+    }
+    free(lo);
+    uint32_t rest = count - h;
+    uint32_t* c1 = (uint32_t*)calloc(rest ? rest : 1, sizeof(uint32_t));
+    uint32_t* c2 = (uint32_t*)calloc(rest ? rest : 1, sizeof(uint32_t));
+    if (!rc && rest) rc = mul_low(a, alo, b + blo, bt - blo, rest, c1);
+    if (!rc && rest) rc = mul_low(a + alo, at - alo, b, blo, rest, c2);
+    for (uint32_t j = 0; !rc && j < rest; ++j) out[h + j] = orc_add(out[h + j], orc_add(c1[j], c2[j]));
+    free(c1);
+    free(c2);
+    return rc;
+}
+
 /* interpolate (interp.cpp:103-137), steps 4-6, for a plan built by
  * orc_build_plan. Writes k coefficients (normalised then re-padded with
  * zeros to k, which is what codec::first_k_coeffs returns, codec.cpp:105-108).
  * Step 5 computes s_j = -N'(r^-(j+1)) as -fnt_forward(N')[n-1-j]
  * (geom_eval_negative visits the forward points in reverse order,
- * test_geom.cpp:74-82). The mul_low fallback (2k > 65536) is out of scope. */
+ * test_geom.cpp:74-82). 2k > 65536 (product_size 0): orc_interpolate_low. */
+static int interpolate_split(uint32_t n, uint32_t k, const uint32_t* positions, const uint32_t* aprime_inv,
+                             const uint32_t* a, const uint32_t* values, uint32_t* out);
+
 int orc_interpolate(uint32_t n, uint32_t k, const uint32_t* positions, const uint32_t* aprime_inv,
                     uint32_t product_size, const uint32_t* a_fnt, const uint32_t* values,
                     uint32_t* out) {
-    if (!product_size) return ORC_E_PRODUCT_TOO_LARGE;
+    if (!product_size) return ORC_E_PRODUCT_TOO_LARGE; /* needs A itself: orc_interpolate_low */
     uint32_t* np = (uint32_t*)calloc(n, sizeof(uint32_t));
     for (uint32_t i = 0; i < k; ++i) np[positions[i]] = orc_mul(values[i], aprime_inv[i]);
     orc_fnt_forward(n, np, np);
@@ -409,6 +449,27 @@ int orc_interpolate(uint32_t n, uint32_t k, const uint32_t* positions, const uin
     memcpy(out, buf, sizeof(uint32_t) * k);
     free(buf);
     return ORC_OK;
+}
+
+/* interpolate step 6 when 2k > 65536 (interp.cpp:133-134): P = mul_low(A, S, k)
+ * with A the locator's k+1 coefficients and S the truncated series. */
+static int interpolate_split(uint32_t n, uint32_t k, const uint32_t* positions, const uint32_t* aprime_inv,
+                             const uint32_t* a, const uint32_t* values, uint32_t* out) {
+    uint32_t* np = (uint32_t*)calloc(n, sizeof(uint32_t));
+    for (uint32_t i = 0; i < k; ++i) np[positions[i]] = orc_mul(values[i], aprime_inv[i]);
+    orc_fnt_forward(n, np, np);
+    uint32_t take = k < n ? k : n;
+    uint32_t* series = (uint32_t*)calloc(k, sizeof(uint32_t));
+    for (uint32_t j = 0; j < take; ++j) series[j] = orc_neg(np[n - 1 - j]);
+    free(np);
+    int rc = mul_low(a, k + 1, series, k, k, out);
+    free(series);
+    return rc;
+}
+
+int orc_interpolate_low(uint32_t n, uint32_t k, const uint32_t* positions, const uint32_t* aprime_inv,
+                        const uint32_t* a, const uint32_t* values, uint32_t* out) {
+    return interpolate_split(n, k, positions, aprime_inv, a, values, out);
 }
 
 /* lagrange_oracle (interp.cpp:139-171): quadratic interpolation through
@@ -534,7 +595,8 @@ int orc_decode(uint32_t k, uint32_t n, uint32_t count, const uint32_t* pos, cons
             memcpy(afnt, a, sizeof(uint32_t) * (k + 1));
             dif_core(afnt, psize, plan_for(psize)->stage);
         }
-        rc = orc_interpolate(nd, k, zp, ainv, psize, afnt, vs, out);
+        rc = psize ? orc_interpolate(nd, k, zp, ainv, psize, afnt, vs, out)
+                   : orc_interpolate_low(nd, k, zp, ainv, a, vs, out); /* 2k > 65536: mul_low */
         free(afnt);
     }
     free(a); free(ainv); free(zp); free(vs);

@@ -48,6 +48,8 @@ int orc_build_plan(uint32_t n, uint32_t k, const uint32_t* positions, uint32_t* 
 int orc_interpolate(uint32_t n, uint32_t k, const uint32_t* positions, const uint32_t* aprime_inv,
                     uint32_t product_size, const uint32_t* a_fnt, const uint32_t* values,
                     uint32_t* out);
+int orc_interpolate_low(uint32_t n, uint32_t k, const uint32_t* positions, const uint32_t* aprime_inv,
+                        const uint32_t* a, const uint32_t* values, uint32_t* out);
 int orc_lagrange(uint32_t k, const uint32_t* xs, const uint32_t* vs, uint32_t* out);
 
 int orc_code_params(uint32_t k, uint32_t n, uint32_t* n_domain);

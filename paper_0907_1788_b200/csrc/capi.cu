@@ -45,6 +45,9 @@ struct fntrs_plans {
     uint2* ahat2 = nullptr;
     bool cols = false;        // served by the general column path (codec_cols.cu)
     bool full = false;        // complete reception
+    bool split = false;       // 2k > 65536: locator halves' spectra (alo, ahi), product_size 0
+    uint32_t* alo = nullptr;  // [65536][np]
+    uint32_t* ahi = nullptr;
 };
 
 namespace {
@@ -122,7 +125,7 @@ constexpr size_t kScratchCap = size_t(2) << 30;  // per four-step intermediate b
 // Per-call stream-ordered scratch (released in stream order by release_scratch),
 // so concurrent calls on different streams never share intermediates.
 struct Scratch {
-    uint32_t* p[3] = {nullptr, nullptr, nullptr};
+    uint32_t* p[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 int get_scratch(fntrs_ctx* ctx, Scratch& s, size_t bytes, int count, cudaStream_t st) {
     for (int i = 0; i < count; ++i) CK(cudaMallocAsync(&s.p[i], bytes, st), "scratch alloc");
@@ -333,14 +336,14 @@ int fntrs_gpu_plans_create(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t kp, 
     if (kp < k) return fail(ctx, FNTRS_E_NOT_ENOUGH_SYMBOLS, "have " + std::to_string(kp) + " symbols, need " + std::to_string(k));
     if (kp != k && !full)
         return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "kp must equal k (or n for complete reception)");
-    if (2ull * k > 65536ull && !full)
-        return fail(ctx, FNTRS_E_UNSUPPORTED, "2k > 65536 needs the split product (mul_low), not in this build");
-    const uint32_t M = 2ull * k > 65536ull ? 0u : next_pow2(2 * k);
+    // 2k > 65536: no product transform fits (interp.cpp:63-67); the product runs by halves
+    const bool split = 2ull * k > 65536ull && !full;
+    const uint32_t M = split ? 65536u : (2ull * k > 65536ull ? 0u : next_pow2(2 * k));
     // locator data: needed for decoding unless complete; kept for export when it fits
     const bool locator = !full || (kp == k && M && M <= kTileMaxN);
-    const bool large = fast::large_supported(N) && !full && kp == k && M == N;
+    const bool large = fast::large_supported(N) && !full && !split && kp == k && M == N;
     // shapes neither the fused nor the tile kernels take: the general column path
-    const bool cols = !large && (N > kTileMaxN || (!full && M > kTileMaxN));
+    const bool cols = split || (!large && (N > kTileMaxN || (!full && M > kTileMaxN)));
     if (npatterns && !positions) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "positions is null");
     // validation (codec.cpp:32-48 order: range first, then duplicates)
     std::vector<uint8_t> seen(n);
@@ -368,6 +371,7 @@ int fntrs_gpu_plans_create(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t kp, 
     pl->np = npatterns;
     pl->cols = cols;
     pl->full = full;
+    pl->split = split;
     pl->ninv = cpow(N % kP, kP - 2);
     const size_t npos = size_t(npatterns) * kp;
     cudaError_t e = cudaSuccess;
@@ -377,7 +381,7 @@ int fntrs_gpu_plans_create(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t kp, 
         if (!e) e = cudaMallocAsync(&pl->ainv, npos * 4, st);
         if (!e && locator) e = cudaMallocAsync(&pl->ahat, size_t(npatterns) * M * 4, st);
         if (!e) e = cudaMemcpyAsync(pl->pos, positions, npos * 4, cudaMemcpyHostToDevice, st);
-        const bool fastplan = !full && kp == k && M == N && (fast::fast_tile_columns(N) || large);
+        const bool fastplan = !full && !split && kp == k && M == N && (fast::fast_tile_columns(N) || large);
         if (!e && fastplan) {
             // log-domain convolution plan (plan_fast.cu): ainv, ahat, rowmap, ahat2 at once
             e = cudaMallocAsync(&pl->rowmap, size_t(npatterns) * N * sizeof(uint2), st);
@@ -412,6 +416,18 @@ int fntrs_gpu_plans_create(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t kp, 
             if (!e) e = fast::build_cols_rowmap(N, kp, npatterns, pl->pos, full ? nullptr : pl->ainv, pl->rowmap, st);
             ctx->launches += 2;
         }
+        if (!e && split) {  // spectra of the locator's halves (build_split_spectra)
+            const size_t words = size_t(M) * npatterns;
+            uint32_t *c = nullptr, *T = nullptr;
+            e = cudaMallocAsync(&pl->alo, words * 4, st);
+            if (!e) e = cudaMallocAsync(&pl->ahi, words * 4, st);
+            if (!e) e = cudaMallocAsync(&c, words * 4, st);
+            if (!e) e = cudaMallocAsync(&T, words * 4, st);
+            if (!e) e = fast::build_split_spectra(ctx->ftab, k, npatterns, pl->ahat, pl->alo, pl->ahi, c, T, st);
+            if (c) cudaFreeAsync(c, st);
+            if (T) cudaFreeAsync(T, st);
+            ctx->launches += 6;
+        }
     }
     if (e) {
         fntrs_gpu_plans_destroy(pl);
@@ -426,7 +442,8 @@ int fntrs_gpu_plans_destroy(fntrs_plans* pl) {
     DeviceGuard g(pl->device);
     // stream-ordered release: work already queued on the plan's stream may
     // still read the buffers; callers using other streams must order them
-    for (void* p : {(void*)pl->pos, (void*)pl->ainv, (void*)pl->ahat, (void*)pl->rowmap, (void*)pl->ahat2})
+    for (void* p : {(void*)pl->pos, (void*)pl->ainv, (void*)pl->ahat, (void*)pl->rowmap, (void*)pl->ahat2,
+                    (void*)pl->alo, (void*)pl->ahi})
         if (p) cudaFreeAsync(p, pl->stream);
     delete pl;
     return FNTRS_OK;
@@ -472,8 +489,8 @@ int fntrs_gpu_plans_export(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t patte
     cudaFree(acoef);
     cudaFree(spec);
     if (a_coeffs) std::memcpy(a_coeffs, a.data(), size_t(kp + 1 <= M ? kp + 1 : M) * 4);
-    if (product_size) *product_size = M;
-    if (a_fnt) {  // dif_forward leaves the spectrum in bit-reversed order (transform.hpp:43-48)
+    if (product_size) *product_size = pl->split ? 0u : M;  // interp.cpp:63-67: no product transform
+    if (a_fnt && !pl->split) {  // dif_forward leaves the spectrum in bit-reversed order (transform.hpp:43-48)
         int lg = 0;
         while ((1u << lg) < M) ++lg;
         for (uint32_t i = 0; i < M; ++i) {
@@ -511,11 +528,12 @@ int fntrs_gpu_decode(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t stripes, ui
             const uint32_t D = std::max(pl->N, pl->M);
             const uint64_t cap = std::min<uint64_t>(uint64_t(stripes) * L, fast::cols_batch_columns(D, kScratchCap));
             Scratch sc;
-            rc = get_scratch(ctx, sc, size_t(D) * cap * 4, 3, st);
+            rc = get_scratch(ctx, sc, size_t(D) * cap * 4, pl->split ? 4 : 3, st);
             if (rc) return rc;
-            fast::ColsPlanView cv{pl->N, pl->full ? pl->N : pl->M, pl->k, pl->kp, pl->full, pl->rowmap, pl->ahat};
+            fast::ColsPlanView cv{pl->N,      pl->full ? pl->N : pl->M, pl->k,      pl->kp,  pl->np, pl->full,
+                                  pl->split,  pl->rowmap,               pl->ahat,   pl->alo, pl->ahi};
             cudaError_t le = fast::launch_decode_cols(ctx->ftab, cv, stripes, L, stripe_pattern, rx, ein, out, eout,
-                                                      sc.p[0], sc.p[1], sc.p[2], cap, st);
+                                                      sc.p[0], sc.p[1], sc.p[3], sc.p[2], cap, st);
             release_scratch(sc, st);
             CK(le, "decode launch");
             ctx->launches += 7 * ((uint64_t(stripes) * L + cap - 1) / cap);

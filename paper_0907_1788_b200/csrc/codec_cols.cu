@@ -19,6 +19,14 @@
 // and a final kernel writes the first k rows as uint16 packets with the
 // 65536 escape list. Encode is FNT_N of the zero-padded source columns
 // (codec.cpp:124-131) written out as n rows.
+//
+// 2k > 65536 (no product transform fits; the reference's poly::mul_low,
+// poly.cpp:139-169): P = A_lo S_lo + x^h (A_lo S_hi + A_hi S_lo) mod x^k with
+// h = ceil(k/2); every partial product has fewer than 65536 coefficients, so
+// each is exact as a size-65536 cyclic convolution. Per codeword: FNT1, the
+// spectra of S_lo and S_hi, and two unscaled inverses (lo*lo, and the two
+// cross terms summed in the frequency domain); the locator halves' spectra
+// -A_lo^/M and -A_hi^/M are per-pattern plan data (build_split_spectra).
 #include <cuda_runtime.h>
 
 #include "fnt_cols.cuh"
@@ -87,6 +95,67 @@ struct LdAhat {
     }
 };
 
+// s'_{j+off} = F[N-1-(j+off)] for j < cnt, else 0 (a slice of the series)
+struct LdRevSlice {
+    const uint32_t* F;
+    uint32_t C, N, off, cnt;
+    __device__ __forceinline__ uint32_t operator()(uint32_t j, uint32_t c) const {
+        return j < cnt ? F[size_t(N - 1u - off - j) * C + c] : 0u;
+    }
+};
+
+// split product inputs: X1 * W1[pattern] (+ X2 * W2[pattern]); W are [M][P] columns
+struct LdSplit {
+    Col col;
+    const uint32_t *X1, *X2, *W1, *W2;
+    const uint32_t* sp;
+    uint32_t C, P;
+    __device__ __forceinline__ uint32_t operator()(uint32_t j, uint32_t c_) const {
+        uint64_t s;
+        uint32_t c;
+        col.at(c_, s, c);
+        const size_t w = size_t(j) * P + __ldg(sp + s);
+        uint32_t v = mulw(X1[size_t(j) * C + c_], __ldg(W1 + w));
+        if (X2) v = red2p(red2p(v) + red2p(mulw(X2[size_t(j) * C + c_], __ldg(W2 + w))));
+        return v;
+    }
+};
+
+// plan arrays [P][M] read as columns (row t of pattern p)
+struct LdPatternRows {
+    const uint32_t* in;
+    uint32_t M;
+    __device__ __forceinline__ uint32_t operator()(uint32_t t, uint32_t p) const { return in[size_t(p) * M + t]; }
+};
+
+// locator halves from its coefficients c[t][p] (= -a_t): lo = t < h, hi = h + t <= k
+struct LdLocatorHalf {
+    const uint32_t* c;
+    uint32_t P, h, k;
+    bool hi;
+    __device__ __forceinline__ uint32_t operator()(uint32_t t, uint32_t p) const {
+        if (!hi) return t < h ? c[size_t(t) * P + p] : 0u;
+        return h + t <= k ? c[size_t(h + t) * P + p] : 0u;
+    }
+};
+
+// P[j] = U[j] + V[j - h] (j >= h), j < rows -> packets, as out_rows_kernel
+__global__ void out_split_kernel(const uint32_t* __restrict__ U, const uint32_t* __restrict__ V, uint32_t C,
+                                 uint32_t rows, uint32_t h, Col col, uint16_t* __restrict__ out, EscOut eout) {
+    const uint64_t total = uint64_t(rows) * C;
+    for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < total; t += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t f = uint32_t(t / C), c_ = uint32_t(t - uint64_t(f) * C);
+        uint64_t s;
+        uint32_t c;
+        col.at(c_, s, c);
+        uint32_t y = U[t];
+        if (f >= h) y = red2p(y + V[uint64_t(f - h) * C + c_]);
+        const uint64_t key = (s * rows + f) * col.L + c;
+        out[key] = uint16_t(y);
+        if (y == 65536u) emit_escape(eout, key);
+    }
+}
+
 // encode input: source row i < k of the codeword, zero padded to N
 struct LdSource {
     Col col;
@@ -139,6 +208,18 @@ constexpr int kOutBlocks = 148 * 8;
 
 }  // namespace
 
+cudaError_t build_split_spectra(const FastTables& t, uint32_t k, uint32_t P, const uint32_t* ahat, uint32_t* alo,
+                                uint32_t* ahi, uint32_t* c, uint32_t* T, cudaStream_t st) {
+    constexpr uint32_t M = 65536;
+    if (!P) return cudaSuccess;
+    const uint32_t h = (k + 1) / 2, minv = cpow(M % kP, kP - 2);
+    // c = IFNT_unscaled(ahat) = -a_t (ahat = -A^/M and deg A = k < M: no wrap)
+    cudaError_t err = run_cols<true>(t, M, LdPatternRows{ahat, M}, P, 1u, T, c, st);
+    if (!err) err = run_cols<false>(t, M, LdLocatorHalf{c, P, h, k, false}, P, minv, T, alo, st);
+    if (!err) err = run_cols<false>(t, M, LdLocatorHalf{c, P, h, k, true}, P, minv, T, ahi, st);
+    return err;
+}
+
 uint64_t cols_batch_columns(uint32_t D, size_t cap_bytes) {
     const uint64_t c = cap_bytes / (uint64_t(D) * 4);
     return c >= 32 ? c / 32 * 32 : 32;
@@ -168,7 +249,8 @@ cudaError_t launch_encode_cols(const FastTables& t, uint32_t k, uint32_t n, uint
 
 cudaError_t launch_decode_cols(const FastTables& t, const ColsPlanView& pv, uint32_t stripes, uint32_t L,
                                const uint32_t* sp, const uint16_t* rx, EscIn ein, uint16_t* out, EscOut eout,
-                               uint32_t* A, uint32_t* B, uint32_t* T, uint64_t cap_cols, cudaStream_t st) {
+                               uint32_t* A, uint32_t* B, uint32_t* X, uint32_t* T, uint64_t cap_cols,
+                               cudaStream_t st) {
     const uint64_t total = uint64_t(stripes) * L;
     const uint32_t N = pv.N, M = pv.M, k = pv.k;
     for (uint64_t g0 = 0; g0 < total; g0 += cap_cols) {
@@ -178,6 +260,18 @@ cudaError_t launch_decode_cols(const FastTables& t, const ColsPlanView& pv, uint
         cudaError_t err;
         if (pv.full) {  // all n = N positions: coefficients = FNT_N^-1 of the received values
             err = run_cols<true>(t, N, scatter, C, cpow(N % kP, kP - 2), T, A, st);
+        } else if (pv.split) {  // 2k > 65536: mul_low by halves (N = M = 65536)
+            const uint32_t h = (k + 1) / 2;
+            if ((err = run_cols<false>(t, N, scatter, C, 1u, T, A, st))) return err;
+            if ((err = run_cols<false>(t, M, LdRevSlice{A, C, N, 0, h}, C, 1u, T, B, st))) return err;      // S_lo^
+            if ((err = run_cols<false>(t, M, LdRevSlice{A, C, N, h, k - h}, C, 1u, T, X, st))) return err;  // S_hi^
+            // U = -(A_lo S_lo) into A; V = -(A_lo S_hi + A_hi S_lo) into B (read fully before written)
+            if ((err = run_cols<true>(t, M, LdSplit{col, B, nullptr, pv.alo, nullptr, sp, C, pv.np}, C, 1u, T, A, st)))
+                return err;
+            if ((err = run_cols<true>(t, M, LdSplit{col, X, B, pv.alo, pv.ahi, sp, C, pv.np}, C, 1u, T, B, st)))
+                return err;
+            out_split_kernel<<<kOutBlocks, kOutThreads, 0, st>>>(A, B, C, k, h, col, out, eout);
+            continue;
         } else {
             if ((err = run_cols<false>(t, N, scatter, C, 1u, T, A, st))) return err;
             if ((err = run_cols<false>(t, M, LdRevTrunc{A, C, N, k}, C, 1u, T, B, st))) return err;

@@ -133,11 +133,17 @@ cudaError_t launch_fnt_cols(const FastTables& t, uint32_t N, bool inverse, uint3
 // ---- general path (codec_cols.cu): column transforms through HBM, any shape
 // with n_domain, M <= 65536
 struct ColsPlanView {
-    uint32_t N, M, k, kp;
+    uint32_t N, M, k, kp, np;
     bool full;             // complete reception: one inverse transform
+    bool split;            // 2k > 65536: product by halves (M = N = 65536)
     const uint2* rowmap;   // [np][N] {received row or ~0, balanced 1/A'(x_i) (1 when full)}
     const uint32_t* ahat;  // [np][M] -A_hat / M (unused when full)
+    const uint32_t* alo;   // split: [M][np] -FNT(A_lo) / M
+    const uint32_t* ahi;   // split: [M][np] -FNT(A_hi) / M
 };
+// split plans: alo/ahi ([65536][P]) from ahat ([P][65536]); c, T: [65536][P] scratch
+cudaError_t build_split_spectra(const FastTables& t, uint32_t k, uint32_t P, const uint32_t* ahat, uint32_t* alo,
+                                uint32_t* ahi, uint32_t* c, uint32_t* T, cudaStream_t st);
 // columns per batch so one [max(N, M)][C] uint32 buffer stays within cap_bytes
 uint64_t cols_batch_columns(uint32_t D, size_t cap_bytes);
 cudaError_t build_cols_rowmap(uint32_t N, uint32_t kp, uint32_t P, const uint32_t* pos, const uint32_t* ainv,
@@ -146,10 +152,11 @@ cudaError_t build_cols_rowmap(uint32_t N, uint32_t kp, uint32_t P, const uint32_
 cudaError_t launch_encode_cols(const FastTables& t, uint32_t k, uint32_t n, uint32_t N, uint32_t stripes, uint32_t L,
                                const uint16_t* src, EscIn ein, uint16_t* out, EscOut eout, uint32_t* A, uint32_t* T,
                                uint64_t cap_cols, cudaStream_t st);
-// A, B, T: [max(N, M)][cap_cols] uint32 scratch each
+// A, B, X, T: [max(N, M)][cap_cols] uint32 scratch each (X only for split plans)
 cudaError_t launch_decode_cols(const FastTables& t, const ColsPlanView& pv, uint32_t stripes, uint32_t L,
                                const uint32_t* sp, const uint16_t* rx, EscIn ein, uint16_t* out, EscOut eout,
-                               uint32_t* A, uint32_t* B, uint32_t* T, uint64_t cap_cols, cudaStream_t st);
+                               uint32_t* A, uint32_t* B, uint32_t* X, uint32_t* T, uint64_t cap_cols,
+                               cudaStream_t st);
 }  // namespace fast
 
 }  // namespace fntrs_gpu

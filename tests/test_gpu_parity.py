@@ -130,6 +130,8 @@ SHAPES = [  # (k, n, L, stripes)
     # general column path (codec_cols.cu): product size M != n_domain above 4096, any L
     (3000, 4096, 16, 1), (2000, 16384, 8, 1), (1000, 8192, 10, 2), (4096, 8192, 40, 1), (5000, 9000, 8, 1),
     (20000, 32768, 8, 1), (40, 10000, 16, 1),
+    # 2k > 65536: the product by halves (reference poly::mul_low)
+    (33000, 65536, 8, 1), (40000, 50000, 4, 2),
 ]
 
 
@@ -170,7 +172,8 @@ def test_decode_matches_oracle(codec, oracle, k, n, L, S):
 
 
 @pytest.mark.parametrize("n,k", [(2, 2), (4, 2), (8, 3), (8, 5), (16, 12), (256, 128), (2048, 1024), (4096, 2048),
-                                 (1000, 300), (200, 100), (64, 17), (16384, 8192), (12000, 5000)])
+                                 (1000, 300), (200, 100), (64, 17), (16384, 8192), (12000, 5000),
+                                 (65536, 33000), (16384, 2000), (8192, 5000)])
 def test_plan_fields_match_oracle(codec, oracle, n, k):
     nd = 1 << (n - 1).bit_length()
     rng = np.random.default_rng(n + k)

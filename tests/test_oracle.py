@@ -256,6 +256,18 @@ def test_oracle_matches_reference_library(oracle, ref):
         assert oracle.decode(*args)[0] == ref.decode(*args)[0]
 
 
+def test_mul_low_split_matches_reference(oracle, ref):  # interp.cpp:133-134, poly.cpp:139-169
+    """2k > 65536: no product transform fits, the reference splits the product."""
+    rng = np.random.default_rng(33)
+    for n, k in [(65536, 32769), (40000, 33000)]:
+        pos = np.sort(rng.choice(n, k, replace=False)).astype(np.uint32)
+        vals = rng.integers(0, P, k).astype(np.uint32)  # arbitrary received values
+        so, go = oracle.decode(k, n, pos, vals)
+        sr, gr = ref.decode(k, n, pos, vals, path=1)
+        assert so == sr == 0 and np.array_equal(go, gr[:k])
+        assert ref.build_plan(1 << (n - 1).bit_length(), pos)[3] == 0  # product_size 0
+
+
 def test_oracle_matches_reference_stripes(oracle, ref):
     from paper_0907_1788_b200 import workload as W
     from oracle_bind import gather_received
