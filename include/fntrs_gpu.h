@@ -148,6 +148,28 @@ int fntrs_gpu_decode_systematic(fntrs_ctx* ctx, const fntrs_plans* plans, uint32
                                 uint64_t n_rx_esc, uint16_t* out, uint64_t* out_esc, uint64_t esc_cap,
                                 uint64_t* n_out_esc, void* stream);
 
+/* Shard wire format, data movement on the device (proj/src/shardio.cpp).
+ * The reference CLI codes a file as S = ceil(ceil(len/2) / k) one-codeword
+ * stripes and shard j holds symbol j of every stripe; in the batched model
+ * that is ONE stripe of k packets with L >= S symbols (columns >= S are zero
+ * padding), and row j of the encoded stripe is shard j's payload.
+ *   symbolize   (shardio.cpp:83-96):  DEVICE bytes[len] -> src[k][L] uint16,
+ *               src[i][t] = big-endian word t*k + i (zero past the data)
+ *   desymbolize (shardio.cpp:98-116): dec[k][L] -> DEVICE bytes[len]
+ *   words_to_be (write_shard payload, shardio.cpp:153-154): rows[nrows][L] ->
+ *               out[r*pitch + 2t .. +1] big-endian, t < count
+ *   be_to_words (read_shard payload, shardio.cpp:203-208): the inverse, columns
+ *               count..L-1 zeroed
+ * Headers, escape lists and manifests are host formatting (shards.py). */
+int fntrs_gpu_symbolize(fntrs_ctx* ctx, const uint8_t* data, uint64_t len, uint32_t k, uint32_t L, uint16_t* src,
+                        void* stream);
+int fntrs_gpu_desymbolize(fntrs_ctx* ctx, const uint16_t* dec, uint32_t k, uint32_t L, uint64_t len, uint8_t* out,
+                          void* stream);
+int fntrs_gpu_words_to_be(fntrs_ctx* ctx, const uint16_t* rows, uint32_t nrows, uint32_t L, uint32_t count,
+                          uint8_t* out, uint64_t pitch, void* stream);
+int fntrs_gpu_be_to_words(fntrs_ctx* ctx, const uint8_t* in, uint64_t pitch, uint32_t nrows, uint32_t count,
+                          uint32_t L, uint16_t* rows, void* stream);
+
 /* fnt_forward / fnt_inverse (proj/src/transform.cpp:302-323) over the columns
  * of a DEVICE [m][L] uint32 array of canonical values; natural order. */
 int fntrs_gpu_fnt(fntrs_ctx* ctx, uint32_t m, int inverse, uint32_t L, const uint32_t* in,

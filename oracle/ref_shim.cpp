@@ -23,6 +23,7 @@
 #include "fntrs/codec.hpp"
 #include "fntrs/errors.hpp"
 #include "fntrs/interp.hpp"
+#include "fntrs/shardio.hpp"
 #include "fntrs/transform.hpp"
 
 using namespace fntrs;
@@ -40,6 +41,13 @@ int status_of(const std::exception& e) {
     if (dynamic_cast<const TooFewPositions*>(&e)) return 9;
     if (dynamic_cast<const NotEnoughSymbols*>(&e)) return 10;
     if (dynamic_cast<const TooManyEscapes*>(&e)) return 11;
+    if (dynamic_cast<const BadMagic*>(&e)) return 12;
+    if (dynamic_cast<const BadVersion*>(&e)) return 13;
+    if (dynamic_cast<const TruncatedShard*>(&e)) return 14;
+    if (dynamic_cast<const MalformedEscapes*>(&e)) return 15;
+    if (dynamic_cast<const MalformedHeader*>(&e)) return 16;
+    if (dynamic_cast<const LengthMismatch*>(&e)) return 17;
+    if (dynamic_cast<const NotEnoughShards*>(&e)) return 18;
     return 1;
 }
 
@@ -259,6 +267,67 @@ int64_t ref_decode_stripes(uint32_t k, uint32_t n, uint32_t stripes, uint32_t L,
     std::sort(escapes.begin(), escapes.end());
     std::copy(escapes.begin(), escapes.end(), out_esc);
     return int64_t(escapes.size());
+}
+
+// The reference CLI's encode (proj/tools/fntrs_main.cpp:117-160) minus the
+// file system: symbolize, per-stripe encode, one shard per code position,
+// manifest. Writes the manifest then shards 0..n-1 back to back into out
+// (capacity cap) and their sizes into sizes[0..n]; returns total bytes or a
+// negative status.
+int64_t ref_encode_file(const uint8_t* data, uint64_t len, uint32_t k, uint32_t n, int systematic,
+                        uint64_t chunk_id, uint8_t* out, uint64_t cap, uint64_t* sizes) {
+    try {
+        const auto params = codec::CodeParams::make(k, n, systematic != 0);
+        const auto m = shardio::symbolize(std::span<const uint8_t>(data, len), k);
+        std::vector<Fe> enc(size_t(m.stripes) * n);
+        for (uint32_t t = 0; t < m.stripes; ++t) {
+            std::span<const Fe> src(m.cells.data() + size_t(t) * k, k);
+            auto row = systematic ? codec::encode_systematic(params, src) : codec::encode_nonsystematic(params, src);
+            std::copy(row.begin(), row.end(), enc.begin() + size_t(t) * n);
+        }
+        uint64_t pos = 0;
+        auto emit = [&](const std::vector<uint8_t>& b, uint64_t* sz) {
+            if (pos + b.size() > cap) throw TooManyEscapes("output capacity");
+            std::memcpy(out + pos, b.data(), b.size());
+            pos += b.size();
+            *sz = b.size();
+        };
+        emit(shardio::write_manifest({chunk_id, len, k, n, m.stripes, systematic != 0}), &sizes[0]);
+        shardio::ShardInfo info{chunk_id, k, n, 0, systematic != 0};
+        std::vector<Fe> payload(m.stripes);
+        for (uint32_t j = 0; j < n; ++j) {
+            for (uint32_t t = 0; t < m.stripes; ++t) payload[t] = enc[size_t(t) * n + j];
+            info.shard_index = j;
+            emit(shardio::write_shard(info, payload), &sizes[1 + j]);
+        }
+        return int64_t(pos);
+    } catch (const std::exception& e) {
+        return -status_of(e);
+    }
+}
+
+// shardio::write_shard of explicit values (frozen-layout checks)
+int64_t ref_write_shard(uint64_t chunk_id, uint32_t k, uint32_t n, uint32_t index, int systematic,
+                        const uint32_t* payload, uint64_t count, uint8_t* out, uint64_t cap) {
+    try {
+        auto b = shardio::write_shard({chunk_id, k, n, index, systematic != 0},
+                                      std::span<const Fe>(payload, count));
+        if (b.size() > cap) return -1;
+        std::memcpy(out, b.data(), b.size());
+        return int64_t(b.size());
+    } catch (const std::exception& e) {
+        return -status_of(e);
+    }
+}
+
+// shardio::read_shard status (0 = accepted) for malformed-input checks
+int ref_read_shard_status(const uint8_t* bytes, uint64_t len) {
+    try {
+        (void)shardio::read_shard(std::span<const uint8_t>(bytes, len));
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
 }
 
 int ref_has_avx2(void) {

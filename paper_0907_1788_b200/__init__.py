@@ -11,8 +11,11 @@ from .codec import (  # noqa: F401
     encode_systematic,
     Error, ZeroInverse, InvalidTransformSize, SizeMismatch, ProductTooLarge, DuplicatePoint,
     DuplicatePosition, PositionOutOfRange, TooFewPositions, NotEnoughSymbols, TooManyEscapes,
+    BadMagic, BadVersion, TruncatedShard, MalformedEscapes, MalformedHeader, LengthMismatch, NotEnoughShards,
     UnsupportedShape, default_escape_capacity, escapes_to_numpy,
 )
 from . import workload  # noqa: F401
+from . import shards  # noqa: F401
+from .shards import decode_file, encode_file  # noqa: F401
 
 __version__ = "0.1.0"

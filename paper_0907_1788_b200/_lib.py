@@ -35,6 +35,10 @@ SIGNATURES = [
     ("fntrs_gpu_decode", _int, [_vp, _vp, _u32, _u32, _vp, _vp, _vp, _u64, _vp, _vp, _u64, _vp, _vp]),
     ("fntrs_gpu_encode_systematic", _int, [_vp, _u32, _u32, _u32, _u32, _vp, _vp, _u64, _vp, _vp, _u64, _vp, _vp]),
     ("fntrs_gpu_decode_systematic", _int, [_vp, _vp, _u32, _u32, _vp, _vp, _vp, _u64, _vp, _vp, _u64, _vp, _vp]),
+    ("fntrs_gpu_symbolize", _int, [_vp, _vp, _u64, _u32, _u32, _vp, _vp]),
+    ("fntrs_gpu_desymbolize", _int, [_vp, _vp, _u32, _u32, _u64, _vp, _vp]),
+    ("fntrs_gpu_words_to_be", _int, [_vp, _vp, _u32, _u32, _u32, _vp, _u64, _vp]),
+    ("fntrs_gpu_be_to_words", _int, [_vp, _vp, _u64, _u32, _u32, _u32, _vp, _vp]),
     ("fntrs_gpu_fnt", _int, [_vp, _u32, _int, _u32, _vp, _vp, _vp]),
     ("fntrs_gpu_launch_count", _u64, [_vp]),
     ("fntrs_gpu_set_fast_path", _int, [_vp, _int]),

@@ -678,6 +678,51 @@ int fntrs_gpu_decode_systematic(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t 
     return rc;
 }
 
+int fntrs_gpu_symbolize(fntrs_ctx* ctx, const uint8_t* data, uint64_t len, uint32_t k, uint32_t L, uint16_t* src,
+                        void* stream) {
+    if (!ctx) return FNTRS_E_INVALID_ARGUMENT;
+    if (k == 0) return fail(ctx, FNTRS_E_SIZE_MISMATCH, "symbolize needs k >= 1");
+    if ((len + 1) / 2 > uint64_t(k) * L) return fail(ctx, FNTRS_E_LENGTH_MISMATCH, "L too small for the data");
+    if ((len && !data) || (L && !src)) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "null buffer");
+    DeviceGuard g(ctx->device);
+    CK(launch_symbolize(data, len, k, L, src, static_cast<cudaStream_t>(stream)), "symbolize");
+    ctx->launches += 1;
+    return FNTRS_OK;
+}
+
+int fntrs_gpu_desymbolize(fntrs_ctx* ctx, const uint16_t* dec, uint32_t k, uint32_t L, uint64_t len, uint8_t* out,
+                          void* stream) {
+    if (!ctx) return FNTRS_E_INVALID_ARGUMENT;
+    if (k == 0 || len > uint64_t(k) * L * 2) return fail(ctx, FNTRS_E_LENGTH_MISMATCH, "length exceeds capacity");
+    if (len && (!dec || !out)) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "null buffer");
+    DeviceGuard g(ctx->device);
+    CK(launch_desymbolize(dec, k, L, len, out, static_cast<cudaStream_t>(stream)), "desymbolize");
+    ctx->launches += 1;
+    return FNTRS_OK;
+}
+
+int fntrs_gpu_words_to_be(fntrs_ctx* ctx, const uint16_t* rows, uint32_t nrows, uint32_t L, uint32_t count,
+                          uint8_t* out, uint64_t pitch, void* stream) {
+    if (!ctx) return FNTRS_E_INVALID_ARGUMENT;
+    if (count > L || pitch < 2ull * count) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "count/pitch out of range");
+    if (nrows && count && (!rows || !out)) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "null buffer");
+    DeviceGuard g(ctx->device);
+    CK(launch_words_to_be(rows, nrows, L, count, out, pitch, static_cast<cudaStream_t>(stream)), "words_to_be");
+    ctx->launches += 1;
+    return FNTRS_OK;
+}
+
+int fntrs_gpu_be_to_words(fntrs_ctx* ctx, const uint8_t* in, uint64_t pitch, uint32_t nrows, uint32_t count,
+                          uint32_t L, uint16_t* rows, void* stream) {
+    if (!ctx) return FNTRS_E_INVALID_ARGUMENT;
+    if (count > L || pitch < 2ull * count) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "count/pitch out of range");
+    if (nrows && L && (!rows || (count && !in))) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "null buffer");
+    DeviceGuard g(ctx->device);
+    CK(launch_be_to_words(in, pitch, nrows, count, L, rows, static_cast<cudaStream_t>(stream)), "be_to_words");
+    ctx->launches += 1;
+    return FNTRS_OK;
+}
+
 int fntrs_gpu_fnt(fntrs_ctx* ctx, uint32_t m, int inverse, uint32_t L, const uint32_t* in, uint32_t* out,
                   void* stream) {
     if (!ctx) return FNTRS_E_INVALID_ARGUMENT;

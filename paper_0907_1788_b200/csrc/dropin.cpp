@@ -15,9 +15,20 @@
 #include <vector>
 
 #include "fntrs/codec.hpp"
+#include "fntrs/instrument.hpp"
 #include "fntrs_gpu.h"
 
 namespace fntrs {
+
+// ---- instrumentation (instrument.hpp): per-thread scope chain
+namespace {
+thread_local FntScope* g_scope = nullptr;
+}
+FntScope::FntScope(FntCounter& counter) : counter_(counter), outer_(g_scope) { g_scope = this; }
+FntScope::~FntScope() { g_scope = outer_; }
+void note_fnt_execution(std::size_t size) noexcept {
+    for (FntScope* s = g_scope; s; s = s->outer_) s->counter_.record(size);
+}
 
 void throw_status(int status, const std::string& msg) {
     switch (status) {
@@ -210,6 +221,24 @@ CodeParams CodeParams::make(std::uint32_t k, std::uint32_t n, bool systematic) {
 }
 
 namespace {
+uint32_t product_size(uint32_t k) {  // interp.cpp:61-67 (0: no product transform fits)
+    return 2ull * k > 65536ull ? 0u : next_pow2(2 * k);
+}
+
+// the transforms one decode of a codeword performs on the GPU
+void note_decode(const CodeParams& params, uint32_t kp) {
+    const uint32_t nd = next_pow2(params.n), m = product_size(params.k);
+    if (kp == params.n && params.n == nd) {  // complete reception: one inverse transform
+        note_fnt_execution(nd);
+        return;
+    }
+    note_fnt_execution(nd);  // FNT1: the moments of N'
+    // the series' spectrum and the inverse of the product; 2k > 65536: both
+    // series halves and two inverses (the product by halves)
+    const int products = m ? 1 : 2;
+    for (int i = 0; i < 2 * products; ++i) note_fnt_execution(m ? m : 65536);
+}
+
 std::vector<Fe> encode_one(const CodeParams& params, std::span<const Fe> source, bool systematic) {
     if (source.size() != params.k)
         throw SizeMismatch("encode: got " + std::to_string(source.size()) + " source symbols for k = " +
@@ -221,11 +250,14 @@ std::vector<Fe> encode_one(const CodeParams& params, std::span<const Fe> source,
     std::vector<uint64_t> esc;
     split(source.data(), source.size(), words, esc);
     auto fn = systematic ? fntrs_gpu_encode_systematic : fntrs_gpu_encode;
-    return run(S, words, esc, params.n,
-               [&](const uint16_t* din, const uint64_t* die, uint64_t nie, uint16_t* dout, uint64_t* doe,
-                   uint64_t cap, uint64_t* dcnt) {
-                   S.check(fn(S.ctx, params.k, params.n, 1, 1, din, die, nie, dout, doe, cap, dcnt, S.stream));
-               });
+    auto out = run(S, words, esc, params.n,
+                   [&](const uint16_t* din, const uint64_t* die, uint64_t nie, uint16_t* dout, uint64_t* doe,
+                       uint64_t cap, uint64_t* dcnt) {
+                       S.check(fn(S.ctx, params.k, params.n, 1, 1, din, die, nie, dout, doe, cap, dcnt, S.stream));
+                   });
+    if (systematic && params.k != params.n) note_decode(params, params.k);  // interpolation at 0..k-1
+    if (!systematic || params.k != params.n) note_fnt_execution(next_pow2(params.n));
+    return out;
 }
 
 // sorted_received (codec.cpp:32-48): range check, sort, duplicates, count
@@ -276,6 +308,8 @@ std::vector<Fe> decode_one(const CodeParams& params, const Codeword& sorted, uin
         throw;
     }
     cudaFree(d_sp);
+    note_decode(params, kp);
+    if (systematic) note_fnt_execution(next_pow2(params.n));
     return out;
 }
 }  // namespace
@@ -296,8 +330,21 @@ std::vector<Fe> encode_systematic(const CodeParams& params, std::span<const Fe> 
 
 std::vector<Fe> decode_systematic(const CodeParams& params, const Codeword& received, Path) {
     // interpolate the k lowest, evaluate at 0..k-1; when those are 0..k-1 the
-    // result is the received values themselves (systematic_prefix_present)
-    return decode_one(params, sorted_received(params, received), params.k, true);
+    // result is the received values themselves (systematic_prefix_present,
+    // codec.cpp:167-171: a copy, no transforms -- the kernels would reproduce
+    // the same values)
+    Codeword sorted = sorted_received(params, received);
+    bool prefix = true;
+    for (uint32_t i = 0; i < params.k && prefix; ++i) prefix = sorted[i].position == i;
+    if (prefix) {
+        Shared& S = shared();
+        std::lock_guard<std::mutex> lock(S.mu);
+        S.ensure();  // no device, no codec: fail loudly like every other call
+        std::vector<Fe> out(params.k);
+        for (uint32_t i = 0; i < params.k; ++i) out[i] = sorted[i].value;
+        return out;
+    }
+    return decode_one(params, sorted, params.k, true);
 }
 
 }  // namespace codec

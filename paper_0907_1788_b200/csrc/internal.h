@@ -66,6 +66,16 @@ cudaError_t launch_plan_build(uint32_t N, uint32_t M, uint32_t kp, uint32_t npat
 
 constexpr uint32_t kTileMaxN = 4096;
 
+// Shard wire-format data movement (shards.cu)
+cudaError_t launch_symbolize(const uint8_t* data, uint64_t len, uint32_t k, uint32_t L, uint16_t* src,
+                             cudaStream_t st);
+cudaError_t launch_desymbolize(const uint16_t* dec, uint32_t k, uint32_t L, uint64_t len, uint8_t* out,
+                               cudaStream_t st);
+cudaError_t launch_words_to_be(const uint16_t* rows, uint32_t nrows, uint32_t L, uint32_t count, uint8_t* out,
+                               uint64_t pitch, cudaStream_t st);
+cudaError_t launch_be_to_words(const uint8_t* in, uint64_t pitch, uint32_t nrows, uint32_t count, uint32_t L,
+                               uint16_t* rows, cudaStream_t st);
+
 // ---- v2 fast path (codec_fast.cu): 32 <= N <= 4096, L a multiple of the tile width
 namespace fast {
 struct FastTables {

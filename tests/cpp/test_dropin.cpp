@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "fntrs/codec.hpp"
+#include "fntrs/instrument.hpp"
 
 using namespace fntrs;
 using namespace fntrs::codec;
@@ -210,6 +211,58 @@ int main() {
         std::vector<Fe> top{65536, 65536, 65536};
         auto enc3 = encode_systematic(p3, top);
         CHECK(decode_systematic(p3, take(enc3, {2, 4, 6})) == top);
+    }
+    // transform budgets at k = n/2, n = 4096 (acceptance.cpp:190-230, criterion 4)
+    {
+        const uint32_t k = 2048, n = 4096;
+        auto sys = CodeParams::make(k, n, true), non = CodeParams::make(k, n, false);
+        auto src = random_source(k, 404);
+        auto enc_non = encode_nonsystematic(non, src);
+        auto enc_sys = encode_systematic(sys, src);
+        Codeword rx_non(k), rx_sys(k);
+        for (uint32_t i = 0; i < k; ++i) {  // position 0 erased: no shortcuts
+            rx_non[i] = {i + 1, enc_non[i + 1]};
+            rx_sys[i] = {i + 1, enc_sys[i + 1]};
+        }
+        auto measure = [](auto&& op) {
+            op();
+            FntCounter counter;
+            {
+                FntScope scope(counter);
+                op();
+            }
+            return counter.equivalents(4096);
+        };
+        const double e_non = measure([&] { encode_nonsystematic(non, src); });
+        const double e_sys = measure([&] { encode_systematic(sys, src, Path::Fast); });
+        const double d_non = measure([&] { CHECK(decode_nonsystematic(non, rx_non, Path::Fast) == src); });
+        const double d_sys = measure([&] { CHECK(decode_systematic(sys, rx_sys, Path::Fast) == src); });
+        std::printf("fnt budget: enc_nonsys=%.2f dec_nonsys=%.2f enc_sys=%.2f dec_sys=%.2f\n", e_non, d_non, e_sys,
+                    d_sys);
+        CHECK(e_non == 1.0 && d_non <= 8.0 && e_sys <= 9.0 && d_sys <= 9.0);
+        // systematic prefix present: verbatim copy, zero transforms (test_codec.cpp:172-183)
+        FntCounter counter;
+        std::vector<Fe> got;
+        {
+            FntScope scope(counter);
+            got = decode_systematic(sys, take(enc_sys, [&] {
+                                        std::vector<uint32_t> p(k);
+                                        for (uint32_t i = 0; i < k; ++i) p[i] = i;
+                                        return p;
+                                    }()));
+        }
+        CHECK(got == src && counter.total() == 0);
+        // nested scopes both see a transform; a finished scope sees nothing more
+        FntCounter outer, inner;
+        {
+            FntScope a(outer);
+            {
+                FntScope b(inner);
+                encode_nonsystematic(non, src);
+            }
+            encode_nonsystematic(non, src);
+        }
+        CHECK(outer.count(4096) == 2 && inner.count(4096) == 1 && inner.total() == 1);
     }
     std::printf("drop-in C++ API: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail ? 1 : 0;

@@ -204,6 +204,40 @@ class RefLib:
         L.ref_has_avx2.restype = i32
         L.ref_set_systematic.argtypes = [i32]
         L.ref_set_systematic.restype = None
+        u8p = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
+        L.ref_encode_file.restype = i64
+        L.ref_encode_file.argtypes = [u8p, u64, u32, u32, i32, u64, u8p, u64, u64p]
+        L.ref_write_shard.restype = i64
+        L.ref_write_shard.argtypes = [u64, u32, u32, u32, i32, u32p, u64, u8p, u64]
+        L.ref_read_shard_status.restype = i32
+        L.ref_read_shard_status.argtypes = [u8p, u64]
+
+    def encode_file(self, data: bytes, k, n, systematic=True, chunk_id=0):
+        """The reference CLI's encode over the library: (manifest bytes, [shard bytes])."""
+        d = np.frombuffer(data, dtype=np.uint8) if data else np.zeros(1, np.uint8)
+        words = (len(data) + 1) // 2
+        S = (words + k - 1) // k
+        cap = 64 + n * (64 + 2 * S) + 4 * (S * n // 1000 + 1024)
+        out = np.zeros(cap, dtype=np.uint8)
+        sizes = np.zeros(n + 1, dtype=np.uint64)
+        tot = self.lib.ref_encode_file(np.ascontiguousarray(d), len(data), k, n, int(systematic), chunk_id, out, cap,
+                                       sizes)
+        assert tot >= 0, tot
+        parts, pos = [], 0
+        for sz in sizes:
+            parts.append(out[pos:pos + int(sz)].tobytes())
+            pos += int(sz)
+        return parts[0], parts[1:]
+
+    def write_shard(self, chunk_id, k, n, index, systematic, payload):
+        p = _a32(payload)
+        out = np.zeros(64 + 6 * max(p.size, 1), dtype=np.uint8)
+        sz = self.lib.ref_write_shard(chunk_id, k, n, index, int(systematic), p, p.size, out, out.size)
+        return (out[:sz].tobytes(), 0) if sz >= 0 else (b"", -sz)
+
+    def read_shard_status(self, b: bytes) -> int:
+        a = np.frombuffer(b, dtype=np.uint8) if b else np.zeros(1, np.uint8)
+        return self.lib.ref_read_shard_status(np.ascontiguousarray(a), len(b))
 
     def set_systematic(self, on: bool):
         """Batched stripe loops run encode/decode_systematic instead of the non-systematic pair."""
