@@ -46,6 +46,7 @@ struct fntrs_plans {
     bool cols = false;        // served by the general column path (codec_cols.cu)
     bool full = false;        // complete reception
     bool split = false;       // 2k > 65536: locator halves' spectra (alo, ahi), product_size 0
+    bool gen = false;         // fused M != N decode (codec_gen.cu): rowmap + ahat2 natural pairs
     uint32_t* alo = nullptr;  // [65536][np]
     uint32_t* ahi = nullptr;
 };
@@ -372,6 +373,7 @@ int fntrs_gpu_plans_create(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t kp, 
     pl->cols = cols;
     pl->full = full;
     pl->split = split;
+    pl->gen = !cols && !full && kp == k && M != N && fast::gen_tile_columns(N, M) != 0;
     pl->ninv = cpow(N % kP, kP - 2);
     const size_t npos = size_t(npatterns) * kp;
     cudaError_t e = cudaSuccess;
@@ -410,6 +412,13 @@ int fntrs_gpu_plans_create(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t kp, 
         } else if (!e && locator) {
             e = launch_plan_build(N, M, kp, npatterns, pl->pos, pl->ainv, pl->ahat, ctx->tab, st);
             ctx->launches += 1;
+        }
+        if (!e && pl->gen) {  // fused M != N decode: row map + Shoup pairs of -A_hat/M
+            e = cudaMallocAsync(&pl->rowmap, size_t(npatterns) * N * sizeof(uint2), st);
+            if (!e) e = cudaMallocAsync(&pl->ahat2, size_t(npatterns) * M * sizeof(uint2), st);
+            if (!e) e = fast::build_cols_rowmap(N, kp, npatterns, pl->pos, pl->ainv, pl->rowmap, st);
+            if (!e) e = fast::build_gen_pairs(M, npatterns, pl->ahat, pl->ahat2, st);
+            ctx->launches += 3;
         }
         if (!e && cols) {  // received-row map for the column path's scatter loader
             e = cudaMallocAsync(&pl->rowmap, size_t(npatterns) * N * sizeof(uint2), st);
@@ -520,8 +529,11 @@ int fntrs_gpu_decode(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t stripes, ui
     EscOut eout{reinterpret_cast<unsigned long long*>(out_esc), reinterpret_cast<unsigned long long*>(n_out_esc),
                 esc_cap};
     const int tcols = fast::fast_tile_columns(pl->N);
-    const bool fast_ok = ctx->fast_enabled && !pl->cols && pl->rowmap && tcols && L % uint32_t(tcols) == 0 &&
-                         reinterpret_cast<uintptr_t>(rx) % 16 == 0;
+    const bool fast_ok = ctx->fast_enabled && !pl->cols && !pl->gen && pl->rowmap && tcols &&
+                         L % uint32_t(tcols) == 0 && reinterpret_cast<uintptr_t>(rx) % 16 == 0;
+    const int gcols = pl->gen ? fast::gen_tile_columns(pl->N, pl->M) : 0;
+    const bool gen_ok = ctx->fast_enabled && gcols && L % uint32_t(gcols) == 0 &&
+                        reinterpret_cast<uintptr_t>(rx) % 16 == 0;
     const bool large_plan = !pl->cols && fast::large_supported(pl->N) && pl->rowmap;
     if (pl->cols || (large_plan && L % fast::large_tile_columns())) {  // general column path
         if (stripes && L) {
@@ -554,6 +566,9 @@ int fntrs_gpu_decode(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t stripes, ui
     } else if (fast_ok) {
         fast::FastPlanView fv{pl->N, pl->k, pl->rowmap, pl->ahat2};
         CK(fast::launch_decode_fast(ctx->ftab, fv, stripes, L, stripe_pattern, rx, ein, out, eout, st), "decode launch");
+    } else if (gen_ok) {
+        fast::GenPlanView gv{pl->N, pl->M, pl->k, pl->rowmap, pl->ahat2};
+        CK(fast::launch_decode_gen(ctx->ftab, gv, stripes, L, stripe_pattern, rx, ein, out, eout, st), "decode launch");
     } else {
         CK(launch_decode_tile(ctx->tab, pv, stripes, L, stripe_pattern, rx, ein, out, eout, st), "decode launch");
     }

@@ -382,6 +382,20 @@ __device__ __forceinline__ uint32_t perm(uint32_t p) {
     return f;
 }
 
+// inverse of perm<E>: the DIF output position holding frequency f
+template <int E>
+__device__ __forceinline__ uint32_t perm_inv(uint32_t f) {
+    uint32_t p = 0;
+    int sh = E;
+#pragma unroll
+    for (int i = 0; i < E / 4; ++i) {
+        sh -= 4;
+        p |= ((f >> (4 * i)) & 15u) << sh;
+    }
+    if constexpr (E % 4) p |= f >> (4 * (E / 4));
+    return p;
+}
+
 // frequency of the leading digits: perm of position (b << rlast) minus the
 // last digit's contribution, i.e. perm<E>(b << RL) where RL = last radix log2.
 template <int E>

@@ -140,6 +140,18 @@ cudaError_t launch_plan_fast(const FastTables& t, const Tables& tab, const LogTa
 cudaError_t launch_fnt_cols(const FastTables& t, uint32_t N, bool inverse, uint32_t C, const uint32_t* in,
                             uint32_t* scratch, uint32_t* out, cudaStream_t st);
 
+// ---- fused decode for M != N (codec_gen.cu): 32 <= N <= 4096, M <= 4096
+struct GenPlanView {
+    uint32_t N, M, k;
+    const uint2* rowmap;  // [np][N] {received row or ~0, balanced 1/A'(x_i)}
+    const uint2* ahat2;   // [np][M] {w, 65535 w} of -A_hat/M, natural order
+};
+int gen_tile_columns(uint32_t N, uint32_t M);  // 0: no fused kernel for (N, M)
+cudaError_t build_gen_pairs(uint32_t M, uint32_t P, const uint32_t* ahat, uint2* pairs, cudaStream_t st);
+cudaError_t launch_decode_gen(const FastTables& t, const GenPlanView& pv, uint32_t stripes, uint32_t L,
+                              const uint32_t* sp, const uint16_t* rx, EscIn ein, uint16_t* out, EscOut eout,
+                              cudaStream_t st);
+
 // ---- general path (codec_cols.cu): column transforms through HBM, any shape
 // with n_domain, M <= 65536
 struct ColsPlanView {

@@ -130,6 +130,9 @@ SHAPES = [  # (k, n, L, stripes)
     # general column path (codec_cols.cu): product size M != n_domain above 4096, any L
     (3000, 4096, 16, 1), (2000, 16384, 8, 1), (1000, 8192, 10, 2), (4096, 8192, 40, 1), (5000, 9000, 8, 1),
     (20000, 32768, 8, 1), (40, 10000, 16, 1),
+    # fused M != n_domain decode (codec_gen.cu): k > N/2 and k <= N/4 at N <= 4096
+    (200, 256, 64, 3), (20, 256, 32, 2), (12, 256, 32, 2), (600, 1024, 32, 1), (100, 1024, 32, 1),
+    (700, 4096, 16, 1), (20, 32, 32, 2), (5, 32, 32, 2), (2, 32, 32, 2), (3000, 3500, 16, 1),
     # 2k > 65536: the product by halves (reference poly::mul_low)
     (33000, 65536, 8, 1), (40000, 50000, 4, 2),
 ]
@@ -239,7 +242,8 @@ def test_complete_reception_large_domain(codec, oracle):  # codec.cpp:137-144 at
     assert np.array_equal(escapes_to_numpy(oe, cnt), np.sort(np.array(want_esc, dtype=np.uint64)))
 
 
-@pytest.mark.parametrize("k,n,L,S", [(128, 256, 128, 3), (1024, 2048, 64, 1), (2048, 4096, 32, 1), (300, 512, 64, 1)])
+@pytest.mark.parametrize("k,n,L,S", [(128, 256, 128, 3), (1024, 2048, 64, 1), (2048, 4096, 32, 1), (300, 512, 64, 1),
+                                     (200, 256, 64, 2), (50, 256, 64, 2), (600, 1024, 32, 1)])
 def test_fast_kernels_match_general_kernels(codec, k, n, L, S):
     """A/B: the fused v2 kernels and the general tile kernels agree bit for bit."""
     from paper_0907_1788_b200 import _lib, escapes_to_numpy, workload as W
