@@ -434,10 +434,34 @@ def run_e2e(args, codec, cfg, dev, stream, seed, world):
     torch.cuda.synchronize(dev)
     ms = max_over_ranks([a.elapsed_time(b) / steps], device=dev)[0]
     total_src = 2 * k * L * S * world
+    link = pcie_peaks(dev)
     return {"value": round(total_src / (ms * 1e-3) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ms, 3),
+            # the e2e bound: PCIe, both directions busy at once (per GPU)
+            "pcie_h2d_gbs": round(h2d / (ms * 1e-3) / 1e9, 2), "pcie_d2h_gbs": round(d2h / (ms * 1e-3) / 1e9, 2),
+            "pcie_peak_h2d_gbs": link[0], "pcie_peak_d2h_gbs": link[1],
             "sample": f"{S} stripes/GPU of {cfg.name} from pinned host memory via HostPipeline "
                       f"(Codec.encode/plans/decode C-ABI calls, {chunk}-stripe chunks on 3 streams)"}
+
+
+def pcie_peaks(dev, nbytes=512 << 20):
+    """Pinned-host copy bandwidth of this GPU's link, each direction alone (GB/s)."""
+    import torch
+    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    out = []
+    for fn in (lambda: d.copy_(h, non_blocking=True), lambda: h.copy_(d, non_blocking=True)):
+        fn()
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(3):
+            fn()
+        b.record()
+        torch.cuda.synchronize(dev)
+        out.append(round(3 * nbytes / (a.elapsed_time(b) * 1e-3) / 1e9, 2))
+    del h, d
+    return out
 
 
 def cpu_baseline(cfg, budget_s):
