@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) enc_fast_kernel(const __grid_c
         auto st_out = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) -> uint32_t {
             const uint32_t f = perm_head<E>(b) + (uint32_t(s) << (E - RLZ));
             if (!PUNCT || f < n) __stcs(outp + (f * L + col), uint16_t(y));
-            return (y == 65536u && (!PUNCT || f < n)) ? 1u : 0u;
+            return (!PUNCT || f < n) ? y >> 16 : 0u;  // canonical: bit 16 set iff y == 65536
         };
         auto flush_out = [&](uint32_t mask, uint32_t, uint32_t b, uint32_t col) {
             if (!mask) return;
@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
             // k = N/2: kept iff s < R/2 (compile time after unrolling)
             const bool keep = HALFK ? (s < RZ / 2) : (f < k);
             if (keep) __stcs(outp + (f * L + col), uint16_t(y));
-            return (y == 65536u && keep) ? 1u : 0u;
+            return keep ? y >> 16 : 0u;  // canonical: bit 16 set iff y == 65536
         };
         auto flush_out = [&](uint32_t mask, uint32_t, uint32_t b, uint32_t col) {
             if (!mask) return;

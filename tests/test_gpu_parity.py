@@ -387,3 +387,41 @@ def test_host_pipeline_multistream_matches_single_stream(codec):
     assert np.array_equal(dec_h.numpy().view(np.uint16), src2)
     assert int(dcnt_h.sum()) == 0
     assert want_esc.size > 0 and want.shape == (S, n, L)
+
+
+# ------------------------------------------------------- randomized sweep ----
+def _random_shapes(seed, count):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < count:
+        e = int(rng.integers(1, 14))                       # n_domain up to 8192
+        n = int(rng.integers((1 << (e - 1)) + 1, (1 << e) + 1)) if e > 1 else int(rng.integers(1, 3))
+        k = int(rng.integers(1, n + 1))
+        L = int(rng.choice([1, 3, 8, 16, 32, 40, 64]))
+        S = int(rng.integers(1, 3))
+        if n * L * S > 400_000 or (k > 2048 and L * S > 16):
+            continue
+        out.append((k, n, L, S))
+    return out
+
+
+@pytest.mark.parametrize("k,n,L,S", _random_shapes(20261019, 40))
+def test_random_shapes_match_oracle(codec, oracle, k, n, L, S):
+    """Seeded random (k, n, L, stripes) across every kernel family; each draw is
+    encoded and decoded (from random k-subsets, including tampered values and
+    input escapes) and compared bit for bit with the oracle."""
+    from oracle_bind import gather_received
+    from paper_0907_1788_b200 import escapes_to_numpy
+    src, esc = source_with_escapes(S, k, L, seed=k * 31 + n * 7 + L, n_esc=2)
+    want, want_esc = oracle.encode_stripes(k, n, src, esc)
+    out, oe, cnt = codec.encode(k, n, dev_u16(src), dev_esc(esc))
+    assert np.array_equal(host_u16(out), want) and np.array_equal(escapes_to_numpy(oe, cnt), want_esc)
+    pats, sp = _patterns(S, n, k, seed=n + L)
+    rx, rx_esc = gather_received(want, want_esc, pats, sp)
+    rx = rx.copy()
+    rx[0, -1, 0] ^= 0x1234  # not a codeword any more
+    rx_esc = rx_esc[rx_esc != np.uint64((k - 1) * L)]
+    dwant, dwant_esc = oracle.decode_stripes(k, n, pats, sp, rx, rx_esc)
+    plans = codec.plans(k, n, pats)
+    dout, de, dc = codec.decode(plans, torch.from_numpy(sp.view(np.int32)).cuda(), dev_u16(rx), dev_esc(rx_esc))
+    assert np.array_equal(host_u16(dout), dwant) and np.array_equal(escapes_to_numpy(de, dc), dwant_esc)
