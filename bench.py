@@ -103,6 +103,16 @@ class ClockSampler:
             except Exception:
                 self.proc.kill()
 
+    def sample_now(self):
+        """One synchronous query (timed regions shorter than the 100 ms poll)."""
+        try:
+            r = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=10)
+            for line in r.stdout.splitlines():
+                self.rows.append([x.strip() for x in line.split(",")])
+        except Exception:
+            pass
+
     def summary(self):
         sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
@@ -294,6 +304,8 @@ def run_gpu(args, rank, world, local_rank):
             _, ev = step(timed=True)
             evs.append(ev)
         t_end.record(stream)
+        if not clocks.rows:
+            clocks.sample_now()  # still inside the timed region (kernels queued)
         torch.cuda.synchronize(dev)
     barrier()
     gpu_launches = codec.launches - launches0
