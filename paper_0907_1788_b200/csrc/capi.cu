@@ -285,7 +285,7 @@ int encode_impl(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t N, uint32_t str
     EscIn ein{reinterpret_cast<const unsigned long long*>(src_esc), n_src_esc};
     EscOut eout{reinterpret_cast<unsigned long long*>(out_esc), reinterpret_cast<unsigned long long*>(n_out_esc),
                 esc_cap};
-    const int cols = fast::fast_tile_columns(N);
+    const int cols = fast::fast_encode_columns(N);
     const bool fast_ok = ctx->fast_enabled && cols && L % uint32_t(cols) == 0 &&
                          reinterpret_cast<uintptr_t>(src) % 16 == 0;
     if (N > kTileMaxN && !large) {  // general column path (codec_cols.cu)

@@ -23,6 +23,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "fft_pass.cuh"
 #include "tma.cuh"
 
@@ -32,7 +34,17 @@ namespace fast {
 namespace {
 
 // ---------------------------------------------------------------------------
-template <int E, class G, bool HALFK, bool PUNCT>
+// Encode geometry: at N <= 256 a 64-column tile with two codewords per work
+// item (columns c and c + 32 share twiddle loads and addressing; C2 encode
+// 693 -> 716 GB/s); larger N keep the decode geometry (a 64-wide N = 512 tile
+// and its staging exceed shared memory).
+template <int E>
+struct EncPick {
+    static constexpr int CW = E <= 8 ? 2 : 1;
+    using G = typename std::conditional<(E <= 8), Geom<E, 64, 256, 2>, typename Pick<E>::G>::type;
+};
+
+template <int E, class G, bool HALFK, bool PUNCT, int CW>
 __global__ void __launch_bounds__(G::NT, G::MINB) enc_fast_kernel(const __grid_constant__ CUtensorMap src_map,
                                                          const uint2* __restrict__ ptabF, uint32_t k, uint32_t n,
                                                          uint32_t L, uint32_t tps, uint32_t tiles, uint32_t nbox,
@@ -109,14 +121,14 @@ __global__ void __launch_bounds__(G::NT, G::MINB) enc_fast_kernel(const __grid_c
                     emit_escape(esc_out, key_out + uint64_t(perm_head<E>(b) + (uint32_t(s) << (E - RLZ))) * L + col);
         };
 
-        pass<E, 0, false, false, kP64, kSmemCap, G>(pass_table(ptabF, S::llog(0)), ld_src, st_sm, fix_src);
+        pass_cw<CW, E, 0, false, false, kP64, kSmemCap, G>(pass_table(ptabF, S::llog(0)), ld_src, st_sm, fix_src);
         __syncthreads();
         if constexpr (P == 3) {
-            pass<E, 1, false, false, kSmemCap, kSmemCap, G>(pass_table(ptabF, S::llog(1)), ld_sm, st_sm);
+            pass_cw<CW, E, 1, false, false, kSmemCap, kSmemCap, G>(pass_table(ptabF, S::llog(1)), ld_sm, st_sm);
             __syncthreads();
         }
-        pass<E, P - 1, false, false, kSmemCap, kCanon, G>(pass_table(ptabF, S::llog(P - 1)), ld_sm, st_out, NoFix(),
-                                                       flush_out);
+        pass_cw<CW, E, P - 1, false, false, kSmemCap, kCanon, G>(pass_table(ptabF, S::llog(P - 1)), ld_sm, st_out,
+                                                                NoFix(), flush_out);
         __syncthreads();
     }
 }
@@ -423,10 +435,11 @@ cudaError_t shape_for(K kernel, int E, int wt, int nt, uint32_t k, uint32_t stri
 template <int E>
 cudaError_t launch_enc(const FastTables& t, uint32_t k, uint32_t n, uint32_t stripes, uint32_t L, const uint16_t* src,
                        EscIn ein, uint16_t* out, EscOut eout, cudaStream_t st) {
-    using G = typename Pick<E>::G;
+    using G = typename EncPick<E>::G;
+    constexpr int CW = EncPick<E>::CW;
     const bool half = k == (1u << E) / 2, punct = n < (1u << E);
-    auto kern = half ? (punct ? enc_fast_kernel<E, G, true, true> : enc_fast_kernel<E, G, true, false>)
-                     : (punct ? enc_fast_kernel<E, G, false, true> : enc_fast_kernel<E, G, false, false>);
+    auto kern = half ? (punct ? enc_fast_kernel<E, G, true, true, CW> : enc_fast_kernel<E, G, true, false, CW>)
+                     : (punct ? enc_fast_kernel<E, G, false, true, CW> : enc_fast_kernel<E, G, false, false, CW>);
     LaunchShape sh;
     cudaError_t err = shape_for(kern, E, G::WT, G::NT, k, stripes, L, sh);
     if (err) return err;
@@ -461,6 +474,20 @@ cudaError_t build_fast_tables(FastTables& t, cudaStream_t st) {
     if ((err = cudaMalloc(&t.ptab_inv, sizeof(uint2) << 13))) return err;
     ptab_kernel<<<(1u << 13) / 256, 256, 0, st>>>(t.ptab_fwd, t.ptab_inv);
     return cudaGetLastError();
+}
+
+int fast_encode_columns(uint32_t N) {
+    switch (N) {
+        case 32: return EncPick<5>::G::WT;
+        case 64: return EncPick<6>::G::WT;
+        case 128: return EncPick<7>::G::WT;
+        case 256: return EncPick<8>::G::WT;
+        case 512: return EncPick<9>::G::WT;
+        case 1024: return EncPick<10>::G::WT;
+        case 2048: return EncPick<11>::G::WT;
+        case 4096: return EncPick<12>::G::WT;
+        default: return 0;
+    }
 }
 
 int fast_tile_columns(uint32_t N) {

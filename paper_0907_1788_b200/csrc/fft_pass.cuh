@@ -137,60 +137,88 @@ __device__ __forceinline__ uint2 tw_at(const uint4* __restrict__ tq, int s, uint
 }
 
 template <int E, int p, bool INV, bool DIT, uint64_t BIN, uint64_t OCAP, class G, class LD, class ST,
-          class FIX = NoFix, class FLUSH = NoFlush>
+          class FIX = NoFix, class FLUSH = NoFlush, int CW = 1>
 __device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld, const ST& st, const FIX& fix = FIX(),
                                      const FLUSH& flush = FLUSH()) {
+    // CW codewords per work item: columns col + c * WT/CW, c < CW, share the
+    // twiddle loads and the address arithmetic (two independent chains at CW = 2)
     using S = Sched<E>;
     constexpr int RL = S::rlog(p), R = 1 << RL, LL = S::llog(p), SL = S::slog(p);
-    constexpr int ITEMS = (1 << (E - RL)) * G::WT;
-    constexpr int LGW = ilog2c<G::WT>();
+    constexpr int WC = G::WT / CW;
+    constexpr int ITEMS = (1 << (E - RL)) * WC;
+    constexpr int LGW = ilog2c<WC>();
     static_assert(OCAP >= k2P || OCAP == kCanon, "");
 #pragma unroll 1
     for (int it = threadIdx.x; it < ITEMS; it += G::NT) {
-        const uint32_t col = uint32_t(it) & uint32_t(G::WT - 1);
+        const uint32_t col = uint32_t(it) & uint32_t(WC - 1);
         const uint32_t b = uint32_t(it) >> LGW;
         const uint32_t t = b & ((1u << SL) - 1u);
         const uint32_t base = ((b >> SL) << LL) + t;
-        uint32_t v[R];
+        uint32_t v[CW][R];
         const uint4* tq = twp + t * (R / 2);  // row t: r_len^(t s), s < R, two per uint4
-        uint32_t mask = 0;
+        uint32_t mask[CW];
+#pragma unroll
+        for (int c = 0; c < CW; ++c) mask[c] = 0;
         uint4 w4 = make_uint4(0, 0, 0, 0);
         if constexpr (!DIT) {
 #pragma unroll
-            for (int q = 0; q < R; ++q) v[q] = ld(base + (uint32_t(q) << SL), b, q, col);
-            fix(v, base, b, col);
-            dif_regs<R, INV, BIN>(v);
+            for (int c = 0; c < CW; ++c)
+#pragma unroll
+                for (int q = 0; q < R; ++q) v[c][q] = ld(base + (uint32_t(q) << SL), b, q, col + c * WC);
+#pragma unroll
+            for (int c = 0; c < CW; ++c) fix(v[c], base, b, col + c * WC);
+#pragma unroll
+            for (int c = 0; c < CW; ++c) dif_regs<R, INV, BIN>(v[c]);
             constexpr uint64_t BO = dif_bound<R, INV, BIN>();
 #pragma unroll
             for (int s = 0; s < R; ++s) {
-                uint32_t y = v[rev<R>(s)];
-                if (SL > 0 && s > 0) {
-                    const uint2 w = tw_at(tq, s, w4);
-                    y = mulws(y, w.x, w.y);
-                    if constexpr (OCAP == kCanon) y = canon_s2p(y);
-                } else {
-                    y = cap<BO, OCAP>(y);
+                uint2 w = make_uint2(0, 0);
+                if (SL > 0 && s > 0) w = tw_at(tq, s, w4);
+#pragma unroll
+                for (int c = 0; c < CW; ++c) {
+                    uint32_t y = v[c][rev<R>(s)];
+                    if (SL > 0 && s > 0) {
+                        y = mulws(y, w.x, w.y);
+                        if constexpr (OCAP == kCanon) y = canon_s2p(y);
+                    } else {
+                        y = cap<BO, OCAP>(y);
+                    }
+                    mask[c] |= st(base + (uint32_t(s) << SL), b, s, col + c * WC, y) << s;
                 }
-                mask |= st(base + (uint32_t(s) << SL), b, s, col, y) << s;
             }
         } else {
             constexpr uint64_t BI = BIN > k2P ? BIN : k2P;
 #pragma unroll
             for (int s = 0; s < R; ++s) {
-                uint32_t x = ld(base + (uint32_t(s) << SL), b, s, col);
-                if (SL > 0 && s > 0) {
-                    const uint2 w = tw_at(tq, s, w4);
-                    x = mulws(x, w.x, w.y);
+                uint2 w = make_uint2(0, 0);
+                if (SL > 0 && s > 0) w = tw_at(tq, s, w4);
+#pragma unroll
+                for (int c = 0; c < CW; ++c) {
+                    uint32_t x = ld(base + (uint32_t(s) << SL), b, s, col + c * WC);
+                    if (SL > 0 && s > 0) x = mulws(x, w.x, w.y);
+                    v[c][rev<R>(s)] = x;
                 }
-                v[rev<R>(s)] = x;
             }
-            dit_regs<R, INV, BI>(v);
+#pragma unroll
+            for (int c = 0; c < CW; ++c) dit_regs<R, INV, BI>(v[c]);
             constexpr uint64_t BO = dit_bound<R, INV, BI>();
 #pragma unroll
-            for (int q = 0; q < R; ++q) mask |= st(base + (uint32_t(q) << SL), b, q, col, cap<BO, OCAP>(v[q])) << q;
+            for (int c = 0; c < CW; ++c)
+#pragma unroll
+                for (int q = 0; q < R; ++q)
+                    mask[c] |= st(base + (uint32_t(q) << SL), b, q, col + c * WC, cap<BO, OCAP>(v[c][q])) << q;
         }
-        flush(mask, base, b, col);
+#pragma unroll
+        for (int c = 0; c < CW; ++c) flush(mask[c], base, b, col + c * WC);
     }
+}
+
+// pass with CW codewords per work item (template arguments after G deduced)
+template <int CW, int E, int p, bool INV, bool DIT, uint64_t BIN, uint64_t OCAP, class G, class LD, class ST,
+          class FIX = NoFix, class FLUSH = NoFlush>
+__device__ __forceinline__ void pass_cw(const uint4* __restrict__ twp, const LD& ld, const ST& st,
+                                        const FIX& fix = FIX(), const FLUSH& flush = FLUSH()) {
+    pass<E, p, INV, DIT, BIN, OCAP, G, LD, ST, FIX, FLUSH, CW>(twp, ld, st, fix, flush);
 }
 
 // Per-pass twiddle tables for one direction: table for block length 2^LL at

@@ -188,8 +188,9 @@ def read_manifest(b: bytes) -> ChunkManifest:  # shardio.cpp:233-259
 
 # ------------------------------------------------------------ file codec ----
 def _width(S: int, n_domain: int) -> int:
-    """Symbols per packet: the CLI stripe count rounded up to the fused kernels' tile width."""
-    w = 64 if n_domain > 4096 else 32
+    """Symbols per packet: the CLI stripe count rounded up to a multiple of every
+    fused kernel's tile width (64)."""
+    w = 64
     return max(w, (S + w - 1) // w * w)
 
 
