@@ -94,12 +94,44 @@ int end_bit_for(uint64_t max_key) {
     return b;
 }
 
+// Small escape buffers: one CTA sorts all `cap` keys in shared memory (bitonic
+// network over the next power of two, padding with ~0) -- one launch instead
+// of the radix sort's several.
+constexpr uint32_t kSmallSort = 4096;
+__global__ void __launch_bounds__(1024) small_sort_kernel(unsigned long long* keys, uint32_t cap) {
+    __shared__ unsigned long long s[kSmallSort];
+    uint32_t m = 1;
+    while (m < cap) m <<= 1;
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) s[i] = i < cap ? keys[i] : ~0ull;
+    __syncthreads();
+    for (uint32_t size = 2; size <= m; size <<= 1)
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t i = threadIdx.x; i < m / 2; i += blockDim.x) {
+                const uint32_t lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const unsigned long long a = s[lo], b = s[hi];
+                if ((a > b) == up) {
+                    s[lo] = b;
+                    s[hi] = a;
+                }
+            }
+            __syncthreads();
+        }
+    for (uint32_t i = threadIdx.x; i < cap; i += blockDim.x) keys[i] = s[i];
+}
+
 // Escape finalisation: keys[0..cap) were pre-filled with ~0 and partially
 // overwritten by the kernel's appends; sorting the whole buffer puts the
 // real indices first, ascending (the reference's per-shard order).
 int sort_escapes(fntrs_ctx* ctx, unsigned long long* keys, uint64_t cap, uint64_t max_key,
                  cudaStream_t st) {
     if (cap <= 1) return FNTRS_OK;
+    if (cap <= kSmallSort) {
+        small_sort_kernel<<<1, 1024, 0, st>>>(keys, uint32_t(cap));
+        CK(cudaGetLastError(), "escape sort");
+        ctx->launches += 1;
+        return FNTRS_OK;
+    }
     if (cap > 0x7FFFFFFFull) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "escape capacity too large");
     // per-call, stream-ordered scratch: calls on different streams never share it
     (void)max_key;
