@@ -425,3 +425,27 @@ def test_random_shapes_match_oracle(codec, oracle, k, n, L, S):
     plans = codec.plans(k, n, pats)
     dout, de, dc = codec.decode(plans, torch.from_numpy(sp.view(np.int32)).cuda(), dev_u16(rx), dev_esc(rx_esc))
     assert np.array_equal(host_u16(dout), dwant) and np.array_equal(escapes_to_numpy(de, dc), dwant_esc)
+
+
+# ------------------------------------------------ committed golden fixtures ----
+def test_gpu_matches_golden_fixtures(codec):
+    """The CUDA path against tests/golden/reference_vectors.npz, generated from the
+    reference library itself (tests/golden/make_golden.py): no oracle involved."""
+    import paper_0907_1788_b200 as F
+    path = os.path.join(ROOT, "tests", "golden", "reference_vectors.npz")
+    g = np.load(path)
+    for name in sorted({x.split("__")[0] for x in g.files}):
+        kind, n, k = name.split("_")[0], int(name.split("_")[1]), int(name.split("_")[2])
+        if kind in ("enc", "senc"):
+            p = F.CodeParams.make(k, n, kind == "senc")
+            fn = F.encode_systematic if kind == "senc" else F.encode_nonsystematic
+            assert fn(p, [int(x) for x in g[name + "__src"]]) == [int(x) for x in g[name + "__out"]], name
+        elif kind in ("dec", "sdec"):
+            p = F.CodeParams.make(k, n, kind == "sdec")
+            rx = [F.Symbol(int(z), int(v)) for z, v in zip(g[name + "__pos"], g[name + "__val"])]
+            fn = F.decode_systematic if kind == "sdec" else F.decode_nonsystematic
+            assert fn(p, rx) == [int(x) for x in g[name + "__out"]], name
+        elif kind == "plan":
+            a, ap, ps, af = codec.plans(k, n, g[name + "__pos"][None, :]).export(0)
+            assert np.array_equal(a, g[name + "__a"]) and np.array_equal(ap, g[name + "__ap"]), name
+            assert np.array_equal(af, g[name + "__afnt"]), name

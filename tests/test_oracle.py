@@ -302,3 +302,10 @@ def test_oracle_matches_golden_fixtures(oracle):
             st, a, ap, ps, af = oracle.build_plan(n, g[name + "__pos"])
             assert np.array_equal(a, g[name + "__a"]) and np.array_equal(ap, g[name + "__ap"])
             assert np.array_equal(af, g[name + "__afnt"]), name
+        elif kind == "senc":
+            assert np.array_equal(oracle.encode_systematic(k, n, g[name + "__src"])[1], g[name + "__out"]), name
+        elif kind == "sdec":
+            st, out = oracle.decode_systematic(k, n, g[name + "__pos"], g[name + "__val"])
+            assert st == 0 and np.array_equal(out, g[name + "__out"]), name
+        else:
+            raise AssertionError(name)
