@@ -411,7 +411,7 @@ def run_e2e(args, codec, cfg, dev, stream, seed, world):
     del enc0, rx0, d_src
     nch = (S + chunk - 1) // chunk
     ranges = escape_ranges(rxe_np, S, chunk, k, L)
-    pipe = HostPipeline(codec, k, n, L, chunk, systematic=SYSTEMATIC)
+    pipe = HostPipeline(codec, k, n, L, chunk, nstreams=args.e2e_streams, systematic=SYSTEMATIC)
     enc_h = torch.empty((S, n, L), dtype=torch.int16).pin_memory()
     dec_h = torch.empty((S, k, L), dtype=torch.int16).pin_memory()
     enc_esc_h = torch.empty((nch, pipe.cap_e), dtype=torch.int64).pin_memory()
@@ -422,10 +422,14 @@ def run_e2e(args, codec, cfg, dev, stream, seed, world):
     d2h = enc_h.numel() * 2 + dec_h.numel() * 2 + enc_esc_h.numel() * 8 + dec_esc_h.numel() * 8 + cnt_h.numel() * 8
 
     def step():
-        pipe.encode_host(src_h, enc_h, enc_esc_h, cnt_h[:nch])
         rxe_d = rxe_h.to(dev, non_blocking=True) if rxe_h is not None else None
         plans = codec.plans(k, n, pats_h)
-        pipe.decode_host(plans, sp_d, rx_h, rxe_d, dec_h, dec_esc_h, cnt_h[nch:], ranges)
+        if args.e2e_sequential:
+            pipe.encode_host(src_h, enc_h, enc_esc_h, cnt_h[:nch])
+            pipe.decode_host(plans, sp_d, rx_h, rxe_d, dec_h, dec_esc_h, cnt_h[nch:], ranges)
+        else:  # encode and decode chunks interleaved: both copy engines busy
+            pipe.code_host(src_h, enc_h, enc_esc_h, cnt_h[:nch], plans, sp_d, rx_h, rxe_d, dec_h, dec_esc_h,
+                           cnt_h[nch:], ranges)
         pipe.join()
         return plans
 
@@ -453,7 +457,8 @@ def run_e2e(args, codec, cfg, dev, stream, seed, world):
             "pcie_h2d_gbs": round(h2d / (ms * 1e-3) / 1e9, 2), "pcie_d2h_gbs": round(d2h / (ms * 1e-3) / 1e9, 2),
             "pcie_peak_h2d_gbs": link[0], "pcie_peak_d2h_gbs": link[1],
             "sample": f"{S} stripes/GPU of {cfg.name} from pinned host memory via HostPipeline "
-                      f"(Codec.encode/plans/decode C-ABI calls, {chunk}-stripe chunks on 3 streams)"}
+                      f"(Codec.encode/plans/decode C-ABI calls, {chunk}-stripe chunks on {args.e2e_streams} streams, "
+                      f"{'encode then decode' if args.e2e_sequential else 'encode and decode chunks interleaved'})"}
 
 
 def pcie_peaks(dev, nbytes=512 << 20):
@@ -533,6 +538,8 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--e2e-stripes", type=int, default=4096)
     ap.add_argument("--e2e-chunk", type=int, default=256)
+    ap.add_argument("--e2e-sequential", action="store_true", help="e2e: all encode chunks, then all decode chunks")
+    ap.add_argument("--e2e-streams", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-step-seconds", type=float, default=6.0)

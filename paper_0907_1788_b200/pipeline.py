@@ -84,6 +84,48 @@ class HostPipeline:
                 esc_h[c].copy_(self.d_esc[i], non_blocking=True)
                 counts_h[c:c + 1].copy_(self.d_cnt[i], non_blocking=True)
 
+    def code_host(self, src_h, enc_h, enc_esc_h, enc_counts_h, plans: Plans, stripe_pattern_dev, rx_h, rx_esc_dev,
+                  dec_h, dec_esc_h, dec_counts_h, esc_ranges=None):
+        """encode_host and decode_host with their chunks interleaved on the
+        streams (encode chunk c, then decode chunk c): the encode's heavy D2H
+        (2n bytes per codeword) overlaps the decode's H2D, so both copy engines
+        stay busy. The received packets must not depend on this call's encode
+        (they are the erasure channel's output of an earlier one)."""
+        torch = self.torch
+        S = src_h.shape[0]
+        ready = torch.cuda.Event()
+        ready.record(torch.cuda.current_stream(self.dev))
+        ns = len(self.streams)
+        for c, (a, b) in enumerate(self._chunks(S)):
+            for phase in (0, 1):
+                i = (2 * c + phase) % ns
+                st = self.streams[i]
+                if phase:
+                    st.wait_event(ready)
+                with torch.cuda.stream(st):
+                    if phase == 0:
+                        d_in, d_enc = self.d_in[i][: b - a], self.d_enc[i][: b - a]
+                        d_in.copy_(src_h[a:b], non_blocking=True)
+                        self.codec.encode(self.k, self.n, d_in, out=d_enc, esc_out=self.d_esc[i], esc_cap=self.cap_e,
+                                          count=self.d_cnt[i], stream=st, systematic=self.systematic)
+                        enc_h[a:b].copy_(d_enc, non_blocking=True)
+                        enc_esc_h[c].copy_(self.d_esc[i], non_blocking=True)
+                        enc_counts_h[c:c + 1].copy_(self.d_cnt[i], non_blocking=True)
+                    else:
+                        d_rx, d_dec = self.d_in[i][: b - a], self.d_dec[i][: b - a]
+                        d_rx.copy_(rx_h[a:b], non_blocking=True)
+                        esc = None
+                        if rx_esc_dev is not None and esc_ranges is not None:
+                            lo, hi = esc_ranges[c]
+                            if hi > lo:
+                                esc = rx_esc_dev[lo:hi] - a * self.k * self.L
+                        self.codec.decode(plans, stripe_pattern_dev[a:b], d_rx, esc, out=d_dec, esc_out=self.d_esc[i],
+                                          esc_cap=self.cap_e, count=self.d_cnt[i], stream=st,
+                                          systematic=self.systematic)
+                        dec_h[a:b].copy_(d_dec, non_blocking=True)
+                        dec_esc_h[c].copy_(self.d_esc[i], non_blocking=True)
+                        dec_counts_h[c:c + 1].copy_(self.d_cnt[i], non_blocking=True)
+
     def join(self):
         """Make the current stream wait for all pipeline streams."""
         cur = self.torch.cuda.current_stream(self.dev)

@@ -1,0 +1,3 @@
+for opt in "" "--e2e-sequential" "--e2e-streams 4" "--e2e-chunk 512" "--e2e-chunk 128 --e2e-streams 4"; do
+  python bench.py --steps 3 --warmup 3 --stripes 2048 --no-cpu-baseline $opt 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read())['e2e']; print('$opt', d['value'], d['pcie_h2d_gbs'], d['pcie_d2h_gbs'], d['pcie_peak_d2h_gbs'])"
+done
