@@ -23,6 +23,7 @@ namespace fntrs_gpu {
 namespace {
 
 constexpr int kPlanThreads = 256;
+constexpr uint32_t kPlanChunk = 16384;  // points staged in shared memory per round (64 KB)
 
 __global__ void __launch_bounds__(kPlanThreads)
 plan_kernel(uint32_t N, uint32_t M, uint32_t kp, uint32_t chunks, const uint32_t* __restrict__ positions,
@@ -32,30 +33,34 @@ plan_kernel(uint32_t N, uint32_t M, uint32_t kp, uint32_t chunks, const uint32_t
     const uint32_t pat = blockIdx.x / chunks;
     const uint32_t chunk = blockIdx.x - pat * chunks;
     const uint32_t* pos = positions + size_t(pat) * kp;
-    for (uint32_t l = threadIdx.x; l < kp; l += blockDim.x) xs[l] = __ldg(twN + __ldg(pos + l));
-    __syncthreads();
-
     const uint32_t idx = chunk * blockDim.x + threadIdx.x;
     const uint32_t npts = kp + M;
-    if (idx >= npts) return;
-    const bool self = idx < kp;
-    const uint32_t y = self ? xs[idx] : __ldg(twM + (idx - kp));
+    const bool valid = idx < npts, self = idx < kp;
+    const uint32_t y = !valid ? 0u : self ? __ldg(twN + __ldg(pos + idx)) : __ldg(twM + (idx - kp));
     // four independent accumulators for ILP; values stay in [0, 2p)
     uint32_t acc[4] = {1u, 1u, 1u, 1u};
-    uint32_t l = 0;
-    for (; l + 4 <= kp; l += 4) {
+    for (uint32_t c0 = 0; c0 < kp; c0 += kPlanChunk) {  // the points, a shared-memory chunk at a time
+        const uint32_t cn = kp - c0 < kPlanChunk ? kp - c0 : kPlanChunk;
+        __syncthreads();
+        for (uint32_t l = threadIdx.x; l < cn; l += blockDim.x) xs[l] = __ldg(twN + __ldg(pos + c0 + l));
+        __syncthreads();
+        if (!valid) continue;
+        uint32_t l = 0;
+        for (; l + 4 <= cn; l += 4) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            uint32_t d = red2p(y + kP - xs[l + u]);  // y - x_l, canonical
-            if (self) d = d ? d : 1u;                // skip the l == i factor
-            acc[u] = mulw(acc[u], d);
+            for (int u = 0; u < 4; ++u) {
+                uint32_t d = red2p(y + kP - xs[l + u]);  // y - x_l, canonical
+                if (self) d = d ? d : 1u;                // skip the l == i factor
+                acc[u] = mulw(acc[u], d);
+            }
+        }
+        for (; l < cn; ++l) {
+            uint32_t d = red2p(y + kP - xs[l]);
+            if (self) d = d ? d : 1u;
+            acc[0] = mulw(acc[0], d);
         }
     }
-    for (; l < kp; ++l) {
-        uint32_t d = red2p(y + kP - xs[l]);
-        if (self) d = d ? d : 1u;
-        acc[0] = mulw(acc[0], d);
-    }
+    if (!valid) return;
     uint32_t prod = red2p(mulw(mulw(red2p(acc[0]), red2p(acc[1])), red2p(mulw(red2p(acc[2]), red2p(acc[3])))));
     if (self) {
         ainv[size_t(pat) * kp + idx] = ginv(prod);
@@ -74,7 +79,7 @@ cudaError_t launch_plan_build(uint32_t N, uint32_t M, uint32_t kp, uint32_t npat
     const uint32_t chunks = (npts + kPlanThreads - 1) / kPlanThreads;
     const uint64_t blocks = uint64_t(npatterns) * chunks;
     if (blocks > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    const size_t smem = size_t(kp) * 4;
+    const size_t smem = size_t(kp < kPlanChunk ? kp : kPlanChunk) * 4;
     cudaError_t err = cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (err) return err;
     const uint32_t neg_minv = kP - cpow(M % kP, kP - 2);  // -1/M

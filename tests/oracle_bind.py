@@ -152,7 +152,7 @@ class Oracle:
         S, kk, L = src.shape
         src = np.ascontiguousarray(src, dtype=np.uint16)
         out = np.zeros((S, n, L), dtype=np.uint16)
-        cap = S * n * L // 1000 + 1024
+        cap = S * n * L + 1024  # worst case: every symbol escaped
         esc = np.zeros(cap, dtype=np.uint64)
         e = None if src_esc is None or len(src_esc) == 0 else np.ascontiguousarray(src_esc, dtype=np.uint64)
         ne = self.lib.orc_encode_stripes(k, n, S, L, src, None if e is None else e.ctypes.data,
@@ -164,7 +164,7 @@ class Oracle:
         S, kp, L = rx.shape
         rx = np.ascontiguousarray(rx, dtype=np.uint16)
         out = np.zeros((S, k, L), dtype=np.uint16)
-        cap = S * k * L // 1000 + 1024
+        cap = S * k * L + 1024
         esc = np.zeros(cap, dtype=np.uint64)
         e = None if rx_esc is None or len(rx_esc) == 0 else np.ascontiguousarray(rx_esc, dtype=np.uint64)
         ne = self.lib.orc_decode_stripes(k, n, S, L, pats.shape[0], _a32(pats), _a32(sp), rx,
@@ -291,7 +291,7 @@ class RefLib:
         S, kk, L = src.shape
         src = np.ascontiguousarray(src, dtype=np.uint16)
         out = np.zeros((S, n, L), dtype=np.uint16)
-        cap = S * n * L // 1000 + 1024
+        cap = S * n * L + 1024  # worst case: every symbol escaped
         esc = np.zeros(cap, dtype=np.uint64)
         e = None if src_esc is None or len(src_esc) == 0 else np.ascontiguousarray(src_esc, dtype=np.uint64)
         ne = self.lib.ref_encode_stripes(k, n, S, L, src, None if e is None else e.ctypes.data,
@@ -303,7 +303,7 @@ class RefLib:
         S, kp, L = rx.shape
         rx = np.ascontiguousarray(rx, dtype=np.uint16)
         out = np.zeros((S, k, L), dtype=np.uint16)
-        cap = S * k * L // 1000 + 1024
+        cap = S * k * L + 1024
         esc = np.zeros(cap, dtype=np.uint64)
         e = None if rx_esc is None or len(rx_esc) == 0 else np.ascontiguousarray(rx_esc, dtype=np.uint64)
         ne = self.lib.ref_decode_stripes(k, n, S, L, pats.shape[0], _a32(pats), _a32(sp), rx,

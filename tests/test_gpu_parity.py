@@ -449,3 +449,41 @@ def test_gpu_matches_golden_fixtures(codec):
             a, ap, ps, af = codec.plans(k, n, g[name + "__pos"][None, :]).export(0)
             assert np.array_equal(a, g[name + "__a"]) and np.array_equal(ap, g[name + "__ap"]), name
             assert np.array_equal(af, g[name + "__afnt"]), name
+
+
+# ------------------------------------------------------------ extreme sizes ----
+@pytest.mark.parametrize("k,n,L", [(65536, 65536, 3), (65535, 65536, 2), (1, 65536, 5), (32768, 65536, 3)])
+def test_maximum_sizes_match_oracle(codec, oracle, k, n, L):
+    """Largest domain: rate 1 (complete reception), 2k > 65536 at its limit, k = 1."""
+    from oracle_bind import gather_received
+    from paper_0907_1788_b200 import escapes_to_numpy
+    S = 1
+    src, esc = source_with_escapes(S, k, L, seed=k + L, n_esc=2)
+    want, want_esc = oracle.encode_stripes(k, n, src, esc)
+    out, oe, cnt = codec.encode(k, n, dev_u16(src), dev_esc(esc), esc_cap=S * n * L)  # k = 1: 65536 everywhere
+    assert np.array_equal(host_u16(out), want) and np.array_equal(escapes_to_numpy(oe, cnt), want_esc)
+    if want_esc.size > 1000:  # the default (statistical) capacity reports the overflow instead of truncating
+        import paper_0907_1788_b200 as F
+        o2, e2, c2 = codec.encode(k, n, dev_u16(src), dev_esc(esc))
+        with pytest.raises(F.TooManyEscapes):
+            escapes_to_numpy(e2, c2)
+    rng = np.random.default_rng(k)
+    kp = n if k == n else k
+    pats = np.sort(rng.choice(n, kp, replace=False)).astype(np.uint32)[None, :]
+    sp = np.zeros(1, dtype=np.uint32)
+    rx, rx_esc = gather_received(want, want_esc, pats, sp)
+    plans = codec.plans(k, n, pats)
+    dec, de, dc = codec.decode(plans, torch.zeros(1, dtype=torch.int32, device="cuda"), dev_u16(rx), dev_esc(rx_esc))
+    assert np.array_equal(host_u16(dec), src)
+    assert np.array_equal(escapes_to_numpy(de, dc), esc)
+
+
+def test_empty_batches_are_no_ops(codec):
+    from paper_0907_1788_b200 import escapes_to_numpy
+    for k, n in [(128, 256), (8192, 16384), (3000, 4096)]:
+        out, oe, cnt = codec.encode(k, n, torch.zeros((0, k, 64), dtype=torch.int16, device="cuda"))
+        assert out.shape == (0, n, 64) and escapes_to_numpy(oe, cnt).size == 0
+        plans = codec.plans(k, n, np.arange(k, dtype=np.uint32)[None, :])
+        dec, de, dc = codec.decode(plans, torch.zeros(0, dtype=torch.int32, device="cuda"),
+                                   torch.zeros((0, k, 64), dtype=torch.int16, device="cuda"))
+        assert dec.shape == (0, k, 64) and escapes_to_numpy(de, dc).size == 0
