@@ -41,22 +41,43 @@ PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback, only if MEASURED_PEAKS.json is absent
 
 
-def profiled_traffic(cfg, chunk, systematic):
-    """DRAM bytes (read + write) of one decode launch from the committed ncu
-    --set full capture (profiles/r01_ncu_full_raw.csv: dec_fast_kernel<8>, one
-    8192-stripe C2 chunk), when this run's launch has that exact shape."""
+def _profile_row(cfg, chunk, systematic):
+    """Header, units and values of the committed ncu --set full capture
+    (profiles/r01_ncu_full_raw.csv: dec_fast_kernel<8>, one 8192-stripe C2
+    chunk) when this run's decode launch has that exact shape."""
     if systematic or cfg.name != "C2" or chunk != 8192:
         return None
     try:
         import csv
         rows = list(csv.reader(open(os.path.join(ROOT, "profiles", "r01_ncu_full_raw.csv"))))
-        h, u, v = rows[0], rows[1], rows[2]
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-        tot = 0.0
-        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-            i = h.index(m)
-            tot += float(v[i]) * scale[u[i]]
-        return int(tot)
+        return rows[0], rows[1], rows[2]
+    except Exception:
+        return None
+
+
+def profiled_traffic(cfg, chunk, systematic):
+    """DRAM bytes (read + write) per decode launch from the committed capture."""
+    row = _profile_row(cfg, chunk, systematic)
+    if row is None:
+        return None
+    h, u, v = row
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    try:
+        return int(sum(float(v[h.index(m)]) * scale[u[h.index(m)]]
+                       for m in ("dram__bytes_read.sum", "dram__bytes_write.sum")))
+    except Exception:
+        return None
+
+
+def profiled_issue(cfg, chunk, systematic):
+    """The decode kernel's SM issue-slot utilisation (its binding roofline: the
+    integer pipes) from the committed capture, as a fraction."""
+    row = _profile_row(cfg, chunk, systematic)
+    if row is None:
+        return None
+    h, u, v = row
+    try:
+        return round(float(v[h.index("smsp__issue_active.avg.pct_of_peak_sustained_active")]) / 100.0, 4)
     except Exception:
         return None
 
@@ -367,6 +388,8 @@ def run_gpu(args, rank, world, local_rank):
             "traffic": args.traffic if args.traffic is not None else profiled_traffic(cfg, chunk, SYSTEMATIC),
             "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum per launch "
                               "(profiles/r01_ncu_full_raw.csv)",
+            # what bounds it instead of HBM: integer issue (ncu smsp__issue_active, same capture)
+            "issue_active_frac": profiled_issue(cfg, chunk, SYSTEMATIC),
             "algorithmic_bytes_per_launch": dec_bytes, "avg_launch_ms": round(dec_launch_ms, 4),
         },
         "roofline_encode": {
