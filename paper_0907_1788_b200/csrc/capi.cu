@@ -611,6 +611,14 @@ int fntrs_gpu_decode(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t stripes, ui
 }  // extern "C"
 
 namespace {
+// The fused systematic kernel serves the plans the fused decode kernel serves
+// (n_domain <= 4096, product size == n_domain, L a multiple of its tile width).
+bool fused_systematic_ok(const fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t L, const void* in) {
+    const int tcols = fast::fast_tile_columns(pl->N);
+    return ctx->fast_enabled && pl->rowmap && pl->ahat2 && !pl->cols && !pl->gen && !pl->full && tcols &&
+           L % uint32_t(tcols) == 0 && reinterpret_cast<uintptr_t>(in) % 16 == 0;
+}
+
 // Interpolation stage of the systematic codec: P = interpolate(plan, rx) into a
 // stream-ordered [stripes][k][L] intermediate with its sorted escape list. The
 // escape count is read back (one stream synchronisation) so the list can never
@@ -696,6 +704,21 @@ int fntrs_gpu_encode_systematic(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t
     uint32_t* sp = nullptr;
     CK(cudaMallocAsync(&sp, size_t(stripes) * 4, st), "systematic pattern map");
     CK(cudaMemsetAsync(sp, 0, size_t(stripes) * 4, st), "systematic pattern map");
+    if (fused_systematic_ok(ctx, pl, L, src)) {  // one kernel: interpolate, re-encode, copy the source rows
+        int rc = prep_escapes(ctx, out_esc, esc_cap, n_out_esc, st);
+        if (!rc) {
+            EscIn ein{reinterpret_cast<const unsigned long long*>(src_esc), n_src_esc};
+            EscOut eout{reinterpret_cast<unsigned long long*>(out_esc), reinterpret_cast<unsigned long long*>(n_out_esc),
+                        esc_cap};
+            fast::FastPlanView fv{pl->N, pl->k, pl->rowmap, pl->ahat2};
+            cudaError_t le = fast::launch_systematic_fast(ctx->ftab, fv, true, n, stripes, L, sp, src, ein, out, eout, st);
+            cudaFreeAsync(sp, st);
+            CK(le, "systematic encode launch");
+            ctx->launches += 1;
+            rc = sort_escapes(ctx, eout.keys, esc_cap, uint64_t(stripes) * n * L, st);
+        }
+        return rc;
+    }
     Interp it;
     int rc = interpolate_stage(ctx, pl, stripes, L, sp, src, src_esc, n_src_esc, st, it);
     if (!rc) rc = encode_impl(ctx, k, n, N, stripes, L, it.coef, it.esc, it.n_esc, out, out_esc, esc_cap, n_out_esc, stream);
@@ -716,6 +739,18 @@ int fntrs_gpu_decode_systematic(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t 
     DeviceGuard g(ctx->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (!stripes || !L) return prep_escapes(ctx, out_esc, esc_cap, n_out_esc, st);
+    if (fused_systematic_ok(ctx, pl, L, rx)) {  // one kernel: interpolate, re-encode rows 0..k-1
+        int rc = prep_escapes(ctx, out_esc, esc_cap, n_out_esc, st);
+        if (rc) return rc;
+        EscIn ein{reinterpret_cast<const unsigned long long*>(rx_esc), n_rx_esc};
+        EscOut eout{reinterpret_cast<unsigned long long*>(out_esc), reinterpret_cast<unsigned long long*>(n_out_esc),
+                    esc_cap};
+        fast::FastPlanView fv{pl->N, pl->k, pl->rowmap, pl->ahat2};
+        CK(fast::launch_systematic_fast(ctx->ftab, fv, false, pl->n, stripes, L, stripe_pattern, rx, ein, out, eout, st),
+           "systematic decode launch");
+        ctx->launches += 1;
+        return sort_escapes(ctx, eout.keys, esc_cap, uint64_t(stripes) * pl->k * L, st);
+    }
     Interp it;
     int rc = interpolate_stage(ctx, pl, stripes, L, stripe_pattern, rx, rx_esc, n_rx_esc, st, it);
     if (!rc)

@@ -142,14 +142,21 @@ struct DecOcc {
     static constexpr int MINB = (E <= 8) ? 5 : Pick<E>::MINB;
 };
 
-template <int E, class G, bool HALFK>
+// MODE 0: decode (interp::interpolate, the k coefficients out).
+// MODE 1: systematic decode (codec.cpp:163-196): the interpolant P is
+//         re-encoded in the tile (FNT4 = FNT_N(P), fused with IFNT3's last
+//         pass in registers) and codeword rows 0..k-1 go out.
+// MODE 2: systematic encode (codec.cpp:151-161) with the plan of positions
+//         0..k-1: source rows are copied to codeword rows 0..k-1 while the
+//         first pass scatters them, and FNT4 rows k..n-1 (the parity) go out.
+template <int E, class G, bool HALFK, int MODE = 0>
 __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const __grid_constant__ CUtensorMap rx_map,
                                                          const uint2* __restrict__ ptabF, const uint2* __restrict__ ptabI,
                                                          const uint2* __restrict__ rowmap,
                                                          const uint2* __restrict__ ahat2, uint32_t k, uint32_t L,
                                                          uint32_t tps, uint32_t tiles, uint32_t nbox, uint32_t box_rows,
                                                          const uint32_t* __restrict__ stripe_pattern, EscIn esc_in,
-                                                         uint16_t* __restrict__ out, EscOut esc_out) {
+                                                         uint16_t* __restrict__ out, EscOut esc_out, uint32_t n = 0) {
     using S = Sched<E>;
     constexpr int N = 1 << E, WT = G::WT, NT = G::NT, P = S::P;
     constexpr int RLZ = G::RLZ, RZ = 1 << RLZ;
@@ -195,7 +202,9 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
         const uint2* __restrict__ rm = rowmap + size_t(pat) * N;
         const uint2* __restrict__ ah = ahat2 + size_t(pat) * N;
         const unsigned long long key = uint64_t(stripe) * k * L + c0;
-        uint16_t* outp = launder(out + key);
+        // output rows per stripe: k (decode, systematic decode) or n (systematic encode)
+        const unsigned long long key_out = MODE == 2 ? uint64_t(stripe) * n * L + c0 : key;
+        uint16_t* outp = launder(out + key_out);
         mbar_wait(&bars[0], iter & 1);
         const uint16_t* st_in = stage0;
 
@@ -203,10 +212,13 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
         // reads the guard row of ones, scales by 0). A received zero word may
         // be an escaped 65536: the group fix-up re-scales it.
         uint32_t zmin = 0xFFFFFFFFu;
-        auto ld_scatter = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t {
+        auto ld_scatter = [&](uint32_t lrow, uint32_t, int q, uint32_t col) -> uint32_t {
             const uint2 m = __ldg(rm + lrow);
             const uint32_t raw = st_in[int(m.x * uint32_t(WT) + col)];
             zmin = min(zmin, raw);
+            if constexpr (MODE == 2) {  // identity plan: row z < k is source row z -> codeword row z
+                if (HALFK ? (q < R0 / 2) : (lrow < k)) __stcs(outp + (lrow * L + col), uint16_t(raw));
+            }
             return mulws(raw, m.y, m.y * 65535u);
         };
         auto fix_scatter = [&](uint32_t (&v)[R0], uint32_t base, uint32_t, uint32_t col) {
@@ -218,8 +230,10 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
                 if (v[q] != 0u) continue;
                 const uint2 m = __ldg(rm + base + (uint32_t(q) << SL0));
                 if (m.x != 0xFFFFFFFFu && st_in[m.x * WT + col] == 0u &&
-                    esc_has(esc_in, key + uint64_t(m.x) * L + col))
+                    esc_has(esc_in, key + uint64_t(m.x) * L + col)) {
                     v[q] = mulws(65536u, m.y, m.y * 65535u);
+                    if constexpr (MODE == 2) emit_escape(esc_out, key_out + uint64_t(m.x) * L + col);
+                }
             }
         };
         auto ld_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t { return work[G::idx(lrow, col)]; };
@@ -338,8 +352,63 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
             pass<E, 1, true, false, kSmemCap, kSmemCap, G>(pass_table(ptabI, S::llog(1)), ld_smf, st_smf);
             __syncthreads();
         }
-        pass<E, P - 1, true, false, kSmemCap, kCanon, G>(pass_table(ptabI, S::llog(P - 1)), ld_smf, st_out, NoFix(),
-                                                      flush_out);
+        if constexpr (MODE == 0) {
+            pass<E, P - 1, true, false, kSmemCap, kCanon, G>(pass_table(ptabI, S::llog(P - 1)), ld_smf, st_out, NoFix(),
+                                                          flush_out);
+        } else {
+            // IFNT3 last pass + truncation to the k coefficients + FNT4 first
+            // DIT pass, in registers on the same rows (reversed view)
+            {
+                constexpr int ITEMS = (N / RZ) * WT;
+                constexpr uint64_t BD = dif_bound<RZ, true, kSmemCap>();
+                constexpr uint64_t BT = dit_bound<RZ, false, BD>();
+#pragma unroll 1
+                for (int it = threadIdx.x; it < ITEMS; it += NT) {
+                    const uint32_t col = uint32_t(it) & uint32_t(WT - 1);
+                    const uint32_t g = uint32_t(it) >> LGW;
+                    uint32_t v[RZ];
+#pragma unroll
+                    for (int q = 0; q < RZ; ++q) v[q] = work[G::template idx_flip<FLIP + 1>((g << RLZ) + q, col)];
+                    dif_regs<RZ, true, kSmemCap>(v);
+                    const uint32_t fh = perm_head<E>(g);
+#pragma unroll
+                    for (int s2 = 0; s2 < RZ; ++s2) {  // output s2 holds coefficient fh + s2 * N/R
+                        const bool live = HALFK ? (s2 < RZ / 2) : (fh + (uint32_t(s2) << (E - RLZ)) < k);
+                        if (!live) v[rev<RZ>(s2)] = 0u;
+                    }
+                    // DIT input x_s = y_s (same rows): v[rev(s)] already is y_s
+                    dit_regs<RZ, false, BD>(v);
+#pragma unroll
+                    for (int q = 0; q < RZ; ++q)
+                        work[G::template idx_flip<FLIP + 1>((g << RLZ) + q, col)] = cap<BT, kSmemCap>(v[q]);
+                }
+            }
+            __syncthreads();
+            if constexpr (P == 3) {
+                pass<E, 1, false, true, kSmemCap, kSmemCap, G>(pass_table(ptabF, S::llog(1)), ld_smf, st_smf);
+                __syncthreads();
+            }
+            // FNT4 last DIT pass: natural order, codeword row f = the position
+            auto st_sys = [&](uint32_t lrow, uint32_t, int q, uint32_t col, uint32_t y) -> uint32_t {
+                constexpr int SLL = S::slog(0);
+                (void)SLL;
+                bool keep;
+                if constexpr (MODE == 1)
+                    keep = HALFK ? (q < R0 / 2) : (lrow < k);
+                else
+                    keep = (HALFK ? (q >= R0 / 2) : (lrow >= k)) && lrow < n;
+                if (keep) __stcs(outp + (lrow * L + col), uint16_t(y));
+                return keep ? y >> 16 : 0u;
+            };
+            auto flush_sys = [&](uint32_t mask, uint32_t base, uint32_t, uint32_t col) {
+                if (!mask) return;
+#pragma unroll 1
+                for (int q = 0; q < 16; ++q)
+                    if (mask & (1u << q))
+                        emit_escape(esc_out, key_out + uint64_t(base + (uint32_t(q) << SL0)) * L + col);
+            };
+            pass<E, 0, false, true, kSmemCap, kCanon, G>(tF0, ld_smf, st_sys, NoFix(), flush_sys);
+        }
         __syncthreads();
     }
 }
@@ -450,11 +519,11 @@ cudaError_t launch_enc(const FastTables& t, uint32_t k, uint32_t n, uint32_t str
     return cudaGetLastError();
 }
 
-template <int E>
+template <int E, int MODE = 0>
 cudaError_t launch_dec(const FastTables& t, const FastPlanView& pv, uint32_t stripes, uint32_t L, const uint32_t* sp,
-                       const uint16_t* rx, EscIn ein, uint16_t* out, EscOut eout, cudaStream_t st) {
+                       const uint16_t* rx, EscIn ein, uint16_t* out, EscOut eout, cudaStream_t st, uint32_t n = 0) {
     using G = typename Pick<E>::G;
-    auto kern = pv.k == (1u << E) / 2 ? dec_fast_kernel<E, G, true> : dec_fast_kernel<E, G, false>;
+    auto kern = pv.k == (1u << E) / 2 ? dec_fast_kernel<E, G, true, MODE> : dec_fast_kernel<E, G, false, MODE>;
     LaunchShape sh;
     cudaError_t err = shape_for(kern, E, G::WT, G::NT, pv.k, stripes, L, sh, kGuardBytes, 1);
     if (err) return err;
@@ -462,7 +531,7 @@ cudaError_t launch_dec(const FastTables& t, const FastPlanView& pv, uint32_t str
     CUtensorMap map;
     if ((err = make_map(&map, rx, uint64_t(stripes) * pv.k, L, G::WT, sh.box_rows))) return err;
     kern<<<sh.grid, G::NT, sh.smem, st>>>(map, t.ptab_fwd, t.ptab_inv, pv.rowmap, pv.ahat2, pv.k, L, sh.tps, sh.tiles,
-                                          sh.nbox, sh.box_rows, sp, ein, out, eout);
+                                          sh.nbox, sh.box_rows, sp, ein, out, eout, n);
     return cudaGetLastError();
 }
 
@@ -533,6 +602,22 @@ cudaError_t launch_decode_fast(const FastTables& t, const FastPlanView& pv, uint
         case 4096: return launch_dec<12>(t, pv, stripes, L, sp, rx, ein, out, eout, st);
         default: return cudaErrorInvalidValue;
     }
+}
+
+// systematic codec, fused (MODE 1: decode, rows 0..k-1 out; MODE 2: encode
+// with the plan of positions 0..k-1, rows 0..n-1 out)
+cudaError_t launch_systematic_fast(const FastTables& t, const FastPlanView& pv, bool encode, uint32_t n,
+                                   uint32_t stripes, uint32_t L, const uint32_t* sp, const uint16_t* in, EscIn ein,
+                                   uint16_t* out, EscOut eout, cudaStream_t st) {
+#define FNTRS_SYS(e)                                                                              \
+    case (1u << e):                                                                               \
+        return encode ? launch_dec<e, 2>(t, pv, stripes, L, sp, in, ein, out, eout, st, n)       \
+                      : launch_dec<e, 1>(t, pv, stripes, L, sp, in, ein, out, eout, st, n);
+    switch (pv.N) {
+        FNTRS_SYS(5) FNTRS_SYS(6) FNTRS_SYS(7) FNTRS_SYS(8) FNTRS_SYS(9) FNTRS_SYS(10) FNTRS_SYS(11) FNTRS_SYS(12)
+        default: return cudaErrorInvalidValue;
+    }
+#undef FNTRS_SYS
 }
 
 cudaError_t launch_fast_plan_tables(uint32_t N, uint32_t kp, uint32_t npatterns, const uint32_t* pos,

@@ -101,6 +101,10 @@ __host__ __device__ inline uint32_t ahat2_slot(uint32_t N, uint32_t j) {
 cudaError_t build_fast_tables(FastTables& t, cudaStream_t st);
 int fast_tile_columns(uint32_t N);  // 0 when N has no fast kernel
 int fast_encode_columns(uint32_t N);  // encode tile width (L must be a multiple)
+// fused systematic codec on a fast plan (M == N); encode: the plan of positions 0..k-1
+cudaError_t launch_systematic_fast(const FastTables& t, const FastPlanView& pv, bool encode, uint32_t n,
+                                   uint32_t stripes, uint32_t L, const uint32_t* sp, const uint16_t* in, EscIn ein,
+                                   uint16_t* out, EscOut eout, cudaStream_t st);
 cudaError_t launch_encode_fast(const FastTables& t, uint32_t k, uint32_t n, uint32_t N, uint32_t stripes,
                                uint32_t L, const uint16_t* src, EscIn ein, uint16_t* out, EscOut eout,
                                cudaStream_t st);
