@@ -275,6 +275,7 @@ int fntrs_gpu_destroy(fntrs_ctx* ctx) {
     cudaFree(ctx->tab.fwd);
     cudaFree(ctx->tab.inv);
     cudaFree(ctx->ftab.ptab_fwd);
+    cudaFree(ctx->ftab.ptab_fwdT);
     cudaFree(ctx->ftab.ptab_inv);
     cudaFree(ctx->ftab.big_fwd);
     cudaFree(ctx->ftab.big_inv);

@@ -156,7 +156,8 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
                                                          const uint2* __restrict__ ahat2, uint32_t k, uint32_t L,
                                                          uint32_t tps, uint32_t tiles, uint32_t nbox, uint32_t box_rows,
                                                          const uint32_t* __restrict__ stripe_pattern, EscIn esc_in,
-                                                         uint16_t* __restrict__ out, EscOut esc_out, uint32_t n = 0) {
+                                                         uint16_t* __restrict__ out, EscOut esc_out, uint32_t n,
+                                                         const uint2* __restrict__ ptabFT) {
     using S = Sched<E>;
     constexpr int N = 1 << E, WT = G::WT, NT = G::NT, P = S::P;
     constexpr int RLZ = G::RLZ, RZ = 1 << RLZ;
@@ -295,8 +296,21 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
                     u[j] = live ? v[RZ - 1 - j] : 0u;
                 }
                 dit_regs<RZ, false, BD>(u);
+                if constexpr (P == 2) {
+                    // FNT2's last DIT pass pre-multiplies logical row t + s*sub0 by r^(t s);
+                    // this element is t = q, s = N/R - 1 - g: apply it here, where the
+                    // multiply also does the reduction the store needed anyway
+                    const uint4* tq = reinterpret_cast<const uint4*>(ptabFT + N + (uint32_t(N / RZ) - 1u - g) * RZ);
 #pragma unroll
-                for (int q = 0; q < RZ; ++q) work[G::idx((g << RLZ) + (RZ - 1 - q), col)] = cap<BT, kSmemCap>(u[q]);
+                    for (int q = 0; q < RZ; q += 2) {
+                        const uint4 w = __ldg(tq + q / 2);
+                        work[G::idx((g << RLZ) + (RZ - 1 - q), col)] = mulws(u[q], w.x, w.y);
+                        work[G::idx((g << RLZ) + (RZ - 2 - q), col)] = mulws(u[q + 1], w.z, w.w);
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < RZ; ++q) work[G::idx((g << RLZ) + (RZ - 1 - q), col)] = cap<BT, kSmemCap>(u[q]);
+                }
             }
         }
         __syncthreads();
@@ -319,13 +333,13 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
 #pragma unroll
                 for (int s = 0; s < R0; ++s) {
                     uint32_t x = work[G::template idx_flip<FLIP + 1>(t + (uint32_t(s) << SL0), col)];
-                    if (s > 0) {
+                    if (P != 2 && s > 0) {  // P == 2: the twiddle was applied by the producing pass
                         const uint2 w = tw_at(tpf, s, w4);
                         x = mulws(x, w.x, w.y);
                     }
                     v[rev<R0>(s)] = x;
                 }
-                dit_regs<R0, false, kSmemCap>(v);
+                dit_regs<R0, false, (P == 2 ? k2P : kSmemCap)>(v);
                 const uint4* ahq = reinterpret_cast<const uint4*>(ah) + t * (R0 / 2);  // ahat2_slot order
 #pragma unroll
                 for (int q = 0; q < R0; q += 2) {
@@ -423,6 +437,17 @@ __global__ void ptab_kernel(uint2* fwd, uint2* inv) {
     const int32_t wf = balanced(gpow(3u, ex)), wi = balanced(gpow(3u, (65536u - ex) & 0xFFFFu));
     fwd[i] = make_uint2(uint32_t(wf), uint32_t(wf * 65535));
     inv[i] = make_uint2(uint32_t(wi), uint32_t(wi * 65535));
+}
+
+// transposed pass-0 twiddles for N = 2^LL <= 256: [N + (N/16) s + t] = r_N^(t s)
+__global__ void ptab_t_kernel(uint2* fwdT) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < 32 || i >= (1u << 9)) return;
+    const int LL = 31 - __clz(i);
+    const uint32_t sub = 1u << (LL - 4), j = i - (1u << LL), s = j / sub, t = j % sub;
+    const uint32_t ex = ((t * s) << (16 - LL)) & 0xFFFFu;
+    const int32_t w = balanced(gpow(3u, ex));
+    fwdT[i] = make_uint2(uint32_t(w), uint32_t(w * 65535));
 }
 
 __global__ void fast_plan_tables_kernel(uint32_t N, const uint32_t* __restrict__ ahat, uint2* __restrict__ rowmap,
@@ -531,7 +556,7 @@ cudaError_t launch_dec(const FastTables& t, const FastPlanView& pv, uint32_t str
     CUtensorMap map;
     if ((err = make_map(&map, rx, uint64_t(stripes) * pv.k, L, G::WT, sh.box_rows))) return err;
     kern<<<sh.grid, G::NT, sh.smem, st>>>(map, t.ptab_fwd, t.ptab_inv, pv.rowmap, pv.ahat2, pv.k, L, sh.tps, sh.tiles,
-                                          sh.nbox, sh.box_rows, sp, ein, out, eout, n);
+                                          sh.nbox, sh.box_rows, sp, ein, out, eout, n, t.ptab_fwdT);
     return cudaGetLastError();
 }
 
@@ -541,7 +566,9 @@ cudaError_t build_fast_tables(FastTables& t, cudaStream_t st) {
     cudaError_t err = cudaMalloc(&t.ptab_fwd, sizeof(uint2) << 13);
     if (err) return err;
     if ((err = cudaMalloc(&t.ptab_inv, sizeof(uint2) << 13))) return err;
+    if ((err = cudaMalloc(&t.ptab_fwdT, sizeof(uint2) << 9))) return err;
     ptab_kernel<<<(1u << 13) / 256, 256, 0, st>>>(t.ptab_fwd, t.ptab_inv);
+    ptab_t_kernel<<<2, 256, 0, st>>>(t.ptab_fwdT);
     return cudaGetLastError();
 }
 

@@ -81,6 +81,7 @@ namespace fast {
 struct FastTables {
     uint2* ptab_fwd = nullptr;  // per-pass twiddles {w, 65535 w}: [2^LL + 16 t + s] = r_(2^LL)^(t s)
     uint2* ptab_inv = nullptr;
+    uint2* ptab_fwdT = nullptr;  // pass-0 twiddles transposed, N <= 256: [N + (N/16) s + t] = r_N^(t s)
     uint2* big_fwd = nullptr;   // {r_m^j, 65535 r_m^j} at [m + j], m <= 65536 (four-step twiddles)
     uint2* big_inv = nullptr;
 };
