@@ -419,7 +419,7 @@ def run_e2e(args, codec, cfg, dev, stream, seed, world):
     import torch
     from paper_0907_1788_b200.pipeline import HostPipeline, escape_ranges
     k, n, L = cfg.k, cfg.n, cfg.L
-    S = min(args.e2e_stripes, cfg.stripes)
+    S = min(args.e2e_stripes, cfg.stripes, pinned_budget_stripes(cfg, world))
     chunk = max(1, min(S, args.e2e_chunk))
     src_h = torch.from_numpy(W.symbols(seed + 7, 0, S * k * L).view(np.int16).reshape(S, k, L)).pin_memory()
     pats, sp = W.patterns(cfg, seed=seed + 7, stripes=S)
@@ -482,6 +482,18 @@ def run_e2e(args, codec, cfg, dev, stream, seed, world):
             "sample": f"{S} stripes/GPU of {cfg.name} from pinned host memory via HostPipeline "
                       f"(Codec.encode/plans/decode C-ABI calls, {chunk}-stripe chunks on {args.e2e_streams} streams, "
                       f"{'encode then decode' if args.e2e_sequential else 'encode and decode chunks interleaved'})"}
+
+
+def pinned_budget_stripes(cfg, world):
+    """e2e sample size the host can pin: all ranks together use at most a quarter
+    of MemAvailable (source, received, encoded and decoded packets per stripe)."""
+    try:
+        with open("/proc/meminfo") as f:
+            avail = next(int(line.split()[1]) * 1024 for line in f if line.startswith("MemAvailable"))
+    except Exception:
+        return 1 << 30
+    per_stripe = (3 * cfg.k + cfg.n) * cfg.L * 2
+    return max(64, int(avail / 4 / max(1, world) / per_stripe))
 
 
 def pcie_peaks(dev, nbytes=512 << 20):
