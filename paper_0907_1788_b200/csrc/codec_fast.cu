@@ -3,10 +3,13 @@
 // Persistent CTAs walk tiles (stripe, WT adjacent codewords). The k input
 // packets of the NEXT tile are fetched by TMA (cp.async.bulk.tensor.2d, one
 // 2-D box of <= 256 packets x WT symbols per request, completion on an
-// mbarrier) into a double-buffered uint16 staging area while the CTA runs the
-// transforms of the current tile, so HBM reads overlap the integer pipes.
+// mbarrier) while the CTA runs the transforms of the current tile, so HBM
+// reads overlap the integer pipes: encode double-buffers the uint16 stage;
+// decode reads its stage only in the first pass and reuses one buffer (the
+// next load is issued after that pass), which fits five CTAs per SM.
 // One work item = one radix-R butterfly of one codeword (thread = codeword,
-// warp = 32 adjacent codewords, conflict-free 32-bit shared-memory rows).
+// warp = 32 adjacent codewords, conflict-free 32-bit shared-memory rows);
+// encode at n_domain <= 256 takes two codewords per item in a 64-wide tile.
 //
 // Encode  (codec::encode_nonsystematic, proj/src/codec.cpp:124-131):
 //   pass 0 reads the staged source rows (the zero padding rows >= k are
