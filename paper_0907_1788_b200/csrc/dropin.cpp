@@ -20,9 +20,35 @@
 
 namespace fntrs {
 
-// ---- instrumentation (instrument.hpp): per-thread scope chain
+// ---- instrumentation (instrument.hpp): counters and the per-thread scope chain
 namespace {
 thread_local FntScope* g_scope = nullptr;
+std::size_t size_bucket(std::size_t size) noexcept {  // ceil(log2 size), capped at 2^16
+    std::size_t lg = 0;
+    while (lg < 16 && (std::size_t{1} << lg) < size) ++lg;
+    return lg;
+}
+}  // namespace
+void FntCounter::record(std::size_t size) noexcept { ++by_log2_[size_bucket(size)]; }
+std::uint64_t FntCounter::count(std::size_t size) const noexcept { return by_log2_[size_bucket(size)]; }
+std::uint64_t FntCounter::total() const noexcept {
+    std::uint64_t sum = 0;
+    for (std::uint64_t c : by_log2_) sum += c;
+    return sum;
+}
+double FntCounter::equivalents(std::size_t base) const noexcept {
+    double work = 0.0;
+    for (std::size_t lg = 0; lg < by_log2_.size(); ++lg) work += double(by_log2_[lg]) * double(std::size_t{1} << lg);
+    return work / double(base);
+}
+void FntCounter::merge(const FntCounter& other) noexcept {
+    for (std::size_t lg = 0; lg < by_log2_.size(); ++lg) by_log2_[lg] += other.by_log2_[lg];
+}
+std::map<std::size_t, std::uint64_t> FntCounter::snapshot() const {
+    std::map<std::size_t, std::uint64_t> out;
+    for (std::size_t lg = 0; lg < by_log2_.size(); ++lg)
+        if (by_log2_[lg]) out[std::size_t{1} << lg] = by_log2_[lg];
+    return out;
 }
 FntScope::FntScope(FntCounter& counter) : counter_(counter), outer_(g_scope) { g_scope = this; }
 FntScope::~FntScope() { g_scope = outer_; }
