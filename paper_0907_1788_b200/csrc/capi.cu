@@ -8,6 +8,7 @@
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cstdio>
+#include <cstdlib>
 #include <algorithm>
 #include <map>
 #include <cstring>
@@ -359,6 +360,25 @@ int encode_impl(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t N, uint32_t str
 
 extern "C" {
 
+}  // extern "C"
+
+namespace {
+// Plan method for the fused kernels' plans. Direct products cost
+// P (k + M) k field multiplies; the log-domain method ~ P N log N (1 + D)
+// plus a fixed chain of small launches. FNTRS_PLAN=direct|log overrides.
+bool plan_direct(uint32_t k, uint32_t M, uint32_t P) {
+    if (const char* m = std::getenv("FNTRS_PLAN")) {
+        if (!std::strcmp(m, "direct")) return true;
+        if (!std::strcmp(m, "log")) return false;
+    }
+    // measured (one B200): 1 pattern, k = 1024: direct 0.05 ms vs 0.09 ms; 2049
+    // patterns, k = 128 (100M multiplies): a tie; k >= 2048: the log domain by 2.5-10x
+    return uint64_t(P) * (uint64_t(k) + M) * k <= (uint64_t(1) << 26);
+}
+}  // namespace
+
+extern "C" {
+
 int fntrs_gpu_plans_create(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t kp, uint32_t npatterns,
                            const uint32_t* positions, fntrs_plans** out, void* stream) {
     if (!ctx || !out) return FNTRS_E_INVALID_ARGUMENT;
@@ -417,7 +437,17 @@ int fntrs_gpu_plans_create(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t kp, 
         if (!e && locator) e = cudaMallocAsync(&pl->ahat, size_t(npatterns) * M * 4, st);
         if (!e) e = cudaMemcpyAsync(pl->pos, positions, npos * 4, cudaMemcpyHostToDevice, st);
         const bool fastplan = !full && !split && kp == k && M == N && (fast::fast_tile_columns(N) || large);
-        if (!e && fastplan) {
+        if (!e && fastplan && plan_direct(k, M, npatterns)) {
+            // few or small patterns: the direct products (plan_build.cu) beat the
+            // log-domain method's chain of column transforms
+            e = cudaMallocAsync(&pl->rowmap, size_t(npatterns) * N * sizeof(uint2), st);
+            if (!e) e = cudaMallocAsync(&pl->ahat2, size_t(npatterns) * N * sizeof(uint2), st);
+            if (!e) e = launch_plan_build(N, M, kp, npatterns, pl->pos, pl->ainv, pl->ahat, ctx->tab, st);
+            if (!e)
+                e = fast::launch_fast_plan_tables(N, kp, npatterns, pl->pos, pl->ainv, pl->ahat, pl->rowmap, pl->ahat2,
+                                                  st);
+            ctx->launches += 3;
+        } else if (!e && fastplan) {
             // log-domain convolution plan (plan_fast.cu): ainv, ahat, rowmap, ahat2 at once
             e = cudaMallocAsync(&pl->rowmap, size_t(npatterns) * N * sizeof(uint2), st);
             if (!e) e = cudaMallocAsync(&pl->ahat2, size_t(npatterns) * N * sizeof(uint2), st);

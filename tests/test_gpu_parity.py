@@ -487,3 +487,27 @@ def test_empty_batches_are_no_ops(codec):
         dec, de, dc = codec.decode(plans, torch.zeros(0, dtype=torch.int32, device="cuda"),
                                    torch.zeros((0, k, 64), dtype=torch.int16, device="cuda"))
         assert dec.shape == (0, k, 64) and escapes_to_numpy(de, dc).size == 0
+
+
+@pytest.mark.parametrize("k,n,P", [(128, 256, 64), (1024, 2048, 3), (16, 32, 500), (2048, 4096, 2)])
+def test_plan_methods_agree(codec, oracle, k, n, P, monkeypatch):
+    """Direct products and the log-domain convolution (plans_create picks by
+    cost; FNTRS_PLAN forces one) give identical plans and decodes."""
+    from oracle_bind import gather_received
+    rng = np.random.default_rng(k + P)
+    pats = np.stack([np.sort(rng.choice(n, k, replace=False)) for _ in range(P)]).astype(np.uint32)
+    L, S = 32, P
+    src, esc = source_with_escapes(S, k, L, seed=P, n_esc=2)
+    want, want_esc = oracle.encode_stripes(k, n, src, esc)
+    sp = np.arange(S, dtype=np.uint32)
+    rx, rx_esc = gather_received(want, want_esc, pats, sp)
+    outs = []
+    for method in ("direct", "log"):
+        monkeypatch.setenv("FNTRS_PLAN", method)
+        plans = codec.plans(k, n, pats)
+        fields = [plans.export(p) for p in (0, P - 1)]
+        dec, _, _ = codec.decode(plans, torch.from_numpy(sp.view(np.int32)).cuda(), dev_u16(rx), dev_esc(rx_esc))
+        outs.append((fields, host_u16(dec)))
+    for (a, b) in zip(outs[0][0], outs[1][0]):
+        assert all(np.array_equal(x, y) if isinstance(x, np.ndarray) else x == y for x, y in zip(a, b))
+    assert np.array_equal(outs[0][1], outs[1][1]) and np.array_equal(outs[0][1], src)
