@@ -30,7 +30,7 @@ constexpr int kLW = 64;   // codewords per CTA
 constexpr int kLNT = 256;  // threads per CTA
 
 template <int E>
-using LG = Geom<E, kLW, kLNT, (1 << E) <= 128 ? 4 : 3>;
+using LG = Geom<E, kLW, kLNT, (1 << E) <= 128 ? 5 : 3>;
 
 struct BlockIdx {
     uint32_t sb, g, c0;
