@@ -387,6 +387,24 @@ def test_host_pipeline_multistream_matches_single_stream(codec):
     assert np.array_equal(dec_h.numpy().view(np.uint16), src2)
     assert int(dcnt_h.sum()) == 0
     assert want_esc.size > 0 and want.shape == (S, n, L)
+    # encode and decode chunks interleaved on the streams (code_host): same results
+    for nstreams in (2, 4):
+        pipe2 = HostPipeline(codec, k, n, L, chunk, nstreams=nstreams)
+        enc2 = torch.empty_like(enc_h).pin_memory()
+        dec2 = torch.empty_like(dec_h).pin_memory()
+        esc2 = torch.empty_like(esc_h).pin_memory()
+        desc2 = torch.empty_like(desc_h).pin_memory()
+        cnt2 = torch.zeros(nch, dtype=torch.int64).pin_memory()
+        dcnt2 = torch.zeros(nch, dtype=torch.int64).pin_memory()
+        pipe2.code_host(src_h, enc2, esc2, cnt2, plans, torch.from_numpy(sp.view(np.int32)).cuda(), rx_h, rxe,
+                        dec2, desc2, dcnt2, escape_ranges(rxe_np, S, chunk, k, L))
+        pipe2.join()
+        torch.cuda.synchronize()
+        assert np.array_equal(enc2.numpy().view(np.uint16), host_u16(w2))
+        assert np.array_equal(dec2.numpy().view(np.uint16), src2) and int(dcnt2.sum()) == 0
+        got2 = np.concatenate([esc2[c, : int(cnt2[c])].numpy().view(np.uint64) + np.uint64(c * chunk * n * L)
+                               for c in range(nch)])
+        assert np.array_equal(got2, escapes_to_numpy(we2, wc2))
 
 
 # ------------------------------------------------------- randomized sweep ----
