@@ -10,9 +10,8 @@
 // call without a usable CUDA device throws fntrs::Error.
 //
 // Also the systematic pair (codec.hpp:56-65 of the reference), through
-// fntrs_gpu_encode_systematic / fntrs_gpu_decode_systematic. Not in this
-// header: the quadratic "direct" encoder variants (encode_systematic_direct,
-// encode_systematic_intermediate_direct), CPU cross-checks in the reference.
+// fntrs_gpu_encode_systematic / fntrs_gpu_decode_systematic, and the
+// reference's quadratic cross-check names (same values, GPU transform path).
 #pragma once
 
 #include <cstdint>
@@ -66,6 +65,15 @@ std::vector<Fe> encode_systematic(const CodeParams& params, std::span<const Fe> 
 // (the k lowest positions are used). Same exceptions as decode_nonsystematic.
 std::vector<Fe> decode_systematic(const CodeParams& params, const Codeword& received,
                                   Path path = Path::Auto);
+
+// The reference's quadratic cross-check entry points (codec.hpp:66-75 there).
+// They return exactly the values of their transform counterparts, which is
+// what the GPU computes them with; the instrumentation (instrument.hpp)
+// therefore records the transforms of that path, not the reference's
+// "one transform" for encode_systematic_intermediate_direct.
+std::vector<Fe> encode_systematic_direct(const CodeParams& params, std::span<const Fe> source);
+std::vector<Fe> encode_systematic_intermediate_direct(const CodeParams& params, std::span<const Fe> source);
+std::vector<Fe> decode_direct(const CodeParams& params, const Codeword& received);
 
 }  // namespace fntrs::codec
 

@@ -354,6 +354,19 @@ std::vector<Fe> encode_systematic(const CodeParams& params, std::span<const Fe> 
     return encode_one(params, source, true);
 }
 
+std::vector<Fe> encode_systematic_direct(const CodeParams& params, std::span<const Fe> source) {
+    return encode_one(params, source, true);
+}
+
+std::vector<Fe> encode_systematic_intermediate_direct(const CodeParams& params, std::span<const Fe> source) {
+    return encode_one(params, source, true);
+}
+
+std::vector<Fe> decode_direct(const CodeParams& params, const Codeword& received) {  // codec.cpp:255-258
+    return params.systematic ? decode_systematic(params, received, Path::Direct)
+                             : decode_nonsystematic(params, received, Path::Direct);
+}
+
 std::vector<Fe> decode_systematic(const CodeParams& params, const Codeword& received, Path) {
     // interpolate the k lowest, evaluate at 0..k-1; when those are 0..k-1 the
     // result is the received values themselves (systematic_prefix_present,

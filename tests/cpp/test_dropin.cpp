@@ -175,6 +175,24 @@ int main() {
             }
         }
     }
+    // all systematic encoder variants agree (test_codec.cpp:138-154)
+    {
+        std::mt19937 rng(7);
+        for (int trial = 0; trial < 20; ++trial) {
+            uint32_t k = std::uniform_int_distribution<uint32_t>(1, 64)(rng);
+            uint32_t n = std::uniform_int_distribution<uint32_t>(k, 150)(rng);
+            auto params = CodeParams::make(k, n);
+            auto src = random_source(k, 200 + trial);
+            auto fast = encode_systematic(params, src, Path::Fast);
+            CHECK(encode_systematic_direct(params, src) == fast);
+            CHECK(encode_systematic_intermediate_direct(params, src) == fast);
+            CHECK(encode_systematic(params, src, Path::Auto) == fast);
+            auto enc = encode_nonsystematic(CodeParams::make(k, n, false), src);
+            Codeword rx;
+            for (uint32_t i = n - k; i < n; ++i) rx.push_back({i, enc[i]});
+            CHECK(decode_direct(CodeParams::make(k, n, false), rx) == src);
+        }
+    }
     // systematic encode frozen examples (test_codec.cpp:126-136)
     {
         CHECK(encode_systematic(CodeParams::make(2, 4), std::vector<Fe>{5, 7}) ==
