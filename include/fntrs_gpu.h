@@ -171,7 +171,9 @@ int fntrs_gpu_be_to_words(fntrs_ctx* ctx, const uint8_t* in, uint64_t pitch, uin
                           uint32_t L, uint16_t* rows, void* stream);
 
 /* fnt_forward / fnt_inverse (proj/src/transform.cpp:302-323) over the columns
- * of a DEVICE [m][L] uint32 array of canonical values; natural order. */
+ * of a DEVICE [m][L] uint32 array of canonical values; natural order.
+ * inverse: 0 forward, 1 inverse (times 1/m), 2 inverse without the 1/m factor
+ * (dit_inverse_unscaled's arithmetic, transform.hpp:43-48, in natural order). */
 int fntrs_gpu_fnt(fntrs_ctx* ctx, uint32_t m, int inverse, uint32_t L, const uint32_t* in,
                   uint32_t* out, void* stream);
 

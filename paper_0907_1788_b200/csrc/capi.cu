@@ -848,13 +848,13 @@ int fntrs_gpu_fnt(fntrs_ctx* ctx, uint32_t m, int inverse, uint32_t L, const uin
         Scratch sc;
         int rc = get_scratch(ctx, sc, size_t(m) * L * 4 + 256, 1, st);
         if (rc) return rc;
-        cudaError_t le = fast::launch_fnt_cols(ctx->ftab, m, inverse != 0, L, in, sc.p[0], out, st);
+        cudaError_t le = fast::launch_fnt_cols(ctx->ftab, m, inverse != 0, L, in, sc.p[0], out, st, inverse == 2);
         release_scratch(sc, st);
         CK(le, "fnt launch");
         ctx->launches += 2;
         return FNTRS_OK;
     }
-    const uint32_t scale = inverse ? cpow(m % kP, kP - 2) : 1u;
+    const uint32_t scale = inverse == 1 ? cpow(m % kP, kP - 2) : 1u;  // 2: unscaled inverse
     CK(launch_fnt_tile(ctx->tab, m, inverse != 0, scale, L, in, out, static_cast<cudaStream_t>(stream)), "fnt launch");
     ctx->launches += 1;
     return FNTRS_OK;

@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
+#include <cstring>
 #include <list>
 #include <memory>
 #include <mutex>
@@ -16,6 +18,8 @@
 
 #include "fntrs/codec.hpp"
 #include "fntrs/instrument.hpp"
+#include "fntrs/interp.hpp"
+#include "fntrs/transform.hpp"
 #include "fntrs_gpu.h"
 
 namespace fntrs {
@@ -387,4 +391,175 @@ std::vector<Fe> decode_systematic(const CodeParams& params, const Codeword& rece
 }
 
 }  // namespace codec
+
+// ---- transform API (transform.hpp) ---------------------------------------
+namespace {
+bool pow2_domain(uint32_t n) { return n >= 1 && n <= 65536 && (n & (n - 1)) == 0; }
+
+uint32_t bitrev(uint32_t i, uint32_t n) {
+    uint32_t r = 0;
+    for (uint32_t b = 1; b < n; b <<= 1, i >>= 1) r = (r << 1) | (i & 1u);
+    return r;
+}
+
+// one vector through fntrs_gpu_fnt (mode 0 forward, 1 inverse, 2 unscaled inverse)
+std::vector<Fe> fnt_device(uint32_t n, const Fe* in, int mode) {
+    Shared& S = shared();
+    std::lock_guard<std::mutex> lock(S.mu);
+    S.ensure();
+    const size_t bytes = (size_t(n) * 4 + 255) / 256 * 256;
+    auto* d = static_cast<uint32_t*>(S.scratch(2 * bytes));
+    cudaMemcpyAsync(d, in, size_t(n) * 4, cudaMemcpyHostToDevice, S.stream);
+    S.check(fntrs_gpu_fnt(S.ctx, n, mode, 1, d, d + bytes / 4, S.stream));
+    std::vector<Fe> out(n);
+    cudaMemcpyAsync(out.data(), d + bytes / 4, size_t(n) * 4, cudaMemcpyDeviceToHost, S.stream);
+    S.sync();
+    note_fnt_execution(n);
+    return out;
+}
+}  // namespace
+
+TransformPlan::TransformPlan(std::uint32_t n) : size(n) {
+    if (!pow2_domain(n)) throw InvalidTransformSize("transform size must be a power of two in [1, 65536], got " +
+                                                    std::to_string(n));
+    root = gf::root_of_unity(n);
+    inverse_root = gf::root_of_unity(n, true);
+    size_inverse = gf::inv(n % gf::prime);
+}
+
+const TransformPlan& plan_for(std::uint32_t n) {
+    static std::mutex mu;
+    static std::array<std::unique_ptr<TransformPlan>, 17> plans;
+    if (!pow2_domain(n)) throw InvalidTransformSize("transform size must be a power of two in [1, 65536], got " +
+                                                    std::to_string(n));
+    uint32_t lg = 0;
+    while ((1u << lg) < n) ++lg;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!plans[lg]) plans[lg] = std::make_unique<TransformPlan>(n);
+    return *plans[lg];
+}
+
+std::vector<Fe> fnt_forward(const TransformPlan& plan, std::span<const Fe> a) {
+    if (a.size() != plan.size) throw SizeMismatch("transform input has " + std::to_string(a.size()) +
+                                                  " values for size " + std::to_string(plan.size));
+    return fnt_device(plan.size, a.data(), 0);
+}
+
+std::vector<Fe> fnt_inverse(const TransformPlan& plan, std::span<const Fe> a) {
+    if (a.size() != plan.size) throw SizeMismatch("transform input has " + std::to_string(a.size()) +
+                                                  " values for size " + std::to_string(plan.size));
+    return fnt_device(plan.size, a.data(), 1);
+}
+
+void dif_forward(const TransformPlan& plan, std::span<Fe> data) {
+    if (data.size() != plan.size) throw SizeMismatch("transform input length mismatch");
+    auto y = fnt_device(plan.size, data.data(), 0);  // natural order
+    for (uint32_t i = 0; i < plan.size; ++i) data[i] = y[bitrev(i, plan.size)];
+}
+
+void dit_inverse_unscaled(const TransformPlan& plan, std::span<Fe> data) {
+    if (data.size() != plan.size) throw SizeMismatch("transform input length mismatch");
+    std::vector<Fe> x(plan.size);
+    for (uint32_t i = 0; i < plan.size; ++i) x[bitrev(i, plan.size)] = data[i];  // to natural order
+    auto y = fnt_device(plan.size, x.data(), 2);
+    std::copy(y.begin(), y.end(), data.begin());
+}
+
+// ---- plan-level API (interp.hpp) ------------------------------------------
+namespace interp {
+
+DecodePlan build_plan(std::uint32_t n, std::span<const std::uint32_t> positions) {  // interp.cpp:23-68 checks
+    if (positions.empty()) throw TooFewPositions("no positions to build a plan from");
+    if (!pow2_domain(n)) throw InvalidTransformSize("plan domain must be a power of two in [1, 65536]");
+    for (uint32_t z : positions)
+        if (z >= n)
+            throw PositionOutOfRange("position " + std::to_string(z) + " not below domain size " + std::to_string(n));
+    {
+        std::vector<uint32_t> sorted(positions.begin(), positions.end());
+        std::sort(sorted.begin(), sorted.end());
+        auto dup = std::adjacent_find(sorted.begin(), sorted.end());
+        if (dup != sorted.end()) throw DuplicatePosition("position " + std::to_string(*dup) + " repeats");
+    }
+    const uint32_t k = uint32_t(positions.size());
+    DecodePlan plan;
+    plan.n = n;
+    plan.k = k;
+    plan.positions.assign(positions.begin(), positions.end());
+    Shared& S = shared();
+    std::lock_guard<std::mutex> lock(S.mu);
+    S.ensure();
+    fntrs_plans* pl = nullptr;
+    S.check(fntrs_gpu_plans_create(S.ctx, k, n, k, 1, plan.positions.data(), &pl, S.stream));
+    plan.device = std::shared_ptr<const void>(pl, [](const void* p) {
+        fntrs_gpu_plans_destroy(static_cast<fntrs_plans*>(const_cast<void*>(p)));
+    });
+    const uint32_t m = 2ull * k > 65536ull ? 65536u : next_pow2(2 * k);
+    plan.a_coeffs.assign(k + 1, 0);
+    plan.aprime_at_x_inv.assign(k, 0);
+    std::vector<Fe> afnt(m);
+    uint32_t ps = 0;
+    S.sync();
+    S.check(fntrs_gpu_plans_export(S.ctx, pl, 0, plan.a_coeffs.data(), plan.aprime_at_x_inv.data(), &ps, afnt.data()));
+    plan.product_size = ps;
+    afnt.resize(ps);
+    plan.a_fnt = std::move(afnt);
+    return plan;
+}
+
+std::shared_ptr<const DecodePlan> plan_for(std::uint32_t n, std::span<const std::uint32_t> positions) {
+    static std::mutex mu;  // interp.cpp:70-101: LRU of 16, canonical ascending positions
+    static std::list<std::pair<std::vector<uint32_t>, std::shared_ptr<const DecodePlan>>> lru;
+    std::vector<uint32_t> key(positions.begin(), positions.end());
+    std::sort(key.begin(), key.end());
+    key.push_back(n);
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        for (auto it = lru.begin(); it != lru.end(); ++it)
+            if (it->first == key) {
+                lru.splice(lru.begin(), lru, it);
+                return lru.front().second;
+            }
+    }
+    auto plan = std::make_shared<const DecodePlan>(build_plan(n, std::span<const uint32_t>(key.data(), key.size() - 1)));
+    std::lock_guard<std::mutex> lock(mu);
+    lru.emplace_front(key, plan);
+    if (lru.size() > 16) lru.pop_back();
+    return plan;
+}
+
+poly::Poly interpolate(const DecodePlan& plan, std::span<const Fe> values) {
+    if (values.size() != plan.k)
+        throw SizeMismatch("interpolate: got " + std::to_string(values.size()) + " values for " +
+                           std::to_string(plan.k) + " positions");
+    auto* pl = static_cast<fntrs_plans*>(const_cast<void*>(plan.device.get()));
+    if (!pl) throw Error("interpolate: plan has no device state");
+    Shared& S = shared();
+    std::lock_guard<std::mutex> lock(S.mu);
+    S.ensure();
+    std::vector<uint16_t> words;
+    std::vector<uint64_t> esc;
+    split(values.data(), values.size(), words, esc);
+    uint32_t* d_sp = nullptr;
+    if (cudaMalloc(&d_sp, 4) != cudaSuccess) throw Error("fntrs: device allocation failed");
+    cudaMemsetAsync(d_sp, 0, 4, S.stream);
+    poly::Poly p;
+    try {
+        p = run(S, words, esc, plan.k,
+                [&](const uint16_t* din, const uint64_t* die, uint64_t nie, uint16_t* dout, uint64_t* doe,
+                    uint64_t cap, uint64_t* dcnt) {
+                    S.check(fntrs_gpu_decode(S.ctx, pl, 1, 1, d_sp, din, die, nie, dout, doe, cap, dcnt, S.stream));
+                });
+    } catch (...) {
+        cudaFree(d_sp);
+        throw;
+    }
+    cudaFree(d_sp);
+    const uint32_t m = plan.product_size ? plan.product_size : 65536u;
+    note_fnt_execution(plan.n);
+    for (int i = 0; i < (plan.product_size ? 2 : 4); ++i) note_fnt_execution(m);
+    while (!p.empty() && p.back() == 0) p.pop_back();  // poly::normalize
+    return p;
+}
+
+}  // namespace interp
 }  // namespace fntrs

@@ -144,7 +144,7 @@ cudaError_t launch_plan_fast(const FastTables& t, const Tables& tab, const LogTa
                              uint32_t* ahat, uint2* rowmap, uint2* ahat2, cudaStream_t st);
 // natural-order column transforms [N][C] of any N <= 65536 (scratch N*C words when N >= 8192)
 cudaError_t launch_fnt_cols(const FastTables& t, uint32_t N, bool inverse, uint32_t C, const uint32_t* in,
-                            uint32_t* scratch, uint32_t* out, cudaStream_t st);
+                            uint32_t* scratch, uint32_t* out, cudaStream_t st, bool unscaled = false);
 
 // ---- fused decode for M != N (codec_gen.cu): 32 <= N <= 4096, M <= 4096
 struct GenPlanView {

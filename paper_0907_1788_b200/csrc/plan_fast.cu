@@ -194,8 +194,8 @@ cudaError_t launch_plan_fast(const FastTables& t, const Tables& tab, const LogTa
 }
 
 cudaError_t launch_fnt_cols(const FastTables& t, uint32_t N, bool inverse, uint32_t C, const uint32_t* in,
-                            uint32_t* scratch, uint32_t* out, cudaStream_t st) {
-    const uint32_t scale = inverse ? cpow(N % kP, kP - 2) : 1u;
+                            uint32_t* scratch, uint32_t* out, cudaStream_t st, bool unscaled) {
+    const uint32_t scale = inverse && !unscaled ? cpow(N % kP, kP - 2) : 1u;
     LdPlain ld{in, C};
     return inverse ? run_cols<true>(t, N, ld, C, scale, scratch, out, st)
                    : run_cols<false>(t, N, ld, C, scale, scratch, out, st);

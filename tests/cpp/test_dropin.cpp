@@ -12,6 +12,8 @@
 
 #include "fntrs/codec.hpp"
 #include "fntrs/instrument.hpp"
+#include "fntrs/interp.hpp"
+#include "fntrs/transform.hpp"
 
 using namespace fntrs;
 using namespace fntrs::codec;
@@ -281,6 +283,50 @@ int main() {
             encode_nonsystematic(non, src);
         }
         CHECK(outer.count(4096) == 2 && inner.count(4096) == 1 && inner.total() == 1);
+    }
+    // transform API golden values (test_transform.cpp:28-71)
+    {
+        CHECK(fnt_forward(plan_for(2), std::vector<Fe>{1, 2}) == (std::vector<Fe>{3, 65536}));
+        CHECK(fnt_forward(plan_for(4), std::vector<Fe>{9, 0, 0, 0}) == (std::vector<Fe>{9, 9, 9, 9}));
+        CHECK(fnt_forward(plan_for(4), std::vector<Fe>{0, 1, 0, 0}) == (std::vector<Fe>{1, 65281, 65536, 256}));
+        std::vector<Fe> x{1, 2, 3, 4, 5, 6, 7, 8};
+        std::vector<Fe> want{36, 50109, 1020, 48061, 65533, 17468, 64509, 15420};
+        CHECK(fnt_forward(plan_for(8), x) == want);
+        CHECK(fnt_inverse(plan_for(8), want) == x);
+        CHECK(throws_as<InvalidTransformSize>([] { plan_for(3); }));
+        CHECK(throws_as<SizeMismatch>([] { fnt_forward(plan_for(8), std::vector<Fe>{1, 2}); }));
+        // dif_forward / dit_inverse_unscaled compose into a cyclic convolution (transform.hpp:43-48)
+        const uint32_t n = 64;
+        auto a = random_source(n, 5), b = random_source(n, 6);
+        std::vector<Fe> want_c(n, 0);
+        for (uint32_t i = 0; i < n; ++i)
+            for (uint32_t j = 0; j < n; ++j) want_c[(i + j) % n] = gf::add(want_c[(i + j) % n], gf::mul(a[i], b[j]));
+        const auto& tp = plan_for(n);
+        dif_forward(tp, a);
+        dif_forward(tp, b);
+        for (uint32_t i = 0; i < n; ++i) a[i] = gf::mul(gf::mul(a[i], b[i]), tp.size_inverse);
+        dit_inverse_unscaled(tp, a);
+        CHECK(a == want_c);
+        CHECK(tp.root == gf::root_of_unity(n) && gf::mul(tp.root, tp.inverse_root) == 1);
+    }
+    // plan-level API golden values (test_interp.cpp:41-100)
+    {
+        using namespace fntrs::interp;
+        std::vector<uint32_t> pos{0, 2, 5};
+        DecodePlan plan = build_plan(8, pos);
+        CHECK(plan.a() == (poly::Poly{16, 61169, 4351, 1}));
+        CHECK(plan.aprime_at_x_inv == (std::vector<Fe>{gf::inv(4337), gf::inv(61712), gf::inv(3600)}));
+        CHECK(plan.product_size == 8 && plan.a_fnt.size() == 8);
+        CHECK(interpolate(plan, std::vector<Fe>{1000, 2000, 3000}) == (poly::Poly{46905, 62038, 23131}));
+        CHECK(interpolate(build_plan(8, std::vector<uint32_t>{3}), std::vector<Fe>{321}) == poly::Poly{321});
+        CHECK(interpolate(build_plan(4, std::vector<uint32_t>{0, 2}), std::vector<Fe>{12, 65535}) == (poly::Poly{5, 7}));
+        auto cached = plan_for(8, std::vector<uint32_t>{5, 0, 2});
+        CHECK(cached->positions == pos && plan_for(8, std::vector<uint32_t>{2, 5, 0}) == cached);
+        CHECK(throws_as<TooFewPositions>([] { build_plan(8, std::vector<uint32_t>{}); }));
+        CHECK(throws_as<PositionOutOfRange>([] { build_plan(8, std::vector<uint32_t>{1, 8}); }));
+        CHECK(throws_as<DuplicatePosition>([] { build_plan(8, std::vector<uint32_t>{1, 1}); }));
+        CHECK(throws_as<InvalidTransformSize>([] { build_plan(12, std::vector<uint32_t>{1}); }));
+        CHECK(throws_as<SizeMismatch>([&] { interpolate(plan, std::vector<Fe>{1}); }));
     }
     std::printf("drop-in C++ API: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail ? 1 : 0;
