@@ -95,6 +95,7 @@ struct Shared {
     // device scratch
     void* dbuf = nullptr;
     size_t dbuf_bytes = 0;
+    uint32_t* zero_pattern = nullptr;  // stripe_pattern of a one-stripe call: {0}
     // plan LRU (interp.cpp:70-101): key (n, k, kp, positions)
     using Key = std::pair<std::vector<uint32_t>, std::vector<uint32_t>>;
     std::list<std::pair<Key, fntrs_plans*>> lru;
@@ -103,6 +104,7 @@ struct Shared {
     ~Shared() {
         for (auto& e : lru) fntrs_gpu_plans_destroy(e.second);
         if (dbuf) cudaFree(dbuf);
+        if (zero_pattern) cudaFree(zero_pattern);
         if (stream) cudaStreamDestroy(stream);
         if (ctx) fntrs_gpu_destroy(ctx);
     }
@@ -123,6 +125,8 @@ struct Shared {
         cudaSetDevice(device);
         if (cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking) != cudaSuccess)
             throw Error("fntrs: cannot create a CUDA stream");
+        if (cudaMalloc(&zero_pattern, 4) != cudaSuccess || cudaMemset(zero_pattern, 0, 4) != cudaSuccess)
+            throw Error("fntrs: device allocation failed");
     }
 
     void* scratch(size_t bytes) {
@@ -226,6 +230,8 @@ void set_device(int device) {
         if (S.dbuf) cudaFree(S.dbuf);
         S.dbuf = nullptr;
         S.dbuf_bytes = 0;
+        if (S.zero_pattern) cudaFree(S.zero_pattern);
+        S.zero_pattern = nullptr;
         if (S.stream) cudaStreamDestroy(S.stream);
         S.stream = nullptr;
         fntrs_gpu_destroy(S.ctx);
@@ -322,22 +328,13 @@ std::vector<Fe> decode_one(const CodeParams& params, const Codeword& sorted, uin
     std::vector<uint16_t> words;
     std::vector<uint64_t> esc;
     split(vals.data(), vals.size(), words, esc);
-    uint32_t* d_sp = nullptr;  // stripe_pattern: a single zero
-    if (cudaMalloc(&d_sp, 4) != cudaSuccess) throw Error("fntrs: device allocation failed");
-    cudaMemsetAsync(d_sp, 0, 4, S.stream);
     auto fn = systematic ? fntrs_gpu_decode_systematic : fntrs_gpu_decode;
-    std::vector<Fe> out;
-    try {
-        out = run(S, words, esc, params.k,
-                  [&](const uint16_t* din, const uint64_t* die, uint64_t nie, uint16_t* dout, uint64_t* doe,
-                      uint64_t cap, uint64_t* dcnt) {
-                      S.check(fn(S.ctx, plan, 1, 1, d_sp, din, die, nie, dout, doe, cap, dcnt, S.stream));
-                  });
-    } catch (...) {
-        cudaFree(d_sp);
-        throw;
-    }
-    cudaFree(d_sp);
+    std::vector<Fe> out = run(S, words, esc, params.k,
+                              [&](const uint16_t* din, const uint64_t* die, uint64_t nie, uint16_t* dout,
+                                  uint64_t* doe, uint64_t cap, uint64_t* dcnt) {
+                                  S.check(fn(S.ctx, plan, 1, 1, S.zero_pattern, din, die, nie, dout, doe, cap, dcnt,
+                                             S.stream));
+                              });
     note_decode(params, kp);
     if (systematic) note_fnt_execution(next_pow2(params.n));
     return out;
@@ -539,21 +536,12 @@ poly::Poly interpolate(const DecodePlan& plan, std::span<const Fe> values) {
     std::vector<uint16_t> words;
     std::vector<uint64_t> esc;
     split(values.data(), values.size(), words, esc);
-    uint32_t* d_sp = nullptr;
-    if (cudaMalloc(&d_sp, 4) != cudaSuccess) throw Error("fntrs: device allocation failed");
-    cudaMemsetAsync(d_sp, 0, 4, S.stream);
-    poly::Poly p;
-    try {
-        p = run(S, words, esc, plan.k,
-                [&](const uint16_t* din, const uint64_t* die, uint64_t nie, uint16_t* dout, uint64_t* doe,
-                    uint64_t cap, uint64_t* dcnt) {
-                    S.check(fntrs_gpu_decode(S.ctx, pl, 1, 1, d_sp, din, die, nie, dout, doe, cap, dcnt, S.stream));
-                });
-    } catch (...) {
-        cudaFree(d_sp);
-        throw;
-    }
-    cudaFree(d_sp);
+    poly::Poly p = run(S, words, esc, plan.k,
+                       [&](const uint16_t* din, const uint64_t* die, uint64_t nie, uint16_t* dout, uint64_t* doe,
+                           uint64_t cap, uint64_t* dcnt) {
+                           S.check(fntrs_gpu_decode(S.ctx, pl, 1, 1, S.zero_pattern, din, die, nie, dout, doe, cap,
+                                                    dcnt, S.stream));
+                       });
     const uint32_t m = plan.product_size ? plan.product_size : 65536u;
     note_fnt_execution(plan.n);
     for (int i = 0; i < (plan.product_size ? 2 : 4); ++i) note_fnt_execution(m);
