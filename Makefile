@@ -40,9 +40,9 @@ oracle:
 
 # C++ drop-in API test program (links the library; runs on a GPU box).
 cpptest: $(BUILD)/test_dropin
-$(BUILD)/test_dropin: tests/cpp/test_dropin.cpp $(LIB) include/fntrs/codec.hpp
+$(BUILD)/test_dropin: tests/cpp/test_dropin.cpp $(LIB) $(wildcard include/fntrs/*.hpp)
 	@mkdir -p $(BUILD)
-	$(CXX) -O2 -std=c++20 -Wall -Iinclude -o $@ tests/cpp/test_dropin.cpp -L$(PKG) -lfntrs_b200 -Wl,-rpath,'$$ORIGIN/../$(PKG)'
+	$(CXX) -O2 -std=c++20 -Wall -pthread -Iinclude -o $@ tests/cpp/test_dropin.cpp -L$(PKG) -lfntrs_b200 -Wl,-rpath,'$$ORIGIN/../$(PKG)'
 
 clean:
 	rm -rf $(BUILD) $(LIB)

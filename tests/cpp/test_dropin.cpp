@@ -8,6 +8,8 @@
 #include <cstdio>
 #include <functional>
 #include <random>
+#include <atomic>
+#include <thread>
 #include <vector>
 
 #include "fntrs/codec.hpp"
@@ -327,6 +329,32 @@ int main() {
         CHECK(throws_as<DuplicatePosition>([] { build_plan(8, std::vector<uint32_t>{1, 1}); }));
         CHECK(throws_as<InvalidTransformSize>([] { build_plan(12, std::vector<uint32_t>{1}); }));
         CHECK(throws_as<SizeMismatch>([&] { interpolate(plan, std::vector<Fe>{1}); }));
+    }
+    // concurrent callers (test_transform.cpp:173-186): threads share the library
+    // and get correct results; FntScope counts stay per thread
+    {
+        std::atomic<int> bad{0};
+        std::vector<std::thread> pool;
+        for (int t = 0; t < 4; ++t)
+            pool.emplace_back([t, &bad] {
+                const uint32_t k = 16u << t, n = 2 * k;
+                auto p = CodeParams::make(k, n, t % 2 == 0);
+                FntCounter counter;
+                FntScope scope(counter);
+                for (int r = 0; r < 10; ++r) {
+                    auto src = random_source(k, 1000 * t + r);
+                    auto enc = t % 2 == 0 ? encode_systematic(p, src) : encode_nonsystematic(p, src);
+                    Codeword rx;
+                    for (uint32_t i = r % 2; i < n; i += 2) rx.push_back({i, enc[i]});
+                    auto dec = t % 2 == 0 ? decode_systematic(p, rx) : decode_nonsystematic(p, rx);
+                    if (dec != src) ++bad;
+                }
+                // 10 encodes + 10 decodes on this thread only
+                const uint64_t want = t % 2 == 0 ? 10 * 4 + 10 * 4 : 10 * 1 + 10 * 3;
+                if (counter.total() != want) ++bad;
+            });
+        for (auto& th : pool) th.join();
+        CHECK(bad.load() == 0);
     }
     std::printf("drop-in C++ API: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail ? 1 : 0;
