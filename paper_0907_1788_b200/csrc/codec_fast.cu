@@ -26,6 +26,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cstring>
 #include <type_traits>
 
 #include "fft_pass.cuh"
@@ -44,15 +45,21 @@ namespace {
 template <int E>
 struct EncPick {
     static constexpr int CW = E <= 8 ? 2 : 1;
+    // output rows through shared memory + one TMA store per tile: C2 encode
+    // 711 -> 819 GB/s (per-symbol 2-byte stores were the bottleneck); not at N = 32 (-2 %)
+    static constexpr bool TS = E >= 6 && E <= 8;
     using G = typename std::conditional<(E <= 8), Geom<E, 64, 256, 2>, typename Pick<E>::G>::type;
 };
 
-template <int E, class G, bool HALFK, bool PUNCT, int CW>
+// TS: single input stage + the n output rows staged in shared memory and
+// written by one TMA tensor store per tile (instead of per-symbol stores).
+template <int E, class G, bool HALFK, bool PUNCT, int CW, bool TS = false>
 __global__ void __launch_bounds__(G::NT, G::MINB) enc_fast_kernel(const __grid_constant__ CUtensorMap src_map,
                                                          const uint2* __restrict__ ptabF, uint32_t k, uint32_t n,
                                                          uint32_t L, uint32_t tps, uint32_t tiles, uint32_t nbox,
                                                          uint32_t box_rows, EscIn esc_in, uint16_t* __restrict__ out,
-                                                         EscOut esc_out) {
+                                                         EscOut esc_out, const __grid_constant__ CUtensorMap out_map,
+                                                         uint32_t obox) {
     using S = Sched<E>;
     constexpr int N = 1 << E, WT = G::WT, P = S::P;
     constexpr int RL0 = S::rlog(0), R0 = 1 << RL0, RLZ = G::RLZ;
@@ -63,8 +70,12 @@ __global__ void __launch_bounds__(G::NT, G::MINB) enc_fast_kernel(const __grid_c
     uint16_t* stage0 = reinterpret_cast<uint16_t*>(smem_raw + size_t(N) * WT * 4);
     const uint32_t stage_elems = nbox * box_rows * WT;
     const uint32_t stage_bytes = stage_elems * 2;
+    // TS: [work | stage | out_s], out_s 128-byte aligned
+    uint16_t* out_s = reinterpret_cast<uint16_t*>(
+        smem_raw + ((size_t(N) * WT * 4 + size_t(stage_bytes) + 127) & ~size_t(127)));
     if (threadIdx.x == 0) {
         tma_prefetch_desc(&src_map);
+        if constexpr (TS) tma_prefetch_desc(&out_map);
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
         fence_mbar_init();
@@ -83,11 +94,11 @@ __global__ void __launch_bounds__(G::NT, G::MINB) enc_fast_kernel(const __grid_c
     if (threadIdx.x == 0 && tile < tiles) issue(tile, 0);
     const bool esc_any = esc_in.n != 0;
     for (uint32_t iter = 0; tile < tiles; ++iter, tile += gridDim.x) {
-        const int bsel = iter & 1;
+        const int bsel = TS ? 0 : (iter & 1);
         const uint32_t stripe = tile / tps;
         const uint32_t c0 = (tile - stripe * tps) * WT;
-        if (threadIdx.x == 0 && tile + gridDim.x < tiles) issue(tile + gridDim.x, bsel ^ 1);
-        mbar_wait(&bars[bsel], (iter >> 1) & 1);
+        if (!TS && threadIdx.x == 0 && tile + gridDim.x < tiles) issue(tile + gridDim.x, bsel ^ 1);
+        mbar_wait(&bars[bsel], TS ? (iter & 1) : ((iter >> 1) & 1));
         const uint16_t* st_in = stage0 + bsel * stage_elems;
         const unsigned long long key_in = uint64_t(stripe) * k * L + c0;
         const unsigned long long key_out = uint64_t(stripe) * n * L + c0;
@@ -113,7 +124,11 @@ __global__ void __launch_bounds__(G::NT, G::MINB) enc_fast_kernel(const __grid_c
         };
         auto st_out = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) -> uint32_t {
             const uint32_t f = perm_head<E>(b) + (uint32_t(s) << (E - RLZ));
-            if (!PUNCT || f < n) __stcs(outp + (f * L + col), uint16_t(y));
+            if constexpr (TS) {
+                out_s[f * WT + col] = uint16_t(y);  // rows >= n are outside the store box
+            } else {
+                if (!PUNCT || f < n) __stcs(outp + (f * L + col), uint16_t(y));
+            }
             return (!PUNCT || f < n) ? y >> 16 : 0u;  // canonical: bit 16 set iff y == 65536
         };
         auto flush_out = [&](uint32_t mask, uint32_t, uint32_t b, uint32_t col) {
@@ -125,14 +140,30 @@ __global__ void __launch_bounds__(G::NT, G::MINB) enc_fast_kernel(const __grid_c
         };
 
         pass_cw<CW, E, 0, false, false, kP64, kSmemCap, G>(pass_table(ptabF, S::llog(0)), ld_src, st_sm, fix_src);
+        if constexpr (TS) {
+            if (threadIdx.x == 0) bulk_wait_read();  // the previous tile's store has read out_s
+        }
         __syncthreads();
+        if constexpr (TS) {  // the stage is consumed: the next tile's packets stream in behind
+            if (threadIdx.x == 0 && tile + gridDim.x < tiles) issue(tile + gridDim.x, 0);
+        }
         if constexpr (P == 3) {
             pass_cw<CW, E, 1, false, false, kSmemCap, kSmemCap, G>(pass_table(ptabF, S::llog(1)), ld_sm, st_sm);
             __syncthreads();
         }
         pass_cw<CW, E, P - 1, false, false, kSmemCap, kCanon, G>(pass_table(ptabF, S::llog(P - 1)), ld_sm, st_out,
                                                                 NoFix(), flush_out);
+        if constexpr (TS) fence_proxy_async();  // generic writes of out_s before the async-proxy store
         __syncthreads();
+        if constexpr (TS) {
+            if (threadIdx.x == 0) {
+                for (uint32_t r0 = 0; r0 < n; r0 += obox) tma_store_3d(&out_map, out_s + r0 * WT, int(c0), int(r0), int(stripe));
+                bulk_commit();
+            }
+        }
+    }
+    if constexpr (TS) {
+        if (threadIdx.x == 0) bulk_wait_all();
     }
 }
 
@@ -502,6 +533,22 @@ cudaError_t make_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// 3-D map over packet-major uint16 stripes [stripes][rows][L], box [1][box_rows][wt]:
+// a box never crosses into the next stripe (rows beyond `rows` are clipped).
+cudaError_t make_map3(CUtensorMap* map, const void* base, uint64_t stripes, uint32_t rows, uint32_t L, uint32_t wt,
+                      uint32_t box_rows) {
+    EncodeTiledFn fn = encode_tiled();
+    if (!fn) return cudaErrorNotSupported;
+    const cuuint64_t dims[3] = {L, rows, stripes};
+    const cuuint64_t strides[2] = {cuuint64_t(L) * 2, cuuint64_t(L) * rows * 2};
+    const cuuint32_t box[3] = {wt, box_rows, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 struct LaunchShape {
     uint32_t tps, tiles, nbox, box_rows, grid;
     size_t smem;
@@ -534,16 +581,22 @@ cudaError_t launch_enc(const FastTables& t, uint32_t k, uint32_t n, uint32_t str
                        EscIn ein, uint16_t* out, EscOut eout, cudaStream_t st) {
     using G = typename EncPick<E>::G;
     constexpr int CW = EncPick<E>::CW;
+    constexpr bool TS = EncPick<E>::TS;
     const bool half = k == (1u << E) / 2, punct = n < (1u << E);
-    auto kern = half ? (punct ? enc_fast_kernel<E, G, true, true, CW> : enc_fast_kernel<E, G, true, false, CW>)
-                     : (punct ? enc_fast_kernel<E, G, false, true, CW> : enc_fast_kernel<E, G, false, false, CW>);
+    auto kern = half ? (punct ? enc_fast_kernel<E, G, true, true, CW, TS> : enc_fast_kernel<E, G, true, false, CW, TS>)
+                     : (punct ? enc_fast_kernel<E, G, false, true, CW, TS> : enc_fast_kernel<E, G, false, false, CW, TS>);
     LaunchShape sh;
-    cudaError_t err = shape_for(kern, E, G::WT, G::NT, k, stripes, L, sh);
+    const size_t out_stage = TS ? (size_t(2) << E) * G::WT + 128 : 0;
+    cudaError_t err = shape_for(kern, E, G::WT, G::NT, k, stripes, L, sh, out_stage, TS ? 1 : 2);
     if (err) return err;
     if (!sh.tiles) return cudaSuccess;
-    CUtensorMap map;
+    CUtensorMap map, omap;
+    std::memset(&omap, 0, sizeof(omap));
     if ((err = make_map(&map, src, uint64_t(stripes) * k, L, G::WT, sh.box_rows))) return err;
-    kern<<<sh.grid, G::NT, sh.smem, st>>>(map, t.ptab_fwd, k, n, L, sh.tps, sh.tiles, sh.nbox, sh.box_rows, ein, out, eout);
+    const uint32_t obox = n < 256 ? n : 256;
+    if (TS && (err = make_map3(&omap, out, stripes, n, L, G::WT, obox))) return err;
+    kern<<<sh.grid, G::NT, sh.smem, st>>>(map, t.ptab_fwd, k, n, L, sh.tps, sh.tiles, sh.nbox, sh.box_rows, ein, out, eout,
+                                          omap, obox);
     return cudaGetLastError();
 }
 
