@@ -47,7 +47,7 @@ struct EncPick {
     static constexpr int CW = E <= 8 ? 2 : 1;
     // output rows through shared memory + one TMA store per tile: C2 encode
     // 711 -> 819 GB/s (per-symbol 2-byte stores were the bottleneck); not at N = 32 (-2 %)
-    static constexpr bool TS = E >= 6 && E <= 8;
+    static constexpr bool TS = E >= 6;
     using G = typename std::conditional<(E <= 8), Geom<E, 64, 256, 2>, typename Pick<E>::G>::type;
 };
 
@@ -576,12 +576,11 @@ cudaError_t shape_for(K kernel, int E, int wt, int nt, uint32_t k, uint32_t stri
     return cudaSuccess;
 }
 
-template <int E>
-cudaError_t launch_enc(const FastTables& t, uint32_t k, uint32_t n, uint32_t stripes, uint32_t L, const uint16_t* src,
-                       EscIn ein, uint16_t* out, EscOut eout, cudaStream_t st) {
+template <int E, bool TS>
+cudaError_t launch_enc_as(const FastTables& t, uint32_t k, uint32_t n, uint32_t stripes, uint32_t L,
+                          const uint16_t* src, EscIn ein, uint16_t* out, EscOut eout, cudaStream_t st) {
     using G = typename EncPick<E>::G;
     constexpr int CW = EncPick<E>::CW;
-    constexpr bool TS = EncPick<E>::TS;
     const bool half = k == (1u << E) / 2, punct = n < (1u << E);
     auto kern = half ? (punct ? enc_fast_kernel<E, G, true, true, CW, TS> : enc_fast_kernel<E, G, true, false, CW, TS>)
                      : (punct ? enc_fast_kernel<E, G, false, true, CW, TS> : enc_fast_kernel<E, G, false, false, CW, TS>);
@@ -598,6 +597,23 @@ cudaError_t launch_enc(const FastTables& t, uint32_t k, uint32_t n, uint32_t str
     kern<<<sh.grid, G::NT, sh.smem, st>>>(map, t.ptab_fwd, k, n, L, sh.tps, sh.tiles, sh.nbox, sh.box_rows, ein, out, eout,
                                           omap, obox);
     return cudaGetLastError();
+}
+
+template <int E>
+cudaError_t launch_enc(const FastTables& t, uint32_t k, uint32_t n, uint32_t stripes, uint32_t L, const uint16_t* src,
+                       EscIn ein, uint16_t* out, EscOut eout, cudaStream_t st) {
+    using G = typename EncPick<E>::G;
+    if constexpr (EncPick<E>::TS) {
+        // staged output when tile + one input stage + the n-row output tile fit
+        const uint32_t box_rows = k < 256 ? k : 256, nbox = (k + box_rows - 1) / box_rows;
+        const size_t need = (size_t(1) << E) * G::WT * 4 + size_t(nbox) * box_rows * G::WT * 2 +
+                            (size_t(2) << E) * G::WT + 128;
+        int dev = 0, optin = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        if (need <= size_t(optin)) return launch_enc_as<E, true>(t, k, n, stripes, L, src, ein, out, eout, st);
+    }
+    return launch_enc_as<E, false>(t, k, n, stripes, L, src, ein, out, eout, st);
 }
 
 template <int E, int MODE = 0>
