@@ -17,9 +17,13 @@
 //   D3  FNT2 pass B + (. A_hat) + FNT3 pass A (both on the coset q2 mod N2)
 //   D4  FNT3 pass B, writing the k decoded packets.
 // Intermediates (uint32, < 2p) go through a stripe-batched HBM scratch.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cstring>
+
 #include "fft_pass.cuh"
+#include "tma.cuh"
 
 namespace fntrs_gpu {
 namespace fast {
@@ -89,10 +93,13 @@ enc_a_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, uin
     pass<E1, 1, false, false, kSmemCap, kSmemCap, G>(pass_table(ptab, S::llog(1)), ld_sm, st_y);
 }
 
-template <int E1, int E2, bool PUNCT>
-__global__ void __launch_bounds__(kLNT, LG<E2>::MINB)
+// TS (n == N): the CTA's N2 output rows m1 + N1 m2 are staged in shared memory
+// and written by one TMA store through the (L, m1, m2, stripe) view of `out`.
+template <int E1, int E2, bool PUNCT, bool TS = false>
+__global__ void __launch_bounds__(kLNT, (TS ? (E2 <= 7 ? 4 : 2) : LG<E2>::MINB))
 enc_b_kernel(const uint2* __restrict__ ptab, uint32_t n, uint32_t L, uint32_t tps, uint32_t stripe0,
-             const uint32_t* __restrict__ Y, uint16_t* __restrict__ out, EscOut esc_out) {
+             const uint32_t* __restrict__ Y, uint16_t* __restrict__ out, EscOut esc_out,
+             const __grid_constant__ CUtensorMap out_map) {
     using G = LG<E2>;
     using S = Sched<E2>;
     constexpr uint32_t N1 = 1u << E1, N2 = 1u << E2, N = N1 * N2;
@@ -110,10 +117,15 @@ enc_b_kernel(const uint2* __restrict__ ptab, uint32_t n, uint32_t L, uint32_t tp
         return 0u;
     };
     auto ld_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t { return work[G::idx(lrow, col)]; };
+    uint16_t* out_s = reinterpret_cast<uint16_t*>(work + N2 * kLW);  // TS staging: [m2][kLW]
     auto st_out = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) -> uint32_t {
-        const uint32_t row = m1 + N1 * (perm_head<E2>(b) + (uint32_t(s) << (E2 - RLZ)));
+        const uint32_t m2 = perm_head<E2>(b) + (uint32_t(s) << (E2 - RLZ));
+        const uint32_t row = m1 + N1 * m2;
         const bool keep = !PUNCT || row < n;
-        if (keep) __stcs(outp + (row * L + col), uint16_t(y));
+        if constexpr (TS)
+            out_s[m2 * kLW + col] = uint16_t(y);
+        else if (keep)
+            __stcs(outp + (row * L + col), uint16_t(y));
         return keep ? y >> 16 : 0u;  // canonical: bit 16 set iff y == 65536
     };
     auto flush = [&](uint32_t mask, uint32_t, uint32_t b, uint32_t col) {
@@ -127,6 +139,15 @@ enc_b_kernel(const uint2* __restrict__ ptab, uint32_t n, uint32_t L, uint32_t tp
     pass<E2, 0, false, false, k2P, kSmemCap, G>(pass_table(ptab, S::llog(0)), ld, st_sm);
     __syncthreads();
     pass<E2, 1, false, false, kSmemCap, kCanon, G>(pass_table(ptab, S::llog(1)), ld_sm, st_out, NoFix(), flush);
+    if constexpr (TS) {
+        fence_proxy_async();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            tma_store_4d(&out_map, out_s, int(bi.c0), int(m1), 0, int(stripe));
+            bulk_commit();
+            bulk_wait_read();  // the CTA's shared memory must outlive the store's reads
+        }
+    }
 }
 
 // ---------------------------------------------------------------- decode ----
@@ -347,6 +368,29 @@ dec_4_kernel(const uint2* __restrict__ ptabI, uint32_t k, uint32_t L, uint32_t t
     pass<E2, 1, true, false, kSmemCap, kCanon, G>(pass_table(ptabI, S::llog(1)), ld_sm, st_out, NoFix(), flush);
 }
 
+// (L, m1, m2, stripe) view of an unpunctured output [stripes][N1 N2][L]: row m1 + N1 m2
+cudaError_t make_rows_map(CUtensorMap* map, void* base, uint64_t stripes, uint32_t N1, uint32_t N2, uint32_t L) {
+    typedef CUresult (*Fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                           const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                           CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Fn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<Fn>(p);
+    }
+    if (!fn || N2 > 256) return cudaErrorNotSupported;
+    const cuuint64_t dims[4] = {L, N1, N2, stripes};
+    const cuuint64_t strides[3] = {cuuint64_t(L) * 2, cuuint64_t(L) * N1 * 2, cuuint64_t(L) * N1 * N2 * 2};
+    const cuuint32_t box[4] = {uint32_t(kLW), 1, N2, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 template <class K>
 cudaError_t prep(K kernel, size_t smem) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -360,13 +404,19 @@ cudaError_t run_encode(const FastTables& t, uint32_t k, uint32_t n, uint32_t str
     const size_t smA = size_t(N1) * kLW * 4, smB = size_t(N2) * kLW * 4;
     const bool half = k == N / 2, punct = n < N;
     auto ka = half ? enc_a_kernel<E1, E2, true> : enc_a_kernel<E1, E2, false>;
-    auto kb = punct ? enc_b_kernel<E1, E2, true> : enc_b_kernel<E1, E2, false>;
+    // unpunctured: staged rows + one TMA store per CTA through the (L, m1, m2, stripe) view
+    CUtensorMap omap;
+    std::memset(&omap, 0, sizeof(omap));
+    // (with 256-row halves the staging costs a CTA per SM: C3 encode 246 -> 229 GB/s, so not there)
+    const bool ts = !punct && E2 <= 7 && make_rows_map(&omap, out, stripes, N1, N2, L) == cudaSuccess;
+    auto kb = punct ? enc_b_kernel<E1, E2, true> : (ts ? enc_b_kernel<E1, E2, false, true> : enc_b_kernel<E1, E2, false>);
+    const size_t smBk = smB + (ts ? size_t(N2) * kLW * 2 : 0);
     cudaError_t err;
-    if ((err = prep(ka, smA)) || (err = prep(kb, smB))) return err;
+    if ((err = prep(ka, smA)) || (err = prep(kb, smBk))) return err;
     for (uint32_t s0 = 0; s0 < stripes; s0 += batch) {
         const uint32_t sb = stripes - s0 < batch ? stripes - s0 : batch;
         ka<<<sb * N2 * tps, kLNT, smA, st>>>(t.ptab_fwd, t.big_fwd, k, L, tps, s0, src, ein, Y);
-        kb<<<sb * N1 * tps, kLNT, smB, st>>>(t.ptab_fwd, n, L, tps, s0, Y, out, eout);
+        kb<<<sb * N1 * tps, kLNT, smBk, st>>>(t.ptab_fwd, n, L, tps, s0, Y, out, eout, omap);
     }
     return cudaGetLastError();
 }
