@@ -47,6 +47,22 @@ __device__ __forceinline__ BlockIdx block_index(uint32_t tps, uint32_t ng) {
     return {rest / ng, rest % ng, ct * kLW};
 }
 
+// The CTA's input block -- ROWS contiguous rows x kLW columns of a uint32
+// intermediate -- lands in the shared work tile with one TMA load (row-major,
+// the unswizzled 64-wide geometry), so the first pass reads shared memory.
+template <int ROWS>
+__device__ __forceinline__ void tile_in(uint32_t* work, const CUtensorMap* map, uint32_t c0, uint32_t row0,
+                                        uint64_t* bar) {
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+        mbar_expect_tx(bar, uint32_t(ROWS) * kLW * 4);
+        tma_load_2d(work, map, int(c0), int(row0), bar);
+    }
+    __syncthreads();
+    mbar_wait(bar, 0);
+}
+
 // ---------------------------------------------------------------- encode ----
 template <int E1, int E2, bool HALFK>
 __global__ void __launch_bounds__(kLNT, LG<E1>::MINB)
@@ -99,7 +115,7 @@ template <int E1, int E2, bool PUNCT, bool TS = false>
 __global__ void __launch_bounds__(kLNT, (TS ? (E2 <= 7 ? 4 : 2) : LG<E2>::MINB))
 enc_b_kernel(const uint2* __restrict__ ptab, uint32_t n, uint32_t L, uint32_t tps, uint32_t stripe0,
              const uint32_t* __restrict__ Y, uint16_t* __restrict__ out, EscOut esc_out,
-             const __grid_constant__ CUtensorMap out_map) {
+             const __grid_constant__ CUtensorMap out_map, const __grid_constant__ CUtensorMap in_map) {
     using G = LG<E2>;
     using S = Sched<E2>;
     constexpr uint32_t N1 = 1u << E1, N2 = 1u << E2, N = N1 * N2;
@@ -136,7 +152,10 @@ enc_b_kernel(const uint2* __restrict__ ptab, uint32_t n, uint32_t L, uint32_t tp
                 emit_escape(esc_out,
                             key_out + uint64_t(m1 + N1 * (perm_head<E2>(b) + (uint32_t(s) << (E2 - RLZ)))) * L + col);
     };
-    pass<E2, 0, false, false, k2P, kSmemCap, G>(pass_table(ptab, S::llog(0)), ld, st_sm);
+    __shared__ __align__(8) uint64_t bar;
+    tile_in<N2>(work, &in_map, bi.c0, bi.sb * N + m1 * N2, &bar);
+    (void)ld;
+    pass<E2, 0, false, false, k2P, kSmemCap, G>(pass_table(ptab, S::llog(0)), ld_sm, st_sm);
     __syncthreads();
     pass<E2, 1, false, false, kSmemCap, kCanon, G>(pass_table(ptab, S::llog(1)), ld_sm, st_out, NoFix(), flush);
     if constexpr (TS) {
@@ -208,7 +227,7 @@ dec_1_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, con
 template <int E1, int E2, bool HALFK>
 __global__ void __launch_bounds__(kLNT, LG<E2>::MINB)
 dec_2_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, uint32_t k, uint32_t L, uint32_t tps,
-             const uint32_t* __restrict__ Y1, uint32_t* __restrict__ Y2) {
+             const uint32_t* __restrict__ Y1, uint32_t* __restrict__ Y2, const __grid_constant__ CUtensorMap in_map) {
     using G = LG<E2>;
     using S = Sched<E2>;
     constexpr uint32_t N1 = 1u << E1, N2 = 1u << E2, N = N1 * N2;
@@ -234,8 +253,12 @@ dec_2_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, uin
         y2[(q2 * N1 + i1p) * L + col] = mulws(y, w.x, w.y);
         return 0u;
     };
-    // FNT1 pass B, first radix pass
-    pass<E2, 0, false, false, k2P, kSmemCap, G>(pass_table(ptab, S::llog(0)), ld, st_sm);
+    // FNT1 pass B, first radix pass (input block by TMA)
+    __shared__ __align__(8) uint64_t bar;
+    tile_in<N2>(work, &in_map, bi.c0, bi.sb * N + m1 * N2, &bar);
+    (void)ld;
+    auto ld_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t { return work[G::idx(lrow, col)]; };
+    pass<E2, 0, false, false, k2P, kSmemCap, G>(pass_table(ptab, S::llog(0)), ld_sm, st_sm);
     __syncthreads();
     // FNT1 pass B last radix pass + FNT2 pass A first DIT pass (reversed view over i2' = N2-1-m2,
     // s'_{i1' + N1 i2'} zeroed when i1' + N1 i2' >= k)
@@ -273,7 +296,8 @@ template <int E1, int E2>
 __global__ void __launch_bounds__(kLNT, LG<E1>::MINB)
 dec_3_kernel(const uint2* __restrict__ ptabF, const uint2* __restrict__ ptabI, const uint2* __restrict__ bigI,
              const uint2* __restrict__ ahat2, uint32_t L, uint32_t tps, uint32_t stripe0,
-             const uint32_t* __restrict__ stripe_pattern, const uint32_t* __restrict__ Y2, uint32_t* __restrict__ Y3) {
+             const uint32_t* __restrict__ stripe_pattern, const uint32_t* __restrict__ Y2, uint32_t* __restrict__ Y3,
+             const __grid_constant__ CUtensorMap in_map) {
     using G = LG<E1>;
     using S = Sched<E1>;
     constexpr uint32_t N1 = 1u << E1, N2 = 1u << E2, N = N1 * N2;
@@ -298,7 +322,10 @@ dec_3_kernel(const uint2* __restrict__ ptabF, const uint2* __restrict__ ptabI, c
         return 0u;
     };
     // FNT2 pass B, first radix pass
-    pass<E1, 0, false, false, k2P, kSmemCap, G>(pass_table(ptabF, S::llog(0)), ld, st_sm);
+    __shared__ __align__(8) uint64_t bar;
+    tile_in<N1>(work, &in_map, bi.c0, bi.sb * N + q2 * N1, &bar);
+    (void)ld;
+    pass<E1, 0, false, false, k2P, kSmemCap, G>(pass_table(ptabF, S::llog(0)), ld_sm, st_sm);
     __syncthreads();
     // FNT2 pass B last radix pass + (. ahat at q2 + N2 q1) + FNT3 pass A first DIT pass (inverse)
     {
@@ -332,7 +359,8 @@ dec_3_kernel(const uint2* __restrict__ ptabF, const uint2* __restrict__ ptabI, c
 template <int E1, int E2, bool HALFK>
 __global__ void __launch_bounds__(kLNT, LG<E2>::MINB)
 dec_4_kernel(const uint2* __restrict__ ptabI, uint32_t k, uint32_t L, uint32_t tps, uint32_t stripe0,
-             const uint32_t* __restrict__ Y3, uint16_t* __restrict__ out, EscOut esc_out) {
+             const uint32_t* __restrict__ Y3, uint16_t* __restrict__ out, EscOut esc_out,
+             const __grid_constant__ CUtensorMap in_map) {
     using G = LG<E2>;
     using S = Sched<E2>;
     constexpr uint32_t N1 = 1u << E1, N2 = 1u << E2, N = N1 * N2;
@@ -363,7 +391,10 @@ dec_4_kernel(const uint2* __restrict__ ptabI, uint32_t k, uint32_t L, uint32_t t
             if (mask & (1u << s))
                 emit_escape(esc_out, key + uint64_t(t1 + N1 * (perm_head<E2>(b) + (uint32_t(s) << (E2 - RLZ)))) * L + col);
     };
-    pass<E2, 0, true, false, k2P, kSmemCap, G>(pass_table(ptabI, S::llog(0)), ld, st_sm);
+    __shared__ __align__(8) uint64_t bar;
+    tile_in<N2>(work, &in_map, bi.c0, bi.sb * N + t1 * N2, &bar);
+    (void)ld;
+    pass<E2, 0, true, false, k2P, kSmemCap, G>(pass_table(ptabI, S::llog(0)), ld_sm, st_sm);
     __syncthreads();
     pass<E2, 1, true, false, kSmemCap, kCanon, G>(pass_table(ptabI, S::llog(1)), ld_sm, st_out, NoFix(), flush);
 }
@@ -391,6 +422,30 @@ cudaError_t make_rows_map(CUtensorMap* map, void* base, uint64_t stripes, uint32
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// 2-D map over a uint32 intermediate [rows][L], box [box_rows][kLW]
+cudaError_t make_u32_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t L, uint32_t box_rows) {
+    typedef CUresult (*Fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                           const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                           CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Fn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<Fn>(p);
+    }
+    if (!fn) return cudaErrorNotSupported;
+    const cuuint64_t dims[2] = {L, rows};
+    const cuuint64_t strides[1] = {cuuint64_t(L) * 4};
+    const cuuint32_t box[2] = {uint32_t(kLW), box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 template <class K>
 cudaError_t prep(K kernel, size_t smem) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -413,10 +468,12 @@ cudaError_t run_encode(const FastTables& t, uint32_t k, uint32_t n, uint32_t str
     const size_t smBk = smB + (ts ? size_t(N2) * kLW * 2 : 0);
     cudaError_t err;
     if ((err = prep(ka, smA)) || (err = prep(kb, smBk))) return err;
+    CUtensorMap ymap;  // kb's input blocks: N2 rows of Y
+    if ((err = make_u32_map(&ymap, Y, uint64_t(batch) * N, L, N2))) return err;
     for (uint32_t s0 = 0; s0 < stripes; s0 += batch) {
         const uint32_t sb = stripes - s0 < batch ? stripes - s0 : batch;
         ka<<<sb * N2 * tps, kLNT, smA, st>>>(t.ptab_fwd, t.big_fwd, k, L, tps, s0, src, ein, Y);
-        kb<<<sb * N1 * tps, kLNT, smBk, st>>>(t.ptab_fwd, n, L, tps, s0, Y, out, eout, omap);
+        kb<<<sb * N1 * tps, kLNT, smBk, st>>>(t.ptab_fwd, n, L, tps, s0, Y, out, eout, omap, ymap);
     }
     return cudaGetLastError();
 }
@@ -435,12 +492,15 @@ cudaError_t run_decode(const FastTables& t, const FastPlanView& pv, uint32_t str
     auto k4 = half ? dec_4_kernel<E1, E2, true> : dec_4_kernel<E1, E2, false>;
     cudaError_t err;
     if ((err = prep(k1, sm1)) || (err = prep(k2, sm2)) || (err = prep(k3, sm1)) || (err = prep(k4, sm2))) return err;
+    CUtensorMap mapA, mapB;  // input blocks: N2 rows of YA (k2, k4), N1 rows of YB (k3)
+    if ((err = make_u32_map(&mapA, YA, uint64_t(batch) * N, L, N2)) || (err = make_u32_map(&mapB, YB, uint64_t(batch) * N, L, N1)))
+        return err;
     for (uint32_t s0 = 0; s0 < stripes; s0 += batch) {
         const uint32_t sb = stripes - s0 < batch ? stripes - s0 : batch;
         k1<<<sb * N2 * tps, kLNT, sm1, st>>>(t.ptab_fwd, t.big_fwd, pv.rowmap, pv.k, L, tps, s0, sp, rx, ein, YA);
-        k2<<<sb * N1 * tps, kLNT, sm2, st>>>(t.ptab_fwd, t.big_fwd, pv.k, L, tps, YA, YB);
-        k3<<<sb * N2 * tps, kLNT, sm1, st>>>(t.ptab_fwd, t.ptab_inv, t.big_inv, pv.ahat2, L, tps, s0, sp, YB, YA);
-        k4<<<sb * N1 * tps, kLNT, sm2, st>>>(t.ptab_inv, pv.k, L, tps, s0, YA, out, eout);
+        k2<<<sb * N1 * tps, kLNT, sm2, st>>>(t.ptab_fwd, t.big_fwd, pv.k, L, tps, YA, YB, mapA);
+        k3<<<sb * N2 * tps, kLNT, sm1, st>>>(t.ptab_fwd, t.ptab_inv, t.big_inv, pv.ahat2, L, tps, s0, sp, YB, YA, mapB);
+        k4<<<sb * N1 * tps, kLNT, sm2, st>>>(t.ptab_inv, pv.k, L, tps, s0, YA, out, eout, mapA);
     }
     return cudaGetLastError();
 }
