@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(kLNT, LG<E1>::MINB)
 dec_3_kernel(const uint2* __restrict__ ptabF, const uint2* __restrict__ ptabI, const uint2* __restrict__ bigI,
              const uint2* __restrict__ ahat2, uint32_t L, uint32_t tps, uint32_t stripe0,
              const uint32_t* __restrict__ stripe_pattern, const uint32_t* __restrict__ Y2, uint32_t* __restrict__ Y3,
-             const __grid_constant__ CUtensorMap in_map) {
+             const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map) {
     using G = LG<E1>;
     using S = Sched<E1>;
     constexpr uint32_t N1 = 1u << E1, N2 = 1u << E2, N = N1 * N2;
@@ -352,8 +352,23 @@ dec_3_kernel(const uint2* __restrict__ ptabF, const uint2* __restrict__ ptabI, c
         }
     }
     __syncthreads();
-    // FNT3 pass A last DIT pass (inverse) -> natural t1, twiddle r_N^(-q2 t1)
-    pass<E1, 0, true, true, kSmemCap, kSmemCap, G>(pass_table(ptabI, S::llog(0)), ld_sm, st_y3);
+    // FNT3 pass A last DIT pass (inverse) -> natural t1, twiddle r_N^(-q2 t1). Each item writes
+    // back the rows it read, now in natural order: the tile becomes the output block
+    // (rows t1 N2 + q2 of Y3), stored with one TMA store through the (L, q2, t1) view.
+    (void)st_y3;
+    auto st_tile = [&](uint32_t t1, uint32_t, int, uint32_t col, uint32_t y) -> uint32_t {
+        const uint2 w = __ldg(bigI + N + ((q2 * t1) & (N - 1)));
+        work[G::idx(t1, col)] = mulws(y, w.x, w.y);
+        return 0u;
+    };
+    pass<E1, 0, true, true, kSmemCap, kSmemCap, G>(pass_table(ptabI, S::llog(0)), ld_sm, st_tile);
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        tma_store_3d(&out_map, work, int(bi.c0), int(q2), int(bi.sb * N1));
+        bulk_commit();
+        bulk_wait_read();
+    }
 }
 
 template <int E1, int E2, bool HALFK>
@@ -446,6 +461,31 @@ cudaError_t make_u32_map(CUtensorMap* map, const void* base, uint64_t rows, uint
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// (L, inner, outer) view of a uint32 intermediate [rows][L] with row = outer * n_inner + inner:
+// box {kLW, 1, box_outer} -- a strided set of rows
+cudaError_t make_u32_strided_map(CUtensorMap* map, void* base, uint64_t outer, uint32_t n_inner, uint32_t L,
+                                 uint32_t box_outer) {
+    typedef CUresult (*Fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                           const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                           CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Fn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<Fn>(p);
+    }
+    if (!fn) return cudaErrorNotSupported;
+    const cuuint64_t dims[3] = {L, n_inner, outer};
+    const cuuint64_t strides[2] = {cuuint64_t(L) * 4, cuuint64_t(L) * n_inner * 4};
+    const cuuint32_t box[3] = {uint32_t(kLW), 1, box_outer};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 template <class K>
 cudaError_t prep(K kernel, size_t smem) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -492,14 +532,16 @@ cudaError_t run_decode(const FastTables& t, const FastPlanView& pv, uint32_t str
     auto k4 = half ? dec_4_kernel<E1, E2, true> : dec_4_kernel<E1, E2, false>;
     cudaError_t err;
     if ((err = prep(k1, sm1)) || (err = prep(k2, sm2)) || (err = prep(k3, sm1)) || (err = prep(k4, sm2))) return err;
-    CUtensorMap mapA, mapB;  // input blocks: N2 rows of YA (k2, k4), N1 rows of YB (k3)
-    if ((err = make_u32_map(&mapA, YA, uint64_t(batch) * N, L, N2)) || (err = make_u32_map(&mapB, YB, uint64_t(batch) * N, L, N1)))
+    CUtensorMap mapA, mapB, map3;  // input blocks: N2 rows of YA (k2, k4), N1 rows of YB (k3); k3's output view
+    if ((err = make_u32_map(&mapA, YA, uint64_t(batch) * N, L, N2)) || (err = make_u32_map(&mapB, YB, uint64_t(batch) * N, L, N1)) ||
+        (err = make_u32_strided_map(&map3, YA, uint64_t(batch) * N1, N2, L, N1)))
         return err;
     for (uint32_t s0 = 0; s0 < stripes; s0 += batch) {
         const uint32_t sb = stripes - s0 < batch ? stripes - s0 : batch;
         k1<<<sb * N2 * tps, kLNT, sm1, st>>>(t.ptab_fwd, t.big_fwd, pv.rowmap, pv.k, L, tps, s0, sp, rx, ein, YA);
         k2<<<sb * N1 * tps, kLNT, sm2, st>>>(t.ptab_fwd, t.big_fwd, pv.k, L, tps, YA, YB, mapA);
-        k3<<<sb * N2 * tps, kLNT, sm1, st>>>(t.ptab_fwd, t.ptab_inv, t.big_inv, pv.ahat2, L, tps, s0, sp, YB, YA, mapB);
+        k3<<<sb * N2 * tps, kLNT, sm1, st>>>(t.ptab_fwd, t.ptab_inv, t.big_inv, pv.ahat2, L, tps, s0, sp, YB, YA, mapB,
+                                              map3);
         k4<<<sb * N1 * tps, kLNT, sm2, st>>>(t.ptab_inv, pv.k, L, tps, s0, YA, out, eout, mapA);
     }
     return cudaGetLastError();
