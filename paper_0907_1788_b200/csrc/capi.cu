@@ -95,15 +95,20 @@ int end_bit_for(uint64_t max_key) {
     return b;
 }
 
-// Small escape buffers: one CTA sorts all `cap` keys in shared memory (bitonic
-// network over the next power of two, padding with ~0) -- one launch instead
-// of the radix sort's several.
-constexpr uint32_t kSmallSort = 4096;
-__global__ void __launch_bounds__(1024) small_sort_kernel(unsigned long long* keys, uint32_t cap) {
-    __shared__ unsigned long long s[kSmallSort];
-    uint32_t m = 1;
-    while (m < cap) m <<= 1;
-    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) s[i] = i < cap ? keys[i] : ~0ull;
+// Small escape buffers: one CTA sorts them in shared memory (bitonic network).
+// The kernel reads the device-side escape count, so it sorts only the next
+// power of two above min(count, cap) -- past the count the buffer already
+// holds the ~0 fill -- in one launch instead of the radix sort's several.
+constexpr uint32_t kSmallSort = 16384;  // 128 KB of 64-bit keys
+__global__ void __launch_bounds__(1024) small_sort_kernel(unsigned long long* keys,
+                                                          const unsigned long long* count, uint32_t cap) {
+    extern __shared__ unsigned long long s[];
+    const unsigned long long c = *count;
+    const uint32_t live = c < cap ? uint32_t(c) : cap;
+    if (live <= 1) return;
+    uint32_t m = 2;
+    while (m < live) m <<= 1;
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) s[i] = i < live ? keys[i] : ~0ull;
     __syncthreads();
     for (uint32_t size = 2; size <= m; size <<= 1)
         for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
@@ -118,34 +123,42 @@ __global__ void __launch_bounds__(1024) small_sort_kernel(unsigned long long* ke
             }
             __syncthreads();
         }
-    for (uint32_t i = threadIdx.x; i < cap; i += blockDim.x) keys[i] = s[i];
+    for (uint32_t i = threadIdx.x; i < live; i += blockDim.x) keys[i] = s[i];
 }
 
 // Escape finalisation: keys[0..cap) were pre-filled with ~0 and partially
-// overwritten by the kernel's appends; sorting the whole buffer puts the
-// real indices first, ascending (the reference's per-shard order).
-int sort_escapes(fntrs_ctx* ctx, unsigned long long* keys, uint64_t cap, uint64_t max_key,
-                 cudaStream_t st) {
+// overwritten by the kernel's appends; sorting puts the real indices first,
+// ascending (the reference's per-shard order).
+int sort_escapes(fntrs_ctx* ctx, const EscOut& eout, uint64_t max_key, cudaStream_t st) {
+    const uint64_t cap = eout.cap;
+    unsigned long long* keys = eout.keys;
     if (cap <= 1) return FNTRS_OK;
     if (cap <= kSmallSort) {
-        small_sort_kernel<<<1, 1024, 0, st>>>(keys, uint32_t(cap));
+        uint32_t m = 2;
+        while (m < cap) m <<= 1;
+        const size_t smem = size_t(m) * sizeof(unsigned long long);
+        if (smem > 48 * 1024)
+            CK(cudaFuncSetAttribute(small_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+               "escape sort attribute");
+        small_sort_kernel<<<1, 1024, smem, st>>>(keys, eout.count, uint32_t(cap));
         CK(cudaGetLastError(), "escape sort");
         ctx->launches += 1;
         return FNTRS_OK;
     }
     if (cap > 0x7FFFFFFFull) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "escape capacity too large");
+    // Real keys are < max_key, so only bits [0, end_bit) need sorting; the ~0
+    // fill has all of those bits set and still sorts last (and keeps its value).
+    const int end_bit = end_bit_for(max_key);
     // per-call, stream-ordered scratch: calls on different streams never share it
-    (void)max_key;
     unsigned long long* alt = nullptr;
     void* tmp = nullptr;
     size_t need = 0;
     CK(cudaMallocAsync(&alt, cap * sizeof(unsigned long long), st), "escape scratch");
     cub::DoubleBuffer<unsigned long long> db(keys, alt);
-    // Keys past the real ones are all ~0; sort the full word so they stay last.
-    CK(cub::DeviceRadixSort::SortKeys(nullptr, need, db, int(cap), 0, 64, st), "escape sort size");
+    CK(cub::DeviceRadixSort::SortKeys(nullptr, need, db, int(cap), 0, end_bit, st), "escape sort size");
     CK(cudaMallocAsync(&tmp, need, st), "escape sort scratch");
-    CK(cub::DeviceRadixSort::SortKeys(tmp, need, db, int(cap), 0, 64, st), "escape sort");
-    ctx->launches += 2 * 8;  // onesweep: histogram + 8 digit passes (approximate)
+    CK(cub::DeviceRadixSort::SortKeys(tmp, need, db, int(cap), 0, end_bit, st), "escape sort");
+    ctx->launches += 2 + (end_bit + 7) / 8;  // onesweep: histogram + exclusive scan + one pass per 8 bits
     if (db.Current() != keys)
         CK(cudaMemcpyAsync(keys, db.Current(), cap * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st),
            "escape copy");
@@ -334,7 +347,7 @@ int encode_impl(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t N, uint32_t str
             CK(le, "encode launch");
             ctx->launches += 3 * ((uint64_t(stripes) * L + cap - 1) / cap);
         }
-        return sort_escapes(ctx, eout.keys, esc_cap, uint64_t(stripes) * n * L, st);
+        return sort_escapes(ctx, eout, uint64_t(stripes) * n * L, st);
     }
     if (large) {
         if (stripes && L) {
@@ -347,14 +360,14 @@ int encode_impl(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t N, uint32_t str
             CK(le, "encode launch");
             ctx->launches += 2 * ((stripes + batch - 1) / batch);
         }
-        return sort_escapes(ctx, eout.keys, esc_cap, uint64_t(stripes) * n * L, st);
+        return sort_escapes(ctx, eout, uint64_t(stripes) * n * L, st);
     }
     if (fast_ok)
         CK(fast::launch_encode_fast(ctx->ftab, k, n, N, stripes, L, src, ein, out, eout, st), "encode launch");
     else
         CK(launch_encode_tile(ctx->tab, k, n, N, stripes, L, src, ein, out, eout, st), "encode launch");
     ctx->launches += 1;
-    return sort_escapes(ctx, eout.keys, esc_cap, uint64_t(stripes) * n * L, st);
+    return sort_escapes(ctx, eout, uint64_t(stripes) * n * L, st);
 }
 }  // namespace
 
@@ -636,7 +649,7 @@ int fntrs_gpu_decode(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t stripes, ui
         CK(launch_decode_tile(ctx->tab, pv, stripes, L, stripe_pattern, rx, ein, out, eout, st), "decode launch");
     }
     ctx->launches += 1;
-    return sort_escapes(ctx, eout.keys, esc_cap, uint64_t(stripes) * pl->k * L, st);
+    return sort_escapes(ctx, eout, uint64_t(stripes) * pl->k * L, st);
 }
 
 }  // extern "C"
@@ -746,7 +759,7 @@ int fntrs_gpu_encode_systematic(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t
             cudaFreeAsync(sp, st);
             CK(le, "systematic encode launch");
             ctx->launches += 1;
-            rc = sort_escapes(ctx, eout.keys, esc_cap, uint64_t(stripes) * n * L, st);
+            rc = sort_escapes(ctx, eout, uint64_t(stripes) * n * L, st);
         }
         return rc;
     }
@@ -780,7 +793,7 @@ int fntrs_gpu_decode_systematic(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t 
         CK(fast::launch_systematic_fast(ctx->ftab, fv, false, pl->n, stripes, L, stripe_pattern, rx, ein, out, eout, st),
            "systematic decode launch");
         ctx->launches += 1;
-        return sort_escapes(ctx, eout.keys, esc_cap, uint64_t(stripes) * pl->k * L, st);
+        return sort_escapes(ctx, eout, uint64_t(stripes) * pl->k * L, st);
     }
     Interp it;
     int rc = interpolate_stage(ctx, pl, stripes, L, stripe_pattern, rx, rx_esc, n_rx_esc, st, it);

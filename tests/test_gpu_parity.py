@@ -529,3 +529,35 @@ def test_plan_methods_agree(codec, oracle, k, n, P, monkeypatch):
     for (a, b) in zip(outs[0][0], outs[1][0]):
         assert all(np.array_equal(x, y) if isinstance(x, np.ndarray) else x == y for x, y in zip(a, b))
     assert np.array_equal(outs[0][1], outs[1][1]) and np.array_equal(outs[0][1], src)
+
+
+@pytest.mark.parametrize("n,L,S,hot,cap", [
+    (16, 64, 4, 0, None),          # no escapes
+    (16, 64, 4, 1, None),          # one codeword: 16 escapes, single-CTA sort
+    (64, 256, 2, 200, 16384),      # 12800 escapes, single-CTA sort at its 16K limit
+    (64, 256, 2, 256, 16384),      # exactly 16384 = cap
+    (256, 512, 2, 300, None),      # 76800 escapes > default cap: count reports the overflow
+    (256, 512, 2, 300, 80000),     # 76800 escapes, radix sort on the key bits below S*n*L
+    (256, 512, 4, 5, 80000),       # few escapes in a large buffer (radix sort, mostly ~0 fill)
+])
+def test_escape_sort_paths(codec, n, L, S, hot, cap):
+    """k = 1: every output of a codeword equals its source symbol, so `hot`
+    codewords sourced with 65536 give exactly hot * n escapes, emitted in
+    kernel order; both escape-sort paths must list them ascending."""
+    from paper_0907_1788_b200 import escapes_to_numpy, TooManyEscapes
+    rng = np.random.default_rng(n * L + hot)
+    src = rng.integers(0, 65536, (S, 1, L)).astype(np.uint16)
+    idx = np.sort(rng.choice(S * L, size=hot, replace=False)).astype(np.uint64)
+    src.reshape(-1)[idx.astype(np.int64)] = 0
+    s_i, c_i = idx // L, idx % L
+    want_esc = np.sort(((s_i[:, None] * n + np.arange(n, dtype=np.uint64)[None, :]) * L + c_i[:, None]).reshape(-1))
+    out, oe, cnt = codec.encode(1, n, dev_u16(src), dev_esc(idx), esc_cap=cap)
+    want = np.repeat(src, n, axis=1)
+    assert np.array_equal(host_u16(out), want)
+    if cap is None and want_esc.size > oe.numel():
+        assert int(cnt.item()) == want_esc.size
+        with pytest.raises(TooManyEscapes):
+            escapes_to_numpy(oe, cnt)
+        return
+    assert np.array_equal(escapes_to_numpy(oe, cnt), want_esc)
+    assert np.all(oe[want_esc.size:].cpu().numpy() == -1)  # the ~0 fill stays after the real keys
