@@ -51,8 +51,8 @@ struct Tw {
 // tracked at compile time (static_assert B < 2^31). Butterfly differences need
 // no offsets, and multiplication by a power of two is three instructions:
 //   x * 2^s == (x mod 2^(16-s)) * 2^s - floor(x / 2^(16-s))       (2^16 == -1)
-//           == (x << s) - xh * 65537   exactly, xh = x >> (16-s) (arithmetic),
-// i.e. SHF + IMAD.SHL + IMAD (one ALU, two FMA-pipe instructions).
+//           == x * 2^s - xh * 65537   exactly, xh = x >> (16-s) (arithmetic),
+// i.e. SHF + LEA (ALU pipe) + one IMAD (multiplier pipe).
 
 // balanced representative of a canonical residue: (-p/2, p/2]
 __host__ __device__ constexpr int32_t balanced(uint32_t w) { return w > 32768u ? int32_t(w) - 65537 : int32_t(w); }
@@ -69,8 +69,8 @@ struct MulPow2 {
             return neg ? 0u - x : x;
         } else {
             const uint32_t xh = uint32_t(int32_t(x) >> (16 - s));
-            const uint32_t xs = x << s;
-            return neg ? xh * 65537u - xs : xs - xh * 65537u;
+            // SHF (ALU) + LEA (ALU) + one IMAD: x 2^s -/+ xh p
+            return neg ? mad_lo(x, 0u - (1u << s), mul_p(xh)) : mad_lo(x, 1u << s, 0u - mul_p(xh));
         }
     }
 };
@@ -82,12 +82,12 @@ struct MulPow2 {
 // signed Shoup product by a balanced twiddle w (w2 = 65535 w): (-p, 2p)
 __device__ __forceinline__ uint32_t mulws(uint32_t x, uint32_t w, uint32_t w2) {
     const uint32_t q = uint32_t(__mulhi(int32_t(x), int32_t(w2)));
-    return x * w - q * kP;
+    return x * w - mul_p(q);
 }
 // signed reduction: (-p, 2p)
 __device__ __forceinline__ uint32_t reds(uint32_t x) {
     const uint32_t q = uint32_t(__mulhi(int32_t(x), 65535));
-    return x - q * kP;
+    return x - mul_p(q);
 }
 // |x| < 2p -> canonical [0, p)
 __device__ __forceinline__ uint32_t canon_s2p(uint32_t x) {
@@ -130,8 +130,8 @@ struct DifStage {
 #pragma unroll
         for (int blk = 0; blk < R; blk += 2 * HALF) {
             const uint32_t a = v[blk + J], b = v[blk + J + HALF];
-            v[blk + J] = a + b;
-            v[blk + J + HALF] = M::apply(a - b);
+            v[blk + J] = add_a(a, b);
+            v[blk + J + HALF] = M::apply(sub_a(a, b));
         }
         if constexpr (J + 1 < HALF) DifStage<R, INV, HALF, J + 1, BIN>::run(v);
     }
@@ -171,8 +171,8 @@ struct DitStage {
         for (int blk = 0; blk < R; blk += 2 * HALF) {
             const uint32_t a = v[blk + J];
             const uint32_t t = M::apply(v[blk + J + HALF]);
-            v[blk + J] = a + t;
-            v[blk + J + HALF] = a - t;
+            v[blk + J] = add_a(a, t);
+            v[blk + J + HALF] = sub_a(a, t);
         }
         if constexpr (J + 1 < HALF) DitStage<R, INV, HALF, J + 1, BIN>::run(v);
     }
@@ -212,12 +212,12 @@ struct Dft4 {
     static constexpr uint64_t OUT = umax(4 * B, 2 * B + M::OUT);
     __device__ __forceinline__ static void run(uint32_t x0, uint32_t x1, uint32_t x2, uint32_t x3, uint32_t& y0,
                                                uint32_t& y1, uint32_t& y2, uint32_t& y3) {
-        const uint32_t b = x1 + x3;
-        const uint32_t d = M::apply(x1 - x3);
-        y0 = x0 + x2 + b;
-        y2 = x0 + x2 - b;
-        y1 = x0 - x2 + d;
-        y3 = x0 - x2 - d;
+        const uint32_t b = add_a(x1, x3);
+        const uint32_t d = M::apply(sub_a(x1, x3));
+        y0 = add3_a(x0, x2, b);
+        y2 = addsub_a(x0, x2, b);
+        y1 = addsub_a(x0, d, x2);
+        y3 = subsub_a(x0, x2, d);
     }
 };
 
@@ -234,8 +234,8 @@ template <bool INV, uint64_t B>
 struct Dft<2, INV, B> {
     static constexpr uint64_t OUT = 2 * B;
     __device__ __forceinline__ static void run(const uint32_t (&x)[2], uint32_t (&y)[2]) {
-        y[0] = x[0] + x[1];
-        y[1] = x[0] - x[1];
+        y[0] = add_a(x[0], x[1]);
+        y[1] = sub_a(x[0], x[1]);
     }
 };
 
@@ -278,8 +278,8 @@ struct Dft<8, INV, B> {
         z1[3] = TwR<8, 3, INV, B1>::apply(z1[3]);
 #pragma unroll
         for (int s1 = 0; s1 < 4; ++s1) {
-            y[s1] = z0[s1] + z1[s1];
-            y[s1 + 4] = z0[s1] - z1[s1];
+            y[s1] = add_a(z0[s1], z1[s1]);
+            y[s1 + 4] = sub_a(z0[s1], z1[s1]);
         }
     }
 };

@@ -8,9 +8,9 @@
 // Shoup constant floor(w * 2^32 / p) is exactly 65535 * w (since
 // 2^32 = 65535 * p + 1), so no second table is needed:
 //     q = umulhi(x, 65535 w);  r = x w - q p   (mod 2^32),  r in [0, 2p)
-// for ANY 32-bit x. That lets butterfly sums grow lazily across stages and
-// keeps the reductions on the FMA pipe (IMAD.HI, IMAD) while the adds use
-// the ALU pipe.
+// for ANY 32-bit x. That lets butterfly sums grow lazily across stages; the
+// reduction is IMAD.HI + IMAD on the multiplier pipe and one LEA (q p) on the
+// ALU pipe.
 #pragma once
 #include <cstdint>
 
@@ -40,22 +40,107 @@ __host__ __device__ constexpr uint32_t croot(uint32_t n, bool inverse) {
     return cpow(3u, inverse ? (uint64_t(65536u / n) * 65535u) % 65536u : 65536u / n);
 }
 
+// Pipe balance. The integer multiplier (the FMA-heavy pipe: IMAD, and
+// IMAD.HI / IMAD.WIDE at two slots each) is the busiest pipe in every codec
+// kernel, and ptxas also places plain adds and shifts there (IMAD.IADD,
+// IMAD.SHL). q * p = (q << 16) + q is one LEA on the ALU pipe; written as
+// PTX shl + add so NVVM cannot fold it back into a multiply. Off by default:
+// ptxas re-balances by moving other adds to IMAD.IADD (executed multiplier
+// instructions unchanged, kernels 1-4 % slower; profiles/README.md).
+#ifndef FNTRS_LEA
+#define FNTRS_LEA 0
+#endif
+__device__ __forceinline__ uint32_t mul_p(uint32_t q) {
+#if FNTRS_LEA
+    uint32_t t;
+    asm("{\n\t.reg .b32 s;\n\tshl.b32 s, %1, 16;\n\tadd.u32 %0, s, %1;\n\t}" : "=r"(t) : "r"(q));
+    return t;
+#else
+    return q * kP;
+#endif
+}
+// a * b + c as exactly one IMAD (instead of a shift on either pipe plus an add)
+__device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+
+// Adds pinned to the ALU pipe. ptxas turns a share of two-input adds into
+// IMAD.IADD to balance pipes, but on sm_100a the multiplier pipe is the
+// saturated one. Adding a zero that only exists at run time (a constant-bank
+// word) inside an opaque PTX block makes every such add a three-input IADD3,
+// which has no IMAD form; three-input sums are pinned the same way so that
+// NVVM cannot re-split them into two-input adds. Off by default: it removes
+// 6.5 % of the multiplier-pipe instructions but the issue rate stays at 66 %
+// (C2 decode +1 %, C2 encode -1.5 %; profiles/README.md).
+#ifndef FNTRS_ALU_ADDS
+#define FNTRS_ALU_ADDS 0
+#endif
+static __constant__ uint32_t g_alu_zero;  // never written: 0
+__device__ __forceinline__ uint32_t add_a(uint32_t a, uint32_t b) {
+#if FNTRS_ALU_ADDS
+    uint32_t r;
+    asm("{\n\t.reg .b32 t;\n\tadd.u32 t, %1, %2;\n\tadd.u32 %0, t, %3;\n\t}" : "=r"(r) : "r"(a), "r"(b), "r"(g_alu_zero));
+    return r;
+#else
+    return a + b;
+#endif
+}
+__device__ __forceinline__ uint32_t sub_a(uint32_t a, uint32_t b) {
+#if FNTRS_ALU_ADDS
+    uint32_t r;
+    asm("{\n\t.reg .b32 t;\n\tsub.u32 t, %1, %2;\n\tadd.u32 %0, t, %3;\n\t}" : "=r"(r) : "r"(a), "r"(b), "r"(g_alu_zero));
+    return r;
+#else
+    return a - b;
+#endif
+}
+// a + b + c, a + b - c, a - b - c as one IADD3 each
+__device__ __forceinline__ uint32_t add3_a(uint32_t a, uint32_t b, uint32_t c) {
+#if FNTRS_ALU_ADDS
+    uint32_t r;
+    asm("{\n\t.reg .b32 t;\n\tadd.u32 t, %1, %2;\n\tadd.u32 %0, t, %3;\n\t}" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+#else
+    return a + b + c;
+#endif
+}
+__device__ __forceinline__ uint32_t addsub_a(uint32_t a, uint32_t b, uint32_t c) {
+#if FNTRS_ALU_ADDS
+    uint32_t r;
+    asm("{\n\t.reg .b32 t;\n\tadd.u32 t, %1, %2;\n\tsub.u32 %0, t, %3;\n\t}" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+#else
+    return a + b - c;
+#endif
+}
+__device__ __forceinline__ uint32_t subsub_a(uint32_t a, uint32_t b, uint32_t c) {
+#if FNTRS_ALU_ADDS
+    uint32_t r;
+    asm("{\n\t.reg .b32 t;\n\tsub.u32 t, %1, %2;\n\tsub.u32 %0, t, %3;\n\t}" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+#else
+    return a - b - c;
+#endif
+}
+
 // x * w mod p into [0, 2p); w < p canonical, x any uint32.
 __device__ __forceinline__ uint32_t mulw(uint32_t x, uint32_t w) {
     const uint32_t q = __umulhi(x, w * 65535u);
-    return x * w - q * kP;
+    return x * w - mul_p(q);
 }
 
 // Same with the Shoup constant supplied (w2 = 65535 * w).
 __device__ __forceinline__ uint32_t mulw2(uint32_t x, uint32_t w, uint32_t w2) {
     const uint32_t q = __umulhi(x, w2);
-    return x * w - q * kP;
+    return x * w - mul_p(q);
 }
 
 // any uint32 -> [0, 2p)
 __device__ __forceinline__ uint32_t red(uint32_t x) {
     const uint32_t q = __umulhi(x, 65535u);
-    return x - q * kP;
+    return x - mul_p(q);
 }
 
 // [0, 2p) -> [0, p)
