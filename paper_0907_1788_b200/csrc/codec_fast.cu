@@ -59,13 +59,14 @@ __global__ void __launch_bounds__(G::NT, G::MINB) enc_fast_kernel(const __grid_c
                                                          uint32_t L, uint32_t tps, uint32_t tiles, uint32_t nbox,
                                                          uint32_t box_rows, EscIn esc_in, uint16_t* __restrict__ out,
                                                          EscOut esc_out, const __grid_constant__ CUtensorMap out_map,
-                                                         uint32_t obox) {
+                                                         uint32_t obox, uint32_t* __restrict__ tile_ctr) {
     using S = Sched<E>;
     constexpr int N = 1 << E, WT = G::WT, P = S::P;
     constexpr int RL0 = S::rlog(0), R0 = 1 << RL0, RLZ = G::RLZ;
     static_assert(P >= 2 && P <= 3, "");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t bars[2];
+    __shared__ uint32_t next_tile[2];  // successor of the tile of iteration i, in slot i & 1
     uint32_t* work = reinterpret_cast<uint32_t*>(smem_raw);
     uint16_t* stage0 = reinterpret_cast<uint16_t*>(smem_raw + size_t(N) * WT * 4);
     const uint32_t stage_elems = nbox * box_rows * WT;
@@ -93,11 +94,16 @@ __global__ void __launch_bounds__(G::NT, G::MINB) enc_fast_kernel(const __grid_c
     uint32_t tile = blockIdx.x;
     if (threadIdx.x == 0 && tile < tiles) issue(tile, 0);
     const bool esc_any = esc_in.n != 0;
-    for (uint32_t iter = 0; tile < tiles; ++iter, tile += gridDim.x) {
+    constexpr bool DYN = G::MINB > 1;  // as in dec_fast_kernel
+    for (uint32_t iter = 0; tile < tiles; tile = DYN ? next_tile[iter & 1] : tile + gridDim.x, ++iter) {
         const int bsel = TS ? 0 : (iter & 1);
         const uint32_t stripe = tile / tps;
         const uint32_t c0 = (tile - stripe * tps) * WT;
-        if (!TS && threadIdx.x == 0 && tile + gridDim.x < tiles) issue(tile + gridDim.x, bsel ^ 1);
+        const uint32_t claimed = !DYN ? tile + gridDim.x : threadIdx.x == 0 ? claim_tile(tile_ctr) : 0u;
+        if (!TS && threadIdx.x == 0) {
+            if constexpr (DYN) next_tile[iter & 1] = claimed;
+            if (claimed < tiles) issue(claimed, bsel ^ 1);
+        }
         mbar_wait(&bars[bsel], TS ? (iter & 1) : ((iter >> 1) & 1));
         const uint16_t* st_in = stage0 + bsel * stage_elems;
         const unsigned long long key_in = uint64_t(stripe) * k * L + c0;
@@ -145,7 +151,10 @@ __global__ void __launch_bounds__(G::NT, G::MINB) enc_fast_kernel(const __grid_c
         }
         __syncthreads();
         if constexpr (TS) {  // the stage is consumed: the next tile's packets stream in behind
-            if (threadIdx.x == 0 && tile + gridDim.x < tiles) issue(tile + gridDim.x, 0);
+            if (threadIdx.x == 0) {
+                if constexpr (DYN) next_tile[iter & 1] = claimed;
+                if (claimed < tiles) issue(claimed, 0);
+            }
         }
         if constexpr (P == 3) {
             pass_cw<CW, E, 1, false, false, kSmemCap, kSmemCap, G>(pass_table(ptabF, S::llog(1)), ld_sm, st_sm);
@@ -191,7 +200,7 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
                                                          uint32_t tps, uint32_t tiles, uint32_t nbox, uint32_t box_rows,
                                                          const uint32_t* __restrict__ stripe_pattern, EscIn esc_in,
                                                          uint16_t* __restrict__ out, EscOut esc_out, uint32_t n,
-                                                         const uint2* __restrict__ ptabFT) {
+                                                         const uint2* __restrict__ ptabFT, uint32_t* __restrict__ tile_ctr) {
     using S = Sched<E>;
     constexpr int N = 1 << E, WT = G::WT, NT = G::NT, P = S::P;
     constexpr int RLZ = G::RLZ, RZ = 1 << RLZ;
@@ -201,6 +210,7 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
     static_assert(P >= 2 && P <= 3, "");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t bars[2];
+    __shared__ uint32_t next_tile[2];  // successor of the tile of iteration i, in slot i & 1
     uint32_t* work = reinterpret_cast<uint32_t*>(smem_raw);
     // [guard | stage]: the guard is the WT-symbol row just below the stage (an
     // erased position's row index ~0 wraps onto it) and holds ones, so raw
@@ -230,10 +240,14 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
     const uint4* tF0 = pass_table(ptabF, S::llog(0));
     const uint4* tI0 = pass_table(ptabI, S::llog(0));
     const bool esc_any = esc_in.n != 0;
-    for (uint32_t iter = 0; tile < tiles; ++iter, tile += gridDim.x) {
+    for (uint32_t iter = 0; tile < tiles; tile = DecOcc<E>::MINB > 1 ? next_tile[iter & 1] : tile + gridDim.x, ++iter) {
         const uint32_t stripe = tile / tps;
         const uint32_t c0 = (tile - stripe * tps) * WT;
         const uint32_t pat = __ldg(stripe_pattern + stripe);
+        // the successor is claimed now and used after the first pass (the atomic's latency hides behind it);
+        // one CTA per SM (n_domain 4096) keeps the static stride: nothing to balance, one register less
+        constexpr bool DYN = DecOcc<E>::MINB > 1;
+        const uint32_t claimed = !DYN ? tile + gridDim.x : threadIdx.x == 0 ? claim_tile(tile_ctr) : 0u;
         const uint2* __restrict__ rm = rowmap + size_t(pat) * N;
         const uint2* __restrict__ ah = ahat2 + size_t(pat) * N;
         const unsigned long long key = uint64_t(stripe) * k * L + c0;
@@ -302,7 +316,10 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
         pass<E, 0, false, false, k2P, kSmemCap, G>(tF0, ld_scatter, st_sm, fix_scatter);
         __syncthreads();
         // the stage is consumed: stream the next tile's packets in behind the remaining passes
-        if (threadIdx.x == 0 && tile + gridDim.x < tiles) issue(tile + gridDim.x, 0);
+        if (threadIdx.x == 0) {
+            if constexpr (DYN) next_tile[iter & 1] = claimed;
+            if (claimed < tiles) issue(claimed, 0);
+        }
         if constexpr (P == 3) {
             pass<E, 1, false, false, kSmemCap, kSmemCap, G>(pass_table(ptabF, S::llog(1)), ld_sm, st_sm);
             __syncthreads();
@@ -594,8 +611,10 @@ cudaError_t launch_enc_as(const FastTables& t, uint32_t k, uint32_t n, uint32_t 
     if ((err = make_map(&map, src, uint64_t(stripes) * k, L, G::WT, sh.box_rows))) return err;
     const uint32_t obox = n < 256 ? n : 256;
     if (TS && (err = make_map3(&omap, out, stripes, n, L, G::WT, obox))) return err;
+    TileCounter ctr;
+    if (G::MINB > 1 && (err = ctr.get(st))) return err;
     kern<<<sh.grid, G::NT, sh.smem, st>>>(map, t.ptab_fwd, k, n, L, sh.tps, sh.tiles, sh.nbox, sh.box_rows, ein, out, eout,
-                                          omap, obox);
+                                          omap, obox, ctr.p);
     return cudaGetLastError();
 }
 
@@ -627,8 +646,10 @@ cudaError_t launch_dec(const FastTables& t, const FastPlanView& pv, uint32_t str
     if (!sh.tiles) return cudaSuccess;
     CUtensorMap map;
     if ((err = make_map(&map, rx, uint64_t(stripes) * pv.k, L, G::WT, sh.box_rows))) return err;
+    TileCounter ctr;
+    if (DecOcc<E>::MINB > 1 && (err = ctr.get(st))) return err;
     kern<<<sh.grid, G::NT, sh.smem, st>>>(map, t.ptab_fwd, t.ptab_inv, pv.rowmap, pv.ahat2, pv.k, L, sh.tps, sh.tiles,
-                                          sh.nbox, sh.box_rows, sp, ein, out, eout, n, t.ptab_fwdT);
+                                          sh.nbox, sh.box_rows, sp, ein, out, eout, n, t.ptab_fwdT, ctr.p);
     return cudaGetLastError();
 }
 

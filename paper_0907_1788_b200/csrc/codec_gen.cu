@@ -45,7 +45,7 @@ dec_gen_kernel(const __grid_constant__ CUtensorMap rx_map, const uint2* __restri
                const uint2* __restrict__ ptabI, const uint2* __restrict__ rowmap, const uint2* __restrict__ ahat2,
                uint32_t k, uint32_t L, uint32_t tps, uint32_t tiles, uint32_t nbox, uint32_t box_rows,
                const uint32_t* __restrict__ stripe_pattern, EscIn esc_in, uint16_t* __restrict__ out,
-               EscOut esc_out) {
+               EscOut esc_out, uint32_t* __restrict__ tile_ctr) {
     using Pk = GenPick<E, EM>;
     constexpr int WT = Pk::WT, NT = Pk::NT;
     using GA = Geom<E, WT, NT, Pk::MINB>;
@@ -58,6 +58,8 @@ dec_gen_kernel(const __grid_constant__ CUtensorMap rx_map, const uint2* __restri
     static_assert(PA >= 2 && PA <= 3 && PB >= 1 && PB <= 3, "");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t bar;
+    __shared__ uint32_t next_tile[2];  // claimed successor of iteration i, slot i & 1 (tma.cuh)
+    constexpr bool DYN = Pk::MINB > 1;
     uint32_t* A = reinterpret_cast<uint32_t*>(smem_raw);
     uint32_t* B = A + N * WT;
     const uint32_t stage_bytes = nbox * box_rows * WT * 2;
@@ -82,10 +84,11 @@ dec_gen_kernel(const __grid_constant__ CUtensorMap rx_map, const uint2* __restri
     uint32_t tile = blockIdx.x;
     if (threadIdx.x == 0 && tile < tiles) issue(tile);
     const bool esc_any = esc_in.n != 0;
-    for (uint32_t iter = 0; tile < tiles; ++iter, tile += gridDim.x) {
+    for (uint32_t iter = 0; tile < tiles; tile = DYN ? next_tile[iter & 1] : tile + gridDim.x, ++iter) {
         const uint32_t stripe = tile / tps;
         const uint32_t c0 = (tile - stripe * tps) * WT;
         const uint32_t pat = __ldg(stripe_pattern + stripe);
+        const uint32_t claimed = !DYN ? tile + gridDim.x : threadIdx.x == 0 ? claim_tile(tile_ctr) : 0u;
         const uint2* __restrict__ rm = rowmap + size_t(pat) * N;
         const uint2* __restrict__ ah = ahat2 + size_t(pat) * M;
         const unsigned long long key = uint64_t(stripe) * k * L + c0;
@@ -125,7 +128,10 @@ dec_gen_kernel(const __grid_constant__ CUtensorMap rx_map, const uint2* __restri
         };
         pass<E, 0, false, false, k2P, kSmemCap, GA>(pass_table(ptabF, SA::llog(0)), ld_scatter, st_a, fix_scatter);
         __syncthreads();
-        if (threadIdx.x == 0 && tile + gridDim.x < tiles) issue(tile + gridDim.x);  // stage consumed
+        if (threadIdx.x == 0) {  // stage consumed
+            if constexpr (DYN) next_tile[iter & 1] = claimed;
+            if (claimed < tiles) issue(claimed);
+        }
         pass<E, 1, false, false, kSmemCap, kSmemCap, GA>(pass_table(ptabF, SA::llog(1)), ld_a, st_a);
         __syncthreads();
         if constexpr (PA == 3) {
@@ -244,9 +250,11 @@ cudaError_t launch_gen(const FastTables& t, const GenPlanView& pv, uint32_t stri
     const uint64_t g = uint64_t(sms) * per;
     CUtensorMap map;
     if ((err = make_rx_map(&map, rx, uint64_t(stripes) * pv.k, L, Pk::WT, box_rows))) return err;
+    TileCounter ctr;
+    if (Pk::MINB > 1 && (err = ctr.get(st))) return err;
     kern<<<uint32_t(g < tiles ? g : tiles), Pk::NT, smem, st>>>(map, t.ptab_fwd, t.ptab_inv, pv.rowmap, pv.ahat2,
                                                                  pv.k, L, tps, uint32_t(tiles), nbox, box_rows, sp, ein,
-                                                                 out, eout);
+                                                                 out, eout, ctr.p);
     return cudaGetLastError();
 }
 

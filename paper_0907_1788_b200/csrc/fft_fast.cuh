@@ -51,8 +51,8 @@ struct Tw {
 // tracked at compile time (static_assert B < 2^31). Butterfly differences need
 // no offsets, and multiplication by a power of two is three instructions:
 //   x * 2^s == (x mod 2^(16-s)) * 2^s - floor(x / 2^(16-s))       (2^16 == -1)
-//           == x * 2^s - xh * 65537   exactly, xh = x >> (16-s) (arithmetic),
-// i.e. SHF + LEA (ALU pipe) + one IMAD (multiplier pipe).
+//           == (x << s) - xh * 65537   exactly, xh = x >> (16-s) (arithmetic),
+// i.e. SHF + IMAD.SHL/SHF + IMAD.
 
 // balanced representative of a canonical residue: (-p/2, p/2]
 __host__ __device__ constexpr int32_t balanced(uint32_t w) { return w > 32768u ? int32_t(w) - 65537 : int32_t(w); }
@@ -69,8 +69,12 @@ struct MulPow2 {
             return neg ? 0u - x : x;
         } else {
             const uint32_t xh = uint32_t(int32_t(x) >> (16 - s));
-            // SHF (ALU) + LEA (ALU) + one IMAD: x 2^s -/+ xh p
+#if FNTRS_LEA  // SHF (ALU) + LEA (ALU) + one IMAD: x 2^s -/+ xh p
             return neg ? mad_lo(x, 0u - (1u << s), mul_p(xh)) : mad_lo(x, 1u << s, 0u - mul_p(xh));
+#else
+            const uint32_t xs = x << s;
+            return neg ? xh * 65537u - xs : xs - xh * 65537u;
+#endif
         }
     }
 };
@@ -212,12 +216,21 @@ struct Dft4 {
     static constexpr uint64_t OUT = umax(4 * B, 2 * B + M::OUT);
     __device__ __forceinline__ static void run(uint32_t x0, uint32_t x1, uint32_t x2, uint32_t x3, uint32_t& y0,
                                                uint32_t& y1, uint32_t& y2, uint32_t& y3) {
+#if FNTRS_ALU_ADDS
         const uint32_t b = add_a(x1, x3);
         const uint32_t d = M::apply(sub_a(x1, x3));
         y0 = add3_a(x0, x2, b);
         y2 = addsub_a(x0, x2, b);
         y1 = addsub_a(x0, d, x2);
         y3 = subsub_a(x0, x2, d);
+#else
+        const uint32_t b = x1 + x3;
+        const uint32_t d = M::apply(x1 - x3);
+        y0 = x0 + x2 + b;
+        y2 = x0 + x2 - b;
+        y1 = x0 - x2 + d;
+        y3 = x0 - x2 - d;
+#endif
     }
 };
 
