@@ -12,7 +12,7 @@ PKG := paper_0907_1788_b200
 CSRC := $(PKG)/csrc
 BUILD := build
 LIB := $(PKG)/libfntrs_b200.so
-CU_SRCS := $(CSRC)/codec_tile.cu $(CSRC)/codec_fast.cu $(CSRC)/codec_large.cu $(CSRC)/codec_cols.cu $(CSRC)/codec_gen.cu $(CSRC)/shards.cu $(CSRC)/plan_build.cu $(CSRC)/plan_fast.cu $(CSRC)/capi.cu
+CU_SRCS := $(CSRC)/codec_tile.cu $(CSRC)/codec_fast.cu $(CSRC)/codec_dec.cu $(CSRC)/codec_large.cu $(CSRC)/codec_cols.cu $(CSRC)/codec_gen.cu $(CSRC)/shards.cu $(CSRC)/plan_build.cu $(CSRC)/plan_fast.cu $(CSRC)/capi.cu
 CXX_SRCS := $(CSRC)/dropin.cpp
 CU_OBJS := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS))
 CXX_OBJS := $(patsubst $(CSRC)/%.cpp,$(BUILD)/%.o,$(CXX_SRCS))
