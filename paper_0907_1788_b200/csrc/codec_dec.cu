@@ -98,14 +98,14 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
     const uint4* tF0 = pass_table(ptabF, S::llog(0));
     const uint4* tI0 = pass_table(ptabI, S::llog(0));
     const bool esc_any = esc_in.n != 0;
-    for (uint32_t iter = 0; tile < tiles; tile = DecOcc<E>::MINB > 1 ? next_tile[iter & 1] : tile + gridDim.x, ++iter) {
+    for (uint32_t iter = 0; tile < tiles; tile = next_tile[iter & 1], ++iter) {
         const uint32_t stripe = tile / tps;
         const uint32_t c0 = (tile - stripe * tps) * WT;
         const uint32_t pat = __ldg(stripe_pattern + stripe);
-        // the successor is claimed now and used after the first pass (the atomic's latency hides behind it);
-        // one CTA per SM (n_domain 4096) keeps the static stride: nothing to balance, one register less
-        constexpr bool DYN = DecOcc<E>::MINB > 1;
-        const uint32_t claimed = !DYN ? tile + gridDim.x : threadIdx.x == 0 ? claim_tile(tile_ctr) : 0u;
+        // the successor is claimed now and used after the first pass (the atomic's latency hides behind it).
+        // Claiming at every occupancy keeps CTAs on adjacent tiles in step: the two halves of a 32-byte
+        // sector (8-column tiles at n_domain 4096) then meet in L2 instead of costing DRAM re-reads
+        const uint32_t claimed = threadIdx.x == 0 ? claim_tile(tile_ctr) : 0u;
         const uint2* __restrict__ rm = rowmap + size_t(pat) * N;
         const uint2* __restrict__ ah = ahat2 + size_t(pat) * N;
         const unsigned long long key = uint64_t(stripe) * k * L + c0;
@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
         __syncthreads();
         // the stage is consumed: stream the next tile's packets in behind the remaining passes
         if (threadIdx.x == 0) {
-            if constexpr (DYN) next_tile[iter & 1] = claimed;
+            next_tile[iter & 1] = claimed;
             if (claimed < tiles) issue(claimed, 0);
         }
         if constexpr (P == 3) {
@@ -348,7 +348,7 @@ cudaError_t launch_dec(const FastTables& t, const FastPlanView& pv, uint32_t str
     CUtensorMap map;
     if ((err = make_map(&map, rx, uint64_t(stripes) * pv.k, L, G::WT, sh.box_rows))) return err;
     TileCounter ctr;
-    if (DecOcc<E>::MINB > 1 && (err = ctr.get(st))) return err;
+    if ((err = ctr.get(st))) return err;
     kern<<<sh.grid, G::NT, sh.smem, st>>>(map, t.ptab_fwd, t.ptab_inv, pv.rowmap, pv.ahat2, pv.k, L, sh.tps, sh.tiles,
                                           sh.nbox, sh.box_rows, sp, ein, out, eout, n, t.ptab_fwdT, ctr.p);
     return cudaGetLastError();

@@ -97,7 +97,8 @@ __global__ void __launch_bounds__(G::NT, G::MINB) enc_fast_kernel(const __grid_c
     uint32_t tile = blockIdx.x;
     if (threadIdx.x == 0 && tile < tiles) issue(tile, 0);
     const bool esc_any = esc_in.n != 0;
-    constexpr bool DYN = G::MINB > 1;  // as in dec_fast_kernel
+    // tiles are claimed from a counter at every occupancy (as in dec_fast_kernel)
+    constexpr bool DYN = true;
     for (uint32_t iter = 0; tile < tiles; tile = DYN ? next_tile[iter & 1] : tile + gridDim.x, ++iter) {
         const int bsel = TS ? 0 : (iter & 1);
         const uint32_t stripe = tile / tps;
@@ -239,7 +240,7 @@ cudaError_t launch_enc_as(const FastTables& t, uint32_t k, uint32_t n, uint32_t 
     const uint32_t obox = n < 256 ? n : 256;
     if (TS && (err = make_map3(&omap, out, stripes, n, L, G::WT, obox))) return err;
     TileCounter ctr;
-    if (G::MINB > 1 && (err = ctr.get(st))) return err;
+    if ((err = ctr.get(st))) return err;
     kern<<<sh.grid, G::NT, sh.smem, st>>>(map, t.ptab_fwd, k, n, L, sh.tps, sh.tiles, sh.nbox, sh.box_rows, ein, out, eout,
                                           omap, obox, ctr.p);
     return cudaGetLastError();

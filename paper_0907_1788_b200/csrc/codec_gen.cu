@@ -59,7 +59,7 @@ dec_gen_kernel(const __grid_constant__ CUtensorMap rx_map, const uint2* __restri
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t bar;
     __shared__ uint32_t next_tile[2];  // claimed successor of iteration i, slot i & 1 (tma.cuh)
-    constexpr bool DYN = Pk::MINB > 1;
+    constexpr bool DYN = true;  // adjacent tiles stay in step (see codec_dec.cu)
     uint32_t* A = reinterpret_cast<uint32_t*>(smem_raw);
     uint32_t* B = A + N * WT;
     const uint32_t stage_bytes = nbox * box_rows * WT * 2;
@@ -251,7 +251,7 @@ cudaError_t launch_gen(const FastTables& t, const GenPlanView& pv, uint32_t stri
     CUtensorMap map;
     if ((err = make_rx_map(&map, rx, uint64_t(stripes) * pv.k, L, Pk::WT, box_rows))) return err;
     TileCounter ctr;
-    if (Pk::MINB > 1 && (err = ctr.get(st))) return err;
+    if ((err = ctr.get(st))) return err;
     kern<<<uint32_t(g < tiles ? g : tiles), Pk::NT, smem, st>>>(map, t.ptab_fwd, t.ptab_inv, pv.rowmap, pv.ahat2,
                                                                  pv.k, L, tps, uint32_t(tiles), nbox, box_rows, sp, ein,
                                                                  out, eout, ctr.p);
