@@ -126,7 +126,8 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
             if constexpr (MODE == 2) {  // identity plan: row z < k is source row z -> codeword row z
                 if (HALFK ? (q < R0 / 2) : (lrow < k)) __stcs(outp + (lrow * L + col), uint16_t(raw));
             }
-            return mulws(raw, m.y, m.y * 65535u);
+            // raw <= 65535 and |1/A'| <= p/2 (balanced): the product is exact in 32 signed bits
+            return reds(raw * m.y);
         };
         auto fix_scatter = [&](uint32_t (&v)[R0], uint32_t base, uint32_t, uint32_t col) {
             const bool any = zmin == 0u;
@@ -230,7 +231,7 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
         // FNT2 last DIT pass + (. ahat) + FNT3 first DIF pass: rows t + q * sub0
         {
             constexpr int ITEMS = (N / R0) * WT;
-            constexpr uint64_t BO = dif_bound<R0, true, k2P>();
+            constexpr uint64_t BO = dif_bound<R0, true, k2P, kLazyLim>();
 #pragma unroll 1
             for (int it = threadIdx.x; it < ITEMS; it += NT) {
                 const uint32_t col = uint32_t(it) & uint32_t(WT - 1);
@@ -248,7 +249,7 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
                     }
                     v[rev<R0>(s)] = x;
                 }
-                dit_regs<R0, false, (P == 2 ? k2P : kSmemCap)>(v);
+                dit_regs<R0, false, (P == 2 ? k2P : kSmemCap), kLazyLim>(v);  // outputs -> (. ahat) Shoup
                 const uint4* ahq = reinterpret_cast<const uint4*>(ah) + t * (R0 / 2);  // ahat2_slot order
 #pragma unroll
                 for (int q = 0; q < R0; q += 2) {
@@ -256,7 +257,7 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
                     v[q] = mulws(v[q], a.x, a.y);
                     v[q + 1] = mulws(v[q + 1], a.z, a.w);
                 }
-                dif_regs<R0, true, k2P>(v);
+                dif_regs<R0, true, k2P, kLazyLim>(v);
 #pragma unroll
                 for (int s = 0; s < R0; ++s) {
                     uint32_t y = v[rev<R0>(s)];

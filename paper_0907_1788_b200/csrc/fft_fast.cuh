@@ -234,17 +234,53 @@ struct Dft4 {
     }
 };
 
-template <int R, bool INV, uint64_t B>
+// Lazy 4-point DFT with a bound per input (|x_i| < Bi). The w4 product
+// d = w4 (x1 - x3) is either reduced (MulPow2, three instructions) or, when
+// every output stays below LIM, left as the exact shift (x3 - x1) << 8
+// (forward, w4 = -2^8) / (x1 - x3) << 8 (inverse): one instruction, and the
+// bound grows by 2^8. LIM = 0 never takes the lazy form. Used where the
+// outputs go into a Shoup product (which reduces any 32-bit signed value).
+#ifndef FNTRS_LAZY_LIM
+#define FNTRS_LAZY_LIM (1ull << 30)
+#endif
+constexpr uint64_t kLazyLim = FNTRS_LAZY_LIM;
+
+template <bool INV, uint64_t B0, uint64_t B1, uint64_t B2, uint64_t B3, uint64_t LIM>
+struct Dft4L {
+    static constexpr int E4 = INV ? 8 : 24;
+    static constexpr uint64_t BD = B1 + B3;
+    using M = MulPow2<E4, BD>;
+    static constexpr bool lazy = LIM != 0 && B0 + B2 + (BD << 8) <= LIM;
+    static constexpr uint64_t D = lazy ? (BD << 8) : M::OUT;
+    static constexpr uint64_t O02 = B0 + B1 + B2 + B3;
+    static constexpr uint64_t O13 = B0 + B2 + D;
+    static constexpr uint64_t OUT = umax(O02, O13);
+    __device__ __forceinline__ static void run(uint32_t x0, uint32_t x1, uint32_t x2, uint32_t x3, uint32_t& y0,
+                                               uint32_t& y1, uint32_t& y2, uint32_t& y3) {
+        const uint32_t b = add_a(x1, x3);
+        uint32_t d;
+        if constexpr (lazy)
+            d = (INV ? sub_a(x1, x3) : sub_a(x3, x1)) << 8;
+        else
+            d = M::apply(sub_a(x1, x3));
+        y0 = add3_a(x0, x2, b);
+        y2 = addsub_a(x0, x2, b);
+        y1 = addsub_a(x0, d, x2);
+        y3 = subsub_a(x0, x2, d);
+    }
+};
+
+template <int R, bool INV, uint64_t B, uint64_t LIM = 0>
 struct Dft;
 
-template <bool INV, uint64_t B>
-struct Dft<1, INV, B> {
+template <bool INV, uint64_t B, uint64_t LIM>
+struct Dft<1, INV, B, LIM> {
     static constexpr uint64_t OUT = B;
     __device__ __forceinline__ static void run(const uint32_t (&)[1], uint32_t (&y)[1]) {}
 };
 
-template <bool INV, uint64_t B>
-struct Dft<2, INV, B> {
+template <bool INV, uint64_t B, uint64_t LIM>
+struct Dft<2, INV, B, LIM> {
     static constexpr uint64_t OUT = 2 * B;
     __device__ __forceinline__ static void run(const uint32_t (&x)[2], uint32_t (&y)[2]) {
         y[0] = add_a(x[0], x[1]);
@@ -252,8 +288,8 @@ struct Dft<2, INV, B> {
     }
 };
 
-template <bool INV, uint64_t B>
-struct Dft<4, INV, B> {
+template <bool INV, uint64_t B, uint64_t LIM>
+struct Dft<4, INV, B, LIM> {
     static constexpr uint64_t OUT = Dft4<INV, B>::OUT;
     __device__ __forceinline__ static void run(const uint32_t (&x)[4], uint32_t (&y)[4]) {
         Dft4<INV, B>::run(x[0], x[1], x[2], x[3], y[0], y[1], y[2], y[3]);
@@ -277,8 +313,8 @@ struct TwR {
 
 // R = 8: 2 x 4 (q = 2 q1 + q2, s = s1 + 4 s2): DFT4 over q1 for each q2,
 // twiddle w8^(q2 s1), DFT2 over q2.
-template <bool INV, uint64_t B>
-struct Dft<8, INV, B> {
+template <bool INV, uint64_t B, uint64_t LIM>
+struct Dft<8, INV, B, LIM> {
     static constexpr uint64_t B1 = Dft4<INV, B>::OUT;
     static constexpr uint64_t BT = umax(umax(TwR<8, 1, INV, B1>::OUT, TwR<8, 2, INV, B1>::OUT), TwR<8, 3, INV, B1>::OUT);
     static constexpr uint64_t OUT = 2 * umax(B1, BT);
@@ -297,34 +333,36 @@ struct Dft<8, INV, B> {
     }
 };
 
-template <bool INV, uint64_t B, int Q2, int S1>
-struct Tw16 {
-    using T = TwR<16, Q2 * S1, INV, Dft4<INV, B>::OUT>;
+// R = 16 as 4 x 4 with a bound per element: stage 1 = four Dft4L over
+// stride-4 inputs (outputs s1 = 0, 2 below 4B; s1 = 1, 3 below 2B + D), the
+// nine twiddles w16^(q2 s1) (reducing shift-multiplies), stage 2 = four Dft4L
+// whose first input is untwiddled. Stage 1 takes the lazy product only when
+// the whole transform then stays below LIM.
+template <bool INV, uint64_t B, bool L1, uint64_t LIM>
+struct Dft16B {
+    using S1 = Dft4L<INV, B, B, B, B, L1 ? (uint64_t(1) << 62) : 0>;
+    static constexpr uint64_t Y(int s1) { return (s1 & 1) ? S1::O13 : S1::O02; }
+    template <int Q2, int S1I>
+    using T = TwR<16, Q2 * S1I, INV, ((S1I & 1) ? S1::O13 : S1::O02)>;
+    template <int S1I>
+    using S2 = Dft4L<INV, ((S1I & 1) ? S1::O13 : S1::O02), T<1, S1I>::OUT, T<2, S1I>::OUT, T<3, S1I>::OUT, LIM>;
+    static constexpr uint64_t OUT = umax(umax(S2<0>::OUT, S2<1>::OUT), umax(S2<2>::OUT, S2<3>::OUT));
 };
 
-template <bool INV, uint64_t B>
-struct Dft<16, INV, B> {
-    static constexpr uint64_t B1 = Dft4<INV, B>::OUT;
-    static constexpr uint64_t tw_bound() {
-        uint64_t m = B1;
-        m = umax(m, TwR<16, 1, INV, B1>::OUT);
-        m = umax(m, TwR<16, 2, INV, B1>::OUT);
-        m = umax(m, TwR<16, 3, INV, B1>::OUT);
-        m = umax(m, TwR<16, 4, INV, B1>::OUT);
-        m = umax(m, TwR<16, 6, INV, B1>::OUT);
-        m = umax(m, TwR<16, 9, INV, B1>::OUT);
-        return m;
-    }
-    static constexpr uint64_t BT = tw_bound();
-    static constexpr uint64_t OUT = Dft4<INV, BT>::OUT;
+template <bool INV, uint64_t B, uint64_t LIM>
+struct Dft<16, INV, B, LIM> {
+    static constexpr bool L1 = LIM != 0 && Dft16B<INV, B, true, LIM>::OUT <= LIM;
+    using D = Dft16B<INV, B, L1, LIM>;
+    static constexpr uint64_t OUT = D::OUT;
     template <int Q2, int S1>
     __device__ __forceinline__ static uint32_t tw(uint32_t x) {
-        return TwR<16, Q2 * S1, INV, B1>::apply(x);
+        return D::template T<Q2, S1>::apply(x);
     }
     __device__ __forceinline__ static void run(const uint32_t (&x)[16], uint32_t (&y)[16]) {
         uint32_t z[4][4];  // z[q2][s1]
 #pragma unroll
-        for (int q2 = 0; q2 < 4; ++q2) Dft4<INV, B>::run(x[q2], x[q2 + 4], x[q2 + 8], x[q2 + 12], z[q2][0], z[q2][1], z[q2][2], z[q2][3]);
+        for (int q2 = 0; q2 < 4; ++q2)
+            D::S1::run(x[q2], x[q2 + 4], x[q2 + 8], x[q2 + 12], z[q2][0], z[q2][1], z[q2][2], z[q2][3]);
         z[1][1] = tw<1, 1>(z[1][1]);
         z[1][2] = tw<1, 2>(z[1][2]);
         z[1][3] = tw<1, 3>(z[1][3]);
@@ -334,33 +372,34 @@ struct Dft<16, INV, B> {
         z[3][1] = tw<3, 1>(z[3][1]);
         z[3][2] = tw<3, 2>(z[3][2]);
         z[3][3] = tw<3, 3>(z[3][3]);
-#pragma unroll
-        for (int s1 = 0; s1 < 4; ++s1)
-            Dft4<INV, BT>::run(z[0][s1], z[1][s1], z[2][s1], z[3][s1], y[s1], y[s1 + 4], y[s1 + 8], y[s1 + 12]);
+        D::template S2<0>::run(z[0][0], z[1][0], z[2][0], z[3][0], y[0], y[4], y[8], y[12]);
+        D::template S2<1>::run(z[0][1], z[1][1], z[2][1], z[3][1], y[1], y[5], y[9], y[13]);
+        D::template S2<2>::run(z[0][2], z[1][2], z[2][2], z[3][2], y[2], y[6], y[10], y[14]);
+        D::template S2<3>::run(z[0][3], z[1][3], z[2][3], z[3][3], y[3], y[7], y[11], y[15]);
     }
 };
 
 // DIF placement: natural in, v[rev(s)] = y_s out. DIT placement: v[rev(s)] in, natural out.
-template <int R, bool INV, uint64_t BIN>
+template <int R, bool INV, uint64_t BIN, uint64_t LIM = 0>
 __device__ __forceinline__ void dif_regs(uint32_t (&v)[R]) {
-    static_assert(Dft<R, INV, BIN>::OUT < (1ull << 31), "lazy bound overflow");
+    static_assert(Dft<R, INV, BIN, LIM>::OUT < (1ull << 31), "lazy bound overflow");
     uint32_t y[R];
-    Dft<R, INV, BIN>::run(v, y);
+    Dft<R, INV, BIN, LIM>::run(v, y);
 #pragma unroll
     for (int s = 0; s < R; ++s) v[rev<R>(s)] = y[s];
 }
-template <int R, bool INV, uint64_t BIN>
+template <int R, bool INV, uint64_t BIN, uint64_t LIM = 0>
 __device__ __forceinline__ void dit_regs(uint32_t (&v)[R]) {
-    static_assert(Dft<R, INV, BIN>::OUT < (1ull << 31), "lazy bound overflow");
+    static_assert(Dft<R, INV, BIN, LIM>::OUT < (1ull << 31), "lazy bound overflow");
     uint32_t x[R];
 #pragma unroll
     for (int s = 0; s < R; ++s) x[s] = v[rev<R>(s)];
-    Dft<R, INV, BIN>::run(x, v);
+    Dft<R, INV, BIN, LIM>::run(x, v);
 }
-template <int R, bool INV, uint64_t BIN>
-constexpr uint64_t dif_bound() { return Dft<R, INV, BIN>::OUT; }
-template <int R, bool INV, uint64_t BIN>
-constexpr uint64_t dit_bound() { return Dft<R, INV, BIN>::OUT; }
+template <int R, bool INV, uint64_t BIN, uint64_t LIM = 0>
+constexpr uint64_t dif_bound() { return Dft<R, INV, BIN, LIM>::OUT; }
+template <int R, bool INV, uint64_t BIN, uint64_t LIM = 0>
+constexpr uint64_t dit_bound() { return Dft<R, INV, BIN, LIM>::OUT; }
 
 template <int R>
 __host__ __device__ constexpr int rev(int i) {

@@ -167,9 +167,12 @@ __device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld
                 for (int q = 0; q < R; ++q) v[c][q] = ld(base + (uint32_t(q) << SL), b, q, col + c * WC);
 #pragma unroll
             for (int c = 0; c < CW; ++c) fix(v[c], base, b, col + c * WC);
+            // outputs with s > 0 go through a Shoup twiddle (any 32-bit input):
+            // the butterfly may leave its w4 products unreduced
+            constexpr uint64_t LZ = SL > 0 ? kLazyLim : 0;
 #pragma unroll
-            for (int c = 0; c < CW; ++c) dif_regs<R, INV, BIN>(v[c]);
-            constexpr uint64_t BO = dif_bound<R, INV, BIN>();
+            for (int c = 0; c < CW; ++c) dif_regs<R, INV, BIN, LZ>(v[c]);
+            constexpr uint64_t BO = dif_bound<R, INV, BIN, LZ>();
 #pragma unroll
             for (int s = 0; s < R; ++s) {
                 uint2 w = make_uint2(0, 0);

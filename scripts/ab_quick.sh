@@ -1,8 +1,8 @@
 #!/bin/bash
-# A/B two library builds with quick_time.py: ab_quick.sh old.so new.so [CFG:S ...]
-old=$1; new=$2; shift 2
+# A/B library builds with quick_time.py: ab_quick.sh "a.so b.so ..." [CFG:S ...]
+libs=$1; shift
 cp paper_0907_1788_b200/libfntrs_b200.so /tmp/cur.so
-for lib in $old $new; do
+for lib in $libs; do
   cp $lib paper_0907_1788_b200/libfntrs_b200.so
   echo "== $lib"; python scripts/quick_time.py "$@" 2>&1 | grep -v "^$"
 done

@@ -14,7 +14,7 @@ def t_ms(fn, reps=5):
     e.record(); torch.cuda.synchronize()
     return s.elapsed_time(e) / reps
 
-for name, stripes in [("C1", 1), ("C2", 4096), ("C5", 256)] + ([(a, int(b)) for a, b in (x.split(":") for x in sys.argv[1:])]):
+for name, stripes in ([("C1", 1), ("C2", 4096), ("C5", 256)] if len(sys.argv) < 2 else []) + ([(a, int(b)) for a, b in (x.split(":") for x in sys.argv[1:])]):
     cfg = W.CONFIGS[name]
     S = stripes
     src = torch.empty((S, cfg.k, cfg.L), dtype=torch.int16, device="cuda")
