@@ -88,10 +88,12 @@ __device__ __forceinline__ uint32_t mulws(uint32_t x, uint32_t w, uint32_t w2) {
     const uint32_t q = uint32_t(__mulhi(int32_t(x), int32_t(w2)));
     return x * w - mul_p(q);
 }
-// signed reduction: (-p, 2p)
+// signed reduction of any 32-bit x: x - floor(x / 2^16) p = (x mod 2^16) - floor(x / 2^16),
+// in [-2^15, 2^16 + 2^15) (inside (-p, 2p)); one shift + one IMAD (the multiplier
+// pipe is the codec kernels' busiest: this saves the two IMAD.HI slots of a Shoup quotient)
 __device__ __forceinline__ uint32_t reds(uint32_t x) {
-    const uint32_t q = uint32_t(__mulhi(int32_t(x), 65535));
-    return x - mul_p(q);
+    const uint32_t q = uint32_t(int32_t(x) >> 16);
+    return x - q * 65537u;
 }
 // |x| < 2p -> canonical [0, p)
 __device__ __forceinline__ uint32_t canon_s2p(uint32_t x) {

@@ -58,8 +58,8 @@ __device__ __forceinline__ uint32_t canon_b(uint32_t v) {
     if constexpr (B <= k2P) {
         return canon_s2p(v);
     } else {
-        static_assert(2 * ceil_p(B) < (1ull << 32), "");
-        return red2p(red(v + uint32_t(ceil_p(B))));  // [0, 2K) -> [0, 2p) -> [0, p)
+        static_assert(B < (1ull << 31), "");
+        return canon_s2p(reds(v));  // (-p, 2p) -> [0, p)
     }
 }
 
