@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
             // k = N/2: kept iff s < R/2 (compile time after unrolling)
             const bool keep = HALFK ? (s < RZ / 2) : (f < k);
             if (keep) __stcs(outp + (f * L + col), uint16_t(y));
-            return keep ? y >> 16 : 0u;  // canonical: bit 16 set iff y == 65536
+            return keep ? y : 0u;  // canonical, kept: bit 16 set iff y == 65536
         };
         auto flush_out = [&](uint32_t mask, uint32_t, uint32_t b, uint32_t col) {
             if (!mask) return;
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
                 else
                     keep = (HALFK ? (q >= R0 / 2) : (lrow >= k)) && lrow < n;
                 if (keep) __stcs(outp + (lrow * L + col), uint16_t(y));
-                return keep ? y >> 16 : 0u;
+                return keep ? y : 0u;
             };
             auto flush_sys = [&](uint32_t mask, uint32_t base, uint32_t, uint32_t col) {
                 if (!mask) return;

@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(G::NT, G::MINB) enc_fast_kernel(const __grid_c
             } else {
                 if (!PUNCT || f < n) __stcs(outp + (f * L + col), uint16_t(y));
             }
-            return (!PUNCT || f < n) ? y >> 16 : 0u;  // canonical: bit 16 set iff y == 65536
+            return (!PUNCT || f < n) ? y : 0u;  // canonical, kept: bit 16 set iff y == 65536
         };
         auto flush_out = [&](uint32_t mask, uint32_t, uint32_t b, uint32_t col) {
             if (!mask) return;

@@ -168,7 +168,7 @@ dec_gen_kernel(const __grid_constant__ CUtensorMap rx_map, const uint2* __restri
             const uint32_t f = perm_head<EM>(b) + (uint32_t(s) << (EM - RLB));
             const bool keep = f < k;
             if (keep) __stcs(outp + (f * L + col), uint16_t(y));
-            return keep ? y >> 16 : 0u;  // canonical: bit 16 set iff y == 65536
+            return keep ? y : 0u;  // canonical, kept: bit 16 set iff y == 65536
         };
         auto flush_out = [&](uint32_t mask, uint32_t, uint32_t b, uint32_t col) {
             if (!mask) return;

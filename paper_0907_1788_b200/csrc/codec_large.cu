@@ -142,7 +142,7 @@ enc_b_kernel(const uint2* __restrict__ ptab, uint32_t n, uint32_t L, uint32_t tp
             out_s[m2 * kLW + col] = uint16_t(y);
         else if (keep)
             __stcs(outp + (row * L + col), uint16_t(y));
-        return keep ? y >> 16 : 0u;  // canonical: bit 16 set iff y == 65536
+        return keep ? y : 0u;  // canonical, kept: bit 16 set iff y == 65536
     };
     auto flush = [&](uint32_t mask, uint32_t, uint32_t b, uint32_t col) {
         if (!mask) return;
@@ -397,7 +397,7 @@ dec_4_kernel(const uint2* __restrict__ ptabI, uint32_t k, uint32_t L, uint32_t t
         const uint32_t row = t1 + N1 * (perm_head<E2>(b) + (uint32_t(s) << (E2 - RLZ)));
         const bool keep = HALFK ? (s < RZ / 2) : (row < k);
         if (keep) __stcs(outp + (row * L + col), uint16_t(y));
-        return keep ? y >> 16 : 0u;  // canonical: bit 16 set iff y == 65536
+        return keep ? y : 0u;  // canonical, kept: bit 16 set iff y == 65536
     };
     auto flush = [&](uint32_t mask, uint32_t, uint32_t b, uint32_t col) {
         if (!mask) return;

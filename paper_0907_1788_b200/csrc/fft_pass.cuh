@@ -156,9 +156,9 @@ __device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld
         const uint32_t base = ((b >> SL) << LL) + t;
         uint32_t v[CW][R];
         const uint4* tq = twp + t * (R / 2);  // row t: r_len^(t s), s < R, two per uint4
-        uint32_t mask[CW];
+        uint32_t acc[CW];
 #pragma unroll
-        for (int c = 0; c < CW; ++c) mask[c] = 0;
+        for (int c = 0; c < CW; ++c) acc[c] = 0;
         uint4 w4 = make_uint4(0, 0, 0, 0);
         if constexpr (!DIT) {
 #pragma unroll
@@ -186,7 +186,9 @@ __device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld
                     } else {
                         y = cap<BO, OCAP>(y);
                     }
-                    mask[c] |= st(base + (uint32_t(s) << SL), b, s, col + c * WC, y) << s;
+                    const uint32_t r = st(base + (uint32_t(s) << SL), b, s, col + c * WC, y);
+                    v[c][rev<R>(s)] = r;
+                    acc[c] |= r;
                 }
             }
         } else {
@@ -208,11 +210,24 @@ __device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld
 #pragma unroll
             for (int c = 0; c < CW; ++c)
 #pragma unroll
-                for (int q = 0; q < R; ++q)
-                    mask[c] |= st(base + (uint32_t(q) << SL), b, q, col + c * WC, cap<BO, OCAP>(v[c][q])) << q;
+                for (int q = 0; q < R; ++q) {
+                    const uint32_t r = st(base + (uint32_t(q) << SL), b, q, col + c * WC, cap<BO, OCAP>(v[c][q]));
+                    v[c][q] = r;
+                    acc[c] |= r;
+                }
         }
+        // escapes are rare: the store functors return the kept canonical value
+        // (0 when not kept), OR-ed per codeword; only a group holding a 65536
+        // rebuilds its bit mask from the values parked in v
 #pragma unroll
-        for (int c = 0; c < CW; ++c) flush(mask[c], base, b, col + c * WC);
+        for (int c = 0; c < CW; ++c) {
+            if (acc[c] >> 16) {
+                uint32_t mask = 0;
+#pragma unroll
+                for (int s = 0; s < R; ++s) mask |= ((v[c][DIT ? s : rev<R>(s)] >> 16) & 1u) << s;
+                flush(mask, base, b, col + c * WC);
+            }
+        }
     }
 }
 
