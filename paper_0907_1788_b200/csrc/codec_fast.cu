@@ -25,6 +25,12 @@
 //   zeroed); FNT2's last DIT pass, the product with A_hat and FNT3's first
 //   DIF pass are fused in registers; FNT3's last pass writes the k decoded
 //   packets.
+// Encode computes q * p (Shoup products, signed reductions) as one LEA on the
+// ALU pipe (field.cuh, FNTRS_LEA): C2 encode 944 -> 972 GB/s (the decode unit,
+// codec_dec.cu, keeps the IMAD form: its ALU pipe is the fuller one).
+#ifndef FNTRS_LEA
+#define FNTRS_LEA 1
+#endif
 #include <cuda.h>
 #include <cuda_runtime.h>
 

@@ -69,7 +69,10 @@ struct MulPow2 {
             return neg ? 0u - x : x;
         } else {
             const uint32_t xh = uint32_t(int32_t(x) >> (16 - s));
-#if FNTRS_LEA  // SHF (ALU) + LEA (ALU) + one IMAD: x 2^s -/+ xh p
+#if FNTRS_POW2_ALU  // no multiplier-pipe IMAD: (x << s) - (xh << 16) - xh as shifts + one IADD3
+            const uint32_t xs = x << s, xh16 = xh << 16;
+            return neg ? add3_a(xh16, xh, 0u - xs) : subsub_a(xs, xh16, xh);
+#elif FNTRS_LEA  // SHF (ALU) + LEA (ALU) + one IMAD: x 2^s -/+ xh p
             return neg ? mad_lo(x, 0u - (1u << s), mul_p(xh)) : mad_lo(x, 1u << s, 0u - mul_p(xh));
 #else
             const uint32_t xs = x << s;

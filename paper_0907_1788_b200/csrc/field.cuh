@@ -44,9 +44,9 @@ __host__ __device__ constexpr uint32_t croot(uint32_t n, bool inverse) {
 // IMAD.HI / IMAD.WIDE at two slots each) is the busiest pipe in every codec
 // kernel, and ptxas also places plain adds and shifts there (IMAD.IADD,
 // IMAD.SHL). q * p = (q << 16) + q is one LEA on the ALU pipe; written as
-// PTX shl + add so NVVM cannot fold it back into a multiply. Off by default:
-// ptxas re-balances by moving other adds to IMAD.IADD (executed multiplier
-// instructions unchanged, kernels 1-4 % slower; profiles/README.md).
+// PTX shl + add so NVVM cannot fold it back into a multiply. Off by default
+// (decode: ptxas re-balances by moving other adds to IMAD.IADD, 1-4 % slower);
+// the encode unit (codec_fast.cu) turns it on (+3 %; profiles/README.md).
 #ifndef FNTRS_LEA
 #define FNTRS_LEA 0
 #endif
