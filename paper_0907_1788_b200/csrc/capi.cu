@@ -167,7 +167,15 @@ int sort_escapes(fntrs_ctx* ctx, const EscOut& eout, uint64_t max_key, cudaStrea
     return FNTRS_OK;
 }
 
-constexpr size_t kScratchCap = size_t(2) << 30;  // per four-step intermediate buffer
+constexpr size_t kScratchCapDefault = size_t(2) << 30;  // per four-step intermediate buffer
+// FNTRS_SCRATCH_MB overrides the four-step batch size (measurement hook)
+size_t scratch_cap() {
+    static const size_t cap = [] {
+        const char* e = getenv("FNTRS_SCRATCH_MB");
+        return e ? size_t(atoll(e)) << 20 : kScratchCapDefault;
+    }();
+    return cap;
+}
 
 // Per-call stream-ordered scratch (released in stream order by release_scratch),
 // so concurrent calls on different streams never share intermediates.
@@ -337,7 +345,7 @@ int encode_impl(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t N, uint32_t str
                          reinterpret_cast<uintptr_t>(src) % 16 == 0;
     if (N > kTileMaxN && !large) {  // general column path (codec_cols.cu)
         if (stripes && L) {
-            const uint64_t cap = std::min<uint64_t>(uint64_t(stripes) * L, fast::cols_batch_columns(N, kScratchCap));
+            const uint64_t cap = std::min<uint64_t>(uint64_t(stripes) * L, fast::cols_batch_columns(N, kScratchCapDefault));
             Scratch sc;
             rc = get_scratch(ctx, sc, size_t(N) * cap * 4, 2, st);
             if (rc) return rc;
@@ -351,7 +359,7 @@ int encode_impl(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t N, uint32_t str
     }
     if (large) {
         if (stripes && L) {
-            const uint32_t batch = std::min(stripes, fast::large_batch(N, L, kScratchCap));
+            const uint32_t batch = std::min(stripes, fast::large_batch(N, L, scratch_cap()));
             Scratch sc;
             rc = get_scratch(ctx, sc, size_t(batch) * N * L * 4, 1, st);
             if (rc) return rc;
@@ -614,7 +622,7 @@ int fntrs_gpu_decode(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t stripes, ui
     if (pl->cols || (large_plan && L % fast::large_tile_columns())) {  // general column path
         if (stripes && L) {
             const uint32_t D = std::max(pl->N, pl->M);
-            const uint64_t cap = std::min<uint64_t>(uint64_t(stripes) * L, fast::cols_batch_columns(D, kScratchCap));
+            const uint64_t cap = std::min<uint64_t>(uint64_t(stripes) * L, fast::cols_batch_columns(D, kScratchCapDefault));
             Scratch sc;
             rc = get_scratch(ctx, sc, size_t(D) * cap * 4, pl->split ? 4 : 3, st);
             if (rc) return rc;
@@ -628,7 +636,7 @@ int fntrs_gpu_decode(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t stripes, ui
         }
     } else if (large_plan) {
         if (stripes && L) {
-            const uint32_t batch = std::min(stripes, fast::large_batch(pl->N, L, kScratchCap));
+            const uint32_t batch = std::min(stripes, fast::large_batch(pl->N, L, scratch_cap()));
             Scratch sc;
             rc = get_scratch(ctx, sc, size_t(batch) * pl->N * L * 4, 2, st);
             if (rc) return rc;
