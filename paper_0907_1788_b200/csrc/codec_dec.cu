@@ -156,11 +156,25 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
             work[G::template idx_flip<FLIP + 1>(lrow, col)] = y;
             return 0u;
         };
+        // output row f = perm_head(b) + s N/R. At n_domain <= 256: one 64-bit
+        // pointer per butterfly group, stepped by N/R rows per output (64-bit adds
+        // on the ALU pipe instead of an IMAD.WIDE per store on the busier
+        // multiplier pipe: C2 decode +1.1 %; at n_domain 4096, one CTA per SM,
+        // the extra live pointer costs 3 %)
+        constexpr bool STEP = E <= 8;
+        uint16_t* op = outp;
+        const uint64_t ostep = opaque_stride(uint64_t(L) << (E - RLZ + 1));
         auto st_out = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) -> uint32_t {
             const uint32_t f = perm_head<E>(b) + (uint32_t(s) << (E - RLZ));
+            if (!STEP)
+                op = outp + (f * L + col);
+            else if (s == 0)
+                op = outp + (perm_head<E>(b) * L + col);
+            else
+                op = step_ptr(op, ostep);
             // k = N/2: kept iff s < R/2 (compile time after unrolling)
             const bool keep = HALFK ? (s < RZ / 2) : (f < k);
-            if (keep) __stcs(outp + (f * L + col), uint16_t(y));
+            if (keep) __stcs(op, uint16_t(y));
             return keep ? y : 0u;  // canonical, kept: bit 16 set iff y == 65536
         };
         auto flush_out = [&](uint32_t mask, uint32_t, uint32_t b, uint32_t col) {

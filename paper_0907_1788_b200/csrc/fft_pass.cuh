@@ -45,6 +45,16 @@ __device__ __forceinline__ T* launder(T* p) {
     return p;
 }
 
+// A byte stride whose high word ptxas cannot prove zero (it carries the
+// run-time zero g_alu_zero), so that p + stride stays a 64-bit add on the ALU
+// pipe (IADD3 + IADD3.X) instead of becoming an IMAD.WIDE (two multiplier slots)
+__device__ __forceinline__ uint64_t opaque_stride(uint64_t bytes) {
+    return bytes | (uint64_t(g_alu_zero) << 32);
+}
+__device__ __forceinline__ uint16_t* step_ptr(uint16_t* p, uint64_t stride_bytes) {
+    return reinterpret_cast<uint16_t*>(reinterpret_cast<uint64_t>(p) + stride_bytes);
+}
+
 template <int N>
 constexpr int ilog2c() {
     int e = 0;
