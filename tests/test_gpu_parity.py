@@ -243,7 +243,12 @@ def test_complete_reception_large_domain(codec, oracle):  # codec.cpp:137-144 at
 
 
 @pytest.mark.parametrize("k,n,L,S", [(128, 256, 128, 3), (1024, 2048, 64, 1), (2048, 4096, 32, 1), (300, 512, 64, 1),
-                                     (200, 256, 64, 2), (50, 256, 64, 2), (600, 1024, 32, 1)])
+                                     (200, 256, 64, 2), (50, 256, 64, 2), (600, 1024, 32, 1),
+                                     # many tiles per persistent CTA (counter-claimed tiles, TMA prefetch of
+                                     # the next tile, mbarrier phases) in every fused family: n_domain 256
+                                     # k = n/2 and k != n/2, M = 2N and M < N, n_domain 4096 at one CTA per SM
+                                     (128, 256, 64, 1200), (100, 256, 64, 1600), (200, 256, 64, 1200),
+                                     (50, 256, 64, 1200), (2048, 4096, 16, 200), (1500, 4096, 16, 200)])
 def test_fast_kernels_match_general_kernels(codec, k, n, L, S):
     """A/B: the fused v2 kernels and the general tile kernels agree bit for bit."""
     from paper_0907_1788_b200 import _lib, escapes_to_numpy, workload as W
