@@ -65,6 +65,8 @@ SYS_SHAPES = [  # (k, n, L, stripes): general kernels, fused N <= 4096 kernels, 
     (1, 6, 8, 2), (2, 4, 16, 3), (4, 8, 8, 2), (5, 13, 7, 2), (300, 700, 8, 1), (8, 8, 16, 2),
     (64, 128, 64, 3), (128, 256, 64, 4), (100, 256, 32, 2), (1024, 2048, 64, 1), (2048, 4096, 32, 1),
     (700, 2048, 32, 1), (4096, 8192, 64, 1), (8192, 16384, 64, 1),
+    # many tiles per persistent CTA (fused MODE 1 / 2 at n_domain 256 and 4096)
+    (128, 256, 64, 1200), (2048, 4096, 16, 200),
 ]
 
 
