@@ -69,17 +69,27 @@ def profiled_traffic(cfg, chunk, systematic):
         return None
 
 
-def profiled_issue(cfg, chunk, systematic):
-    """The decode kernel's SM issue-slot utilisation (its binding roofline: the
-    integer pipes) from the committed capture, as a fraction."""
+def profiled_pct(cfg, chunk, systematic, metric):
+    """A percentage metric of the decode launch from the committed capture, as a fraction."""
     row = _profile_row(cfg, chunk, systematic)
     if row is None:
         return None
     h, u, v = row
     try:
-        return round(float(v[h.index("smsp__issue_active.avg.pct_of_peak_sustained_active")]) / 100.0, 4)
+        return round(float(v[h.index(metric)]) / 100.0, 4)
     except Exception:
         return None
+
+
+def profiled_issue(cfg, chunk, systematic):
+    """The decode kernel's SM issue-slot utilisation from the committed capture."""
+    return profiled_pct(cfg, chunk, systematic, "smsp__issue_active.avg.pct_of_peak_sustained_active")
+
+
+def profiled_multiplier(cfg, chunk, systematic):
+    """The decode kernel's busiest unit, the integer multiplier (FMA-heavy) pipe:
+    its binding roofline in place of HBM (same capture)."""
+    return profiled_pct(cfg, chunk, systematic, "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed")
 
 
 def hbm_peak():
@@ -446,8 +456,9 @@ def run_gpu(args, rank, world, local_rank):
             "traffic": args.traffic if args.traffic is not None else profiled_traffic(cfg, chunk, SYSTEMATIC),
             "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum per launch "
                               "(profiles/r01_ncu_full_raw.csv)",
-            # what bounds it instead of HBM: integer issue (ncu smsp__issue_active, same capture)
+            # what bounds it instead of HBM: the integer multiplier pipe and SM issue (same capture)
             "issue_active_frac": profiled_issue(cfg, chunk, SYSTEMATIC),
+            "multiplier_pipe_busy_frac": profiled_multiplier(cfg, chunk, SYSTEMATIC),
             "algorithmic_bytes_per_launch": dec_bytes, "avg_launch_ms": round(dec_launch_ms, 4),
         },
         "roofline_encode": {
