@@ -11,7 +11,13 @@ namespace fntrs_gpu {
 namespace fast {
 namespace {
 
-constexpr uint64_t kSmemCap = 1ull << 20;  // bound of values kept in shared memory
+#ifndef FNTRS_SMEM_CAP
+#define FNTRS_SMEM_CAP (2ull * 65537ull)
+#endif
+constexpr uint64_t kSmemCap = FNTRS_SMEM_CAP;
+#ifndef FNTRS_LAZY_LAST
+#define FNTRS_LAZY_LAST 1
+#endif  // bound of values kept in shared memory
 constexpr uint64_t k2P = 2 * kP64;
 constexpr uint32_t kGuardBytes = 128;  // guard row slot below each decode stage buffer
 
@@ -179,7 +185,8 @@ __device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld
             for (int c = 0; c < CW; ++c) fix(v[c], base, b, col + c * WC);
             // outputs with s > 0 go through a Shoup twiddle (any 32-bit input):
             // the butterfly may leave its w4 products unreduced
-            constexpr uint64_t LZ = SL > 0 ? kLazyLim : 0;
+            // (a canonical last pass reduces every output anyway: lazy there too, FNTRS_LAZY_LAST)
+            constexpr uint64_t LZ = (SL > 0 || (FNTRS_LAZY_LAST && OCAP == kCanon)) ? kLazyLim : 0;
 #pragma unroll
             for (int c = 0; c < CW; ++c) dif_regs<R, INV, BIN, LZ>(v[c]);
             constexpr uint64_t BO = dif_bound<R, INV, BIN, LZ>();
