@@ -19,6 +19,12 @@
 #ifndef FNTRS_ALU_ADDS
 #define FNTRS_ALU_ADDS 1
 #endif
+#ifndef FNTRS_R2D_LIM
+#define FNTRS_R2D_LIM (1ull << 22)
+#endif
+#ifndef FNTRS_R2T_LIM
+#define FNTRS_R2T_LIM (1ull << 30)
+#endif
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -201,8 +207,11 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
         // logical group b' = N/R - 1 - g holds s'_j = F[N-1-j]; j >= k zeroed.
         {
             constexpr int ITEMS = (N / RZ) * WT;
-            constexpr uint64_t BD = dif_bound<RZ, false, kSmemCap>();
-            constexpr uint64_t BT = dit_bound<RZ, false, BD>();
+            // P == 2: the DIT outputs go into Shoup products (lazy w4 products up to 2^30); the
+            // DIF feeding it may be lazy up to R2D_LIM
+            constexpr uint64_t L2D = P == 2 ? uint64_t(FNTRS_R2D_LIM) : 0, L2T = P == 2 ? uint64_t(FNTRS_R2T_LIM) : 0;
+            constexpr uint64_t BD = dif_bound<RZ, false, kSmemCap, L2D>();
+            constexpr uint64_t BT = dit_bound<RZ, false, BD, L2T>();
 #pragma unroll 1
             for (int it = threadIdx.x; it < ITEMS; it += NT) {
                 const uint32_t col = uint32_t(it) & uint32_t(WT - 1);
@@ -210,7 +219,7 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
                 uint32_t v[RZ];
 #pragma unroll
                 for (int q = 0; q < RZ; ++q) v[q] = work[G::idx((g << RLZ) + q, col)];
-                dif_regs<RZ, false, kSmemCap>(v);
+                dif_regs<RZ, false, kSmemCap, L2D>(v);
                 const uint32_t fh = perm_head<E>(uint32_t(N / RZ) - 1u - g);
                 uint32_t u[RZ];
 #pragma unroll
@@ -219,7 +228,7 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
                     const bool live = HALFK ? ((j & 1) == 0) : (fh + (uint32_t(rev<RZ>(j)) << (E - RLZ)) < k);
                     u[j] = live ? v[RZ - 1 - j] : 0u;
                 }
-                dit_regs<RZ, false, BD>(u);
+                dit_regs<RZ, false, BD, L2T>(u);
                 if constexpr (P == 2) {
                     // FNT2's last DIT pass pre-multiplies logical row t + s*sub0 by r^(t s);
                     // this element is t = q, s = N/R - 1 - g: apply it here, where the
