@@ -31,6 +31,12 @@
 #ifndef FNTRS_LEA
 #define FNTRS_LEA 1
 #endif
+// Two-codeword encode items pin the second codeword's butterfly adds to the ALU
+// pipe and leave the first to ptxas, which otherwise moves ~1200 adds per 32
+// codewords onto the multiplier pipe as IMAD.IADD (C2 encode 976 -> 1023 GB/s).
+#ifndef FNTRS_SPLIT_PIN
+#define FNTRS_SPLIT_PIN 1
+#endif
 #include <cuda.h>
 #include <cuda_runtime.h>
 

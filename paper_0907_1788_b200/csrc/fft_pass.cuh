@@ -15,6 +15,9 @@ namespace {
 #define FNTRS_SMEM_CAP (2ull * 65537ull)
 #endif
 constexpr uint64_t kSmemCap = FNTRS_SMEM_CAP;
+#ifndef FNTRS_SPLIT_PIN
+#define FNTRS_SPLIT_PIN 0
+#endif
 #ifndef FNTRS_LAZY_LAST
 #define FNTRS_LAZY_LAST 1
 #endif  // bound of values kept in shared memory
@@ -187,8 +190,15 @@ __device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld
             // the butterfly may leave its w4 products unreduced
             // (a canonical last pass reduces every output anyway: lazy there too, FNTRS_LAZY_LAST)
             constexpr uint64_t LZ = (SL > 0 || (FNTRS_LAZY_LAST && OCAP == kCanon)) ? kLazyLim : 0;
+            // FNTRS_SPLIT_PIN: the second codeword of a two-codeword item pins its
+            // butterfly adds to the ALU pipe (ptxas balances the first)
 #pragma unroll
-            for (int c = 0; c < CW; ++c) dif_regs<R, INV, BIN, LZ>(v[c]);
+            for (int c = 0; c < CW; ++c) {
+                if (FNTRS_SPLIT_PIN && c == 1)
+                    dif_regs<R, INV, BIN, LZ, true>(v[c]);
+                else
+                    dif_regs<R, INV, BIN, LZ>(v[c]);
+            }
             constexpr uint64_t BO = dif_bound<R, INV, BIN, LZ>();
 #pragma unroll
             for (int s = 0; s < R; ++s) {

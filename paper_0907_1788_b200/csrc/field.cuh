@@ -78,52 +78,65 @@ __device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {
 #define FNTRS_ALU_ADDS 0
 #endif
 static __constant__ uint32_t g_alu_zero;  // never written: 0
-__device__ __forceinline__ uint32_t add_a(uint32_t a, uint32_t b) {
-#if FNTRS_ALU_ADDS
-    uint32_t r;
-    asm("{\n\t.reg .b32 t;\n\tadd.u32 t, %1, %2;\n\tadd.u32 %0, t, %3;\n\t}" : "=r"(r) : "r"(a), "r"(b), "r"(g_alu_zero));
-    return r;
-#else
-    return a + b;
-#endif
+// P = true: pinned to the ALU pipe as described; P = false: plain C++ adds
+// (ptxas places them). The *_a forms follow FNTRS_ALU_ADDS.
+template <bool P>
+__device__ __forceinline__ uint32_t add_p(uint32_t a, uint32_t b) {
+    if constexpr (P) {
+        uint32_t r;
+        asm("{\n\t.reg .b32 t;\n\tadd.u32 t, %1, %2;\n\tadd.u32 %0, t, %3;\n\t}" : "=r"(r) : "r"(a), "r"(b), "r"(g_alu_zero));
+        return r;
+    } else {
+        return a + b;
+    }
 }
-__device__ __forceinline__ uint32_t sub_a(uint32_t a, uint32_t b) {
-#if FNTRS_ALU_ADDS
-    uint32_t r;
-    asm("{\n\t.reg .b32 t;\n\tsub.u32 t, %1, %2;\n\tadd.u32 %0, t, %3;\n\t}" : "=r"(r) : "r"(a), "r"(b), "r"(g_alu_zero));
-    return r;
-#else
-    return a - b;
-#endif
+template <bool P>
+__device__ __forceinline__ uint32_t sub_p(uint32_t a, uint32_t b) {
+    if constexpr (P) {
+        uint32_t r;
+        asm("{\n\t.reg .b32 t;\n\tsub.u32 t, %1, %2;\n\tadd.u32 %0, t, %3;\n\t}" : "=r"(r) : "r"(a), "r"(b), "r"(g_alu_zero));
+        return r;
+    } else {
+        return a - b;
+    }
 }
 // a + b + c, a + b - c, a - b - c as one IADD3 each
-__device__ __forceinline__ uint32_t add3_a(uint32_t a, uint32_t b, uint32_t c) {
-#if FNTRS_ALU_ADDS
-    uint32_t r;
-    asm("{\n\t.reg .b32 t;\n\tadd.u32 t, %1, %2;\n\tadd.u32 %0, t, %3;\n\t}" : "=r"(r) : "r"(a), "r"(b), "r"(c));
-    return r;
-#else
-    return a + b + c;
-#endif
+template <bool P>
+__device__ __forceinline__ uint32_t add3_p(uint32_t a, uint32_t b, uint32_t c) {
+    if constexpr (P) {
+        uint32_t r;
+        asm("{\n\t.reg .b32 t;\n\tadd.u32 t, %1, %2;\n\tadd.u32 %0, t, %3;\n\t}" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+        return r;
+    } else {
+        return a + b + c;
+    }
 }
-__device__ __forceinline__ uint32_t addsub_a(uint32_t a, uint32_t b, uint32_t c) {
-#if FNTRS_ALU_ADDS
-    uint32_t r;
-    asm("{\n\t.reg .b32 t;\n\tadd.u32 t, %1, %2;\n\tsub.u32 %0, t, %3;\n\t}" : "=r"(r) : "r"(a), "r"(b), "r"(c));
-    return r;
-#else
-    return a + b - c;
-#endif
+template <bool P>
+__device__ __forceinline__ uint32_t addsub_p(uint32_t a, uint32_t b, uint32_t c) {
+    if constexpr (P) {
+        uint32_t r;
+        asm("{\n\t.reg .b32 t;\n\tadd.u32 t, %1, %2;\n\tsub.u32 %0, t, %3;\n\t}" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+        return r;
+    } else {
+        return a + b - c;
+    }
 }
-__device__ __forceinline__ uint32_t subsub_a(uint32_t a, uint32_t b, uint32_t c) {
-#if FNTRS_ALU_ADDS
-    uint32_t r;
-    asm("{\n\t.reg .b32 t;\n\tsub.u32 t, %1, %2;\n\tsub.u32 %0, t, %3;\n\t}" : "=r"(r) : "r"(a), "r"(b), "r"(c));
-    return r;
-#else
-    return a - b - c;
-#endif
+template <bool P>
+__device__ __forceinline__ uint32_t subsub_p(uint32_t a, uint32_t b, uint32_t c) {
+    if constexpr (P) {
+        uint32_t r;
+        asm("{\n\t.reg .b32 t;\n\tsub.u32 t, %1, %2;\n\tsub.u32 %0, t, %3;\n\t}" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+        return r;
+    } else {
+        return a - b - c;
+    }
 }
+constexpr bool kAluAdds = FNTRS_ALU_ADDS != 0;
+__device__ __forceinline__ uint32_t add_a(uint32_t a, uint32_t b) { return add_p<kAluAdds>(a, b); }
+__device__ __forceinline__ uint32_t sub_a(uint32_t a, uint32_t b) { return sub_p<kAluAdds>(a, b); }
+__device__ __forceinline__ uint32_t add3_a(uint32_t a, uint32_t b, uint32_t c) { return add3_p<kAluAdds>(a, b, c); }
+__device__ __forceinline__ uint32_t addsub_a(uint32_t a, uint32_t b, uint32_t c) { return addsub_p<kAluAdds>(a, b, c); }
+__device__ __forceinline__ uint32_t subsub_a(uint32_t a, uint32_t b, uint32_t c) { return subsub_p<kAluAdds>(a, b, c); }
 
 // x * w mod p into [0, 2p); w < p canonical, x any uint32.
 __device__ __forceinline__ uint32_t mulw(uint32_t x, uint32_t w) {
