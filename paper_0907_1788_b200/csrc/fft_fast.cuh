@@ -249,6 +249,9 @@ struct Dft4 {
 #define FNTRS_LAZY_LIM (1ull << 30)
 #endif
 constexpr uint64_t kLazyLim = FNTRS_LAZY_LIM;
+#ifndef FNTRS_PIN_SHIFT
+#define FNTRS_PIN_SHIFT 0
+#endif
 
 template <bool INV, uint64_t B0, uint64_t B1, uint64_t B2, uint64_t B3, uint64_t LIM, bool PIN = kAluAdds>
 struct Dft4L {
@@ -265,7 +268,7 @@ struct Dft4L {
         const uint32_t b = add_p<PIN>(x1, x3);
         uint32_t d;
         if constexpr (lazy)
-            d = (INV ? sub_p<PIN>(x1, x3) : sub_p<PIN>(x3, x1)) << 8;
+            d = shl_p<PIN && FNTRS_PIN_SHIFT, 8>(INV ? sub_p<PIN>(x1, x3) : sub_p<PIN>(x3, x1));
         else
             d = M::apply(sub_p<PIN>(x1, x3));
         y0 = add3_p<PIN>(x0, x2, b);

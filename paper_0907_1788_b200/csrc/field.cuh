@@ -131,6 +131,18 @@ __device__ __forceinline__ uint32_t subsub_p(uint32_t a, uint32_t b, uint32_t c)
         return a - b - c;
     }
 }
+// x << S on the ALU pipe when P (a funnel shift whose low word is the run-time
+// zero, so ptxas cannot fold it into an IMAD with the following add)
+template <bool P, int S>
+__device__ __forceinline__ uint32_t shl_p(uint32_t x) {
+    if constexpr (P) {
+        uint32_t r;
+        asm("shf.l.clamp.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(g_alu_zero), "r"(x), "n"(S));
+        return r;
+    } else {
+        return x << S;
+    }
+}
 constexpr bool kAluAdds = FNTRS_ALU_ADDS != 0;
 __device__ __forceinline__ uint32_t add_a(uint32_t a, uint32_t b) { return add_p<kAluAdds>(a, b); }
 __device__ __forceinline__ uint32_t sub_a(uint32_t a, uint32_t b) { return sub_p<kAluAdds>(a, b); }
