@@ -17,6 +17,10 @@
 //   D3  FNT2 pass B + (. A_hat) + FNT3 pass A (both on the coset q2 mod N2)
 //   D4  FNT3 pass B, writing the k decoded packets.
 // Intermediates (uint32, < 2p) go through a stripe-batched HBM scratch.
+// q * p as LEA (field.cuh, FNTRS_LEA): C4 decode +0.9 %, C3 encode +1.7 %
+#ifndef FNTRS_LEA
+#define FNTRS_LEA 1
+#endif
 #include <cuda.h>
 #include <cuda_runtime.h>
 
