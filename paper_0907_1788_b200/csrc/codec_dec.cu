@@ -212,9 +212,9 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
         // logical group b' = N/R - 1 - g holds s'_j = F[N-1-j]; j >= k zeroed.
         {
             constexpr int ITEMS = (N / RZ) * WT;
-            // P == 2: the DIT outputs go into Shoup products (lazy w4 products up to 2^30); the
-            // DIF feeding it may be lazy up to R2D_LIM
-            constexpr uint64_t L2D = P == 2 ? uint64_t(FNTRS_R2D_LIM) : 0, L2T = P == 2 ? uint64_t(FNTRS_R2T_LIM) : 0;
+            // the DIT outputs go into Shoup products (P == 2) or are folded to 2p for the tile
+            // (P == 3) either way: lazy w4 products up to 2^30; the DIF feeding it up to R2D_LIM
+            constexpr uint64_t L2D = uint64_t(FNTRS_R2D_LIM), L2T = uint64_t(FNTRS_R2T_LIM);
             constexpr uint64_t BD = dif_bound<RZ, false, kSmemCap, L2D>();
             constexpr uint64_t BT = dit_bound<RZ, false, BD, L2T>();
 #pragma unroll 1
@@ -312,8 +312,8 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
             // DIT pass, in registers on the same rows (reversed view)
             {
                 constexpr int ITEMS = (N / RZ) * WT;
-                constexpr uint64_t BD = dif_bound<RZ, true, kSmemCap>();
-                constexpr uint64_t BT = dit_bound<RZ, false, BD>();
+                constexpr uint64_t BD = dif_bound<RZ, true, kSmemCap, uint64_t(FNTRS_R2D_LIM)>();
+                constexpr uint64_t BT = dit_bound<RZ, false, BD, uint64_t(FNTRS_R2T_LIM)>();  // folded to 2p below
 #pragma unroll 1
                 for (int it = threadIdx.x; it < ITEMS; it += NT) {
                     const uint32_t col = uint32_t(it) & uint32_t(WT - 1);
@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
                     uint32_t v[RZ];
 #pragma unroll
                     for (int q = 0; q < RZ; ++q) v[q] = work[G::template idx_flip<FLIP + 1>((g << RLZ) + q, col)];
-                    dif_regs<RZ, true, kSmemCap>(v);
+                    dif_regs<RZ, true, kSmemCap, uint64_t(FNTRS_R2D_LIM)>(v);
                     const uint32_t fh = perm_head<E>(g);
 #pragma unroll
                     for (int s2 = 0; s2 < RZ; ++s2) {  // output s2 holds coefficient fh + s2 * N/R
@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
                         if (!live) v[rev<RZ>(s2)] = 0u;
                     }
                     // DIT input x_s = y_s (same rows): v[rev(s)] already is y_s
-                    dit_regs<RZ, false, BD>(v);
+                    dit_regs<RZ, false, BD, uint64_t(FNTRS_R2T_LIM)>(v);
 #pragma unroll
                     for (int q = 0; q < RZ; ++q)
                         work[G::template idx_flip<FLIP + 1>((g << RLZ) + q, col)] = cap<BT, kSmemCap>(v[q]);

@@ -268,8 +268,9 @@ dec_2_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, uin
     // s'_{i1' + N1 i2'} zeroed when i1' + N1 i2' >= k)
     {
         constexpr int ITEMS = (int(N2) / RZ) * kLW;
-        constexpr uint64_t BD = dif_bound<RZ, false, kSmemCap>();
-        constexpr uint64_t BT = dit_bound<RZ, false, BD>();
+        // the DIT outputs are folded to 2p for the tile anyway: lazy w4 products (fft_fast.cuh)
+        constexpr uint64_t BD = dif_bound<RZ, false, kSmemCap, (1ull << 22)>();
+        constexpr uint64_t BT = dit_bound<RZ, false, BD, kLazyLim>();
 #pragma unroll 1
         for (int it = threadIdx.x; it < ITEMS; it += kLNT) {
             const uint32_t col = uint32_t(it) & uint32_t(kLW - 1);
@@ -277,7 +278,7 @@ dec_2_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, uin
             uint32_t v[RZ];
 #pragma unroll
             for (int q = 0; q < RZ; ++q) v[q] = work[G::idx((g << RLZ) + q, col)];
-            dif_regs<RZ, false, kSmemCap>(v);
+            dif_regs<RZ, false, kSmemCap, (1ull << 22)>(v);
             const uint32_t fh = perm_head<E2>(N2 / RZ - 1u - g);
             uint32_t u[RZ];
 #pragma unroll
@@ -286,7 +287,7 @@ dec_2_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, uin
                 const bool live = HALFK ? ((j & 1) == 0) : (i1p + N1 * i2p < k);
                 u[j] = live ? v[RZ - 1 - j] : 0u;
             }
-            dit_regs<RZ, false, BD>(u);
+            dit_regs<RZ, false, BD, kLazyLim>(u);
 #pragma unroll
             for (int q = 0; q < RZ; ++q) work[G::idx((g << RLZ) + (RZ - 1 - q), col)] = cap<BT, kSmemCap>(u[q]);
         }
@@ -334,7 +335,7 @@ dec_3_kernel(const uint2* __restrict__ ptabF, const uint2* __restrict__ ptabI, c
     // FNT2 pass B last radix pass + (. ahat at q2 + N2 q1) + FNT3 pass A first DIT pass (inverse)
     {
         constexpr int ITEMS = (int(N1) / RZ) * kLW;
-        constexpr uint64_t BT = dit_bound<RZ, true, k2P>();
+        constexpr uint64_t BT = dit_bound<RZ, true, k2P, kLazyLim>();  // folded to 2p for the tile
 #pragma unroll 1
         for (int it = threadIdx.x; it < ITEMS; it += kLNT) {
             const uint32_t col = uint32_t(it) & uint32_t(kLW - 1);
@@ -342,7 +343,7 @@ dec_3_kernel(const uint2* __restrict__ ptabF, const uint2* __restrict__ ptabI, c
             uint32_t v[RZ];
 #pragma unroll
             for (int q = 0; q < RZ; ++q) v[q] = work[G::idx((g << RLZ) + q, col)];
-            dif_regs<RZ, false, kSmemCap>(v);  // v[rev(s)] = X2 at q1 = fh + s * N1/RZ
+            dif_regs<RZ, false, kSmemCap, kLazyLim>(v);  // v[rev(s)] = X2 at q1 = fh + s * N1/RZ (Shoup'd by ahat)
             const uint32_t fh = perm_head<E1>(g);
 #pragma unroll
             for (int s = 0; s < RZ; ++s) {
@@ -350,7 +351,7 @@ dec_3_kernel(const uint2* __restrict__ ptabF, const uint2* __restrict__ ptabI, c
                 const uint2 a = __ldg(ah + q2 + N2 * q1);
                 v[rev<RZ>(s)] = mulws(v[rev<RZ>(s)], a.x, a.y);  // DIT input order: u[rev(s)] = x_s
             }
-            dit_regs<RZ, true, k2P>(v);
+            dit_regs<RZ, true, k2P, kLazyLim>(v);
 #pragma unroll
             for (int q = 0; q < RZ; ++q) work[G::idx((g << RLZ) + q, col)] = cap<BT, kSmemCap>(v[q]);
         }
