@@ -44,3 +44,19 @@ def max_over_ranks(values, device=None):
     t = torch.tensor(vals, dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return [float(x) for x in t.cpu()]
+
+
+def sum_over_ranks(values, device=None):
+    """Element-wise sum of a list of integers over all ranks (identity when not
+    distributed): gathers per-rank mismatch counts to every rank, outside any
+    timed region (NCCL only for digests / counts)."""
+    import torch
+    import torch.distributed as dist
+    vals = [int(v) for v in values]
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return vals
+    if dist.get_backend() == "gloo":
+        device = "cpu"
+    t = torch.tensor(vals, dtype=torch.int64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return [int(x) for x in t.cpu()]

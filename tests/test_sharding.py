@@ -4,7 +4,7 @@ import socket
 
 import pytest
 
-from paper_0907_1788_b200.sharding import max_over_ranks, rank_seed, rank_stripes
+from paper_0907_1788_b200.sharding import max_over_ranks, rank_seed, rank_stripes, sum_over_ranks
 
 
 def test_strong_ranges_partition_exactly():
@@ -44,8 +44,10 @@ def _worker(rank, world, port, q):
         lo, hi = rank_stripes(2048, rank, world, "strong")
         # per-rank "times": the max over ranks must come back on every rank
         got = max_over_ranks([10.0 + rank, 100.0 - rank, float(hi - lo)])
+        # per-rank mismatch / checked-stripe counts summed over ranks (bench's verification gather)
+        tot = sum_over_ranks([rank, hi - lo])
         dist.barrier()
-        q.put((rank, lo, hi, got))
+        q.put((rank, lo, hi, got, tot))
     finally:
         dist.destroy_process_group()
 
@@ -65,3 +67,4 @@ def test_gloo_world2_max_over_ranks():
     assert [(r[1], r[2]) for r in res] == [(0, 1024), (1024, 2048)]
     for r in res:
         assert r[3] == [11.0, 100.0, 1024.0]
+        assert r[4] == [1, 2048]
