@@ -279,6 +279,7 @@ int fntrs_gpu_create(int device, fntrs_ctx** out) {
     }
     if (e == cudaSuccess) e = build_tables(ctx->tab, ctx->internal);
     if (e == cudaSuccess) e = fast::build_fast_tables(ctx->ftab, ctx->internal);
+    if (e == cudaSuccess) e = fast::upload_const_twiddles(ctx->ftab, ctx->internal);
     if (e == cudaSuccess) e = fast::build_large_tables(ctx->ftab, ctx->internal);
     if (e == cudaSuccess) e = fast::build_log_tables(ctx->ltab, ctx->internal);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->internal);

@@ -43,6 +43,15 @@
 namespace fntrs_gpu {
 namespace fast {
 
+// n_domain <= 256: copies of the pass-0 twiddle tables (uint2 entries [0, 512) of
+// ptab_fwd, ptab_inv, ptab_fwdT; 12 KB) in constant memory. Their rows are
+// warp-uniform, so the constant cache serves them without L1 data-pipe
+// wavefronts (the decode kernel's busiest unit). FNTRS_CONST_TW selects them.
+#ifndef FNTRS_CONST_TW
+#define FNTRS_CONST_TW 1
+#endif
+__constant__ uint4 c_twF[256], c_twI[256], c_twFT[256];
+
 namespace {
 
 // ---------------------------------------------------------------------------
@@ -106,8 +115,10 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
     };
     uint32_t tile = blockIdx.x;
     if (threadIdx.x == 0 && tile < tiles) issue(tile, 0);
-    const uint4* tF0 = pass_table(ptabF, S::llog(0));
-    const uint4* tI0 = pass_table(ptabI, S::llog(0));
+    constexpr bool CT = FNTRS_CONST_TW && E <= 8;
+    const uint4* tF0 = CT ? pass_table(reinterpret_cast<const uint2*>(c_twF), S::llog(0)) : pass_table(ptabF, S::llog(0));
+    const uint4* tI0 = CT ? pass_table(reinterpret_cast<const uint2*>(c_twI), S::llog(0)) : pass_table(ptabI, S::llog(0));
+    if constexpr (CT) ptabFT = reinterpret_cast<const uint2*>(c_twFT);
     const bool esc_any = esc_in.n != 0;
     for (uint32_t iter = 0; tile < tiles; tile = next_tile[iter & 1], ++iter) {
         const uint32_t stripe = tile / tps;
@@ -197,7 +208,8 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
         };
 
         // FNT1 = FNT_N(N'), DIF, natural -> perm order (flip 0)
-        pass<E, 0, false, false, k2P, kSmemCap, G>(tF0, ld_scatter, st_sm, fix_scatter);
+        pass<E, 0, false, false, k2P, kSmemCap, G, decltype(ld_scatter), decltype(st_sm), decltype(fix_scatter), NoFlush, 1,
+             CT>(tF0, ld_scatter, st_sm, fix_scatter);
         __syncthreads();
         // the stage is consumed: stream the next tile's packets in behind the remaining passes
         if (threadIdx.x == 0) {
@@ -241,7 +253,7 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
                     const uint4* tq = reinterpret_cast<const uint4*>(ptabFT + N + (uint32_t(N / RZ) - 1u - g) * RZ);
 #pragma unroll
                     for (int q = 0; q < RZ; q += 2) {
-                        const uint4 w = __ldg(tq + q / 2);
+                        const uint4 w = CT ? tq[q / 2] : __ldg(tq + q / 2);
                         work[G::idx((g << RLZ) + (RZ - 1 - q), col)] = mulws(u[q], w.x, w.y);
                         work[G::idx((g << RLZ) + (RZ - 2 - q), col)] = mulws(u[q + 1], w.z, w.w);
                     }
@@ -272,7 +284,7 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
                 for (int s = 0; s < R0; ++s) {
                     uint32_t x = work[G::template idx_flip<FLIP + 1>(t + (uint32_t(s) << SL0), col)];
                     if (P != 2 && s > 0) {  // P == 2: the twiddle was applied by the producing pass
-                        const uint2 w = tw_at(tpf, s, w4);
+                        const uint2 w = tw_at<CT>(tpf, s, w4);
                         x = mulws(x, w.x, w.y);
                     }
                     v[rev<R0>(s)] = x;
@@ -290,7 +302,7 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
                 for (int s = 0; s < R0; ++s) {
                     uint32_t y = v[rev<R0>(s)];
                     if (s > 0) {
-                        const uint2 w = tw_at(tpi, s, w4);
+                        const uint2 w = tw_at<CT>(tpi, s, w4);
                         y = mulws(y, w.x, w.y);
                     } else {
                         y = cap<BO, kSmemCap>(y);
@@ -359,7 +371,8 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
                     if (mask & (1u << q))
                         emit_escape(esc_out, key_out + uint64_t(base + (uint32_t(q) << SL0)) * L + col);
             };
-            pass<E, 0, false, true, kSmemCap, kCanon, G>(tF0, ld_smf, st_sys, NoFix(), flush_sys);
+            pass<E, 0, false, true, kSmemCap, kCanon, G, decltype(ld_smf), decltype(st_sys), NoFix, decltype(flush_sys), 1,
+                 CT>(tF0, ld_smf, st_sys, NoFix(), flush_sys);
         }
         __syncthreads();
     }
@@ -384,6 +397,13 @@ cudaError_t launch_dec(const FastTables& t, const FastPlanView& pv, uint32_t str
 }
 
 }  // namespace
+
+cudaError_t upload_const_twiddles(const FastTables& t, cudaStream_t st) {
+    cudaError_t e = cudaMemcpyToSymbolAsync(c_twF, t.ptab_fwd, sizeof(c_twF), 0, cudaMemcpyDeviceToDevice, st);
+    if (!e) e = cudaMemcpyToSymbolAsync(c_twI, t.ptab_inv, sizeof(c_twI), 0, cudaMemcpyDeviceToDevice, st);
+    if (!e) e = cudaMemcpyToSymbolAsync(c_twFT, t.ptab_fwdT, sizeof(c_twFT), 0, cudaMemcpyDeviceToDevice, st);
+    return e;
+}
 
 cudaError_t launch_decode_fast(const FastTables& t, const FastPlanView& pv, uint32_t stripes, uint32_t L,
                                const uint32_t* sp, const uint16_t* rx, EscIn ein, uint16_t* out, EscOut eout,

@@ -149,14 +149,17 @@ struct NoFlush {
 };
 
 // twiddle s of a row stored as uint4 pairs; s is a compile-time constant after
-// unrolling, so each pair is loaded once (on its first use, s = 1 or s even)
+// unrolling, so each pair is loaded once (on its first use, s = 1 or s even).
+// CT: the table is in constant memory (codec_dec.cu, FNTRS_CONST_TW): a plain
+// load, which compiles to LDC; otherwise a read-only global load.
+template <bool CT = false>
 __device__ __forceinline__ uint2 tw_at(const uint4* __restrict__ tq, int s, uint4& w4) {
-    if (s == 1 || (s & 1) == 0) w4 = __ldg(tq + (s >> 1));
+    if (s == 1 || (s & 1) == 0) w4 = CT ? tq[s >> 1] : __ldg(tq + (s >> 1));
     return (s & 1) ? make_uint2(w4.z, w4.w) : make_uint2(w4.x, w4.y);
 }
 
 template <int E, int p, bool INV, bool DIT, uint64_t BIN, uint64_t OCAP, class G, class LD, class ST,
-          class FIX = NoFix, class FLUSH = NoFlush, int CW = 1>
+          class FIX = NoFix, class FLUSH = NoFlush, int CW = 1, bool CTW = false>
 __device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld, const ST& st, const FIX& fix = FIX(),
                                      const FLUSH& flush = FLUSH()) {
     // CW codewords per work item: columns col + c * WT/CW, c < CW, share the
@@ -203,7 +206,7 @@ __device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld
 #pragma unroll
             for (int s = 0; s < R; ++s) {
                 uint2 w = make_uint2(0, 0);
-                if (SL > 0 && s > 0) w = tw_at(tq, s, w4);
+                if (SL > 0 && s > 0) w = tw_at<CTW>(tq, s, w4);
 #pragma unroll
                 for (int c = 0; c < CW; ++c) {
                     uint32_t y = v[c][rev<R>(s)];
@@ -223,7 +226,7 @@ __device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld
 #pragma unroll
             for (int s = 0; s < R; ++s) {
                 uint2 w = make_uint2(0, 0);
-                if (SL > 0 && s > 0) w = tw_at(tq, s, w4);
+                if (SL > 0 && s > 0) w = tw_at<CTW>(tq, s, w4);
 #pragma unroll
                 for (int c = 0; c < CW; ++c) {
                     uint32_t x = ld(base + (uint32_t(s) << SL), b, s, col + c * WC);

@@ -100,6 +100,8 @@ __host__ __device__ inline uint32_t ahat2_slot(uint32_t N, uint32_t j) {
     return ((j & ((1u << sl0) - 1u)) << 4) | (j >> sl0);
 }
 cudaError_t build_fast_tables(FastTables& t, cudaStream_t st);
+// constant-memory copies of the n_domain <= 256 pass-0 twiddle tables (codec_dec.cu)
+cudaError_t upload_const_twiddles(const FastTables& t, cudaStream_t st);
 int fast_tile_columns(uint32_t N);  // 0 when N has no fast kernel
 int fast_encode_columns(uint32_t N);  // encode tile width (L must be a multiple)
 // fused systematic codec on a fast plan (M == N); encode: the plan of positions 0..k-1
