@@ -21,6 +21,13 @@
 #ifndef FNTRS_LEA
 #define FNTRS_LEA 1
 #endif
+// FNTRS_LSTEP: per-symbol HBM addresses are one 64-bit pointer per butterfly
+// group stepped by a run-time stride, and four-step twiddle addresses are
+// formed with ALU adds (fft_pass.cuh step_ptr / ldg_alu), so that neither
+// costs an IMAD.WIDE on the multiplier pipe (83 % busy in enc_a / dec_1).
+#ifndef FNTRS_LSTEP
+#define FNTRS_LSTEP 1
+#endif
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -34,6 +41,7 @@ namespace fast {
 
 namespace {
 
+constexpr bool kStep = FNTRS_LSTEP != 0;
 constexpr int kLW = 64;   // codewords per CTA
 constexpr int kLNT = 256;  // threads per CTA
 
@@ -84,10 +92,14 @@ enc_a_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, uin
     uint32_t* yp = launder(Y + (uint64_t(bi.sb) * N) * L + bi.c0);
     const bool esc_any = esc_in.n != 0;
 
+    const uint16_t* sq = srcp;
+    const uint64_t sstep = opaque_stride((uint64_t(N2) * L * 2) << S::slog(0));
     auto ld = [&](uint32_t i1, uint32_t, int q, uint32_t col) -> uint32_t {
         const uint32_t row = i1 * N2 + i2;
         if ((HALFK && q >= R0 / 2) || (!HALFK && row >= k)) return 0u;
-        return srcp[row * L + col];
+        if (!kStep) return srcp[row * L + col];
+        sq = q == 0 ? srcp + (row * L + col) : step_ptr(sq, sstep);
+        return *sq;
     };
     auto fix = [&](uint32_t (&v)[R0], uint32_t base, uint32_t, uint32_t col) {
         if (!esc_any || !any_zero(v)) return;
@@ -102,10 +114,27 @@ enc_a_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, uin
         return 0u;
     };
     auto ld_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t { return work[G::idx(lrow, col)]; };
+    uint32_t* yq = yp;
+    uint32_t tix = 0;
+    const uint64_t ystep = opaque_stride((uint64_t(N2) * L * 4) << (E1 - RLZ));
+    const uint2* bigN = launder(bigF + N);
     auto st_y = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) -> uint32_t {
-        const uint32_t m1 = perm_head<E1>(b) + (uint32_t(s) << (E1 - RLZ));
-        const uint2 w = __ldg(bigF + N + ((i2 * m1) & (N - 1)));
-        yp[(m1 * N2 + i2) * L + col] = mulws(y, w.x, w.y);
+        if (!kStep) {
+            const uint32_t m1 = perm_head<E1>(b) + (uint32_t(s) << (E1 - RLZ));
+            const uint2 w = __ldg(bigF + N + ((i2 * m1) & (N - 1)));
+            yp[(m1 * N2 + i2) * L + col] = mulws(y, w.x, w.y);
+            return 0u;
+        }
+        if (s == 0) {
+            const uint32_t m1 = perm_head<E1>(b);
+            yq = yp + ((m1 * N2 + i2) * L + col);
+            tix = i2 * m1;
+        } else {
+            yq = step_ptr(yq, ystep);
+            tix += i2 << (E1 - RLZ);
+        }
+        const uint2 w = ldg_alu(bigN, tix & (N - 1));
+        *yq = mulws(y, w.x, w.y);
         return 0u;
     };
     pass<E1, 0, false, false, kP64, kSmemCap, G>(pass_table(ptab, S::llog(0)), ld, st_sm, fix);
@@ -138,14 +167,18 @@ enc_b_kernel(const uint2* __restrict__ ptab, uint32_t n, uint32_t L, uint32_t tp
     };
     auto ld_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t { return work[G::idx(lrow, col)]; };
     uint16_t* out_s = reinterpret_cast<uint16_t*>(work + N2 * kLW);  // TS staging: [m2][kLW]
+    uint16_t* oq = outp;
+    const uint64_t ostep = opaque_stride((uint64_t(N1) * L * 2) << (E2 - RLZ));
     auto st_out = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) -> uint32_t {
         const uint32_t m2 = perm_head<E2>(b) + (uint32_t(s) << (E2 - RLZ));
         const uint32_t row = m1 + N1 * m2;
         const bool keep = !PUNCT || row < n;
-        if constexpr (TS)
+        if constexpr (TS) {
             out_s[m2 * kLW + col] = uint16_t(y);
-        else if (keep)
-            __stcs(outp + (row * L + col), uint16_t(y));
+        } else {
+            if (kStep) oq = s == 0 ? outp + (row * L + col) : step_ptr(oq, ostep);
+            if (keep) __stcs(kStep ? oq : outp + (row * L + col), uint16_t(y));
+        }
         return keep ? y : 0u;  // canonical, kept: bit 16 set iff y == 65536
     };
     auto flush = [&](uint32_t mask, uint32_t, uint32_t b, uint32_t col) {
@@ -217,10 +250,27 @@ dec_1_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, con
         return 0u;
     };
     auto ld_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t { return work[G::idx(lrow, col)]; };
+    uint32_t* yq = yp;
+    uint32_t tix = 0;
+    const uint64_t ystep = opaque_stride((uint64_t(N2) * L * 4) << (E1 - RLZ));
+    const uint2* bigN = launder(bigF + N);
     auto st_y = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) -> uint32_t {
-        const uint32_t m1 = perm_head<E1>(b) + (uint32_t(s) << (E1 - RLZ));
-        const uint2 w = __ldg(bigF + N + ((i2 * m1) & (N - 1)));
-        yp[(m1 * N2 + i2) * L + col] = mulws(y, w.x, w.y);
+        if (!kStep) {
+            const uint32_t m1 = perm_head<E1>(b) + (uint32_t(s) << (E1 - RLZ));
+            const uint2 w = __ldg(bigF + N + ((i2 * m1) & (N - 1)));
+            yp[(m1 * N2 + i2) * L + col] = mulws(y, w.x, w.y);
+            return 0u;
+        }
+        if (s == 0) {
+            const uint32_t m1 = perm_head<E1>(b);
+            yq = yp + ((m1 * N2 + i2) * L + col);
+            tix = i2 * m1;
+        } else {
+            yq = step_ptr(yq, ystep);
+            tix += i2 << (E1 - RLZ);
+        }
+        const uint2 w = ldg_alu(bigN, tix & (N - 1));
+        *yq = mulws(y, w.x, w.y);
         return 0u;
     };
     pass<E1, 0, false, false, k2P, kSmemCap, G>(pass_table(ptab, S::llog(0)), ld, st_sm, fix);
@@ -252,9 +302,25 @@ dec_2_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, uin
     auto ld_smf = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t {
         return work[G::template idx_flip<FLIP + 1>(lrow, col)];
     };
-    auto st_y2 = [&](uint32_t q2, uint32_t, int, uint32_t col, uint32_t y) -> uint32_t {
-        const uint2 w = __ldg(bigF + N + ((i1p * q2) & (N - 1)));
-        y2[(q2 * N1 + i1p) * L + col] = mulws(y, w.x, w.y);
+    uint32_t* yq = y2;
+    uint32_t tix = 0;
+    const uint64_t ystep = opaque_stride((uint64_t(N1) * L * 4) << S::slog(0));
+    const uint2* bigN = launder(bigF + N);
+    auto st_y2 = [&](uint32_t q2, uint32_t, int q, uint32_t col, uint32_t y) -> uint32_t {
+        if (!kStep) {
+            const uint2 w = __ldg(bigF + N + ((i1p * q2) & (N - 1)));
+            y2[(q2 * N1 + i1p) * L + col] = mulws(y, w.x, w.y);
+            return 0u;
+        }
+        if (q == 0) {
+            yq = y2 + ((q2 * N1 + i1p) * L + col);
+            tix = i1p * q2;
+        } else {
+            yq = step_ptr(yq, ystep);
+            tix += i1p << S::slog(0);
+        }
+        const uint2 w = ldg_alu(bigN, tix & (N - 1));
+        *yq = mulws(y, w.x, w.y);
         return 0u;
     };
     // FNT1 pass B, first radix pass (input block by TMA)
@@ -361,8 +427,16 @@ dec_3_kernel(const uint2* __restrict__ ptabF, const uint2* __restrict__ ptabI, c
     // back the rows it read, now in natural order: the tile becomes the output block
     // (rows t1 N2 + q2 of Y3), stored with one TMA store through the (L, q2, t1) view.
     (void)st_y3;
-    auto st_tile = [&](uint32_t t1, uint32_t, int, uint32_t col, uint32_t y) -> uint32_t {
-        const uint2 w = __ldg(bigI + N + ((q2 * t1) & (N - 1)));
+    uint32_t tix = 0;
+    const uint2* bigN = launder(bigI + N);
+    auto st_tile = [&](uint32_t t1, uint32_t, int q, uint32_t col, uint32_t y) -> uint32_t {
+        if (!kStep) {
+            const uint2 w = __ldg(bigI + N + ((q2 * t1) & (N - 1)));
+            work[G::idx(t1, col)] = mulws(y, w.x, w.y);
+            return 0u;
+        }
+        tix = q == 0 ? q2 * t1 : tix + (q2 << S::slog(0));
+        const uint2 w = ldg_alu(bigN, tix & (N - 1));
         work[G::idx(t1, col)] = mulws(y, w.x, w.y);
         return 0u;
     };
@@ -398,10 +472,13 @@ dec_4_kernel(const uint2* __restrict__ ptabI, uint32_t k, uint32_t L, uint32_t t
         return 0u;
     };
     auto ld_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t { return work[G::idx(lrow, col)]; };
+    uint16_t* oq = outp;
+    const uint64_t ostep = opaque_stride((uint64_t(N1) * L * 2) << (E2 - RLZ));
     auto st_out = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) -> uint32_t {
         const uint32_t row = t1 + N1 * (perm_head<E2>(b) + (uint32_t(s) << (E2 - RLZ)));
         const bool keep = HALFK ? (s < RZ / 2) : (row < k);
-        if (keep) __stcs(outp + (row * L + col), uint16_t(y));
+        if (kStep) oq = s == 0 ? outp + (row * L + col) : step_ptr(oq, ostep);
+        if (keep) __stcs(kStep ? oq : outp + (row * L + col), uint16_t(y));
         return keep ? y : 0u;  // canonical, kept: bit 16 set iff y == 65536
     };
     auto flush = [&](uint32_t mask, uint32_t, uint32_t b, uint32_t col) {

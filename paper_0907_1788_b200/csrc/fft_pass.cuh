@@ -60,8 +60,14 @@ __device__ __forceinline__ T* launder(T* p) {
 __device__ __forceinline__ uint64_t opaque_stride(uint64_t bytes) {
     return bytes | (uint64_t(g_alu_zero) << 32);
 }
-__device__ __forceinline__ uint16_t* step_ptr(uint16_t* p, uint64_t stride_bytes) {
-    return reinterpret_cast<uint16_t*>(reinterpret_cast<uint64_t>(p) + stride_bytes);
+template <class T>
+__device__ __forceinline__ T* step_ptr(T* p, uint64_t stride_bytes) {
+    return reinterpret_cast<T*>(reinterpret_cast<uint64_t>(p) + stride_bytes);
+}
+// base[idx] of an 8-byte table with the address formed on the ALU pipe
+// (shift + 64-bit add against an opaque high word) instead of IMAD.WIDE
+__device__ __forceinline__ uint2 ldg_alu(const uint2* base, uint32_t idx) {
+    return __ldg(step_ptr(base, opaque_stride(uint64_t(idx) << 3)));
 }
 
 template <int N>
