@@ -37,6 +37,12 @@
 #ifndef FNTRS_SPLIT_PIN
 #define FNTRS_SPLIT_PIN 1
 #endif
+// One-codeword items (n_domain >= 512) pin the adds of the second 4 x 4 stage of
+// each radix-16 to the ALU (fft_pass.cuh): encode n = 4096 476 -> 492,
+// n = 1024 530 -> 545, n = 2048 523 -> 528 GB/s (pinning both stages: 479 / 538 / 538)
+#ifndef FNTRS_CW1_PIN
+#define FNTRS_CW1_PIN 2
+#endif
 #include <cuda.h>
 #include <cuda_runtime.h>
 

@@ -278,17 +278,18 @@ struct Dft4L {
     }
 };
 
-template <int R, bool INV, uint64_t B, uint64_t LIM = 0, bool PIN = kAluAdds>
+// PIN2: the second 4 x 4 stage of a radix-16 pins its adds independently (half pinning)
+template <int R, bool INV, uint64_t B, uint64_t LIM = 0, bool PIN = kAluAdds, bool PIN2 = PIN>
 struct Dft;
 
-template <bool INV, uint64_t B, uint64_t LIM, bool PIN>
-struct Dft<1, INV, B, LIM, PIN> {
+template <bool INV, uint64_t B, uint64_t LIM, bool PIN, bool PIN2>
+struct Dft<1, INV, B, LIM, PIN, PIN2> {
     static constexpr uint64_t OUT = B;
     __device__ __forceinline__ static void run(const uint32_t (&)[1], uint32_t (&y)[1]) {}
 };
 
-template <bool INV, uint64_t B, uint64_t LIM, bool PIN>
-struct Dft<2, INV, B, LIM, PIN> {
+template <bool INV, uint64_t B, uint64_t LIM, bool PIN, bool PIN2>
+struct Dft<2, INV, B, LIM, PIN, PIN2> {
     static constexpr uint64_t OUT = 2 * B;
     __device__ __forceinline__ static void run(const uint32_t (&x)[2], uint32_t (&y)[2]) {
         y[0] = add_a(x[0], x[1]);
@@ -296,8 +297,8 @@ struct Dft<2, INV, B, LIM, PIN> {
     }
 };
 
-template <bool INV, uint64_t B, uint64_t LIM, bool PIN>
-struct Dft<4, INV, B, LIM, PIN> {
+template <bool INV, uint64_t B, uint64_t LIM, bool PIN, bool PIN2>
+struct Dft<4, INV, B, LIM, PIN, PIN2> {
     static constexpr uint64_t OUT = Dft4<INV, B>::OUT;
     __device__ __forceinline__ static void run(const uint32_t (&x)[4], uint32_t (&y)[4]) {
         Dft4<INV, B>::run(x[0], x[1], x[2], x[3], y[0], y[1], y[2], y[3]);
@@ -321,8 +322,8 @@ struct TwR {
 
 // R = 8: 2 x 4 (q = 2 q1 + q2, s = s1 + 4 s2): DFT4 over q1 for each q2,
 // twiddle w8^(q2 s1), DFT2 over q2.
-template <bool INV, uint64_t B, uint64_t LIM, bool PIN>
-struct Dft<8, INV, B, LIM, PIN> {
+template <bool INV, uint64_t B, uint64_t LIM, bool PIN, bool PIN2>
+struct Dft<8, INV, B, LIM, PIN, PIN2> {
     static constexpr uint64_t B1 = Dft4<INV, B>::OUT;
     static constexpr uint64_t BT = umax(umax(TwR<8, 1, INV, B1>::OUT, TwR<8, 2, INV, B1>::OUT), TwR<8, 3, INV, B1>::OUT);
     static constexpr uint64_t OUT = 2 * umax(B1, BT);
@@ -346,21 +347,21 @@ struct Dft<8, INV, B, LIM, PIN> {
 // nine twiddles w16^(q2 s1) (reducing shift-multiplies), stage 2 = four Dft4L
 // whose first input is untwiddled. Stage 1 takes the lazy product only when
 // the whole transform then stays below LIM.
-template <bool INV, uint64_t B, bool L1, uint64_t LIM, bool PIN = kAluAdds>
+template <bool INV, uint64_t B, bool L1, uint64_t LIM, bool PIN = kAluAdds, bool PIN2 = PIN>
 struct Dft16B {
     using S1 = Dft4L<INV, B, B, B, B, L1 ? (uint64_t(1) << 62) : 0, PIN>;
     static constexpr uint64_t Y(int s1) { return (s1 & 1) ? S1::O13 : S1::O02; }
     template <int Q2, int S1I>
     using T = TwR<16, Q2 * S1I, INV, ((S1I & 1) ? S1::O13 : S1::O02)>;
     template <int S1I>
-    using S2 = Dft4L<INV, ((S1I & 1) ? S1::O13 : S1::O02), T<1, S1I>::OUT, T<2, S1I>::OUT, T<3, S1I>::OUT, LIM, PIN>;
+    using S2 = Dft4L<INV, ((S1I & 1) ? S1::O13 : S1::O02), T<1, S1I>::OUT, T<2, S1I>::OUT, T<3, S1I>::OUT, LIM, PIN2>;
     static constexpr uint64_t OUT = umax(umax(S2<0>::OUT, S2<1>::OUT), umax(S2<2>::OUT, S2<3>::OUT));
 };
 
-template <bool INV, uint64_t B, uint64_t LIM, bool PIN>
-struct Dft<16, INV, B, LIM, PIN> {
+template <bool INV, uint64_t B, uint64_t LIM, bool PIN, bool PIN2>
+struct Dft<16, INV, B, LIM, PIN, PIN2> {
     static constexpr bool L1 = LIM != 0 && Dft16B<INV, B, true, LIM>::OUT <= LIM;
-    using D = Dft16B<INV, B, L1, LIM, PIN>;
+    using D = Dft16B<INV, B, L1, LIM, PIN, PIN2>;
     static constexpr uint64_t OUT = D::OUT;
     template <int Q2, int S1>
     __device__ __forceinline__ static uint32_t tw(uint32_t x) {
@@ -388,21 +389,21 @@ struct Dft<16, INV, B, LIM, PIN> {
 };
 
 // DIF placement: natural in, v[rev(s)] = y_s out. DIT placement: v[rev(s)] in, natural out.
-template <int R, bool INV, uint64_t BIN, uint64_t LIM = 0, bool PIN = kAluAdds>
+template <int R, bool INV, uint64_t BIN, uint64_t LIM = 0, bool PIN = kAluAdds, bool PIN2 = PIN>
 __device__ __forceinline__ void dif_regs(uint32_t (&v)[R]) {
     static_assert(Dft<R, INV, BIN, LIM>::OUT < (1ull << 31), "lazy bound overflow");
     uint32_t y[R];
-    Dft<R, INV, BIN, LIM, PIN>::run(v, y);
+    Dft<R, INV, BIN, LIM, PIN, PIN2>::run(v, y);
 #pragma unroll
     for (int s = 0; s < R; ++s) v[rev<R>(s)] = y[s];
 }
-template <int R, bool INV, uint64_t BIN, uint64_t LIM = 0, bool PIN = kAluAdds>
+template <int R, bool INV, uint64_t BIN, uint64_t LIM = 0, bool PIN = kAluAdds, bool PIN2 = PIN>
 __device__ __forceinline__ void dit_regs(uint32_t (&v)[R]) {
     static_assert(Dft<R, INV, BIN, LIM>::OUT < (1ull << 31), "lazy bound overflow");
     uint32_t x[R];
 #pragma unroll
     for (int s = 0; s < R; ++s) x[s] = v[rev<R>(s)];
-    Dft<R, INV, BIN, LIM, PIN>::run(x, v);
+    Dft<R, INV, BIN, LIM, PIN, PIN2>::run(x, v);
 }
 template <int R, bool INV, uint64_t BIN, uint64_t LIM = 0>
 constexpr uint64_t dif_bound() { return Dft<R, INV, BIN, LIM>::OUT; }

@@ -146,6 +146,12 @@ struct Pick {
 // transform. Loaded values must be below BIN; stored values are below OCAP.
 // twp: per-pass twiddle table, row t holds {r_len^(t s), 65535 r_len^(t s)}
 // for s < R (only read when sub > 1).
+// FNTRS_CW1_PIN (one codeword per work item): 0 = adds placed by ptxas (or
+// FNTRS_ALU_ADDS); bit 0 / bit 1 pin the adds of the first / second 4 x 4
+// stage of each radix-16 butterfly to the ALU pipe.
+#ifndef FNTRS_CW1_PIN
+#define FNTRS_CW1_PIN 0
+#endif
 struct NoFix {
     template <int R>
     __device__ __forceinline__ void operator()(uint32_t (&)[R], uint32_t, uint32_t, uint32_t) const {}
@@ -205,6 +211,8 @@ __device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld
             for (int c = 0; c < CW; ++c) {
                 if (FNTRS_SPLIT_PIN && c == 1)
                     dif_regs<R, INV, BIN, LZ, true>(v[c]);
+                else if (CW == 1 && FNTRS_CW1_PIN)
+                    dif_regs<R, INV, BIN, LZ, (FNTRS_CW1_PIN & 1) != 0, (FNTRS_CW1_PIN & 2) != 0>(v[c]);
                 else
                     dif_regs<R, INV, BIN, LZ>(v[c]);
             }
@@ -241,7 +249,12 @@ __device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld
                 }
             }
 #pragma unroll
-            for (int c = 0; c < CW; ++c) dit_regs<R, INV, BI>(v[c]);
+            for (int c = 0; c < CW; ++c) {
+                if (CW == 1 && FNTRS_CW1_PIN)
+                    dit_regs<R, INV, BI, 0, (FNTRS_CW1_PIN & 1) != 0, (FNTRS_CW1_PIN & 2) != 0>(v[c]);
+                else
+                    dit_regs<R, INV, BI>(v[c]);
+            }
             constexpr uint64_t BO = dit_bound<R, INV, BI>();
 #pragma unroll
             for (int c = 0; c < CW; ++c)
