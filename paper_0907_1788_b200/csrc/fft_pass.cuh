@@ -152,6 +152,13 @@ struct Pick {
 #ifndef FNTRS_CW1_PIN
 #define FNTRS_CW1_PIN 0
 #endif
+// two-codeword items (FNTRS_SPLIT_PIN): the same stage masks for codeword 0 / 1
+#ifndef FNTRS_CW2_PIN0
+#define FNTRS_CW2_PIN0 0
+#endif
+#ifndef FNTRS_CW2_PIN1
+#define FNTRS_CW2_PIN1 3
+#endif
 struct NoFix {
     template <int R>
     __device__ __forceinline__ void operator()(uint32_t (&)[R], uint32_t, uint32_t, uint32_t) const {}
@@ -210,7 +217,9 @@ __device__ __forceinline__ void pass(const uint4* __restrict__ twp, const LD& ld
 #pragma unroll
             for (int c = 0; c < CW; ++c) {
                 if (FNTRS_SPLIT_PIN && c == 1)
-                    dif_regs<R, INV, BIN, LZ, true>(v[c]);
+                    dif_regs<R, INV, BIN, LZ, (FNTRS_CW2_PIN1 & 1) != 0, (FNTRS_CW2_PIN1 & 2) != 0>(v[c]);
+                else if (FNTRS_SPLIT_PIN && CW == 2 && FNTRS_CW2_PIN0)
+                    dif_regs<R, INV, BIN, LZ, (FNTRS_CW2_PIN0 & 1) != 0, (FNTRS_CW2_PIN0 & 2) != 0>(v[c]);
                 else if (CW == 1 && FNTRS_CW1_PIN)
                     dif_regs<R, INV, BIN, LZ, (FNTRS_CW1_PIN & 1) != 0, (FNTRS_CW1_PIN & 2) != 0>(v[c]);
                 else
