@@ -347,14 +347,21 @@ struct Dft<8, INV, B, LIM, PIN, PIN2> {
 // nine twiddles w16^(q2 s1) (reducing shift-multiplies), stage 2 = four Dft4L
 // whose first input is untwiddled. Stage 1 takes the lazy product only when
 // the whole transform then stays below LIM.
+// per-unit masks over every radix-16 pin request (A/B knobs; 1 = as requested)
+#ifndef FNTRS_STAGE1_PIN
+#define FNTRS_STAGE1_PIN 1
+#endif
+#ifndef FNTRS_STAGE2_PIN
+#define FNTRS_STAGE2_PIN 1
+#endif
 template <bool INV, uint64_t B, bool L1, uint64_t LIM, bool PIN = kAluAdds, bool PIN2 = PIN>
 struct Dft16B {
-    using S1 = Dft4L<INV, B, B, B, B, L1 ? (uint64_t(1) << 62) : 0, PIN>;
+    using S1 = Dft4L<INV, B, B, B, B, L1 ? (uint64_t(1) << 62) : 0, PIN && FNTRS_STAGE1_PIN>;
     static constexpr uint64_t Y(int s1) { return (s1 & 1) ? S1::O13 : S1::O02; }
     template <int Q2, int S1I>
     using T = TwR<16, Q2 * S1I, INV, ((S1I & 1) ? S1::O13 : S1::O02)>;
     template <int S1I>
-    using S2 = Dft4L<INV, ((S1I & 1) ? S1::O13 : S1::O02), T<1, S1I>::OUT, T<2, S1I>::OUT, T<3, S1I>::OUT, LIM, PIN2>;
+    using S2 = Dft4L<INV, ((S1I & 1) ? S1::O13 : S1::O02), T<1, S1I>::OUT, T<2, S1I>::OUT, T<3, S1I>::OUT, LIM, PIN2 && FNTRS_STAGE2_PIN>;
     static constexpr uint64_t OUT = umax(umax(S2<0>::OUT, S2<1>::OUT), umax(S2<2>::OUT, S2<3>::OUT));
 };
 
