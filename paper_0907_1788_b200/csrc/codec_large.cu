@@ -42,11 +42,17 @@ namespace fast {
 namespace {
 
 constexpr bool kStep = FNTRS_LSTEP != 0;
-constexpr int kLW = 64;   // codewords per CTA
+#ifndef FNTRS_LW
+#define FNTRS_LW 64
+#endif
+#ifndef FNTRS_LMINB
+#define FNTRS_LMINB 5  // CTAs per SM the register budget targets at size <= 128 (3 above)
+#endif
+constexpr int kLW = FNTRS_LW;   // codewords per CTA
 constexpr int kLNT = 256;  // threads per CTA
 
 template <int E>
-using LG = Geom<E, kLW, kLNT, (1 << E) <= 128 ? 5 : 3>;
+using LG = Geom<E, kLW, kLNT, (1 << E) <= 128 ? FNTRS_LMINB : 3>;
 
 struct BlockIdx {
     uint32_t sb, g, c0;
