@@ -57,6 +57,11 @@ struct Tw {
 // balanced representative of a canonical residue: (-p/2, p/2]
 __host__ __device__ constexpr int32_t balanced(uint32_t w) { return w > 32768u ? int32_t(w) - 65537 : int32_t(w); }
 
+// FNTRS_POW2_LEA: the power-of-two products below take the LEA form
+// independently of the Shoup q * p (FNTRS_LEA)
+#ifndef FNTRS_POW2_LEA
+#define FNTRS_POW2_LEA FNTRS_LEA
+#endif
 // x * 2^E mod p, E in [0, 32), |x| < B.
 template <int E, uint64_t B>
 struct MulPow2 {
@@ -72,8 +77,8 @@ struct MulPow2 {
 #if FNTRS_POW2_ALU  // no multiplier-pipe IMAD: (x << s) - (xh << 16) - xh as shifts + one IADD3
             const uint32_t xs = x << s, xh16 = xh << 16;
             return neg ? add3_a(xh16, xh, 0u - xs) : subsub_a(xs, xh16, xh);
-#elif FNTRS_LEA  // SHF (ALU) + LEA (ALU) + one IMAD: x 2^s -/+ xh p
-            return neg ? mad_lo(x, 0u - (1u << s), mul_p(xh)) : mad_lo(x, 1u << s, 0u - mul_p(xh));
+#elif FNTRS_POW2_LEA  // SHF (ALU) + LEA (ALU) + one IMAD: x 2^s -/+ xh p
+            return neg ? mad_lo(x, 0u - (1u << s), mul_p_lea(xh)) : mad_lo(x, 1u << s, 0u - mul_p_lea(xh));
 #else
             const uint32_t xs = x << s;
             return neg ? xh * 65537u - xs : xs - xh * 65537u;

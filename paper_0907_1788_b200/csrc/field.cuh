@@ -50,11 +50,15 @@ __host__ __device__ constexpr uint32_t croot(uint32_t n, bool inverse) {
 #ifndef FNTRS_LEA
 #define FNTRS_LEA 0
 #endif
-__device__ __forceinline__ uint32_t mul_p(uint32_t q) {
-#if FNTRS_LEA
+// q * p as shift + add (one LEA on the ALU pipe)
+__device__ __forceinline__ uint32_t mul_p_lea(uint32_t q) {
     uint32_t t;
     asm("{\n\t.reg .b32 s;\n\tshl.b32 s, %1, 16;\n\tadd.u32 %0, s, %1;\n\t}" : "=r"(t) : "r"(q));
     return t;
+}
+__device__ __forceinline__ uint32_t mul_p(uint32_t q) {
+#if FNTRS_LEA
+    return mul_p_lea(q);
 #else
     return q * kP;
 #endif
