@@ -41,23 +41,27 @@ PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback, only if MEASURED_PEAKS.json is absent
 
 
-def _profile_row(cfg, chunk, systematic):
+PROFILE_CSV = {"decode": "r01_ncu_full_raw.csv", "encode": "r01_ncu_full_enc_raw.csv"}
+
+
+def _profile_row(cfg, chunk, systematic, kernel="decode"):
     """Header, units and values of the committed ncu --set full capture
-    (profiles/r01_ncu_full_raw.csv: dec_fast_kernel<8>, one 8192-stripe C2
-    chunk) when this run's decode launch has that exact shape."""
+    (profiles/r01_ncu_full_raw.csv: dec_fast_kernel<8>; r01_ncu_full_enc_raw.csv:
+    enc_fast_kernel<8>; one 8192-stripe C2 chunk each) when this run's launch
+    has that exact shape."""
     if systematic or cfg.name != "C2" or chunk != 8192:
         return None
     try:
         import csv
-        rows = list(csv.reader(open(os.path.join(ROOT, "profiles", "r01_ncu_full_raw.csv"))))
+        rows = list(csv.reader(open(os.path.join(ROOT, "profiles", PROFILE_CSV[kernel]))))
         return rows[0], rows[1], rows[2]
     except Exception:
         return None
 
 
-def profiled_traffic(cfg, chunk, systematic):
-    """DRAM bytes (read + write) per decode launch from the committed capture."""
-    row = _profile_row(cfg, chunk, systematic)
+def profiled_traffic(cfg, chunk, systematic, kernel="decode"):
+    """DRAM bytes (read + write) per launch from the committed capture."""
+    row = _profile_row(cfg, chunk, systematic, kernel)
     if row is None:
         return None
     h, u, v = row
@@ -69,9 +73,9 @@ def profiled_traffic(cfg, chunk, systematic):
         return None
 
 
-def profiled_pct(cfg, chunk, systematic, metric):
-    """A percentage metric of the decode launch from the committed capture, as a fraction."""
-    row = _profile_row(cfg, chunk, systematic)
+def profiled_pct(cfg, chunk, systematic, metric, kernel="decode"):
+    """A percentage metric of the launch from the committed capture, as a fraction."""
+    row = _profile_row(cfg, chunk, systematic, kernel)
     if row is None:
         return None
     h, u, v = row
@@ -81,15 +85,16 @@ def profiled_pct(cfg, chunk, systematic, metric):
         return None
 
 
-def profiled_issue(cfg, chunk, systematic):
-    """The decode kernel's SM issue-slot utilisation from the committed capture."""
-    return profiled_pct(cfg, chunk, systematic, "smsp__issue_active.avg.pct_of_peak_sustained_active")
+def profiled_issue(cfg, chunk, systematic, kernel="decode"):
+    """The kernel's SM issue-slot utilisation from the committed capture."""
+    return profiled_pct(cfg, chunk, systematic, "smsp__issue_active.avg.pct_of_peak_sustained_active", kernel)
 
 
-def profiled_multiplier(cfg, chunk, systematic):
-    """The decode kernel's busiest unit, the integer multiplier (FMA-heavy) pipe:
+def profiled_multiplier(cfg, chunk, systematic, kernel="decode"):
+    """The kernel's busiest unit, the integer multiplier (FMA-heavy) pipe:
     its binding roofline in place of HBM (same capture)."""
-    return profiled_pct(cfg, chunk, systematic, "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed")
+    return profiled_pct(cfg, chunk, systematic, "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed",
+                        kernel)
 
 
 def hbm_peak():
@@ -470,6 +475,11 @@ def run_gpu(args, rank, world, local_rank):
             "bound": "hbm", "kernel": "enc_fast_kernel", "achieved": round(enc_achieved, 2), "peak": peak,
             "unit": "GB/s", "frac": round(enc_achieved / peak, 4), "algorithmic_bytes_per_launch": enc_bytes,
             "avg_launch_ms": round(enc_launch_ms, 4),
+            "traffic": profiled_traffic(cfg, chunk, SYSTEMATIC, "encode"),
+            "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum per launch "
+                              "(profiles/r01_ncu_full_enc_raw.csv)",
+            "issue_active_frac": profiled_issue(cfg, chunk, SYSTEMATIC, "encode"),
+            "multiplier_pipe_busy_frac": profiled_multiplier(cfg, chunk, SYSTEMATIC, "encode"),
         },
         "gpu_launches": int(gpu_launches),
         "verified": verified,
