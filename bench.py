@@ -459,7 +459,7 @@ def run_gpu(args, rank, world, local_rank):
         "decode_with_plans_gbs": round(src_bytes_rank / ((phase_ms[2] + phase_ms[0]) * 1e-3) / 1e9, 2),
         "roofline": {
             "bound": "hbm",
-            "kernel": ("decode_systematic call per chunk (interpolation kernel + transform kernel)" if SYSTEMATIC
+            "kernel": ("dec_fast_kernel MODE 3 (fused systematic decode: one cyclic convolution, two transforms; one launch per chunk)" if SYSTEMATIC
                        else "dec_fast_kernel (fused decode, one launch per chunk)"),
             "achieved": round(dec_achieved, 2), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
             "frac": round(dec_achieved / peak, 4),

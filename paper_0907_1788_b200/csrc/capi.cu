@@ -302,6 +302,7 @@ int fntrs_gpu_destroy(fntrs_ctx* ctx) {
     cudaFree(ctx->ftab.ptab_inv);
     cudaFree(ctx->ftab.big_fwd);
     cudaFree(ctx->ftab.big_inv);
+    cudaFree(ctx->ftab.sys_conv);
     cudaDeviceSynchronize();
     cudaFree(ctx->ltab.exp3);
     cudaFree(ctx->ltab.log3);

@@ -9,7 +9,8 @@
 //   zeroed); FNT2's last DIT pass, the product with A_hat and FNT3's first
 //   DIF pass are fused in registers; FNT3's last pass writes the k decoded
 //   packets. Systematic encode / decode (codec.cpp:151-196) are MODE 1 / 2
-//   of the same kernel.
+//   of the same kernel (four transforms), or MODE 4 / 3 (two transforms: the
+//   evaluations P(r^j) come straight out of one cyclic convolution, see below).
 //
 // Separate translation unit because decode is compiled with ALU-pinned adds
 // (field.cuh, FNTRS_ALU_ADDS): decode spends more of its instructions on
@@ -47,6 +48,10 @@ namespace fast {
 // ptab_fwd, ptab_inv, ptab_fwdT; 12 KB) in constant memory. Their rows are
 // warp-uniform, so the constant cache serves them without L1 data-pipe
 // wavefronts (the decode kernel's busiest unit). FNTRS_CONST_TW selects them.
+// systematic codec by one convolution (MODE 3 / 4) instead of interpolate + re-encode (MODE 1 / 2)
+#ifndef FNTRS_SYS_CONV
+#define FNTRS_SYS_CONV 1
+#endif
 #ifndef FNTRS_CONST_TW
 #define FNTRS_CONST_TW 1
 #endif
@@ -70,6 +75,16 @@ struct DecOcc {
 // MODE 2: systematic encode (codec.cpp:151-161) with the plan of positions
 //         0..k-1: source rows are copied to codeword rows 0..k-1 while the
 //         first pass scatters them, and FNT4 rows k..n-1 (the parity) go out.
+// MODE 3 / 4: systematic decode / encode by the Cauchy form of the interpolant.
+//         P(x) = A(x) sum_i c_i / (x - x_i), c_i = v_i / A'(x_i), so at a
+//         non-received position j
+//           P(r^j) = A(r^j) r^-j sum_z c[z] G'[j - z],  G'[e] = 1 / (1 - r^-e), G'[0] = 0,
+//         a cyclic convolution of the scattered c with a constant of N:
+//         FNT_N(c) (DIF) x Q (Q = -FNT_N(G'), table sysc) -> unscaled inverse DIT
+//         -> x r^-j x ahat_j (ahat = -A(r^j)/N, 0 on received rows). Two
+//         transforms instead of four (MODE 1 / 2); the same values, exactly.
+//         Received rows j < k (MODE 3) / source rows (MODE 4) are copied by the
+//         scatter pass.
 template <int E, class G, bool HALFK, int MODE = 0>
 __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const __grid_constant__ CUtensorMap rx_map,
                                                          const uint2* __restrict__ ptabF, const uint2* __restrict__ ptabI,
@@ -78,7 +93,8 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
                                                          uint32_t tps, uint32_t tiles, uint32_t nbox, uint32_t box_rows,
                                                          const uint32_t* __restrict__ stripe_pattern, EscIn esc_in,
                                                          uint16_t* __restrict__ out, EscOut esc_out, uint32_t n,
-                                                         const uint2* __restrict__ ptabFT, uint32_t* __restrict__ tile_ctr) {
+                                                         const uint2* __restrict__ ptabFT, uint32_t* __restrict__ tile_ctr,
+                                                         const uint2* __restrict__ sysc) {
     using S = Sched<E>;
     constexpr int N = 1 << E, WT = G::WT, NT = G::NT, P = S::P;
     constexpr int RLZ = G::RLZ, RZ = 1 << RLZ;
@@ -132,7 +148,8 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
         const uint2* __restrict__ ah = ahat2 + size_t(pat) * N;
         const unsigned long long key = uint64_t(stripe) * k * L + c0;
         // output rows per stripe: k (decode, systematic decode) or n (systematic encode)
-        const unsigned long long key_out = MODE == 2 ? uint64_t(stripe) * n * L + c0 : key;
+        constexpr bool ENC = MODE == 2 || MODE == 4;
+        const unsigned long long key_out = ENC ? uint64_t(stripe) * n * L + c0 : key;
         uint16_t* outp = launder(out + key_out);
         mbar_wait(&bars[0], iter & 1);
         const uint16_t* st_in = stage0;
@@ -145,8 +162,11 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
             const uint2 m = __ldg(rm + lrow);
             const uint32_t raw = st_in[int(m.x * uint32_t(WT) + col)];
             zmin = min(zmin, raw);
-            if constexpr (MODE == 2) {  // identity plan: row z < k is source row z -> codeword row z
+            if constexpr (ENC) {  // identity plan: row z < k is source row z -> codeword row z
                 if (HALFK ? (q < R0 / 2) : (lrow < k)) __stcs(outp + (lrow * L + col), uint16_t(raw));
+            } else if constexpr (MODE == 3) {  // received row z < k: P(r^z) is the received word
+                if ((HALFK ? (q < R0 / 2) : (lrow < k)) && m.x != 0xFFFFFFFFu)
+                    __stcs(outp + (lrow * L + col), uint16_t(raw));
             }
             // raw <= 65535 and |1/A'| <= p/2 (balanced): the product is exact in 32 signed bits
             return reds(raw * m.y);
@@ -162,7 +182,11 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
                 if (m.x != 0xFFFFFFFFu && st_in[m.x * WT + col] == 0u &&
                     esc_has(esc_in, key + uint64_t(m.x) * L + col)) {
                     v[q] = mulws(65536u, m.y, m.y * 65535u);
-                    if constexpr (MODE == 2) emit_escape(esc_out, key_out + uint64_t(m.x) * L + col);
+                    if constexpr (ENC) emit_escape(esc_out, key_out + uint64_t(m.x) * L + col);
+                    if constexpr (MODE == 3) {
+                        const uint32_t z = base + (uint32_t(q) << SL0);
+                        if (z < k) emit_escape(esc_out, key_out + uint64_t(z) * L + col);
+                    }
                 }
             }
         };
@@ -220,6 +244,65 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
             pass<E, 1, false, false, kSmemCap, kSmemCap, G>(pass_table(ptabF, S::llog(1)), ld_sm, st_sm);
             __syncthreads();
         }
+        if constexpr (MODE >= 3) {
+            // FNT_N(c) last DIF pass (sub 1), x Q, first pass of the unscaled inverse DIT, in registers
+            {
+                constexpr int ITEMS = (N / RZ) * WT;
+                constexpr uint64_t BD = dif_bound<RZ, false, kSmemCap, kLazyLim>();
+                static_assert(BD < (1ull << 31), "Shoup inputs are signed 32-bit");
+                constexpr uint64_t BT = dit_bound<RZ, true, k2P, uint64_t(FNTRS_R2T_LIM)>();  // folded to 2p below
+                const uint4* __restrict__ qt = reinterpret_cast<const uint4*>(sysc);
+#pragma unroll 1
+                for (int it = threadIdx.x; it < ITEMS; it += NT) {
+                    const uint32_t col = uint32_t(it) & uint32_t(WT - 1);
+                    const uint32_t g = uint32_t(it) >> LGW;
+                    uint32_t v[RZ];
+#pragma unroll
+                    for (int q = 0; q < RZ; ++q) v[q] = work[G::idx((g << RLZ) + q, col)];
+                    dif_regs<RZ, false, kSmemCap, kLazyLim>(v);
+                    // v[j] holds frequency perm_head(g) + rev(j) N/R; sysc is stored in that order
+                    const uint4* tq = qt + g * (RZ / 2);
+#pragma unroll
+                    for (int q = 0; q < RZ; q += 2) {
+                        const uint4 w = __ldg(tq + q / 2);
+                        v[q] = mulws(v[q], w.x, w.y);
+                        v[q + 1] = mulws(v[q + 1], w.z, w.w);
+                    }
+                    dit_regs<RZ, true, k2P, uint64_t(FNTRS_R2T_LIM)>(v);
+#pragma unroll
+                    for (int q = 0; q < RZ; ++q) work[G::idx((g << RLZ) + q, col)] = cap<BT, kSmemCap>(v[q]);
+                }
+            }
+            __syncthreads();
+            if constexpr (P == 3) {
+                pass<E, 1, true, true, kSmemCap, kSmemCap, G>(pass_table(ptabI, S::llog(1)), ld_sm, st_sm);
+                __syncthreads();
+            }
+            // last inverse DIT pass: natural order; P(r^j) = U[j] r^-j ahat_j on the rows kept
+            const uint2* __restrict__ rinv = sysc + N;
+            auto st_conv = [&](uint32_t lrow, uint32_t, int q, uint32_t col, uint32_t y) -> uint32_t {
+                bool keep;
+                if constexpr (MODE == 3)
+                    keep = HALFK ? (q < R0 / 2) : (lrow < k);
+                else
+                    keep = (HALFK ? (q >= R0 / 2) : (lrow >= k)) && lrow < n;
+                if (!keep) return 0u;
+                const uint2 a = __ldg(ah + ahat2_slot(uint32_t(N), lrow));
+                if (MODE == 3 && a.x == 0u) return 0u;  // received: written by the scatter pass
+                const uint2 w = __ldg(rinv + lrow);
+                const uint32_t z = canon_s2p(mulws(mulws(y, w.x, w.y), a.x, a.y));
+                __stcs(outp + (lrow * L + col), uint16_t(z));
+                return z;
+            };
+            auto flush_conv = [&](uint32_t mask, uint32_t base, uint32_t, uint32_t col) {
+                if (!mask) return;
+#pragma unroll 1
+                for (int q = 0; q < 16; ++q)
+                    if (mask & (1u << q)) emit_escape(esc_out, key_out + uint64_t(base + (uint32_t(q) << SL0)) * L + col);
+            };
+            pass<E, 0, true, true, kSmemCap, kCanon, G, decltype(ld_sm), decltype(st_conv), NoFix, decltype(flush_conv), 1,
+                 CT>(tI0, ld_sm, st_conv, NoFix(), flush_conv);
+        } else {
         // FNT1 last pass (sub 1) + FNT2 first DIT pass on the reversed view:
         // logical group b' = N/R - 1 - g holds s'_j = F[N-1-j]; j >= k zeroed.
         {
@@ -374,6 +457,7 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
             pass<E, 0, false, true, kSmemCap, kCanon, G, decltype(ld_smf), decltype(st_sys), NoFix, decltype(flush_sys), 1,
                  CT>(tF0, ld_smf, st_sys, NoFix(), flush_sys);
         }
+        }
         __syncthreads();
     }
 }
@@ -392,7 +476,8 @@ cudaError_t launch_dec(const FastTables& t, const FastPlanView& pv, uint32_t str
     TileCounter ctr;
     if ((err = ctr.get(st))) return err;
     kern<<<sh.grid, G::NT, sh.smem, st>>>(map, t.ptab_fwd, t.ptab_inv, pv.rowmap, pv.ahat2, pv.k, L, sh.tps, sh.tiles,
-                                          sh.nbox, sh.box_rows, sp, ein, out, eout, n, t.ptab_fwdT, ctr.p);
+                                          sh.nbox, sh.box_rows, sp, ein, out, eout, n, t.ptab_fwdT, ctr.p,
+                                          t.sys_conv ? t.sys_conv + 2 * (1u << E) : nullptr);
     return cudaGetLastError();
 }
 
@@ -421,6 +506,50 @@ cudaError_t launch_decode_fast(const FastTables& t, const FastPlanView& pv, uint
     }
 }
 
+// Q (group order of the fused conv pass) and r^-j (natural) Shoup pairs for
+// N = 2^E at sys_conv + 2N: Q[f] = -sum_e G'[e] r^(e f), G'[e] = 1/(1 - r^-e).
+// Built once per context; O(N^2) per size, N/128 CTAs each (every CTA rebuilds the power tables).
+template <int E>
+__global__ void sys_conv_kernel(uint2* __restrict__ base) {
+    using G = typename Pick<E>::G;
+    constexpr uint32_t N = 1u << E;
+    constexpr int RLZ = G::RLZ, RZ = 1 << RLZ;
+    __shared__ uint32_t rp[N], gp[N];
+    uint2* out = base + 2 * N;
+    const uint32_t r = gpow(3u, 65536u / N);
+    for (uint32_t e = threadIdx.x; e < N; e += blockDim.x) rp[e] = gpow(r, e);
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < N; e += blockDim.x) {
+        const uint32_t x = rp[(N - e) & (N - 1u)];           // r^-e
+        gp[e] = e ? ginv(1u + kP - x) : 0u;                  // 1 - r^-e in [2, p)
+        const int32_t b = balanced(x);
+        if (blockIdx.x == 0) out[N + e] = make_uint2(uint32_t(b), uint32_t(b * 65535));
+    }
+    __syncthreads();
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+        const uint32_t g = i >> RLZ, j = i & uint32_t(RZ - 1);
+        const uint32_t f = perm_head<E>(g) + (uint32_t(rev<RZ>(int(j))) << (E - RLZ));
+        uint32_t acc = 0;
+        for (uint32_t e = 1; e < N; ++e) acc = red2p(acc + gmul(gp[e], rp[(e * f) & (N - 1u)]));
+        const int32_t b = balanced(acc ? kP - acc : 0u);
+        out[i] = make_uint2(uint32_t(b), uint32_t(b * 65535));
+    }
+}
+
+cudaError_t build_sys_conv(FastTables& t, cudaStream_t st) {
+    cudaError_t err = cudaMalloc(&t.sys_conv, sizeof(uint2) << 14);  // [2N, 4N) per N = 32..4096
+    if (err) return err;
+    sys_conv_kernel<5><<<1, 128, 0, st>>>(t.sys_conv);
+    sys_conv_kernel<6><<<1, 128, 0, st>>>(t.sys_conv);
+    sys_conv_kernel<7><<<1, 128, 0, st>>>(t.sys_conv);
+    sys_conv_kernel<8><<<2, 128, 0, st>>>(t.sys_conv);
+    sys_conv_kernel<9><<<4, 128, 0, st>>>(t.sys_conv);
+    sys_conv_kernel<10><<<8, 128, 0, st>>>(t.sys_conv);
+    sys_conv_kernel<11><<<16, 128, 0, st>>>(t.sys_conv);
+    sys_conv_kernel<12><<<32, 128, 0, st>>>(t.sys_conv);
+    return cudaGetLastError();
+}
+
 // systematic codec, fused (MODE 1: decode, rows 0..k-1 out; MODE 2: encode
 // with the plan of positions 0..k-1, rows 0..n-1 out)
 cudaError_t launch_systematic_fast(const FastTables& t, const FastPlanView& pv, bool encode, uint32_t n,
@@ -428,6 +557,9 @@ cudaError_t launch_systematic_fast(const FastTables& t, const FastPlanView& pv, 
                                    uint16_t* out, EscOut eout, cudaStream_t st) {
 #define FNTRS_SYS(e)                                                                              \
     case (1u << e):                                                                               \
+        if (FNTRS_SYS_CONV)                                                                       \
+            return encode ? launch_dec<e, 4>(t, pv, stripes, L, sp, in, ein, out, eout, st, n)   \
+                          : launch_dec<e, 3>(t, pv, stripes, L, sp, in, ein, out, eout, st, n);  \
         return encode ? launch_dec<e, 2>(t, pv, stripes, L, sp, in, ein, out, eout, st, n)       \
                       : launch_dec<e, 1>(t, pv, stripes, L, sp, in, ein, out, eout, st, n);
     switch (pv.N) {

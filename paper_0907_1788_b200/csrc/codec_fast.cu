@@ -295,7 +295,8 @@ cudaError_t build_fast_tables(FastTables& t, cudaStream_t st) {
     if ((err = cudaMalloc(&t.ptab_fwdT, sizeof(uint2) << 9))) return err;
     ptab_kernel<<<(1u << 13) / 256, 256, 0, st>>>(t.ptab_fwd, t.ptab_inv);
     ptab_t_kernel<<<2, 256, 0, st>>>(t.ptab_fwdT);
-    return cudaGetLastError();
+    if ((err = cudaGetLastError())) return err;
+    return build_sys_conv(t, st);
 }
 
 int fast_encode_columns(uint32_t N) {

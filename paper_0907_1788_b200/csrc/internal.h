@@ -84,6 +84,7 @@ struct FastTables {
     uint2* ptab_fwdT = nullptr;  // pass-0 twiddles transposed, N <= 256: [N + (N/16) s + t] = r_N^(t s)
     uint2* big_fwd = nullptr;   // {r_m^j, 65535 r_m^j} at [m + j], m <= 65536 (four-step twiddles)
     uint2* big_inv = nullptr;
+    uint2* sys_conv = nullptr;  // systematic convolution tables, N = 32..4096 at [2N, 4N) (codec_dec.cu)
 };
 struct FastPlanView {
     uint32_t N, k;
@@ -100,6 +101,7 @@ __host__ __device__ inline uint32_t ahat2_slot(uint32_t N, uint32_t j) {
     return ((j & ((1u << sl0) - 1u)) << 4) | (j >> sl0);
 }
 cudaError_t build_fast_tables(FastTables& t, cudaStream_t st);
+cudaError_t build_sys_conv(FastTables& t, cudaStream_t st);
 // constant-memory copies of the n_domain <= 256 pass-0 twiddle tables (codec_dec.cu)
 cudaError_t upload_const_twiddles(const FastTables& t, cudaStream_t st);
 int fast_tile_columns(uint32_t N);  // 0 when N has no fast kernel
