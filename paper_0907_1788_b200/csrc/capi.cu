@@ -44,6 +44,7 @@ struct fntrs_plans {
     uint32_t ninv = 1;
     uint2* rowmap = nullptr;  // fast-path tables (N == M, kp == k), and the general column path
     uint2* ahat2 = nullptr;
+    mutable uint2* sys_w = nullptr;  // systematic conv form: {ahat_j r^-j} Shoup pairs, natural order (built on first use)
     bool cols = false;        // served by the general column path (codec_cols.cu)
     bool full = false;        // complete reception
     bool split = false;       // 2k > 65536: locator halves' spectra (alo, ahi), product_size 0
@@ -538,7 +539,7 @@ int fntrs_gpu_plans_destroy(fntrs_plans* pl) {
     // stream-ordered release: work already queued on the plan's stream may
     // still read the buffers; callers using other streams must order them
     for (void* p : {(void*)pl->pos, (void*)pl->ainv, (void*)pl->ahat, (void*)pl->rowmap, (void*)pl->ahat2,
-                    (void*)pl->alo, (void*)pl->ahi})
+                    (void*)pl->alo, (void*)pl->ahi, (void*)pl->sys_w})
         if (p) cudaFreeAsync(p, pl->stream);
     delete pl;
     return FNTRS_OK;
@@ -667,6 +668,22 @@ int fntrs_gpu_decode(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t stripes, ui
 namespace {
 // The fused systematic kernel serves the plans the fused decode kernel serves
 // (n_domain <= 4096, product size == n_domain, L a multiple of its tile width).
+// output weights of the convolution-form systematic kernels (codec_dec.cu MODE 3 / 4),
+// built once per plan set; synchronised so later calls on any stream see them
+cudaError_t ensure_sys_weights(const fntrs_ctx* ctx, const fntrs_plans* pl, cudaStream_t st) {
+    if (pl->sys_w || !FNTRS_SYS_CONV_HOST) return cudaSuccess;
+    uint2* w = nullptr;
+    cudaError_t e = cudaMallocAsync(&w, size_t(pl->np) * pl->N * sizeof(uint2), st);
+    if (!e) e = fast::launch_sys_weights(ctx->ftab, pl->N, pl->np, pl->ahat2, w, st);
+    if (!e) e = cudaStreamSynchronize(st);
+    if (e) {
+        if (w) cudaFreeAsync(w, st);
+        return e;
+    }
+    pl->sys_w = w;
+    return cudaSuccess;
+}
+
 bool fused_systematic_ok(const fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t L, const void* in) {
     const int tcols = fast::fast_tile_columns(pl->N);
     return ctx->fast_enabled && pl->rowmap && pl->ahat2 && !pl->cols && !pl->gen && !pl->full && tcols &&
@@ -764,8 +781,9 @@ int fntrs_gpu_encode_systematic(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t
             EscIn ein{reinterpret_cast<const unsigned long long*>(src_esc), n_src_esc};
             EscOut eout{reinterpret_cast<unsigned long long*>(out_esc), reinterpret_cast<unsigned long long*>(n_out_esc),
                         esc_cap};
-            fast::FastPlanView fv{pl->N, pl->k, pl->rowmap, pl->ahat2};
-            cudaError_t le = fast::launch_systematic_fast(ctx->ftab, fv, true, n, stripes, L, sp, src, ein, out, eout, st);
+            cudaError_t le = ensure_sys_weights(ctx, pl, st);
+            fast::FastPlanView fv{pl->N, pl->k, pl->rowmap, pl->ahat2, pl->sys_w};
+            if (!le) le = fast::launch_systematic_fast(ctx->ftab, fv, true, n, stripes, L, sp, src, ein, out, eout, st);
             cudaFreeAsync(sp, st);
             CK(le, "systematic encode launch");
             ctx->launches += 1;
@@ -799,7 +817,8 @@ int fntrs_gpu_decode_systematic(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t 
         EscIn ein{reinterpret_cast<const unsigned long long*>(rx_esc), n_rx_esc};
         EscOut eout{reinterpret_cast<unsigned long long*>(out_esc), reinterpret_cast<unsigned long long*>(n_out_esc),
                     esc_cap};
-        fast::FastPlanView fv{pl->N, pl->k, pl->rowmap, pl->ahat2};
+        CK(ensure_sys_weights(ctx, pl, st), "systematic weights");
+        fast::FastPlanView fv{pl->N, pl->k, pl->rowmap, pl->ahat2, pl->sys_w};
         CK(fast::launch_systematic_fast(ctx->ftab, fv, false, pl->n, stripes, L, stripe_pattern, rx, ein, out, eout, st),
            "systematic decode launch");
         ctx->launches += 1;

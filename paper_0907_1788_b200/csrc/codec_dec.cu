@@ -279,7 +279,6 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
                 __syncthreads();
             }
             // last inverse DIT pass: natural order; P(r^j) = U[j] r^-j ahat_j on the rows kept
-            const uint2* __restrict__ rinv = sysc + N;
             auto st_conv = [&](uint32_t lrow, uint32_t, int q, uint32_t col, uint32_t y) -> uint32_t {
                 bool keep;
                 if constexpr (MODE == 3)
@@ -287,10 +286,9 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
                 else
                     keep = (HALFK ? (q >= R0 / 2) : (lrow >= k)) && lrow < n;
                 if (!keep) return 0u;
-                const uint2 a = __ldg(ah + ahat2_slot(uint32_t(N), lrow));
+                const uint2 a = __ldg(ah + lrow);  // MODE 3 / 4: sysw, {ahat_j r^-j} in natural order
                 if (MODE == 3 && a.x == 0u) return 0u;  // received: written by the scatter pass
-                const uint2 w = __ldg(rinv + lrow);
-                const uint32_t z = canon_s2p(mulws(mulws(y, w.x, w.y), a.x, a.y));
+                const uint32_t z = canon_s2p(mulws(y, a.x, a.y));
                 __stcs(outp + (lrow * L + col), uint16_t(z));
                 return z;
             };
@@ -475,7 +473,7 @@ cudaError_t launch_dec(const FastTables& t, const FastPlanView& pv, uint32_t str
     if ((err = make_map(&map, rx, uint64_t(stripes) * pv.k, L, G::WT, sh.box_rows))) return err;
     TileCounter ctr;
     if ((err = ctr.get(st))) return err;
-    kern<<<sh.grid, G::NT, sh.smem, st>>>(map, t.ptab_fwd, t.ptab_inv, pv.rowmap, pv.ahat2, pv.k, L, sh.tps, sh.tiles,
+    kern<<<sh.grid, G::NT, sh.smem, st>>>(map, t.ptab_fwd, t.ptab_inv, pv.rowmap, MODE >= 3 ? pv.sysw : pv.ahat2, pv.k, L, sh.tps, sh.tiles,
                                           sh.nbox, sh.box_rows, sp, ein, out, eout, n, t.ptab_fwdT, ctr.p,
                                           t.sys_conv ? t.sys_conv + 2 * (1u << E) : nullptr);
     return cudaGetLastError();
@@ -534,6 +532,26 @@ __global__ void sys_conv_kernel(uint2* __restrict__ base) {
         const int32_t b = balanced(acc ? kP - acc : 0u);
         out[i] = make_uint2(uint32_t(b), uint32_t(b * 65535));
     }
+}
+
+// sysw[p][j] = ahat[p][j] r^-j as balanced Shoup pairs (natural order), from the
+// plan's ahat2 (slot order) and the r^-j half of the conv table
+__global__ void sys_weights_kernel(uint32_t N, uint64_t total, const uint2* __restrict__ ahat2,
+                                   const uint2* __restrict__ rinv, uint2* __restrict__ out) {
+    for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < total; t += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t j = uint32_t(t & (N - 1u));
+        const int32_t a = int32_t(ahat2[(t - j) + ahat2_slot(N, j)].x), r = int32_t(__ldg(rinv + j).x);
+        const uint32_t ac = uint32_t(a < 0 ? a + int32_t(kP) : a), rc = uint32_t(r < 0 ? r + int32_t(kP) : r);
+        const int32_t b = balanced(gmul(ac, rc));
+        out[t] = make_uint2(uint32_t(b), uint32_t(b * 65535));
+    }
+}
+
+cudaError_t launch_sys_weights(const FastTables& t, uint32_t N, uint32_t np, const uint2* ahat2, uint2* out,
+                               cudaStream_t st) {
+    if (N < 32 || N > 4096 || !np) return cudaSuccess;
+    sys_weights_kernel<<<148 * 8, 256, 0, st>>>(N, uint64_t(np) * N, ahat2, t.sys_conv + 3 * N, out);
+    return cudaGetLastError();
 }
 
 cudaError_t build_sys_conv(FastTables& t, cudaStream_t st) {

@@ -90,6 +90,7 @@ struct FastPlanView {
     uint32_t N, k;
     const uint2* rowmap;  // [np][N] {received row or ~0, 1/A'(x_i)}
     const uint2* ahat2;   // [np][N] {ahat_j, 65535 ahat_j} at slot ahat2_slot(N, j)
+    const uint2* sysw = nullptr;  // [np][N] {ahat_j r^-j, 65535 ...} natural order (systematic conv form)
 };
 // Storage slot of ahat2 entry j (0 <= j < N, N a power of two). For the fused
 // N <= 4096 decode kernel the table is kept in first-pass order, j = t + q 2^(E-4)
@@ -102,6 +103,16 @@ __host__ __device__ inline uint32_t ahat2_slot(uint32_t N, uint32_t j) {
 }
 cudaError_t build_fast_tables(FastTables& t, cudaStream_t st);
 cudaError_t build_sys_conv(FastTables& t, cudaStream_t st);
+cudaError_t launch_sys_weights(const FastTables& t, uint32_t N, uint32_t np, const uint2* ahat2, uint2* out,
+                               cudaStream_t st);
+// host mirror of codec_dec.cu's FNTRS_SYS_CONV (the weights are only built when the conv form runs)
+#ifndef FNTRS_SYS_CONV_HOST
+#ifdef FNTRS_SYS_CONV
+#define FNTRS_SYS_CONV_HOST FNTRS_SYS_CONV
+#else
+#define FNTRS_SYS_CONV_HOST 1
+#endif
+#endif
 // constant-memory copies of the n_domain <= 256 pass-0 twiddle tables (codec_dec.cu)
 cudaError_t upload_const_twiddles(const FastTables& t, cudaStream_t st);
 int fast_tile_columns(uint32_t N);  // 0 when N has no fast kernel
