@@ -52,6 +52,13 @@ namespace fast {
 #ifndef FNTRS_SYS_CONV
 #define FNTRS_SYS_CONV 1
 #endif
+// MODE 3 / 4 at two passes per transform: the last DIT pass's twiddles applied by the producer
+#ifndef FNTRS_SYS_PRETW
+#define FNTRS_SYS_PRETW 1
+#endif
+// sys_conv layout: N = 32..4096 at [2N, 4N) (Q, r^-j); transposed inverse pass-0 twiddles
+// for N <= 256 at kSysInvT + [N + (N/16) s + t] = r_N^-(t s)
+constexpr uint32_t kSysInvT = 16384;
 #ifndef FNTRS_CONST_TW
 #define FNTRS_CONST_TW 1
 #endif
@@ -269,8 +276,22 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
                         v[q + 1] = mulws(v[q + 1], w.z, w.w);
                     }
                     dit_regs<RZ, true, k2P, uint64_t(FNTRS_R2T_LIM)>(v);
+                    if constexpr (P == 2 && FNTRS_SYS_PRETW) {
+                        // the last DIT pass's input twiddle of row t + s sub0 is r^-(t s); this
+                        // element is t = q, s = g: applied here, where the Shoup product also
+                        // does the reduction the store needed
+                        static_assert(BT < (1ull << 31), "Shoup inputs are signed 32-bit");
+                        const uint4* tq = reinterpret_cast<const uint4*>(sysc - 2 * N + kSysInvT + N + g * RZ);
 #pragma unroll
-                    for (int q = 0; q < RZ; ++q) work[G::idx((g << RLZ) + q, col)] = cap<BT, kSmemCap>(v[q]);
+                        for (int q = 0; q < RZ; q += 2) {
+                            const uint4 w = __ldg(tq + q / 2);
+                            work[G::idx((g << RLZ) + q, col)] = mulws(v[q], w.x, w.y);
+                            work[G::idx((g << RLZ) + q + 1, col)] = mulws(v[q + 1], w.z, w.w);
+                        }
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < RZ; ++q) work[G::idx((g << RLZ) + q, col)] = cap<BT, kSmemCap>(v[q]);
+                    }
                 }
             }
             __syncthreads();
@@ -298,8 +319,35 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
                 for (int q = 0; q < 16; ++q)
                     if (mask & (1u << q)) emit_escape(esc_out, key_out + uint64_t(base + (uint32_t(q) << SL0)) * L + col);
             };
-            pass<E, 0, true, true, kSmemCap, kCanon, G, decltype(ld_sm), decltype(st_conv), NoFix, decltype(flush_conv), 1,
-                 CT>(tI0, ld_sm, st_conv, NoFix(), flush_conv);
+            if constexpr (P == 2 && FNTRS_SYS_PRETW) {  // twiddles applied by the producing pass
+                constexpr int ITEMS = (N / R0) * WT;
+                constexpr uint64_t BO = dit_bound<R0, true, k2P>();
+#pragma unroll 1
+                for (int it = threadIdx.x; it < ITEMS; it += NT) {
+                    const uint32_t col = uint32_t(it) & uint32_t(WT - 1);
+                    const uint32_t t = uint32_t(it) >> LGW;
+                    uint32_t v[R0];
+#pragma unroll
+                    for (int s2 = 0; s2 < R0; ++s2) v[rev<R0>(s2)] = work[G::idx(t + (uint32_t(s2) << SL0), col)];
+                    dit_regs<R0, true, k2P>(v);
+                    uint32_t acc = 0;
+#pragma unroll
+                    for (int q = 0; q < R0; ++q) {
+                        const uint32_t r = st_conv(t + (uint32_t(q) << SL0), t, q, col, cap<BO, kCanon>(v[q]));
+                        v[q] = r;
+                        acc |= r;
+                    }
+                    if (acc >> 16) {
+                        uint32_t mask = 0;
+#pragma unroll
+                        for (int q = 0; q < R0; ++q) mask |= ((v[q] >> 16) & 1u) << q;
+                        flush_conv(mask, t, t, col);
+                    }
+                }
+            } else {
+                pass<E, 0, true, true, kSmemCap, kCanon, G, decltype(ld_sm), decltype(st_conv), NoFix, decltype(flush_conv),
+                     1, CT>(tI0, ld_sm, st_conv, NoFix(), flush_conv);
+            }
         } else {
         // FNT1 last pass (sub 1) + FNT2 first DIT pass on the reversed view:
         // logical group b' = N/R - 1 - g holds s'_j = F[N-1-j]; j >= k zeroed.
@@ -554,9 +602,20 @@ cudaError_t launch_sys_weights(const FastTables& t, uint32_t N, uint32_t np, con
     return cudaGetLastError();
 }
 
+__global__ void sys_invt_kernel(uint2* invT) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < 32 || i >= 512u) return;
+    const int LL = 31 - __clz(i);
+    const uint32_t sub = 1u << (LL - 4), j = i - (1u << LL), s = j / sub, t = j % sub;
+    const uint32_t ex = (65536u - (((t * s) << (16 - LL)) & 0xFFFFu)) & 0xFFFFu;
+    const int32_t w = balanced(gpow(3u, ex));
+    invT[i] = make_uint2(uint32_t(w), uint32_t(w * 65535));
+}
+
 cudaError_t build_sys_conv(FastTables& t, cudaStream_t st) {
-    cudaError_t err = cudaMalloc(&t.sys_conv, sizeof(uint2) << 14);  // [2N, 4N) per N = 32..4096
+    cudaError_t err = cudaMalloc(&t.sys_conv, sizeof(uint2) * (kSysInvT + 512));
     if (err) return err;
+    sys_invt_kernel<<<2, 256, 0, st>>>(t.sys_conv + kSysInvT);
     sys_conv_kernel<5><<<1, 128, 0, st>>>(t.sys_conv);
     sys_conv_kernel<6><<<1, 128, 0, st>>>(t.sys_conv);
     sys_conv_kernel<7><<<1, 128, 0, st>>>(t.sys_conv);
