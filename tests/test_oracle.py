@@ -309,3 +309,54 @@ def test_oracle_matches_golden_fixtures(oracle):
             assert st == 0 and np.array_equal(out, g[name + "__out"]), name
         else:
             raise AssertionError(name)
+
+
+# ------------------------------------------- systematic convolution form ----
+@pytest.mark.parametrize("k,n,seed", [(4, 8, 1), (8, 16, 2), (5, 16, 3), (16, 32, 4), (3, 13, 5), (32, 64, 6)])
+def test_systematic_convolution_identity(oracle, k, n, seed):
+    """The identity the fused systematic kernels (codec_dec.cu MODE 3 / 4) compute:
+    P(r^j) = A(r^j) r^-j (c (*) G')[j] with c[z] = v_z / A'(r^z) on the k lowest
+    received positions and G'[e] = 1 / (1 - r^-e), G'[0] = 0 (cyclic, size N),
+    checked against the oracle's encode_systematic / decode_systematic, i.e.
+    interpolate + re-evaluate (proj/src/codec.cpp:151-196)."""
+    o = oracle
+    N = 1
+    while N < n:
+        N <<= 1
+    st, r = o.root(N)
+    assert st == 0
+    rng = np.random.default_rng(seed)
+    src = rng.integers(0, 65537, k).astype(np.uint32)
+    st, cw = o.encode_systematic(k, n, src)
+    assert st == 0
+
+    def conv_eval(pos, vals):
+        xs = [pow(r, int(z), P) for z in pos]
+        def A(x):
+            a = 1
+            for xi in xs:
+                a = a * (x - xi) % P
+            return a
+        c = np.zeros(N, dtype=np.uint32)
+        for z, v, xi in zip(pos, vals, xs):
+            d = 1
+            for xl in xs:
+                if xl != xi:
+                    d = d * (xi - xl) % P
+            c[z] = int(v) * pow(d, P - 2, P) % P
+        g = np.array([0] + [pow((1 - pow(r, N - e, P)) % P, P - 2, P) for e in range(1, N)], dtype=np.uint32)
+        ch, gh = o.fnt(c), o.fnt(g)
+        h = o.fnt(np.array([int(a) * int(b) % P for a, b in zip(ch, gh)], dtype=np.uint32), inverse=True)
+        return [A(pow(r, j, P)) * pow(r, (N - j) % N, P) % P * int(h[j]) % P for j in range(N)]
+
+    # encode: parity rows k..n-1 from the source at positions 0..k-1
+    ev = conv_eval(list(range(k)), src)
+    assert [int(x) for x in cw[k:]] == ev[k:n]
+    # decode: erased rows < k from the k lowest of a random received subset
+    recv = np.sort(rng.choice(n, size=min(n, k + 2), replace=False))
+    use = recv[:k]
+    st, want = o.decode_systematic(k, n, recv, cw[recv])
+    assert st == 0 and np.array_equal(want, cw[:k])
+    ev = conv_eval(list(use), cw[use])
+    got = [int(cw[j]) if j in set(use.tolist()) else ev[j] for j in range(k)]
+    assert got == [int(x) for x in want]
