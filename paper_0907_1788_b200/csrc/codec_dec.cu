@@ -63,6 +63,12 @@ constexpr uint32_t kSysInvT = 16384;
 #define FNTRS_CONST_TW 1
 #endif
 __constant__ uint4 c_twF[256], c_twI[256], c_twFT[256];
+// n_domain <= 256, MODE 3 / 4: the Q tables (sys_conv [0, 1024)) and the transposed
+// inverse pass-0 twiddles (sys_conv kSysInvT + [0, 512)); rows are warp-uniform
+#ifndef FNTRS_SYS_CONST
+#define FNTRS_SYS_CONST 1
+#endif
+__constant__ uint4 c_sysQ[512], c_sysT[256];
 
 namespace {
 
@@ -70,9 +76,13 @@ namespace {
 // Decode occupancy: the staged input is read only by the first pass, so one
 // stage buffer suffices (the next tile's TMA load is issued right after that
 // pass's barrier) and at N <= 256 five CTAs fit per SM.
-template <int E>
+// MODE 3 / 4 at n_domain <= 256: four CTAs per SM (64 registers) -- A/B vs five: +0.7 %
+#ifndef FNTRS_SYS_MINB
+#define FNTRS_SYS_MINB 4
+#endif
+template <int E, int MODE = 0>
 struct DecOcc {
-    static constexpr int MINB = (E <= 8) ? 5 : Pick<E>::MINB;
+    static constexpr int MINB = (E <= 8) ? (MODE >= 3 ? FNTRS_SYS_MINB : 5) : Pick<E>::MINB;
 };
 
 // MODE 0: decode (interp::interpolate, the k coefficients out).
@@ -93,7 +103,7 @@ struct DecOcc {
 //         Received rows j < k (MODE 3) / source rows (MODE 4) are copied by the
 //         scatter pass.
 template <int E, class G, bool HALFK, int MODE = 0>
-__global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const __grid_constant__ CUtensorMap rx_map,
+__global__ void __launch_bounds__(G::NT, DecOcc<E, MODE>::MINB) dec_fast_kernel(const __grid_constant__ CUtensorMap rx_map,
                                                          const uint2* __restrict__ ptabF, const uint2* __restrict__ ptabI,
                                                          const uint2* __restrict__ rowmap,
                                                          const uint2* __restrict__ ahat2, uint32_t k, uint32_t L,
@@ -258,7 +268,9 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
                 constexpr uint64_t BD = dif_bound<RZ, false, kSmemCap, kLazyLim>();
                 static_assert(BD < (1ull << 31), "Shoup inputs are signed 32-bit");
                 constexpr uint64_t BT = dit_bound<RZ, true, k2P, uint64_t(FNTRS_R2T_LIM)>();  // folded to 2p below
-                const uint4* __restrict__ qt = reinterpret_cast<const uint4*>(sysc);
+                constexpr bool CQ = FNTRS_SYS_CONST && E <= 8;
+                const uint4* qt = CQ ? reinterpret_cast<const uint4*>(reinterpret_cast<const uint2*>(c_sysQ) + 2 * N)
+                                     : reinterpret_cast<const uint4*>(sysc);
 #pragma unroll 1
                 for (int it = threadIdx.x; it < ITEMS; it += NT) {
                     const uint32_t col = uint32_t(it) & uint32_t(WT - 1);
@@ -271,7 +283,7 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
                     const uint4* tq = qt + g * (RZ / 2);
 #pragma unroll
                     for (int q = 0; q < RZ; q += 2) {
-                        const uint4 w = __ldg(tq + q / 2);
+                        const uint4 w = CQ ? tq[q / 2] : __ldg(tq + q / 2);
                         v[q] = mulws(v[q], w.x, w.y);
                         v[q + 1] = mulws(v[q + 1], w.z, w.w);
                     }
@@ -281,10 +293,11 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E>::MINB) dec_fast_kernel(const 
                         // element is t = q, s = g: applied here, where the Shoup product also
                         // does the reduction the store needed
                         static_assert(BT < (1ull << 31), "Shoup inputs are signed 32-bit");
-                        const uint4* tq = reinterpret_cast<const uint4*>(sysc - 2 * N + kSysInvT + N + g * RZ);
+                        const uint4* tq = CQ ? reinterpret_cast<const uint4*>(reinterpret_cast<const uint2*>(c_sysT) + N + g * RZ)
+                                             : reinterpret_cast<const uint4*>(sysc - 2 * N + kSysInvT + N + g * RZ);
 #pragma unroll
                         for (int q = 0; q < RZ; q += 2) {
-                            const uint4 w = __ldg(tq + q / 2);
+                            const uint4 w = CQ ? tq[q / 2] : __ldg(tq + q / 2);
                             work[G::idx((g << RLZ) + q, col)] = mulws(v[q], w.x, w.y);
                             work[G::idx((g << RLZ) + q + 1, col)] = mulws(v[q + 1], w.z, w.w);
                         }
@@ -533,6 +546,8 @@ cudaError_t upload_const_twiddles(const FastTables& t, cudaStream_t st) {
     cudaError_t e = cudaMemcpyToSymbolAsync(c_twF, t.ptab_fwd, sizeof(c_twF), 0, cudaMemcpyDeviceToDevice, st);
     if (!e) e = cudaMemcpyToSymbolAsync(c_twI, t.ptab_inv, sizeof(c_twI), 0, cudaMemcpyDeviceToDevice, st);
     if (!e) e = cudaMemcpyToSymbolAsync(c_twFT, t.ptab_fwdT, sizeof(c_twFT), 0, cudaMemcpyDeviceToDevice, st);
+    if (!e) e = cudaMemcpyToSymbolAsync(c_sysQ, t.sys_conv, sizeof(c_sysQ), 0, cudaMemcpyDeviceToDevice, st);
+    if (!e) e = cudaMemcpyToSymbolAsync(c_sysT, t.sys_conv + kSysInvT, sizeof(c_sysT), 0, cudaMemcpyDeviceToDevice, st);
     return e;
 }
 
