@@ -87,6 +87,8 @@ def _patterns(S, n, k, seed):
     rng = np.random.default_rng(seed)
     pats = [np.arange(k)]  # stripe 0: the systematic prefix (reference's verbatim-copy case)
     pats += [np.sort(rng.choice(n, k, replace=False)) for _ in range(1, S)]
+    if S > 2:  # stripe 1: parity only (no row < k received; every output row is computed)
+        pats[1] = np.arange(n - k, n)
     return np.stack(pats).astype(np.uint32), np.arange(S, dtype=np.uint32)
 
 
