@@ -174,11 +174,16 @@ def reference_lib():
 SYSTEMATIC = False  # --codec systematic
 
 
-def cpu_reference_sample(cfg, seed, stripes, threads):
+PATHS = {"auto": 0, "fast": 1}  # codec::Path (proj/include/fntrs/codec.hpp:39)
+
+
+def cpu_reference_sample(cfg, seed, stripes, threads, path="fast"):
     """Time the reference library (oracle/_ref, the unmodified reference codec)
     on `stripes` stripes of the config, the way the reference CLI runs it
     (per-codeword encode/decode_nonsystematic -- or the systematic pair with
-    --codec systematic -- Path::Auto, threads over codewords).
+    --codec systematic -- threads over codewords), decoding with codec::Path
+    `path`: "auto" is the CLI's default (Lagrange when k <= 256,
+    proj/src/codec.cpp:21-23), "fast" the O(n log n) interpolation.
     Returns (enc_s, dec_s, source_bytes)."""
     ref = reference_lib()
     if ref is None:
@@ -192,22 +197,58 @@ def cpu_reference_sample(cfg, seed, stripes, threads):
     t1 = time.perf_counter()
     rx, rxe = gather_received(enc, esc, pats, sp)
     t2 = time.perf_counter()
-    dec, _ = ref.decode_stripes(cfg.k, cfg.n, pats, sp, rx, rxe, path=0, threads=threads)
+    dec, _ = ref.decode_stripes(cfg.k, cfg.n, pats, sp, rx, rxe, path=PATHS[path], threads=threads)
     t3 = time.perf_counter()
     if not np.array_equal(dec, src):
         raise RuntimeError("reference decode mismatch")
     return t1 - t0, t3 - t2, src.nbytes
 
 
-def pick_cpu_sample(cfg, threads, budget_s):
+def pick_cpu_sample(cfg, threads, budget_s, path="fast"):
     """Stripes (and codewords) so the reference run takes ~budget_s."""
     # calibrate on one stripe
-    e, d, b = cpu_reference_sample(cfg, W.SEED, 1, threads)
+    e, d, b = cpu_reference_sample(cfg, W.SEED, 1, threads, path)
     per = max(e + d, 1e-4)
     return max(1, min(cfg.stripes, int(budget_s / per))), per
 
 
+def cpu_info(ref=None):
+    """Host CPU model, logical cores and whether the reference's AVX2 kernels
+    run here (the same __builtin_cpu_supports("avx2") test as
+    proj/src/transform.cpp:255-279)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next((line.split(":", 1)[1].strip() for line in f if line.startswith("model name")), None)
+    except Exception:
+        pass
+    avx2 = None
+    if ref is None:
+        ref = reference_lib()
+    if ref is not None:
+        avx2 = bool(ref.lib.ref_has_avx2())
+    return {"cpu_model": model, "logical_cores": os.cpu_count(), "avx2_path": avx2}
+
+
 # ------------------------------------------------------------ GPU arm ----
+def rank_layout(cfg, S, rank, world, scaling):
+    """Stripe range [lo, hi), data seed, and the erasure patterns (with the
+    stripe -> pattern map) that rank `rank` codes.
+    weak: every rank codes S stripes of its own seeded data;
+    strong: rank g codes stripes [g*S/G, (g+1)*S/G) of one global workload,
+    with the patterns those stripes use."""
+    lo, hi = rank_stripes(S, rank, world, scaling)
+    seed = rank_seed(W.SEED, rank) if scaling == "weak" else W.SEED
+    if lo == 0:
+        pats, sp = W.patterns(cfg, seed=seed, stripes=hi - lo)
+    else:  # strong scaling: this rank's slice of the global stripes and the patterns they use
+        pats_all, sp_all = W.patterns(cfg, seed=seed, stripes=S)
+        used, sp = np.unique(sp_all[lo:hi], return_inverse=True)
+        pats, sp = pats_all[used], sp.astype(np.uint32)
+    return lo, hi, seed, pats, sp
+
+
+
 def run_gpu(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -221,6 +262,8 @@ def run_gpu(args, rank, world, local_rank):
     lo, hi = rank_stripes(S, rank, world, args.scaling)
     S_rank = hi - lo
     seed = rank_seed(W.SEED, rank) if args.scaling == "weak" else W.SEED
+    if S_rank == 0:
+        raise SystemExit(f"rank {rank}: no stripes (S={S}, world={world})")
     k, n, L = cfg.k, cfg.n, cfg.L
     lib = _lib.load()
     codec = Codec(local_rank)
@@ -249,12 +292,7 @@ def run_gpu(args, rank, world, local_rank):
 
     for c in range(nchunks):
         encode_chunk(c)
-    if lo == 0:
-        pats, sp = W.patterns(cfg, seed=seed, stripes=S_rank)
-    else:  # strong scaling: this rank's slice of the global stripes and the patterns they use
-        pats_all, sp_all = W.patterns(cfg, seed=seed, stripes=S)
-        used, sp = np.unique(sp_all[lo:hi], return_inverse=True)
-        pats, sp = pats_all[used], sp.astype(np.uint32)
+    _, _, _, pats, sp = rank_layout(cfg, S, rank, world, args.scaling)
     rx = torch.empty((S_rank, k, L), dtype=torch.int16, device=dev)
     rx_esc = []
     for c in range(nchunks):
@@ -602,16 +640,28 @@ def pcie_peaks(dev, nbytes=512 << 20):
 
 
 def cpu_baseline(cfg, budget_s):
+    """The unmodified reference library on all host cores: Path::Fast (the
+    faster decode, the value) and Path::Auto (the CLI default) on bounded
+    samples of the workload."""
     threads = os.cpu_count() or 1
+    out = {}
     try:
-        stripes, per = pick_cpu_sample(cfg, threads, budget_s)
-        e, d, b = cpu_reference_sample(cfg, W.SEED + 99, stripes, threads)
+        for path in ("fast", "auto"):
+            stripes, per = pick_cpu_sample(cfg, threads, budget_s / 2, path)
+            e, d, b = cpu_reference_sample(cfg, W.SEED + 99, stripes, threads, path)
+            out[path] = {"value": round(b / (e + d) / 1e9, 6), "encode_gbs": round(b / e / 1e9, 6),
+                         "decode_gbs": round(b / d / 1e9, 6), "stripes": stripes}
     except Exception as ex:  # reported, never fatal for the GPU arm
-        return {"value": None, "error": str(ex)[:200]}
-    return {"value": round(b / (e + d) / 1e9, 6), "unit": "GB/s", "cores": threads, "kind": "reference",
-            "encode_gbs": round(b / e / 1e9, 6), "decode_gbs": round(b / d / 1e9, 6),
-            "sample": f"{stripes} stripes of {cfg.name} (encode + Path::Auto decode incl. plan build), "
-                      f"{threads} threads over codewords, AVX2 path, oracle/_ref = unmodified reference library"}
+        return {"value": None, "error": str(ex)[:200], **out}
+    info = cpu_info()
+    f = out["fast"]
+    return {"value": f["value"], "unit": "GB/s", "cores": threads, "kind": "reference",
+            "encode_gbs": f["encode_gbs"], "decode_gbs": f["decode_gbs"], "path": "fast",
+            "paths": out, **info,
+            "sample": f"{f['stripes']} stripes of {cfg.name} (encode + Path::Fast decode incl. plan build; "
+                      f"Path::Auto on {out['auto']['stripes']} stripes under 'paths'), {threads} threads over "
+                      f"codewords, oracle/_ref = unmodified reference library, "
+                      f"AVX2 kernels {'active' if info['avx2_path'] else 'inactive'}"}
 
 
 # ----------------------------------------------------- reference arm ----
@@ -623,14 +673,19 @@ def run_reference(args, rank, world):
     ref = reference_lib()
     if ref is None:
         return {"impl": "reference", "unavailable": "reference library (oracle/_ref) not built"}
-    stripes, per = pick_cpu_sample(cfg, threads, args.ref_step_seconds)
+    path = args.ref_path
+    stripes, per = pick_cpu_sample(cfg, threads, args.ref_step_seconds, path)
     times = []
     for i in range(args.warmup + args.steps):
-        e, d, b = cpu_reference_sample(cfg, W.SEED + i, stripes, threads)
+        e, d, b = cpu_reference_sample(cfg, W.SEED + i, stripes, threads, path)
         if i >= args.warmup:
             times.append(e + d)
     ms = 1e3 * float(np.mean(times))
     value = 2 * cfg.k * cfg.L * stripes / (ms * 1e-3) / 1e9
+    other = "auto" if path == "fast" else "fast"
+    o_stripes, _ = pick_cpu_sample(cfg, threads, args.ref_step_seconds / 2, other)
+    oe, od, ob = cpu_reference_sample(cfg, W.SEED + 99, o_stripes, threads, other)
+    info = cpu_info(ref)
     return {
         "impl": "reference",
         "metric": "encode & decode GB/s of source data per GPU (1/2/4/8 B200), % of HBM roofline",
@@ -639,9 +694,13 @@ def run_reference(args, rank, world):
         "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "u32 (GF(65537))", "data": "synthetic (same generator and erasure classes)",
         "config": {"workload": f"{cfg.name}: n={cfg.n} k={cfg.k} L={cfg.L}; step = encode + decode "
-                               f"(incl. plan build) of a {stripes}-stripe sample", "stripes_per_step": stripes},
+                               f"(incl. plan build) of a {stripes}-stripe sample", "stripes_per_step": stripes,
+                   "decode_path": path},
         "cpu_baseline": {"value": round(value, 6), "unit": "GB/s", "cores": threads, "kind": "reference",
-                         "sample": f"{stripes} stripes per step, {threads} threads, Path::Auto"},
+                         "path": path, **info,
+                         "sample": f"{stripes} stripes per step, {threads} threads, Path::{path.capitalize()}",
+                         "other_path": {"path": other, "value": round(ob / (oe + od) / 1e9, 6),
+                                        "decode_gbs": round(ob / od / 1e9, 6), "stripes": o_stripes}},
         "e2e": {"value": round(value, 6), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -665,6 +724,14 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-step-seconds", type=float, default=6.0)
+    ap.add_argument("--ref-path", default="fast", choices=sorted(PATHS),
+                    help="reference arm decode path (fast = the faster; auto = the CLI default, Lagrange at k <= 256)")
+    ap.add_argument("--sweep", default="C5:strong",
+                    help="second workload measured after the headline and nested in the line as 'sweep' "
+                         "(north_star's multi-GPU sweep: C5 sharded by stripe); 'none' to skip")
+    ap.add_argument("--sweep-steps", type=int, default=5)
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU test mode: the launcher, rank layout and cross-rank reductions without a GPU")
     ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes per decode launch (profiles/)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo = test mode for several ranks on fewer GPUs (host-side barrier/max only)")
@@ -676,32 +743,141 @@ def main():
     global SYSTEMATIC
     SYSTEMATIC = args.codec == "systematic"
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-launch this command under torch.distributed.run
+        sys.exit(spawn_ranks(args.gpus))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print(f"[bench] note: --gpus {args.gpus} but WORLD_SIZE={world}; measuring {world} rank(s)", file=sys.stderr)
     if args.impl == "reference":
         out = run_reference(args, rank, world)
         if out is not None:
             print(json.dumps(out), flush=True)
         return
+    if args.dry_run:
+        args.dist_backend = "gloo"
     if world > 1:
         import torch
         import torch.distributed as dist
-        ndev = torch.cuda.device_count()
         if args.dist_backend == "gloo":
-            # test mode: ranks may share GPUs; the barrier / max-over-ranks run on the host
-            local_rank = local_rank % max(1, ndev)
-            torch.cuda.set_device(local_rank)
+            # test mode: ranks may share GPUs (or run on no GPU at all with --dry-run);
+            # the barrier / max-over-ranks run on the host
+            ndev = torch.cuda.device_count()
+            if ndev:
+                local_rank = local_rank % ndev
+                torch.cuda.set_device(local_rank)
             dist.init_process_group("gloo")
         else:
             torch.cuda.set_device(local_rank)
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
-    res = run_gpu(args, rank, world, local_rank)
+    comm = communicator_report(rank, world, local_rank, args)
+    if args.dry_run:
+        res = run_dry(args, rank, world)
+    else:
+        res = run_gpu(args, rank, world, local_rank)
+        sweep = parse_sweep(args.sweep)
+        if sweep and (sweep[0] != args.config or sweep[1] != args.scaling):
+            import torch
+            torch.cuda.empty_cache()
+            sub = argparse.Namespace(**vars(args))
+            sub.config, sub.scaling, sub.stripes, sub.steps = sweep[0], sweep[1], 0, max(1, args.sweep_steps)
+            sub.e2e_stripes, sub.no_cpu_baseline, sub.graph = 0, True, False
+            r2 = run_gpu(sub, rank, world, local_rank)
+            res["sweep"] = {key: r2[key] for key in ("value", "unit", "n_gpus", "ms_per_step", "scaling", "steps",
+                                                     "encode_gbs", "decode_gbs", "decode_with_plans_gbs",
+                                                     "phases_ms", "config", "gpu_launches", "verified", "clocks")}
+            res["sweep"]["roofline_decode_frac"] = r2["roofline"]["frac"]
+            res["sweep"]["roofline_encode_frac"] = r2["roofline_encode"]["frac"]
+            res["sweep"]["note"] = ("north_star's multi-GPU sweep: the config's stripes sharded evenly over the ranks "
+                                    "(strong scaling), value = total source bytes / max-over-ranks step time")
+    res["communicator"] = comm
     if rank == 0:
         print(json.dumps(res), flush=True)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def parse_sweep(spec):
+    if not spec or spec == "none":
+        return None
+    cfg, _, scaling = spec.partition(":")
+    if cfg not in W.CONFIGS or scaling not in ("weak", "strong"):
+        raise SystemExit(f"bad --sweep {spec!r} (want e.g. C5:strong)")
+    return cfg, scaling
+
+
+def free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def spawn_ranks(n):
+    """`python bench.py --gpus N` without torchrun: start N ranks (one per GPU)
+    with torch.distributed.run on 127.0.0.1, exactly as the driver does; rank 0
+    prints the line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    print(f"[bench] launching {n} ranks: {' '.join(cmd[1:6])} ...", file=sys.stderr, flush=True)
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "4"))
+    return subprocess.call(cmd, env=env)
+
+
+def communicator_report(rank, world, local_rank, args):
+    """Every rank logs its place in the communicator; an all-reduce of ones
+    proves how many ranks took part (outside any timed region)."""
+    seen = world
+    backend = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        backend = dist.get_backend()
+        dev = "cpu" if backend == "gloo" else torch.device(f"cuda:{local_rank}")
+        t = torch.ones(1, dtype=torch.int64, device=dev)
+        dist.all_reduce(t)
+        seen = int(t.item())
+    dev_name = f"cuda:{local_rank}" if not args.dry_run else "cpu"
+    print(f"[bench] rank {rank}/{world} on {dev_name}: backend={backend or 'none'} communicator ranks={seen}",
+          file=sys.stderr, flush=True)
+    return {"backend": backend or "none", "world_size": world, "ranks_seen_allreduce": seen}
+
+
+def run_dry(args, rank, world):
+    """The multi-rank control flow of run_gpu without a GPU (CPU tests): the
+    same stripe ranges, seeds and pattern slices, a barrier-bracketed timed
+    region of host work sized by the rank's stripes, max-over-ranks timing and
+    the summed verification counts."""
+    import torch.distributed as dist
+    cfg = W.CONFIGS[args.config]
+    S = args.stripes or cfg.stripes
+    lo, hi, seed, pats, sp = rank_layout(cfg, S, rank, world, args.scaling)
+    src = W.symbols(seed, lo * cfg.k * 4, (hi - lo) * cfg.k * 4)  # a 4-column slice of the rank's source
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        digest = int(np.bitwise_xor.reduce(src.astype(np.uint64))) if src.size else 0
+    ms = (time.perf_counter() - t0) * 1e3 / max(1, args.steps)
+    if world > 1:
+        dist.barrier()
+    mx = max_over_ranks([ms])[0]
+    tot = sum_over_ranks([0, hi - lo, len(pats)])
+    ranges = [None] * world
+    if world > 1:
+        dist.all_gather_object(ranges, (rank, lo, hi, seed, int(sp.size)))
+    else:
+        ranges = [(rank, lo, hi, seed, int(sp.size))]
+    return {"metric": "dry run (no GPU): rank layout and reductions", "n_gpus": world, "scaling": args.scaling,
+            "config": {"workload": cfg.name, "stripes": S}, "ms_per_step_max": mx, "digest_rank0": digest,
+            "verified": {"stripes_checked_all_ranks": tot[1], "mismatched_stripes_all_ranks": tot[0],
+                         "patterns_all_ranks": tot[2]},
+            "ranks": [{"rank": r, "lo": a, "hi": b, "seed": sd, "stripes": n} for r, a, b, sd, n in ranges]}
 
 
 if __name__ == "__main__":

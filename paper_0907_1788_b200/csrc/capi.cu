@@ -44,7 +44,7 @@ struct fntrs_plans {
     uint32_t ninv = 1;
     uint2* rowmap = nullptr;  // fast-path tables (N == M, kp == k), and the general column path
     uint2* ahat2 = nullptr;
-    mutable uint2* sys_w = nullptr;  // systematic conv form: {ahat_j r^-j} Shoup pairs, natural order (built on first use)
+    uint2* sys_w = nullptr;  // systematic conv form: {ahat_j r^-j} Shoup pairs, natural order (fused plans, N <= 4096)
     bool cols = false;        // served by the general column path (codec_cols.cu)
     bool full = false;        // complete reception
     bool split = false;       // 2k > 65536: locator halves' spectra (alo, ahi), product_size 0
@@ -56,6 +56,12 @@ struct fntrs_plans {
 namespace {
 
 const char* kVersion = "fntrs_b200 0.1 (sm_100a)";
+
+// The fused, generic-fused and four-step kernels form per-stripe symbol
+// offsets row * L + col in 32 bits (one IMAD on the multiplier-bound path);
+// a stripe whose rows * L reaches 2^32 goes to the tile or column kernels,
+// whose offsets are 64-bit.
+bool narrow_rows(uint32_t rows, uint32_t L) { return uint64_t(rows) * L < (uint64_t(1) << 32); }
 
 uint32_t next_pow2(uint32_t n) {
     uint32_t m = 1;
@@ -333,7 +339,7 @@ namespace {
 int encode_impl(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t N, uint32_t stripes, uint32_t L,
                 const uint16_t* src, const uint64_t* src_esc, uint64_t n_src_esc, uint16_t* out,
                 uint64_t* out_esc, uint64_t esc_cap, uint64_t* n_out_esc, void* stream) {
-    const bool large = fast::large_supported(N) && L % fast::large_tile_columns() == 0;
+    const bool large = fast::large_supported(N) && L % fast::large_tile_columns() == 0 && narrow_rows(N, L);
     if (stripes && L && (!src || !out)) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "null buffer");
     if (n_src_esc && !src_esc) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "src_esc is null");
     DeviceGuard g(ctx->device);
@@ -344,7 +350,7 @@ int encode_impl(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t N, uint32_t str
     EscOut eout{reinterpret_cast<unsigned long long*>(out_esc), reinterpret_cast<unsigned long long*>(n_out_esc),
                 esc_cap};
     const int cols = fast::fast_encode_columns(N);
-    const bool fast_ok = ctx->fast_enabled && cols && L % uint32_t(cols) == 0 &&
+    const bool fast_ok = ctx->fast_enabled && cols && L % uint32_t(cols) == 0 && narrow_rows(N, L) &&
                          reinterpret_cast<uintptr_t>(src) % 16 == 0;
     if (N > kTileMaxN && !large) {  // general column path (codec_cols.cu)
         if (stripes && L) {
@@ -500,6 +506,13 @@ int fntrs_gpu_plans_create(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t kp, 
             e = launch_plan_build(N, M, kp, npatterns, pl->pos, pl->ainv, pl->ahat, ctx->tab, st);
             ctx->launches += 1;
         }
+        if (!e && fastplan && N <= kTileMaxN && FNTRS_SYS_CONV_HOST && fast::fast_tile_columns(N)) {
+            // output weights of the convolution-form systematic kernels (codec_dec.cu MODE 3 / 4),
+            // queued on the plan's stream like rowmap / ahat2 (no synchronisation: capturable)
+            e = cudaMallocAsync(&pl->sys_w, size_t(npatterns) * N * sizeof(uint2), st);
+            if (!e) e = fast::launch_sys_weights(ctx->ftab, N, npatterns, pl->ahat2, pl->sys_w, st);
+            ctx->launches += 1;
+        }
         if (!e && pl->gen) {  // fused M != N decode: row map + Shoup pairs of -A_hat/M
             e = cudaMallocAsync(&pl->rowmap, size_t(npatterns) * N * sizeof(uint2), st);
             if (!e) e = cudaMallocAsync(&pl->ahat2, size_t(npatterns) * M * sizeof(uint2), st);
@@ -616,13 +629,14 @@ int fntrs_gpu_decode(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t stripes, ui
     EscOut eout{reinterpret_cast<unsigned long long*>(out_esc), reinterpret_cast<unsigned long long*>(n_out_esc),
                 esc_cap};
     const int tcols = fast::fast_tile_columns(pl->N);
-    const bool fast_ok = ctx->fast_enabled && !pl->cols && !pl->gen && pl->rowmap && tcols &&
+    const bool narrow = narrow_rows(std::max(pl->N, pl->M), L);
+    const bool fast_ok = ctx->fast_enabled && !pl->cols && !pl->gen && pl->rowmap && tcols && narrow &&
                          L % uint32_t(tcols) == 0 && reinterpret_cast<uintptr_t>(rx) % 16 == 0;
     const int gcols = pl->gen ? fast::gen_tile_columns(pl->N, pl->M) : 0;
-    const bool gen_ok = ctx->fast_enabled && gcols && L % uint32_t(gcols) == 0 &&
+    const bool gen_ok = ctx->fast_enabled && gcols && L % uint32_t(gcols) == 0 && narrow &&
                         reinterpret_cast<uintptr_t>(rx) % 16 == 0;
     const bool large_plan = !pl->cols && fast::large_supported(pl->N) && pl->rowmap;
-    if (pl->cols || (large_plan && L % fast::large_tile_columns())) {  // general column path
+    if (pl->cols || (large_plan && (L % fast::large_tile_columns() || !narrow))) {  // general column path
         if (stripes && L) {
             const uint32_t D = std::max(pl->N, pl->M);
             const uint64_t cap = std::min<uint64_t>(uint64_t(stripes) * L, fast::cols_batch_columns(D, kScratchCapDefault));
@@ -668,25 +682,9 @@ int fntrs_gpu_decode(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t stripes, ui
 namespace {
 // The fused systematic kernel serves the plans the fused decode kernel serves
 // (n_domain <= 4096, product size == n_domain, L a multiple of its tile width).
-// output weights of the convolution-form systematic kernels (codec_dec.cu MODE 3 / 4),
-// built once per plan set; synchronised so later calls on any stream see them
-cudaError_t ensure_sys_weights(const fntrs_ctx* ctx, const fntrs_plans* pl, cudaStream_t st) {
-    if (pl->sys_w || !FNTRS_SYS_CONV_HOST) return cudaSuccess;
-    uint2* w = nullptr;
-    cudaError_t e = cudaMallocAsync(&w, size_t(pl->np) * pl->N * sizeof(uint2), st);
-    if (!e) e = fast::launch_sys_weights(ctx->ftab, pl->N, pl->np, pl->ahat2, w, st);
-    if (!e) e = cudaStreamSynchronize(st);
-    if (e) {
-        if (w) cudaFreeAsync(w, st);
-        return e;
-    }
-    pl->sys_w = w;
-    return cudaSuccess;
-}
-
 bool fused_systematic_ok(const fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t L, const void* in) {
     const int tcols = fast::fast_tile_columns(pl->N);
-    return ctx->fast_enabled && pl->rowmap && pl->ahat2 && !pl->cols && !pl->gen && !pl->full && tcols &&
+    return ctx->fast_enabled && narrow_rows(pl->N, L) && pl->rowmap && pl->ahat2 && !pl->cols && !pl->gen && !pl->full && tcols &&
            L % uint32_t(tcols) == 0 && reinterpret_cast<uintptr_t>(in) % 16 == 0;
 }
 
@@ -781,9 +779,8 @@ int fntrs_gpu_encode_systematic(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t
             EscIn ein{reinterpret_cast<const unsigned long long*>(src_esc), n_src_esc};
             EscOut eout{reinterpret_cast<unsigned long long*>(out_esc), reinterpret_cast<unsigned long long*>(n_out_esc),
                         esc_cap};
-            cudaError_t le = ensure_sys_weights(ctx, pl, st);
             fast::FastPlanView fv{pl->N, pl->k, pl->rowmap, pl->ahat2, pl->sys_w};
-            if (!le) le = fast::launch_systematic_fast(ctx->ftab, fv, true, n, stripes, L, sp, src, ein, out, eout, st);
+            cudaError_t le = fast::launch_systematic_fast(ctx->ftab, fv, true, n, stripes, L, sp, src, ein, out, eout, st);
             cudaFreeAsync(sp, st);
             CK(le, "systematic encode launch");
             ctx->launches += 1;
@@ -817,7 +814,6 @@ int fntrs_gpu_decode_systematic(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t 
         EscIn ein{reinterpret_cast<const unsigned long long*>(rx_esc), n_rx_esc};
         EscOut eout{reinterpret_cast<unsigned long long*>(out_esc), reinterpret_cast<unsigned long long*>(n_out_esc),
                     esc_cap};
-        CK(ensure_sys_weights(ctx, pl, st), "systematic weights");
         fast::FastPlanView fv{pl->N, pl->k, pl->rowmap, pl->ahat2, pl->sys_w};
         CK(fast::launch_systematic_fast(ctx->ftab, fv, false, pl->n, stripes, L, stripe_pattern, rx, ein, out, eout, st),
            "systematic decode launch");

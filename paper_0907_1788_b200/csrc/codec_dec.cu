@@ -649,7 +649,7 @@ cudaError_t launch_systematic_fast(const FastTables& t, const FastPlanView& pv, 
                                    uint16_t* out, EscOut eout, cudaStream_t st) {
 #define FNTRS_SYS(e)                                                                              \
     case (1u << e):                                                                               \
-        if (FNTRS_SYS_CONV)                                                                       \
+        if (FNTRS_SYS_CONV && pv.sysw)  /* weights built with the plan (capi.cu) */             \
             return encode ? launch_dec<e, 4>(t, pv, stripes, L, sp, in, ein, out, eout, st, n)   \
                           : launch_dec<e, 3>(t, pv, stripes, L, sp, in, ein, out, eout, st, n);  \
         return encode ? launch_dec<e, 2>(t, pv, stripes, L, sp, in, ein, out, eout, st, n)       \

@@ -291,11 +291,14 @@ class RefLib:
         S, kk, L = src.shape
         src = np.ascontiguousarray(src, dtype=np.uint16)
         out = np.zeros((S, n, L), dtype=np.uint16)
-        cap = S * n * L + 1024  # worst case: every symbol escaped
-        esc = np.zeros(cap, dtype=np.uint64)
         e = None if src_esc is None or len(src_esc) == 0 else np.ascontiguousarray(src_esc, dtype=np.uint64)
-        ne = self.lib.ref_encode_stripes(k, n, S, L, src, None if e is None else e.ctypes.data,
-                                         0 if e is None else e.size, out, esc, cap, threads)
+        # escapes are rare (~1 per 65537 symbols); grow to the worst case only on overflow (-11)
+        for cap in (S * n * L // 4096 + 4096, S * n * L + 1024):
+            esc = np.zeros(cap, dtype=np.uint64)
+            ne = self.lib.ref_encode_stripes(k, n, S, L, src, None if e is None else e.ctypes.data,
+                                             0 if e is None else e.size, out, esc, cap, threads)
+            if ne != -11:
+                break
         assert ne >= 0, ne
         return out, esc[:ne]
 
@@ -303,12 +306,14 @@ class RefLib:
         S, kp, L = rx.shape
         rx = np.ascontiguousarray(rx, dtype=np.uint16)
         out = np.zeros((S, k, L), dtype=np.uint16)
-        cap = S * k * L + 1024
-        esc = np.zeros(cap, dtype=np.uint64)
         e = None if rx_esc is None or len(rx_esc) == 0 else np.ascontiguousarray(rx_esc, dtype=np.uint64)
-        ne = self.lib.ref_decode_stripes(k, n, S, L, pats.shape[0], _a32(pats), _a32(sp), rx,
-                                         None if e is None else e.ctypes.data, 0 if e is None else e.size,
-                                         out, esc, cap, path, threads)
+        for cap in (S * k * L // 4096 + 4096, S * k * L + 1024):
+            esc = np.zeros(cap, dtype=np.uint64)
+            ne = self.lib.ref_decode_stripes(k, n, S, L, pats.shape[0], _a32(pats), _a32(sp), rx,
+                                             None if e is None else e.ctypes.data, 0 if e is None else e.size,
+                                             out, esc, cap, path, threads)
+            if ne != -11:
+                break
         assert ne >= 0, ne
         return out, esc[:ne]
 

@@ -566,3 +566,34 @@ def test_escape_sort_paths(codec, n, L, S, hot, cap):
         return
     assert np.array_equal(escapes_to_numpy(oe, cnt), want_esc)
     assert np.all(oe[want_esc.size:].cpu().numpy() == -1)  # the ~0 fill stays after the real keys
+
+
+def test_wide_stripe_offsets_beyond_32_bits(codec, oracle):
+    """One stripe whose rows * L exceeds 2^32 symbols (a > 4 GiB file coded as
+    one stripe, shards.encode_file): the fused kernels' 32-bit row offsets
+    would wrap, so the C ABI routes it to the 64-bit tile kernels. The last
+    columns (offsets above 2^32) are checked against the oracle, and
+    decode(encode(s)) == s on the same columns."""
+    from paper_0907_1788_b200 import escapes_to_numpy
+    k, n, L = 16, 32, (1 << 27) + 64
+    assert n * L >= 1 << 32
+    src = torch.randint(-32768, 32767, (1, k, L), dtype=torch.int16, device="cuda")
+    out, oe, cnt = codec.encode(k, n, src)
+    tail = slice(L - 64, L)
+    s_h = src[0, :, tail].cpu().numpy().view(np.uint16)[None].copy()
+    want, want_esc = oracle.encode_stripes(k, n, s_h)
+    got = out[0, :, tail].cpu().numpy().view(np.uint16)[None]
+    assert np.array_equal(got, want)
+    esc = escapes_to_numpy(oe, cnt)
+    tail_esc = [int(e // L) * 64 + int(e % L) - (L - 64) for e in esc if e % L >= L - 64]
+    assert tail_esc == [int(e) for e in want_esc]
+    pats = np.array([np.arange(n - k, n)], dtype=np.uint32)  # parity rows only
+    plans = codec.plans(k, n, pats)
+    rx = out[:, n - k:, :].contiguous()
+    rx_esc = [int(e) - (n - k) * L for e in esc if e >= (n - k) * L]
+    rxe = torch.tensor(rx_esc, dtype=torch.int64, device="cuda") if rx_esc else None
+    del out
+    dec, de, dc = codec.decode(plans, torch.zeros(1, dtype=torch.int32, device="cuda"), rx, rxe)
+    assert torch.equal(dec[0, :, tail], src[0, :, tail])
+    assert torch.equal(dec[0, :, :4096], src[0, :, :4096])
+    assert escapes_to_numpy(de, dc).size == 0

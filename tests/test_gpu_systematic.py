@@ -67,6 +67,9 @@ SYS_SHAPES = [  # (k, n, L, stripes): general kernels, fused N <= 4096 kernels, 
     (700, 2048, 32, 1), (4096, 8192, 64, 1), (8192, 16384, 64, 1),
     # many tiles per persistent CTA (fused MODE 1 / 2 at n_domain 256 and 4096)
     (128, 256, 64, 1200), (2048, 4096, 16, 200),
+    # fused conv-form kernels (MODE 3 / 4) at every n_domain 32..1024, HALFK and not
+    (16, 32, 32, 3), (10, 32, 32, 3), (20, 64, 32, 3), (32, 64, 64, 2), (40, 128, 32, 2),
+    (256, 512, 32, 2), (200, 512, 32, 2), (512, 1024, 16, 2), (300, 1024, 16, 2),
 ]
 
 

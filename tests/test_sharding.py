@@ -68,3 +68,39 @@ def test_gloo_world2_max_over_ranks():
     for r in res:
         assert r[3] == [11.0, 100.0, 1024.0]
         assert r[4] == [1, 2048]
+
+
+def _bench(*argv, timeout=300):
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), *argv], capture_output=True, text=True,
+                       timeout=timeout, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    return json.loads(lines[0]), r.stderr
+
+
+def test_bench_gpus2_spawns_two_ranks_strong():
+    """`bench.py --gpus 2` launches two ranks itself (torch.distributed.run on
+    127.0.0.1); the ranks split C5's stripes evenly, share the seed, and the
+    line carries the max over ranks and the counts summed over ranks."""
+    res, err = _bench("--gpus", "2", "--dry-run", "--config", "C5", "--scaling", "strong", "--steps", "2")
+    assert res["n_gpus"] == 2
+    assert res["communicator"] == {"backend": "gloo", "world_size": 2, "ranks_seen_allreduce": 2}
+    assert [(r["lo"], r["hi"]) for r in res["ranks"]] == [(0, 1024), (1024, 2048)]
+    assert len({r["seed"] for r in res["ranks"]}) == 1
+    assert res["verified"]["stripes_checked_all_ranks"] == 2048
+    assert res["verified"]["patterns_all_ranks"] == 2048  # C5: one pattern per stripe, none shared across ranks
+    assert err.count("communicator ranks=2") == 2  # logged by every rank
+
+
+def test_bench_gpus2_weak_seeds_differ():
+    res, _ = _bench("--gpus", "2", "--dry-run", "--config", "C4", "--scaling", "weak", "--steps", "1")
+    assert [(r["lo"], r["hi"]) for r in res["ranks"]] == [(0, 256), (0, 256)]
+    assert res["ranks"][0]["seed"] != res["ranks"][1]["seed"]
+    assert res["verified"]["stripes_checked_all_ranks"] == 512
