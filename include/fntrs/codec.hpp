@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "fntrs/field.hpp"
+#include "fntrs/instrument.hpp"
 
 namespace fntrs::codec {
 

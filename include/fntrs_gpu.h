@@ -193,6 +193,65 @@ int fntrs_gpu_set_fast_path(fntrs_ctx* ctx, int enabled);
 /* Launch accounting: number of kernels this context has launched. */
 uint64_t fntrs_gpu_launch_count(const fntrs_ctx* ctx);
 
+/* Transform accounting (the reference's note_fnt_execution tally,
+ * proj/src/transform.cpp:292-316 -> proj/src/instrument.cpp:15-18): counts[e]
+ * = transforms of size 2^e this context's kernels have executed so far
+ * (e = 0..16), added by each launch from the schedule of the kernel family it
+ * actually ran (codewords x transforms per codeword at each size). A caller
+ * diffs two snapshots around a call. */
+int fntrs_gpu_transform_counts(const fntrs_ctx* ctx, uint64_t counts[17]);
+
+/* ---- the rest of the reference's public API, on the device ---------------
+ * Not on the batched codec path; these let the reference's own consumers
+ * (proj/tests/acceptance.cpp) link against the drop-in. All pointers DEVICE,
+ * values canonical in [0, 65536]. */
+
+/* naive_dft (proj/include/fntrs/transform.hpp:52, transform.cpp:325-343):
+ * out_j = sum_i in_i root^(ij) for ANY root (inverse: root^-1 and * 1/n). */
+int fntrs_gpu_naive_dft(fntrs_ctx* ctx, uint32_t root, int inverse, uint32_t n, const uint32_t* in,
+                        uint32_t* out, void* stream);
+
+/* TransformPlan's tables (transform.hpp:17-28, transform.cpp:31-63) for size
+ * n (power of two <= 65536): twiddles / inverse_twiddles [n/2], bit_reversal
+ * [n], stage_twiddles / stage_inverse_twiddles [n-1]. Any pointer may be NULL. */
+int fntrs_gpu_transform_tables(fntrs_ctx* ctx, uint32_t n, uint32_t* twiddles, uint32_t* inverse_twiddles,
+                               uint32_t* bit_reversal, uint32_t* stage_twiddles, uint32_t* stage_inverse_twiddles,
+                               void* stream);
+
+/* One polynomial product: out[a_len + b_len - 1] = a * b, coefficient
+ * segments of one DEVICE word array (poly::mul, proj/src/poly.cpp:22-137). */
+typedef struct fntrs_poly_pair {
+    uint64_t a_off, b_off, out_off;
+    uint32_t a_len, b_len;
+} fntrs_poly_pair;
+/* Batched products: pairs is a HOST array of npairs descriptors into `in`
+ * (read) and `out` (written); in and out may be the same array when the
+ * written segments do not overlap the read ones. */
+int fntrs_gpu_poly_products(fntrs_ctx* ctx, uint32_t npairs, const fntrs_poly_pair* pairs, const uint32_t* in,
+                            uint32_t* out, void* stream);
+
+/* Subproduct tree of k points (poly::build_subproduct_tree,
+ * proj/src/poly.cpp:216-242): leaves (x - x_i), each level pairing adjacent
+ * nodes and carrying an odd last node up. fntrs_gpu_subproduct_tree_layout
+ * gives the level count, nodes per level (cap >= levels entries) and the
+ * coefficient count per node in level order (node_len may be NULL; count in
+ * *n_nodes), the total in *n_coeffs; coeffs receives all nodes back to back. */
+int fntrs_gpu_subproduct_tree_layout(uint32_t k, uint32_t* n_levels, uint32_t* level_nodes, uint32_t level_cap,
+                                     uint32_t* node_len, uint64_t* n_nodes, uint64_t* n_coeffs);
+int fntrs_gpu_subproduct_tree(fntrs_ctx* ctx, uint32_t k, const uint32_t* points, uint32_t* coeffs, void* stream);
+
+/* interp::lagrange_oracle (proj/include/fntrs/interp.hpp:56,
+ * proj/src/interp.cpp:139-171): the unique P, deg P < k, with P(xs[i]) = vs[i]
+ * for k DISTINCT points (the caller validates), out[k] coefficients
+ * (trailing zeros not trimmed). */
+int fntrs_gpu_lagrange(fntrs_ctx* ctx, uint32_t k, const uint32_t* xs, const uint32_t* vs, uint32_t* out,
+                       void* stream);
+
+/* poly::derivative (out[len-1]) and poly::eval_horner (*out = a(x)),
+ * proj/src/poly.cpp:201-214. */
+int fntrs_gpu_poly_derivative(fntrs_ctx* ctx, uint32_t len, const uint32_t* a, uint32_t* out, void* stream);
+int fntrs_gpu_poly_eval(fntrs_ctx* ctx, uint32_t len, const uint32_t* a, uint32_t x, uint32_t* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

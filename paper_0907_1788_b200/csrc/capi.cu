@@ -28,6 +28,7 @@ struct fntrs_ctx {
     bool fast_enabled = true;
     cudaStream_t internal = nullptr;
     uint64_t launches = 0;
+    uint64_t fnt_counts[17] = {};  // transforms executed, by log2 size (fntrs_gpu_transform_counts)
     std::string err;
     fast::LogTables ltab;
     std::map<std::pair<uint32_t, uint32_t>, uint32_t*> digit_spectra;  // (N, w) -> Dh [N][D]
@@ -62,6 +63,20 @@ const char* kVersion = "fntrs_b200 0.1 (sm_100a)";
 // a stripe whose rows * L reaches 2^32 goes to the tile or column kernels,
 // whose offsets are 64-bit.
 bool narrow_rows(uint32_t rows, uint32_t L) { return uint64_t(rows) * L < (uint64_t(1) << 32); }
+
+// The transforms a launch executed: `count` transforms of size m (power of two).
+void note_fnt(fntrs_ctx* ctx, uint32_t m, uint64_t count) {
+    int e = 0;
+    while (e < 16 && (1u << e) < m) ++e;
+    ctx->fnt_counts[e] += count;
+}
+
+// Per-codeword schedule of the decode kernels for a plan (every kernel family
+// computes the same transforms; interp.cpp:103-137): complete reception is one
+// inverse FNT_N; otherwise FNT1 = FNT_N of N', FNT2 = FNT_M of the truncated
+// series, the unscaled inverse FNT_M of the product -- and with 2k > 65536 the
+// product by halves: the spectra of S_lo and S_hi and two inverses (size 65536).
+void note_decode_schedule(fntrs_ctx* ctx, const fntrs_plans* pl, uint64_t codewords);
 
 uint32_t next_pow2(uint32_t n) {
     uint32_t m = 1;
@@ -255,6 +270,12 @@ const char* fntrs_gpu_last_error(const fntrs_ctx* ctx) { return ctx ? ctx->err.c
 int fntrs_gpu_device(const fntrs_ctx* ctx) { return ctx ? ctx->device : -1; }
 uint64_t fntrs_gpu_launch_count(const fntrs_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+int fntrs_gpu_transform_counts(const fntrs_ctx* ctx, uint64_t counts[17]) {
+    if (!ctx || !counts) return FNTRS_E_INVALID_ARGUMENT;
+    std::memcpy(counts, ctx->fnt_counts, sizeof(ctx->fnt_counts));
+    return FNTRS_OK;
+}
+
 int fntrs_gpu_set_fast_path(fntrs_ctx* ctx, int enabled) {
     if (!ctx) return FNTRS_E_INVALID_ARGUMENT;
     ctx->fast_enabled = enabled != 0;
@@ -349,6 +370,7 @@ int encode_impl(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t N, uint32_t str
     EscIn ein{reinterpret_cast<const unsigned long long*>(src_esc), n_src_esc};
     EscOut eout{reinterpret_cast<unsigned long long*>(out_esc), reinterpret_cast<unsigned long long*>(n_out_esc),
                 esc_cap};
+    note_fnt(ctx, N, uint64_t(stripes) * L);  // every encode kernel: one FNT_N per codeword
     const int cols = fast::fast_encode_columns(N);
     const bool fast_ok = ctx->fast_enabled && cols && L % uint32_t(cols) == 0 && narrow_rows(N, L) &&
                          reinterpret_cast<uintptr_t>(src) % 16 == 0;
@@ -492,6 +514,7 @@ int fntrs_gpu_plans_create(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t kp, 
                 if (tmp) cudaFreeAsync(tmp, st);
                 if (!e) ctx->digit_spectra[{N, w}] = Dh;
                 ctx->launches += 2;
+                note_fnt(ctx, N, D);
             } else if (!e) {
                 Dh = it->second;
             }
@@ -502,6 +525,7 @@ int fntrs_gpu_plans_create(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t kp, 
                                            pl->ainv, pl->ahat, pl->rowmap, pl->ahat2, st);
             if (scratch) cudaFreeAsync(scratch, st);
             ctx->launches += 8;
+            note_fnt(ctx, N, uint64_t(npatterns) * (1 + D));  // indicator spectra + D digit convolutions
         } else if (!e && locator) {
             e = launch_plan_build(N, M, kp, npatterns, pl->pos, pl->ainv, pl->ahat, ctx->tab, st);
             ctx->launches += 1;
@@ -533,6 +557,7 @@ int fntrs_gpu_plans_create(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t kp, 
             if (!e) e = cudaMallocAsync(&c, words * 4, st);
             if (!e) e = cudaMallocAsync(&T, words * 4, st);
             if (!e) e = fast::build_split_spectra(ctx->ftab, k, npatterns, pl->ahat, pl->alo, pl->ahi, c, T, st);
+            note_fnt(ctx, 65536, 3ull * npatterns);
             if (c) cudaFreeAsync(c, st);
             if (T) cudaFreeAsync(T, st);
             ctx->launches += 6;
@@ -628,6 +653,7 @@ int fntrs_gpu_decode(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t stripes, ui
     EscIn ein{reinterpret_cast<const unsigned long long*>(rx_esc), n_rx_esc};
     EscOut eout{reinterpret_cast<unsigned long long*>(out_esc), reinterpret_cast<unsigned long long*>(n_out_esc),
                 esc_cap};
+    note_decode_schedule(ctx, pl, uint64_t(stripes) * L);
     const int tcols = fast::fast_tile_columns(pl->N);
     const bool narrow = narrow_rows(std::max(pl->N, pl->M), L);
     const bool fast_ok = ctx->fast_enabled && !pl->cols && !pl->gen && pl->rowmap && tcols && narrow &&
@@ -780,6 +806,7 @@ int fntrs_gpu_encode_systematic(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t
             EscOut eout{reinterpret_cast<unsigned long long*>(out_esc), reinterpret_cast<unsigned long long*>(n_out_esc),
                         esc_cap};
             fast::FastPlanView fv{pl->N, pl->k, pl->rowmap, pl->ahat2, pl->sys_w};
+            note_fnt(ctx, pl->N, (pl->sys_w ? 2ull : 4ull) * stripes * L);  // conv form: 2 transforms; else 3 + 1
             cudaError_t le = fast::launch_systematic_fast(ctx->ftab, fv, true, n, stripes, L, sp, src, ein, out, eout, st);
             cudaFreeAsync(sp, st);
             CK(le, "systematic encode launch");
@@ -815,6 +842,7 @@ int fntrs_gpu_decode_systematic(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t 
         EscOut eout{reinterpret_cast<unsigned long long*>(out_esc), reinterpret_cast<unsigned long long*>(n_out_esc),
                     esc_cap};
         fast::FastPlanView fv{pl->N, pl->k, pl->rowmap, pl->ahat2, pl->sys_w};
+        note_fnt(ctx, pl->N, (pl->sys_w ? 2ull : 4ull) * stripes * L);
         CK(fast::launch_systematic_fast(ctx->ftab, fv, false, pl->n, stripes, L, stripe_pattern, rx, ein, out, eout, st),
            "systematic decode launch");
         ctx->launches += 1;
@@ -881,6 +909,7 @@ int fntrs_gpu_fnt(fntrs_ctx* ctx, uint32_t m, int inverse, uint32_t L, const uin
         return fail(ctx, FNTRS_E_INVALID_TRANSFORM_SIZE, "transform size must be a power of two in [1, 65536]");
     if (L && (!in || !out)) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "null buffer");
     DeviceGuard g(ctx->device);
+    note_fnt(ctx, m, L);
     if (m > kTileMaxN) {  // column-batched four-step kernels (plan_fast.cu)
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         Scratch sc;
@@ -920,3 +949,116 @@ extern "C" int fntrs_gpu_fill_symbols(uint64_t seed, uint64_t first_index, uint6
     fill_symbols_kernel<<<148 * 16, 256, 0, static_cast<cudaStream_t>(stream)>>>(seed, first_index, count, out);
     return cudaGetLastError() == cudaSuccess ? FNTRS_OK : FNTRS_E_CUDA;
 }
+
+namespace {
+void note_decode_schedule(fntrs_ctx* ctx, const fntrs_plans* pl, uint64_t codewords) {
+    if (!codewords) return;
+    if (pl->full) {
+        note_fnt(ctx, pl->N, codewords);
+        return;
+    }
+    note_fnt(ctx, pl->N, codewords);
+    if (pl->split) note_fnt(ctx, 65536, 4 * codewords);
+    else note_fnt(ctx, pl->M, 2 * codewords);
+}
+}  // namespace
+
+// ---- the rest of the reference's public API (poly_aux.cu) -------------------
+extern "C" {
+
+int fntrs_gpu_naive_dft(fntrs_ctx* ctx, uint32_t root, int inverse, uint32_t n, const uint32_t* in, uint32_t* out,
+                        void* stream) {
+    if (!ctx) return FNTRS_E_INVALID_ARGUMENT;
+    if (n && (!in || !out)) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "null buffer");
+    DeviceGuard g(ctx->device);
+    root %= kP;
+    const uint32_t r = inverse ? cpow(root, kP - 2) : root;                  // gf::inv (field.hpp:47-50)
+    const uint32_t scale = inverse ? cpow(uint32_t(n % kP), kP - 2) : 1u;  // inv(n mod p)
+    CK(launch_naive_dft(r, scale, n, in, out, static_cast<cudaStream_t>(stream)), "naive dft");
+    ctx->launches += 1;
+    return FNTRS_OK;
+}
+
+int fntrs_gpu_transform_tables(fntrs_ctx* ctx, uint32_t n, uint32_t* twiddles, uint32_t* inverse_twiddles,
+                               uint32_t* bit_reversal, uint32_t* stage_twiddles, uint32_t* stage_inverse_twiddles,
+                               void* stream) {
+    if (!ctx) return FNTRS_E_INVALID_ARGUMENT;
+    if (n == 0 || n > 65536 || (n & (n - 1)))
+        return fail(ctx, FNTRS_E_INVALID_TRANSFORM_SIZE, "transform size must be a power of two in [1, 65536]");
+    DeviceGuard g(ctx->device);
+    CK(launch_transform_tables(n, croot(n, false), croot(n, true), twiddles, inverse_twiddles, bit_reversal,
+                               stage_twiddles, stage_inverse_twiddles, static_cast<cudaStream_t>(stream)),
+       "transform tables");
+    ctx->launches += 1;
+    return FNTRS_OK;
+}
+
+int fntrs_gpu_poly_products(fntrs_ctx* ctx, uint32_t npairs, const fntrs_poly_pair* pairs, const uint32_t* in,
+                            uint32_t* out, void* stream) {
+    if (!ctx) return FNTRS_E_INVALID_ARGUMENT;
+    if (npairs && (!pairs || !in || !out)) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "null buffer");
+    DeviceGuard g(ctx->device);
+    CK(launch_pair_products(npairs, pairs, in, out, static_cast<cudaStream_t>(stream)), "poly products");
+    ctx->launches += 1;
+    return FNTRS_OK;
+}
+
+int fntrs_gpu_subproduct_tree_layout(uint32_t k, uint32_t* n_levels, uint32_t* level_nodes, uint32_t level_cap,
+                                     uint32_t* node_len, uint64_t* n_nodes, uint64_t* n_coeffs) {
+    if (k == 0) return FNTRS_E_SIZE_MISMATCH;
+    std::vector<uint32_t> lvl;
+    const std::vector<uint32_t> len = tree_node_lengths(k, &lvl);
+    if (n_levels) *n_levels = uint32_t(lvl.size());
+    if (level_nodes) {
+        if (level_cap < lvl.size()) return FNTRS_E_INVALID_ARGUMENT;
+        std::copy(lvl.begin(), lvl.end(), level_nodes);
+    }
+    if (node_len) std::copy(len.begin(), len.end(), node_len);
+    if (n_nodes) *n_nodes = len.size();
+    if (n_coeffs) {
+        uint64_t t = 0;
+        for (uint32_t l : len) t += l;
+        *n_coeffs = t;
+    }
+    return FNTRS_OK;
+}
+
+int fntrs_gpu_subproduct_tree(fntrs_ctx* ctx, uint32_t k, const uint32_t* points, uint32_t* coeffs, void* stream) {
+    if (!ctx) return FNTRS_E_INVALID_ARGUMENT;
+    if (k == 0) return fail(ctx, FNTRS_E_SIZE_MISMATCH, "subproduct tree needs at least one point");
+    if (!points || !coeffs) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "null buffer");
+    DeviceGuard g(ctx->device);
+    CK(launch_subproduct_tree(k, points, coeffs, static_cast<cudaStream_t>(stream)), "subproduct tree");
+    ctx->launches += 2;
+    return FNTRS_OK;
+}
+
+int fntrs_gpu_lagrange(fntrs_ctx* ctx, uint32_t k, const uint32_t* xs, const uint32_t* vs, uint32_t* out,
+                       void* stream) {
+    if (!ctx) return FNTRS_E_INVALID_ARGUMENT;
+    if (k && (!xs || !vs || !out)) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "null buffer");
+    DeviceGuard g(ctx->device);
+    CK(launch_lagrange(k, xs, vs, out, static_cast<cudaStream_t>(stream)), "lagrange");
+    ctx->launches += 3;
+    return FNTRS_OK;
+}
+
+int fntrs_gpu_poly_derivative(fntrs_ctx* ctx, uint32_t len, const uint32_t* a, uint32_t* out, void* stream) {
+    if (!ctx) return FNTRS_E_INVALID_ARGUMENT;
+    if (len > 1 && (!a || !out)) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "null buffer");
+    DeviceGuard g(ctx->device);
+    CK(launch_derivative(len, a, out, static_cast<cudaStream_t>(stream)), "derivative");
+    ctx->launches += 1;
+    return FNTRS_OK;
+}
+
+int fntrs_gpu_poly_eval(fntrs_ctx* ctx, uint32_t len, const uint32_t* a, uint32_t x, uint32_t* out, void* stream) {
+    if (!ctx) return FNTRS_E_INVALID_ARGUMENT;
+    if (!out || (len && !a)) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "null buffer");
+    DeviceGuard g(ctx->device);
+    CK(launch_eval(len, x, a, out, static_cast<cudaStream_t>(stream)), "eval");
+    ctx->launches += 1;
+    return FNTRS_OK;
+}
+
+}  // extern "C"

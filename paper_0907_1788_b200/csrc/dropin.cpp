@@ -21,6 +21,8 @@
 #include "fntrs/interp.hpp"
 #include "fntrs/transform.hpp"
 #include "fntrs_gpu.h"
+#include "dropin_shared.h"
+#include "fntrs/poly.hpp"
 
 namespace fntrs {
 
@@ -83,142 +85,13 @@ void throw_status(int status, const std::string& msg) {
     }
 }
 
-namespace {
-
-// One shared context + scratch for the per-codeword API; calls serialise on
-// its mutex (the C ABI requires serialised calls per context).
-struct Shared {
-    std::mutex mu;
-    int device = 0;
-    fntrs_ctx* ctx = nullptr;
-    cudaStream_t stream = nullptr;
-    // device scratch
-    void* dbuf = nullptr;
-    size_t dbuf_bytes = 0;
-    uint32_t* zero_pattern = nullptr;  // stripe_pattern of a one-stripe call: {0}
-    // plan LRU (interp.cpp:70-101): key (n, k, kp, positions)
-    using Key = std::pair<std::vector<uint32_t>, std::vector<uint32_t>>;
-    std::list<std::pair<Key, fntrs_plans*>> lru;
-    static constexpr size_t kCapacity = 16;
-
-    ~Shared() {
-        for (auto& e : lru) fntrs_gpu_plans_destroy(e.second);
-        if (dbuf) cudaFree(dbuf);
-        if (zero_pattern) cudaFree(zero_pattern);
-        if (stream) cudaStreamDestroy(stream);
-        if (ctx) fntrs_gpu_destroy(ctx);
-    }
-
-    void check(int status) {
-        if (status) throw_status(status, std::string(fntrs_gpu_status_string(status)) + ": " +
-                                             fntrs_gpu_last_error(ctx));
-    }
-
-    void ensure() {
-        if (ctx) return;
-        int rc = fntrs_gpu_create(device, &ctx);
-        if (rc) {
-            ctx = nullptr;
-            throw Error("fntrs: no usable CUDA device " + std::to_string(device) +
-                        " (the codec has no CPU fallback)");
-        }
-        cudaSetDevice(device);
-        if (cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking) != cudaSuccess)
-            throw Error("fntrs: cannot create a CUDA stream");
-        if (cudaMalloc(&zero_pattern, 4) != cudaSuccess || cudaMemset(zero_pattern, 0, 4) != cudaSuccess)
-            throw Error("fntrs: device allocation failed");
-    }
-
-    void* scratch(size_t bytes) {
-        if (bytes > dbuf_bytes) {
-            if (dbuf) cudaFree(dbuf);
-            dbuf = nullptr;
-            if (cudaMalloc(&dbuf, bytes) != cudaSuccess) throw Error("fntrs: device allocation failed");
-            dbuf_bytes = bytes;
-        }
-        return dbuf;
-    }
-
-    void sync() {
-        cudaError_t e = cudaStreamSynchronize(stream);
-        if (e != cudaSuccess) throw Error(std::string("fntrs: CUDA error: ") + cudaGetErrorString(e));
-    }
-
-    fntrs_plans* plan_for(uint32_t k, uint32_t n, const std::vector<uint32_t>& pos) {
-        Key key{{n, k, uint32_t(pos.size())}, pos};
-        for (auto it = lru.begin(); it != lru.end(); ++it)
-            if (it->first == key) {
-                lru.splice(lru.begin(), lru, it);
-                return lru.front().second;
-            }
-        fntrs_plans* pl = nullptr;
-        check(fntrs_gpu_plans_create(ctx, k, n, uint32_t(pos.size()), 1, pos.data(), &pl, stream));
-        lru.emplace_front(std::move(key), pl);
-        if (lru.size() > kCapacity) {
-            sync();  // the evicted plan may still be read by queued work
-            fntrs_gpu_plans_destroy(lru.back().second);
-            lru.pop_back();
-        }
-        return pl;
-    }
-};
-
+namespace dropin {
 Shared& shared() {
     static Shared s;
     return s;
 }
-
-uint32_t next_pow2(uint32_t n) {
-    uint32_t m = 1;
-    while (m < n) m <<= 1;
-    return m;
-}
-
-// Fe values -> uint16 words + ascending escape indices (shardio.cpp:131-137).
-void split(const Fe* v, size_t count, std::vector<uint16_t>& words, std::vector<uint64_t>& esc) {
-    words.resize(count);
-    esc.clear();
-    for (size_t i = 0; i < count; ++i) {
-        if (v[i] > 65536) throw SizeMismatch("value " + std::to_string(v[i]) + " outside the field");
-        words[i] = v[i] == 65536 ? 0 : uint16_t(v[i]);
-        if (v[i] == 65536) esc.push_back(i);
-    }
-}
-
-// Runs fn(d_in_words, d_in_esc, d_out_words, d_out_esc, d_count) with the
-// host arrays staged on the device, then joins the result back into Fe.
-template <typename Fn>
-std::vector<Fe> run(Shared& S, const std::vector<uint16_t>& in_words, const std::vector<uint64_t>& in_esc,
-                    size_t out_count, Fn&& fn) {
-    const size_t cap = out_count;  // at most one escape per output symbol
-    const size_t b_in = (in_words.size() * 2 + 255) / 256 * 256;
-    const size_t b_ie = (in_esc.size() * 8 + 255) / 256 * 256 + 256;
-    const size_t b_out = (out_count * 2 + 255) / 256 * 256;
-    const size_t b_oe = (cap * 8 + 255) / 256 * 256 + 256;
-    char* base = static_cast<char*>(S.scratch(b_in + b_ie + b_out + b_oe + 256));
-    auto* d_in = reinterpret_cast<uint16_t*>(base);
-    auto* d_ie = reinterpret_cast<uint64_t*>(base + b_in);
-    auto* d_out = reinterpret_cast<uint16_t*>(base + b_in + b_ie);
-    auto* d_oe = reinterpret_cast<uint64_t*>(base + b_in + b_ie + b_out);
-    auto* d_cnt = reinterpret_cast<uint64_t*>(base + b_in + b_ie + b_out + b_oe);
-    cudaMemcpyAsync(d_in, in_words.data(), in_words.size() * 2, cudaMemcpyHostToDevice, S.stream);
-    if (!in_esc.empty())
-        cudaMemcpyAsync(d_ie, in_esc.data(), in_esc.size() * 8, cudaMemcpyHostToDevice, S.stream);
-    fn(d_in, in_esc.empty() ? nullptr : d_ie, uint64_t(in_esc.size()), d_out, d_oe, uint64_t(cap), d_cnt);
-    std::vector<uint16_t> words(out_count);
-    std::vector<uint64_t> esc(cap);
-    uint64_t ne = 0;
-    cudaMemcpyAsync(words.data(), d_out, out_count * 2, cudaMemcpyDeviceToHost, S.stream);
-    cudaMemcpyAsync(&ne, d_cnt, 8, cudaMemcpyDeviceToHost, S.stream);
-    if (cap) cudaMemcpyAsync(esc.data(), d_oe, cap * 8, cudaMemcpyDeviceToHost, S.stream);
-    S.sync();
-    if (ne > cap) throw TooManyEscapes("escape list overflow");
-    std::vector<Fe> out(words.begin(), words.end());
-    for (uint64_t e = 0; e < ne; ++e) out[esc[e]] = 65536;
-    return out;
-}
-
-}  // namespace
+}  // namespace dropin
+using namespace dropin;
 
 namespace gpu {
 void set_device(int device) {
@@ -257,24 +130,6 @@ CodeParams CodeParams::make(std::uint32_t k, std::uint32_t n, bool systematic) {
 }
 
 namespace {
-uint32_t product_size(uint32_t k) {  // interp.cpp:61-67 (0: no product transform fits)
-    return 2ull * k > 65536ull ? 0u : next_pow2(2 * k);
-}
-
-// the transforms one decode of a codeword performs on the GPU
-void note_decode(const CodeParams& params, uint32_t kp) {
-    const uint32_t nd = next_pow2(params.n), m = product_size(params.k);
-    if (kp == params.n && params.n == nd) {  // complete reception: one inverse transform
-        note_fnt_execution(nd);
-        return;
-    }
-    note_fnt_execution(nd);  // FNT1: the moments of N'
-    // the series' spectrum and the inverse of the product; 2k > 65536: both
-    // series halves and two inverses (the product by halves)
-    const int products = m ? 1 : 2;
-    for (int i = 0; i < 2 * products; ++i) note_fnt_execution(m ? m : 65536);
-}
-
 std::vector<Fe> encode_one(const CodeParams& params, std::span<const Fe> source, bool systematic) {
     if (source.size() != params.k)
         throw SizeMismatch("encode: got " + std::to_string(source.size()) + " source symbols for k = " +
@@ -291,8 +146,7 @@ std::vector<Fe> encode_one(const CodeParams& params, std::span<const Fe> source,
                        uint64_t cap, uint64_t* dcnt) {
                        S.check(fn(S.ctx, params.k, params.n, 1, 1, din, die, nie, dout, doe, cap, dcnt, S.stream));
                    });
-    if (systematic && params.k != params.n) note_decode(params, params.k);  // interpolation at 0..k-1
-    if (!systematic || params.k != params.n) note_fnt_execution(next_pow2(params.n));
+    S.note_transforms();
     return out;
 }
 
@@ -335,8 +189,7 @@ std::vector<Fe> decode_one(const CodeParams& params, const Codeword& sorted, uin
                                   S.check(fn(S.ctx, plan, 1, 1, S.zero_pattern, din, die, nie, dout, doe, cap, dcnt,
                                              S.stream));
                               });
-    note_decode(params, kp);
-    if (systematic) note_fnt_execution(next_pow2(params.n));
+    S.note_transforms();
     return out;
 }
 }  // namespace
@@ -411,7 +264,7 @@ std::vector<Fe> fnt_device(uint32_t n, const Fe* in, int mode) {
     std::vector<Fe> out(n);
     cudaMemcpyAsync(out.data(), d + bytes / 4, size_t(n) * 4, cudaMemcpyDeviceToHost, S.stream);
     S.sync();
-    note_fnt_execution(n);
+    S.note_transforms();
     return out;
 }
 }  // namespace
@@ -422,6 +275,41 @@ TransformPlan::TransformPlan(std::uint32_t n) : size(n) {
     root = gf::root_of_unity(n);
     inverse_root = gf::root_of_unity(n, true);
     size_inverse = gf::inv(n % gf::prime);
+    // the reference's tables (transform.cpp:31-63), filled on the device
+    const size_t h = n / 2, st = n > 1 ? n - 1 : 0;
+    twiddles.resize(h);
+    inverse_twiddles.resize(h);
+    bit_reversal.resize(n);
+    stage_twiddles.resize(st);
+    stage_inverse_twiddles.resize(st);
+    Shared& S = shared();
+    std::lock_guard<std::mutex> lock(S.mu);
+    S.ensure();
+    DevBuf d((2 * h + n + 2 * st + 1) * 4, S.stream);
+    uint32_t* p = d.as<uint32_t>();
+    S.check(fntrs_gpu_transform_tables(S.ctx, n, p, p + h, p + 2 * h, p + 2 * h + n, p + 2 * h + n + st, S.stream));
+    download(S, twiddles.data(), d, h, 0);
+    download(S, inverse_twiddles.data(), d, h, h);
+    download(S, bit_reversal.data(), d, n, 2 * h);
+    download(S, stage_twiddles.data(), d, st, 2 * h + n);
+    download(S, stage_inverse_twiddles.data(), d, st, 2 * h + n + st);
+    S.sync();
+}
+
+std::vector<Fe> naive_dft(Fe root, std::span<const Fe> a, bool inverse) {  // transform.cpp:325-343
+    const size_t n = a.size();
+    std::vector<Fe> out(n);
+    Shared& S = shared();
+    std::lock_guard<std::mutex> lock(S.mu);
+    S.ensure();
+    if (!n) return out;
+    DevBuf d(2 * n * 4, S.stream);
+    upload(S, d, a.data(), n);
+    S.check(fntrs_gpu_naive_dft(S.ctx, root, inverse ? 1 : 0, uint32_t(n), d.as<uint32_t>(), d.as<uint32_t>() + n,
+                                S.stream));
+    download(S, out.data(), d, n, n);
+    S.sync();
+    return out;
 }
 
 const TransformPlan& plan_for(std::uint32_t n) {
@@ -465,6 +353,45 @@ void dit_inverse_unscaled(const TransformPlan& plan, std::span<Fe> data) {
 // ---- plan-level API (interp.hpp) ------------------------------------------
 namespace interp {
 
+namespace {
+std::vector<Fe> points_of(uint32_t n, const std::vector<uint32_t>& positions) {
+    const Fe r = gf::root_of_unity(n);
+    std::vector<Fe> xs(positions.size());
+    for (size_t i = 0; i < xs.size(); ++i) xs[i] = gf::pow(r, positions[i]);
+    return xs;
+}
+}  // namespace
+
+poly::Poly lagrange_oracle(std::span<const std::pair<Fe, Fe>> points) {  // interp.cpp:139-171
+    const size_t k = points.size();
+    std::vector<Fe> xs(k), vs(k);
+    for (size_t i = 0; i < k; ++i) {
+        xs[i] = points[i].first;
+        vs[i] = points[i].second;
+    }
+    {
+        std::vector<Fe> sorted(xs);
+        std::sort(sorted.begin(), sorted.end());
+        auto dup = std::adjacent_find(sorted.begin(), sorted.end());
+        if (dup != sorted.end()) throw DuplicatePoint("interpolation point " + std::to_string(*dup) + " repeats");
+    }
+    Shared& S = shared();
+    std::lock_guard<std::mutex> lock(S.mu);
+    S.ensure();
+    if (k == 0) return {};
+    DevBuf d(3 * k * 4, S.stream);
+    upload(S, d, xs.data(), k);
+    uint32_t* p = d.as<uint32_t>();
+    if (cudaMemcpyAsync(p + k, vs.data(), k * 4, cudaMemcpyHostToDevice, S.stream) != cudaSuccess)
+        throw Error("fntrs: host-to-device copy failed");
+    S.check(fntrs_gpu_lagrange(S.ctx, uint32_t(k), p, p + k, p + 2 * k, S.stream));
+    poly::Poly out(k);
+    download(S, out.data(), d, k, 2 * k);
+    S.sync();
+    poly::normalize(out);
+    return out;
+}
+
 DecodePlan build_plan(std::uint32_t n, std::span<const std::uint32_t> positions) {  // interp.cpp:23-68 checks
     if (positions.empty()) throw TooFewPositions("no positions to build a plan from");
     if (!pow2_domain(n)) throw InvalidTransformSize("plan domain must be a power of two in [1, 65536]");
@@ -491,15 +418,16 @@ DecodePlan build_plan(std::uint32_t n, std::span<const std::uint32_t> positions)
         fntrs_gpu_plans_destroy(static_cast<fntrs_plans*>(const_cast<void*>(p)));
     });
     const uint32_t m = 2ull * k > 65536ull ? 65536u : next_pow2(2 * k);
-    plan.a_coeffs.assign(k + 1, 0);
     plan.aprime_at_x_inv.assign(k, 0);
     std::vector<Fe> afnt(m);
     uint32_t ps = 0;
     S.sync();
-    S.check(fntrs_gpu_plans_export(S.ctx, pl, 0, plan.a_coeffs.data(), plan.aprime_at_x_inv.data(), &ps, afnt.data()));
+    S.check(fntrs_gpu_plans_export(S.ctx, pl, 0, nullptr, plan.aprime_at_x_inv.data(), &ps, afnt.data()));
     plan.product_size = ps;
     afnt.resize(ps);
     plan.a_fnt = std::move(afnt);
+    plan.a_tree = tree_on_device(S, points_of(n, plan.positions));  // x_i = r^(z_i), interp.cpp:30-35
+    S.note_transforms();
     return plan;
 }
 
@@ -542,9 +470,7 @@ poly::Poly interpolate(const DecodePlan& plan, std::span<const Fe> values) {
                            S.check(fntrs_gpu_decode(S.ctx, pl, 1, 1, S.zero_pattern, din, die, nie, dout, doe, cap,
                                                     dcnt, S.stream));
                        });
-    const uint32_t m = plan.product_size ? plan.product_size : 65536u;
-    note_fnt_execution(plan.n);
-    for (int i = 0; i < (plan.product_size ? 2 : 4); ++i) note_fnt_execution(m);
+    S.note_transforms();
     while (!p.empty() && p.back() == 0) p.pop_back();  // poly::normalize
     return p;
 }

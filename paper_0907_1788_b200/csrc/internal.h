@@ -3,6 +3,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
+
+#include "../../include/fntrs_gpu.h"
 
 namespace fntrs_gpu {
 
@@ -56,6 +59,19 @@ cudaError_t launch_decode_tile(const Tables& t, const PlanView& pv, uint32_t str
 
 // Generic batched transform over columns: in/out [m][L] uint32 (natural order).
 // scale multiplies every output (1/m for fnt_inverse, see launch site).
+// poly_aux.cu: the reference's quadratic checkers, TransformPlan tables and polynomial helpers
+cudaError_t launch_naive_dft(uint32_t r, uint32_t scale, uint32_t n, const uint32_t* in, uint32_t* out,
+                             cudaStream_t st);
+cudaError_t launch_transform_tables(uint32_t n, uint32_t root, uint32_t iroot, uint32_t* tw, uint32_t* itw,
+                                    uint32_t* bitrev, uint32_t* stw, uint32_t* sitw, cudaStream_t st);
+cudaError_t launch_pair_products(uint32_t npairs, const fntrs_poly_pair* pairs, const uint32_t* in, uint32_t* out,
+                                 cudaStream_t st);
+std::vector<uint32_t> tree_node_lengths(uint32_t k, std::vector<uint32_t>* level_nodes);
+cudaError_t launch_subproduct_tree(uint32_t k, const uint32_t* xs, uint32_t* coeffs, cudaStream_t st);
+cudaError_t launch_lagrange(uint32_t k, const uint32_t* xs, const uint32_t* vs, uint32_t* out, cudaStream_t st);
+cudaError_t launch_derivative(uint32_t len, const uint32_t* a, uint32_t* out, cudaStream_t st);
+cudaError_t launch_eval(uint32_t len, uint32_t x, const uint32_t* a, uint32_t* out, cudaStream_t st);
+
 cudaError_t launch_fnt_tile(const Tables& t, uint32_t m, bool inverse, uint32_t scale, uint32_t L,
                             const uint32_t* in, uint32_t* out, cudaStream_t st);
 

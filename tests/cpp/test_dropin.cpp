@@ -15,6 +15,8 @@
 #include "fntrs/codec.hpp"
 #include "fntrs/instrument.hpp"
 #include "fntrs/interp.hpp"
+#include "fntrs/poly.hpp"
+#include "fntrs/shardio.hpp"
 #include "fntrs/transform.hpp"
 
 using namespace fntrs;
@@ -355,6 +357,88 @@ int main() {
             });
         for (auto& th : pool) th.join();
         CHECK(bad.load() == 0);
+    }
+    // TransformPlan tables (transform.cpp:31-63) filled on the device
+    {
+        const auto& p8 = plan_for(8);
+        CHECK(p8.twiddles == (std::vector<Fe>{1, 4096, 65281, 16}));  // r8 = 2^12, r8^3 = 2^36 = 16
+        CHECK(p8.bit_reversal == (std::vector<uint32_t>{0, 4, 2, 6, 1, 5, 3, 7}));
+        CHECK(p8.stage_twiddles == (std::vector<Fe>{1, 4096, 65281, 16, 1, 65281, 1}));
+        for (uint32_t n : {1u, 2u, 1024u, 65536u}) {
+            const auto& p = plan_for(n);
+            bool ok = p.twiddles.size() == n / 2 && p.stage_twiddles.size() == (n > 1 ? n - 1 : 0);
+            for (uint32_t j = 0; ok && j < n / 2; j += 97) ok = p.twiddles[j] == gf::pow(p.root, j) &&
+                                                                  gf::mul(p.twiddles[j], p.inverse_twiddles[j]) == 1;
+            size_t off = 0;
+            for (uint32_t len = n; ok && len >= 2; len >>= 1) {
+                for (uint32_t j = 0; j < len / 2; j += 31)
+                    ok = ok && p.stage_twiddles[off + j] == p.twiddles[j * (n / len)] &&
+                         p.stage_inverse_twiddles[off + j] == p.inverse_twiddles[j * (n / len)];
+                off += len / 2;
+            }
+            CHECK(ok);
+        }
+    }
+    // naive_dft (transform.cpp:325-343) against the fast transform; any root
+    {
+        std::mt19937_64 rng(11);
+        for (uint32_t n : {1u, 8u, 256u, 1024u}) {
+            std::vector<Fe> a(n);
+            for (auto& x : a) x = Fe(rng() % 65537);
+            CHECK(naive_dft(plan_for(n).root, a, false) == fnt_forward(plan_for(n), a));
+            CHECK(naive_dft(plan_for(n).root, a, true) == fnt_inverse(plan_for(n), a));
+        }
+        CHECK(naive_dft(5, std::vector<Fe>{1, 1, 1}) == (std::vector<Fe>{3, 31, 651}));  // 1+5+25, 1+25+625
+    }
+    // subproduct tree / a() (test_interp.cpp:41-70 golden plan) and lagrange_oracle
+    {
+        auto plan = interp::build_plan(8, std::vector<uint32_t>{0, 2, 5});
+        CHECK(plan.a() == (poly::Poly{16, 61169, 4351, 1}));
+        CHECK(plan.a_tree.levels.size() == 3 && plan.a_tree.levels[0].size() == 3 &&
+              plan.a_tree.levels[1].size() == 2 && plan.a_tree.levels[1][1] == plan.a_tree.levels[0][2]);
+        std::mt19937_64 rng(12);
+        for (uint32_t k : {1u, 7u, 64u, 300u}) {
+            std::vector<std::pair<Fe, Fe>> pts;
+            std::vector<uint32_t> pos;
+            const uint32_t n = 1024;
+            for (uint32_t z = 0; pos.size() < k; z += 1 + uint32_t(rng() % 3)) pos.push_back(z);
+            std::vector<Fe> vals(k);
+            for (uint32_t i = 0; i < k; ++i) {
+                vals[i] = Fe(rng() % 65537);
+                pts.push_back({gf::pow(plan_for(n).root, pos[i]), vals[i]});
+            }
+            auto pl = interp::build_plan(n, pos);
+            CHECK(interp::interpolate(pl, vals) == interp::lagrange_oracle(pts));
+            poly::Poly prod{1};
+            for (auto& leaf : pl.a_tree.levels[0]) prod = poly::mul_schoolbook(prod, leaf);
+            CHECK(prod == pl.a());
+        }
+        CHECK(throws_as<DuplicatePoint>([] { interp::lagrange_oracle(std::vector<std::pair<Fe, Fe>>{{3, 1}, {3, 2}}); }));
+        CHECK(poly::derivative(poly::Poly{5, 3, 65536, 2}) == (poly::Poly{3, 65535, 6}));
+        CHECK(poly::eval_horner(poly::Poly{1, 2, 3}, 10) == 321);
+        CHECK(poly::middle_product(poly::Poly{1, 1}, poly::Poly{1, 2, 3}) == (std::vector<Fe>{3, 5}));
+        CHECK(throws_as<ProductTooLarge>([] { poly::mul_fnt(poly::Poly(40000, 1), poly::Poly(40000, 1)); }));
+    }
+    // shard wire format golden bytes (test_shardio.cpp:70-87) and round trips
+    {
+        const shardio::ShardInfo info{7, 2, 4, 1, true};
+        const auto b = shardio::write_shard(info, std::vector<Fe>{5, 65536, 7});
+        const std::vector<uint8_t> want{'F', 'N', 'T', 'C', 1, 0, 0, 0, 0, 0, 0, 0, 7, 0, 2, 0, 4, 0, 1, 1,
+                                        0, 0, 0, 3, 0, 1, 0, 0, 0, 1, 0, 5, 0, 0, 0, 7};
+        CHECK(b == want);
+        auto r = shardio::read_shard(b);
+        CHECK(r.info == info && r.payload == (std::vector<Fe>{5, 65536, 7}));
+        auto bad = b;
+        bad[29] = 9;
+        CHECK(throws_as<MalformedEscapes>([&] { shardio::read_shard(bad); }));
+        const std::vector<uint8_t> data{1, 2, 3, 4, 5};
+        auto m = shardio::symbolize(data, 2);
+        CHECK(m.stripes == 2 && m.cells == (std::vector<Fe>{0x0102, 0x0304, 0x0500, 0}));
+        CHECK(shardio::desymbolize(m, 5) == data);
+        CHECK(throws_as<LengthMismatch>([&] { shardio::desymbolize(m, 9); }));
+        const shardio::ChunkManifest man{9, 5, 2, 65536, 2, false};
+        CHECK(shardio::read_manifest(shardio::write_manifest(man)) == man);
+        CHECK(shardio::shard_filename(255, 3) == "00000000000000ff.3.fnt");
     }
     std::printf("drop-in C++ API: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail ? 1 : 0;
