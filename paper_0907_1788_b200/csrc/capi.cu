@@ -335,7 +335,16 @@ int fntrs_gpu_destroy(fntrs_ctx* ctx) {
     cudaFree(ctx->ltab.exp3);
     cudaFree(ctx->ltab.log3);
     for (auto& kv : ctx->digit_spectra) cudaFree(kv.second);
-    for (auto& kv : ctx->sys_plans) fntrs_gpu_plans_destroy(kv.second);
+    // the context's own systematic plans: the device is idle (synchronised
+    // above), so free them directly rather than on the stream they were built
+    // on, which the caller may already have destroyed
+    for (auto& kv : ctx->sys_plans) {
+        fntrs_plans* pl = kv.second;
+        for (void* p : {(void*)pl->pos, (void*)pl->ainv, (void*)pl->ahat, (void*)pl->rowmap, (void*)pl->ahat2,
+                        (void*)pl->alo, (void*)pl->ahi, (void*)pl->sys_w})
+            if (p) cudaFree(p);
+        delete pl;
+    }
     if (ctx->internal) cudaStreamDestroy(ctx->internal);
     delete ctx;
     return FNTRS_OK;

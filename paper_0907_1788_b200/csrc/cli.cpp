@@ -59,10 +59,11 @@ struct Gpu {
         if (fntrs_gpu_create(0, &ctx)) throw Error("fntrs: no usable CUDA device (the codec has no CPU fallback)");
         if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) throw Error("fntrs: cannot create a stream");
     }
-    ~Gpu() {
+    ~Gpu() {  // the context first: its cached plans release on this stream
+        if (st) cudaStreamSynchronize(st);
+        if (ctx) fntrs_gpu_destroy(ctx);
         for (void* p : bufs) cudaFree(p);
         if (st) cudaStreamDestroy(st);
-        if (ctx) fntrs_gpu_destroy(ctx);
     }
     template <typename T>
     T* alloc(size_t n) {

@@ -87,8 +87,10 @@ void throw_status(int status, const std::string& msg) {
 
 namespace dropin {
 Shared& shared() {
-    static Shared s;
-    return s;
+    // never destroyed: releasing device state from a static destructor can run
+    // after the CUDA runtime has shut down; the process exit frees it all
+    static Shared* s = new Shared;
+    return *s;
 }
 }  // namespace dropin
 using namespace dropin;

@@ -63,7 +63,7 @@ __global__ void tables_kernel(uint32_t n, uint32_t bits, uint32_t root, uint32_t
         }
         if (bitrev) bitrev[i] = bits ? __brev(i) >> (32 - bits) : 0u;
         if (i + 1 < n) {  // stage entry i: offset off(len) = n - len, j = i - off
-            const uint32_t len = n >> (31 - __clz(n - 1 - i));  // largest len with n - len <= i
+            const uint32_t len = 1u << (32 - __clz(n - i - 1));  // next_pow2(n - i): n - len <= i < n - len/2
             const uint32_t j = i - (n - len), stride = n / len;
             if (stw) stw[i] = cpow(root, uint64_t(j) * stride);
             if (sitw) sitw[i] = cpow(iroot, uint64_t(j) * stride);
