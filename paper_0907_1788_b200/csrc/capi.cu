@@ -397,6 +397,18 @@ int encode_impl(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t N, uint32_t str
         }
         return sort_escapes(ctx, eout, uint64_t(stripes) * n * L, st);
     }
+    if (large && fast::stream_enabled()) {
+        if (stripes && L) {
+            Scratch sc;
+            rc = get_scratch(ctx, sc, fast::stream_scratch_words(N, stripes, L, false) * 4, 1, st);
+            if (rc) return rc;
+            cudaError_t le = fast::launch_encode_stream(ctx->ftab, k, n, N, stripes, L, src, ein, out, eout, sc.p[0], st);
+            release_scratch(sc, st);
+            CK(le, "encode launch");
+            ctx->launches += 1;
+        }
+        return sort_escapes(ctx, eout, uint64_t(stripes) * n * L, st);
+    }
     if (large) {
         if (stripes && L) {
             const uint32_t batch = std::min(stripes, fast::large_batch(N, L, scratch_cap()));
@@ -685,6 +697,18 @@ int fntrs_gpu_decode(fntrs_ctx* ctx, const fntrs_plans* pl, uint32_t stripes, ui
             release_scratch(sc, st);
             CK(le, "decode launch");
             ctx->launches += 7 * ((uint64_t(stripes) * L + cap - 1) / cap);
+        }
+    } else if (large_plan && fast::stream_enabled()) {
+        if (stripes && L) {
+            Scratch sc;
+            rc = get_scratch(ctx, sc, fast::stream_scratch_words(pl->N, stripes, L, true) * 4, 1, st);
+            if (rc) return rc;
+            fast::FastPlanView fv{pl->N, pl->k, pl->rowmap, pl->ahat2};
+            cudaError_t le = fast::launch_decode_stream(ctx->ftab, fv, stripes, L, stripe_pattern, rx, ein, out, eout,
+                                                        sc.p[0], st);
+            release_scratch(sc, st);
+            CK(le, "decode launch");
+            ctx->launches += 1;
         }
     } else if (large_plan) {
         if (stripes && L) {

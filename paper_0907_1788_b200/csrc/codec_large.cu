@@ -31,6 +31,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "fft_pass.cuh"
@@ -65,6 +67,31 @@ __device__ __forceinline__ BlockIdx block_index(uint32_t tps, uint32_t ng) {
     return {rest / ng, rest % ng, ct * kLW};
 }
 
+// One unit of work of a four-step pass: inner index g of 64 codewords
+// (columns c0..c0+63 of stripe `stripe`), and where the unit's block of the
+// uint32 intermediates lives -- element offset of its row 0 / first column,
+// and the TMA coordinates of that corner. The batched kernels address a
+// [stripes][N][L] scratch (row stride L); the streamed kernel a ring of
+// [N][64] slots (row stride 64), LY = 64.
+struct Unit {
+    uint32_t stripe, g, c0;
+    uint64_t yoff;
+    uint32_t yx0, yrow0;
+};
+
+template <uint32_t N>
+__device__ __forceinline__ Unit batch_unit(uint32_t tps, uint32_t ng, uint32_t stripe0, uint32_t L) {
+    const BlockIdx bi = block_index(tps, ng);
+    return {stripe0 + bi.sb, bi.g, bi.c0, uint64_t(bi.sb) * N * L + bi.c0, bi.c0, bi.sb * N};
+}
+
+// A consumed intermediate block is dead: drop its L2 lines without a write
+// back (each block is read by exactly one unit, after its TMA load landed).
+__device__ __forceinline__ void discard_block(const uint32_t* base, uint32_t bytes) {
+    for (uint32_t off = threadIdx.x * 128u; off < bytes; off += kLNT * 128u)
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(reinterpret_cast<const char*>(base) + off) : "memory");
+}
+
 // The CTA's input block -- ROWS contiguous rows x kLW columns of a uint32
 // intermediate -- lands in the shared work tile with one TMA load (row-major,
 // the unswizzled 64-wide geometry), so the first pass reads shared memory.
@@ -82,20 +109,20 @@ __device__ __forceinline__ void tile_in(uint32_t* work, const CUtensorMap* map, 
 }
 
 // ---------------------------------------------------------------- encode ----
-template <int E1, int E2, bool HALFK>
-__global__ void __launch_bounds__(kLNT, LG<E1>::MINB)
-enc_a_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, uint32_t k, uint32_t L, uint32_t tps,
-             uint32_t stripe0, const uint16_t* __restrict__ src, EscIn esc_in, uint32_t* __restrict__ Y) {
+template <int E1, int E2, bool HALFK, int LY>
+__device__ __forceinline__ void enc_a_body(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, uint32_t k,
+                                           uint32_t L, const uint16_t* __restrict__ src, EscIn esc_in,
+                                           uint32_t* __restrict__ Y, const Unit& u) {
     using G = LG<E1>;
     using S = Sched<E1>;
     constexpr uint32_t N1 = 1u << E1, N2 = 1u << E2, N = N1 * N2;
     constexpr int R0 = 1 << S::rlog(0), RLZ = G::RLZ;
     extern __shared__ __align__(128) uint32_t work[];
-    const BlockIdx bi = block_index(tps, N2);
-    const uint32_t i2 = bi.g, stripe = stripe0 + bi.sb;
-    const unsigned long long key_in = uint64_t(stripe) * k * L + bi.c0;
+    const uint32_t Ly = LY ? uint32_t(LY) : L;
+    const uint32_t i2 = u.g, stripe = u.stripe;
+    const unsigned long long key_in = uint64_t(stripe) * k * L + u.c0;
     const uint16_t* srcp = launder(src + key_in);
-    uint32_t* yp = launder(Y + (uint64_t(bi.sb) * N) * L + bi.c0);
+    uint32_t* yp = launder(Y + u.yoff);
     const bool esc_any = esc_in.n != 0;
 
     const uint16_t* sq = srcp;
@@ -122,18 +149,18 @@ enc_a_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, uin
     auto ld_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t { return work[G::idx(lrow, col)]; };
     uint32_t* yq = yp;
     uint32_t tix = 0;
-    const uint64_t ystep = opaque_stride((uint64_t(N2) * L * 4) << (E1 - RLZ));
+    const uint64_t ystep = opaque_stride((uint64_t(N2) * Ly * 4) << (E1 - RLZ));
     const uint2* bigN = launder(bigF + N);
     auto st_y = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) -> uint32_t {
         if (!kStep) {
             const uint32_t m1 = perm_head<E1>(b) + (uint32_t(s) << (E1 - RLZ));
             const uint2 w = __ldg(bigF + N + ((i2 * m1) & (N - 1)));
-            yp[(m1 * N2 + i2) * L + col] = mulws(y, w.x, w.y);
+            yp[(m1 * N2 + i2) * Ly + col] = mulws(y, w.x, w.y);
             return 0u;
         }
         if (s == 0) {
             const uint32_t m1 = perm_head<E1>(b);
-            yq = yp + ((m1 * N2 + i2) * L + col);
+            yq = yp + ((m1 * N2 + i2) * Ly + col);
             tix = i2 * m1;
         } else {
             yq = step_ptr(yq, ystep);
@@ -148,25 +175,32 @@ enc_a_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, uin
     pass<E1, 1, false, false, kSmemCap, kSmemCap, G>(pass_table(ptab, S::llog(1)), ld_sm, st_y);
 }
 
+template <int E1, int E2, bool HALFK>
+__global__ void __launch_bounds__(kLNT, LG<E1>::MINB)
+enc_a_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, uint32_t k, uint32_t L, uint32_t tps,
+             uint32_t stripe0, const uint16_t* __restrict__ src, EscIn esc_in, uint32_t* __restrict__ Y) {
+    constexpr uint32_t N = 1u << (E1 + E2);
+    enc_a_body<E1, E2, HALFK, 0>(ptab, bigF, k, L, src, esc_in, Y, batch_unit<N>(tps, 1u << E2, stripe0, L));
+}
+
 // TS (n == N): the CTA's N2 output rows m1 + N1 m2 are staged in shared memory
 // and written by one TMA store through the (L, m1, m2, stripe) view of `out`.
-template <int E1, int E2, bool PUNCT, bool TS = false>
-__global__ void __launch_bounds__(kLNT, (TS ? (E2 <= 7 ? 4 : 2) : LG<E2>::MINB))
-enc_b_kernel(const uint2* __restrict__ ptab, uint32_t n, uint32_t L, uint32_t tps, uint32_t stripe0,
-             const uint32_t* __restrict__ Y, uint16_t* __restrict__ out, EscOut esc_out,
-             const __grid_constant__ CUtensorMap out_map, const __grid_constant__ CUtensorMap in_map) {
+template <int E1, int E2, bool PUNCT, bool TS, int LY>
+__device__ __forceinline__ void enc_b_body(const uint2* __restrict__ ptab, uint32_t n, uint32_t L,
+                                           const uint32_t* __restrict__ Y, uint16_t* __restrict__ out, EscOut esc_out,
+                                           const CUtensorMap* out_map, const CUtensorMap* in_map, const Unit& u) {
     using G = LG<E2>;
     using S = Sched<E2>;
-    constexpr uint32_t N1 = 1u << E1, N2 = 1u << E2, N = N1 * N2;
+    constexpr uint32_t N1 = 1u << E1, N2 = 1u << E2;
     constexpr int RLZ = G::RLZ;
     extern __shared__ __align__(128) uint32_t work[];
-    const BlockIdx bi = block_index(tps, N1);
-    const uint32_t m1 = bi.g, stripe = stripe0 + bi.sb;
-    const uint32_t* yp = launder(Y + (uint64_t(bi.sb) * N + m1 * N2) * L + bi.c0);
-    const unsigned long long key_out = uint64_t(stripe) * n * L + bi.c0;
+    const uint32_t Ly = LY ? uint32_t(LY) : L;
+    const uint32_t m1 = u.g, stripe = u.stripe;
+    const uint32_t* yp = launder(Y + u.yoff + uint64_t(m1 * N2) * Ly);
+    const unsigned long long key_out = uint64_t(stripe) * n * L + u.c0;
     uint16_t* outp = launder(out + key_out);
 
-    auto ld = [&](uint32_t i2, uint32_t, int, uint32_t col) -> uint32_t { return yp[i2 * L + col]; };
+    auto ld = [&](uint32_t i2, uint32_t, int, uint32_t col) -> uint32_t { return yp[i2 * Ly + col]; };
     auto st_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col, uint32_t y) -> uint32_t {
         work[G::idx(lrow, col)] = y;
         return 0u;
@@ -196,7 +230,8 @@ enc_b_kernel(const uint2* __restrict__ ptab, uint32_t n, uint32_t L, uint32_t tp
                             key_out + uint64_t(m1 + N1 * (perm_head<E2>(b) + (uint32_t(s) << (E2 - RLZ)))) * L + col);
     };
     __shared__ __align__(8) uint64_t bar;
-    tile_in<N2>(work, &in_map, bi.c0, bi.sb * N + m1 * N2, &bar);
+    tile_in<N2>(work, in_map, u.yx0, u.yrow0 + m1 * N2, &bar);
+    if constexpr (LY != 0) discard_block(yp, N2 * kLW * 4);
     (void)ld;
     pass<E2, 0, false, false, k2P, kSmemCap, G>(pass_table(ptab, S::llog(0)), ld_sm, st_sm);
     __syncthreads();
@@ -205,30 +240,41 @@ enc_b_kernel(const uint2* __restrict__ ptab, uint32_t n, uint32_t L, uint32_t tp
         fence_proxy_async();
         __syncthreads();
         if (threadIdx.x == 0) {
-            tma_store_4d(&out_map, out_s, int(bi.c0), int(m1), 0, int(stripe));
+            tma_store_4d(out_map, out_s, int(u.c0), int(m1), 0, int(stripe));
             bulk_commit();
             bulk_wait_read();  // the CTA's shared memory must outlive the store's reads
         }
     }
 }
 
+template <int E1, int E2, bool PUNCT, bool TS = false>
+__global__ void __launch_bounds__(kLNT, (TS ? (E2 <= 7 ? 4 : 2) : LG<E2>::MINB))
+enc_b_kernel(const uint2* __restrict__ ptab, uint32_t n, uint32_t L, uint32_t tps, uint32_t stripe0,
+             const uint32_t* __restrict__ Y, uint16_t* __restrict__ out, EscOut esc_out,
+             const __grid_constant__ CUtensorMap out_map, const __grid_constant__ CUtensorMap in_map) {
+    constexpr uint32_t N = 1u << (E1 + E2);
+    enc_b_body<E1, E2, PUNCT, TS, 0>(ptab, n, L, Y, out, esc_out, &out_map, &in_map,
+                                     batch_unit<N>(tps, 1u << E1, stripe0, L));
+}
+
 // ---------------------------------------------------------------- decode ----
-template <int E1, int E2>
-__global__ void __launch_bounds__(kLNT, LG<E1>::MINB)
-dec_1_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, const uint2* __restrict__ rowmap,
-             uint32_t k, uint32_t L, uint32_t tps, uint32_t stripe0, const uint32_t* __restrict__ stripe_pattern,
-             const uint16_t* __restrict__ rx, EscIn esc_in, uint32_t* __restrict__ Y) {
+template <int E1, int E2, int LY>
+__device__ __forceinline__ void dec_1_body(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF,
+                                           const uint2* __restrict__ rowmap, uint32_t k, uint32_t L,
+                                           const uint32_t* __restrict__ stripe_pattern,
+                                           const uint16_t* __restrict__ rx, EscIn esc_in, uint32_t* __restrict__ Y,
+                                           const Unit& u) {
     using G = LG<E1>;
     using S = Sched<E1>;
     constexpr uint32_t N1 = 1u << E1, N2 = 1u << E2, N = N1 * N2;
     constexpr int R0 = 1 << S::rlog(0), RLZ = G::RLZ;
     extern __shared__ __align__(128) uint32_t work[];
-    const BlockIdx bi = block_index(tps, N2);
-    const uint32_t i2 = bi.g, stripe = stripe0 + bi.sb;
+    const uint32_t Ly = LY ? uint32_t(LY) : L;
+    const uint32_t i2 = u.g, stripe = u.stripe;
     const uint2* __restrict__ rm = rowmap + size_t(__ldg(stripe_pattern + stripe)) * N;
-    const unsigned long long key = uint64_t(stripe) * k * L + bi.c0;
+    const unsigned long long key = uint64_t(stripe) * k * L + u.c0;
     const uint16_t* rxp = launder(rx + key);
-    uint32_t* yp = launder(Y + (uint64_t(bi.sb) * N) * L + bi.c0);
+    uint32_t* yp = launder(Y + u.yoff);
     const bool esc_any = esc_in.n != 0;
 
     uint32_t zflag = 0;  // a received (non-erased) zero word in this butterfly group
@@ -258,18 +304,18 @@ dec_1_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, con
     auto ld_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t { return work[G::idx(lrow, col)]; };
     uint32_t* yq = yp;
     uint32_t tix = 0;
-    const uint64_t ystep = opaque_stride((uint64_t(N2) * L * 4) << (E1 - RLZ));
+    const uint64_t ystep = opaque_stride((uint64_t(N2) * Ly * 4) << (E1 - RLZ));
     const uint2* bigN = launder(bigF + N);
     auto st_y = [&](uint32_t, uint32_t b, int s, uint32_t col, uint32_t y) -> uint32_t {
         if (!kStep) {
             const uint32_t m1 = perm_head<E1>(b) + (uint32_t(s) << (E1 - RLZ));
             const uint2 w = __ldg(bigF + N + ((i2 * m1) & (N - 1)));
-            yp[(m1 * N2 + i2) * L + col] = mulws(y, w.x, w.y);
+            yp[(m1 * N2 + i2) * Ly + col] = mulws(y, w.x, w.y);
             return 0u;
         }
         if (s == 0) {
             const uint32_t m1 = perm_head<E1>(b);
-            yq = yp + ((m1 * N2 + i2) * L + col);
+            yq = yp + ((m1 * N2 + i2) * Ly + col);
             tix = i2 * m1;
         } else {
             yq = step_ptr(yq, ystep);
@@ -284,10 +330,20 @@ dec_1_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, con
     pass<E1, 1, false, false, kSmemCap, kSmemCap, G>(pass_table(ptab, S::llog(1)), ld_sm, st_y);
 }
 
-template <int E1, int E2, bool HALFK>
-__global__ void __launch_bounds__(kLNT, LG<E2>::MINB)
-dec_2_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, uint32_t k, uint32_t L, uint32_t tps,
-             const uint32_t* __restrict__ Y1, uint32_t* __restrict__ Y2, const __grid_constant__ CUtensorMap in_map) {
+template <int E1, int E2>
+__global__ void __launch_bounds__(kLNT, LG<E1>::MINB)
+dec_1_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, const uint2* __restrict__ rowmap,
+             uint32_t k, uint32_t L, uint32_t tps, uint32_t stripe0, const uint32_t* __restrict__ stripe_pattern,
+             const uint16_t* __restrict__ rx, EscIn esc_in, uint32_t* __restrict__ Y) {
+    constexpr uint32_t N = 1u << (E1 + E2);
+    dec_1_body<E1, E2, 0>(ptab, bigF, rowmap, k, L, stripe_pattern, rx, esc_in, Y,
+                          batch_unit<N>(tps, 1u << E2, stripe0, L));
+}
+
+template <int E1, int E2, bool HALFK, int LY>
+__device__ __forceinline__ void dec_2_body(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, uint32_t k,
+                                           uint32_t L, const uint32_t* __restrict__ Y1, uint32_t* __restrict__ Y2,
+                                           const CUtensorMap* in_map, const Unit& u) {
     using G = LG<E2>;
     using S = Sched<E2>;
     constexpr uint32_t N1 = 1u << E1, N2 = 1u << E2, N = N1 * N2;
@@ -295,12 +351,12 @@ dec_2_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, uin
     constexpr uint32_t FLIP = N2 - 1;
     constexpr int LGW = ilog2c<kLW>();
     extern __shared__ __align__(128) uint32_t work[];
-    const BlockIdx bi = block_index(tps, N1);
-    const uint32_t m1 = bi.g, i1p = N1 - 1 - m1;
-    const uint32_t* y1 = launder(Y1 + (uint64_t(bi.sb) * N + m1 * N2) * L + bi.c0);
-    uint32_t* y2 = launder(Y2 + (uint64_t(bi.sb) * N) * L + bi.c0);
+    const uint32_t Ly = LY ? uint32_t(LY) : L;
+    const uint32_t m1 = u.g, i1p = N1 - 1 - m1;
+    const uint32_t* y1 = launder(Y1 + u.yoff + uint64_t(m1 * N2) * Ly);
+    uint32_t* y2 = launder(Y2 + u.yoff);
 
-    auto ld = [&](uint32_t i2, uint32_t, int, uint32_t col) -> uint32_t { return y1[i2 * L + col]; };
+    auto ld = [&](uint32_t i2, uint32_t, int, uint32_t col) -> uint32_t { return y1[i2 * Ly + col]; };
     auto st_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col, uint32_t y) -> uint32_t {
         work[G::idx(lrow, col)] = y;
         return 0u;
@@ -310,16 +366,16 @@ dec_2_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, uin
     };
     uint32_t* yq = y2;
     uint32_t tix = 0;
-    const uint64_t ystep = opaque_stride((uint64_t(N1) * L * 4) << S::slog(0));
+    const uint64_t ystep = opaque_stride((uint64_t(N1) * Ly * 4) << S::slog(0));
     const uint2* bigN = launder(bigF + N);
     auto st_y2 = [&](uint32_t q2, uint32_t, int q, uint32_t col, uint32_t y) -> uint32_t {
         if (!kStep) {
             const uint2 w = __ldg(bigF + N + ((i1p * q2) & (N - 1)));
-            y2[(q2 * N1 + i1p) * L + col] = mulws(y, w.x, w.y);
+            y2[(q2 * N1 + i1p) * Ly + col] = mulws(y, w.x, w.y);
             return 0u;
         }
         if (q == 0) {
-            yq = y2 + ((q2 * N1 + i1p) * L + col);
+            yq = y2 + ((q2 * N1 + i1p) * Ly + col);
             tix = i1p * q2;
         } else {
             yq = step_ptr(yq, ystep);
@@ -331,7 +387,8 @@ dec_2_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, uin
     };
     // FNT1 pass B, first radix pass (input block by TMA)
     __shared__ __align__(8) uint64_t bar;
-    tile_in<N2>(work, &in_map, bi.c0, bi.sb * N + m1 * N2, &bar);
+    tile_in<N2>(work, in_map, u.yx0, u.yrow0 + m1 * N2, &bar);
+    if constexpr (LY != 0) discard_block(y1, N2 * kLW * 4);
     (void)ld;
     auto ld_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t { return work[G::idx(lrow, col)]; };
     pass<E2, 0, false, false, k2P, kSmemCap, G>(pass_table(ptab, S::llog(0)), ld_sm, st_sm);
@@ -369,25 +426,33 @@ dec_2_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, uin
     pass<E2, 0, false, true, kSmemCap, kSmemCap, G>(pass_table(ptab, S::llog(0)), ld_smf, st_y2);
 }
 
-template <int E1, int E2>
-__global__ void __launch_bounds__(kLNT, LG<E1>::MINB)
-dec_3_kernel(const uint2* __restrict__ ptabF, const uint2* __restrict__ ptabI, const uint2* __restrict__ bigI,
-             const uint2* __restrict__ ahat2, uint32_t L, uint32_t tps, uint32_t stripe0,
-             const uint32_t* __restrict__ stripe_pattern, const uint32_t* __restrict__ Y2, uint32_t* __restrict__ Y3,
-             const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map) {
+template <int E1, int E2, bool HALFK>
+__global__ void __launch_bounds__(kLNT, LG<E2>::MINB)
+dec_2_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, uint32_t k, uint32_t L, uint32_t tps,
+             const uint32_t* __restrict__ Y1, uint32_t* __restrict__ Y2, const __grid_constant__ CUtensorMap in_map) {
+    constexpr uint32_t N = 1u << (E1 + E2);
+    dec_2_body<E1, E2, HALFK, 0>(ptab, bigF, k, L, Y1, Y2, &in_map, batch_unit<N>(tps, 1u << E1, 0, L));
+}
+
+template <int E1, int E2, int LY>
+__device__ __forceinline__ void dec_3_body(const uint2* __restrict__ ptabF, const uint2* __restrict__ ptabI,
+                                           const uint2* __restrict__ bigI, const uint2* __restrict__ ahat2, uint32_t L,
+                                           const uint32_t* __restrict__ stripe_pattern,
+                                           const uint32_t* __restrict__ Y2, uint32_t* __restrict__ Y3,
+                                           const CUtensorMap* in_map, const CUtensorMap* out_map, const Unit& u) {
     using G = LG<E1>;
     using S = Sched<E1>;
     constexpr uint32_t N1 = 1u << E1, N2 = 1u << E2, N = N1 * N2;
     constexpr int RLZ = G::RLZ, RZ = 1 << RLZ;
     constexpr int LGW = ilog2c<kLW>();
     extern __shared__ __align__(128) uint32_t work[];
-    const BlockIdx bi = block_index(tps, N2);
-    const uint32_t q2 = bi.g, stripe = stripe0 + bi.sb;
+    const uint32_t Ly = LY ? uint32_t(LY) : L;
+    const uint32_t q2 = u.g, stripe = u.stripe;
     const uint2* __restrict__ ah = ahat2 + size_t(__ldg(stripe_pattern + stripe)) * N;
-    const uint32_t* y2 = launder(Y2 + (uint64_t(bi.sb) * N + q2 * N1) * L + bi.c0);
-    uint32_t* y3 = launder(Y3 + (uint64_t(bi.sb) * N) * L + bi.c0);
+    const uint32_t* y2 = launder(Y2 + u.yoff + uint64_t(q2 * N1) * Ly);
+    uint32_t* y3 = launder(Y3 + u.yoff);
 
-    auto ld = [&](uint32_t i1p, uint32_t, int, uint32_t col) -> uint32_t { return y2[i1p * L + col]; };
+    auto ld = [&](uint32_t i1p, uint32_t, int, uint32_t col) -> uint32_t { return y2[i1p * Ly + col]; };
     auto st_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col, uint32_t y) -> uint32_t {
         work[G::idx(lrow, col)] = y;
         return 0u;
@@ -395,12 +460,13 @@ dec_3_kernel(const uint2* __restrict__ ptabF, const uint2* __restrict__ ptabI, c
     auto ld_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col) -> uint32_t { return work[G::idx(lrow, col)]; };
     auto st_y3 = [&](uint32_t t1, uint32_t, int, uint32_t col, uint32_t y) -> uint32_t {
         const uint2 w = __ldg(bigI + N + ((q2 * t1) & (N - 1)));
-        y3[(t1 * N2 + q2) * L + col] = mulws(y, w.x, w.y);
+        y3[(t1 * N2 + q2) * Ly + col] = mulws(y, w.x, w.y);
         return 0u;
     };
     // FNT2 pass B, first radix pass
     __shared__ __align__(8) uint64_t bar;
-    tile_in<N1>(work, &in_map, bi.c0, bi.sb * N + q2 * N1, &bar);
+    tile_in<N1>(work, in_map, u.yx0, u.yrow0 + q2 * N1, &bar);
+    if constexpr (LY != 0) discard_block(y2, N1 * kLW * 4);
     (void)ld;
     pass<E1, 0, false, false, k2P, kSmemCap, G>(pass_table(ptabF, S::llog(0)), ld_sm, st_sm);
     __syncthreads();
@@ -450,29 +516,39 @@ dec_3_kernel(const uint2* __restrict__ ptabF, const uint2* __restrict__ ptabI, c
     fence_proxy_async();
     __syncthreads();
     if (threadIdx.x == 0) {
-        tma_store_3d(&out_map, work, int(bi.c0), int(q2), int(bi.sb * N1));
+        tma_store_3d(out_map, work, int(u.yx0), int(q2), int(u.yrow0 / N2));
         bulk_commit();
         bulk_wait_read();
     }
 }
 
-template <int E1, int E2, bool HALFK>
-__global__ void __launch_bounds__(kLNT, LG<E2>::MINB)
-dec_4_kernel(const uint2* __restrict__ ptabI, uint32_t k, uint32_t L, uint32_t tps, uint32_t stripe0,
-             const uint32_t* __restrict__ Y3, uint16_t* __restrict__ out, EscOut esc_out,
-             const __grid_constant__ CUtensorMap in_map) {
+template <int E1, int E2>
+__global__ void __launch_bounds__(kLNT, LG<E1>::MINB)
+dec_3_kernel(const uint2* __restrict__ ptabF, const uint2* __restrict__ ptabI, const uint2* __restrict__ bigI,
+             const uint2* __restrict__ ahat2, uint32_t L, uint32_t tps, uint32_t stripe0,
+             const uint32_t* __restrict__ stripe_pattern, const uint32_t* __restrict__ Y2, uint32_t* __restrict__ Y3,
+             const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map) {
+    constexpr uint32_t N = 1u << (E1 + E2);
+    dec_3_body<E1, E2, 0>(ptabF, ptabI, bigI, ahat2, L, stripe_pattern, Y2, Y3, &in_map, &out_map,
+                          batch_unit<N>(tps, 1u << E2, stripe0, L));
+}
+
+template <int E1, int E2, bool HALFK, int LY>
+__device__ __forceinline__ void dec_4_body(const uint2* __restrict__ ptabI, uint32_t k, uint32_t L,
+                                           const uint32_t* __restrict__ Y3, uint16_t* __restrict__ out,
+                                           EscOut esc_out, const CUtensorMap* in_map, const Unit& u) {
     using G = LG<E2>;
     using S = Sched<E2>;
-    constexpr uint32_t N1 = 1u << E1, N2 = 1u << E2, N = N1 * N2;
+    constexpr uint32_t N1 = 1u << E1, N2 = 1u << E2;
     constexpr int RLZ = G::RLZ, RZ = 1 << RLZ;
     extern __shared__ __align__(128) uint32_t work[];
-    const BlockIdx bi = block_index(tps, N1);
-    const uint32_t t1 = bi.g, stripe = stripe0 + bi.sb;
-    const uint32_t* y3 = launder(Y3 + (uint64_t(bi.sb) * N + t1 * N2) * L + bi.c0);
-    const unsigned long long key = uint64_t(stripe) * k * L + bi.c0;
+    const uint32_t Ly = LY ? uint32_t(LY) : L;
+    const uint32_t t1 = u.g, stripe = u.stripe;
+    const uint32_t* y3 = launder(Y3 + u.yoff + uint64_t(t1 * N2) * Ly);
+    const unsigned long long key = uint64_t(stripe) * k * L + u.c0;
     uint16_t* outp = launder(out + key);
 
-    auto ld = [&](uint32_t i2, uint32_t, int, uint32_t col) -> uint32_t { return y3[i2 * L + col]; };
+    auto ld = [&](uint32_t i2, uint32_t, int, uint32_t col) -> uint32_t { return y3[i2 * Ly + col]; };
     auto st_sm = [&](uint32_t lrow, uint32_t, int, uint32_t col, uint32_t y) -> uint32_t {
         work[G::idx(lrow, col)] = y;
         return 0u;
@@ -495,11 +571,185 @@ dec_4_kernel(const uint2* __restrict__ ptabI, uint32_t k, uint32_t L, uint32_t t
                 emit_escape(esc_out, key + uint64_t(t1 + N1 * (perm_head<E2>(b) + (uint32_t(s) << (E2 - RLZ)))) * L + col);
     };
     __shared__ __align__(8) uint64_t bar;
-    tile_in<N2>(work, &in_map, bi.c0, bi.sb * N + t1 * N2, &bar);
+    tile_in<N2>(work, in_map, u.yx0, u.yrow0 + t1 * N2, &bar);
+    if constexpr (LY != 0) discard_block(y3, N2 * kLW * 4);
     (void)ld;
     pass<E2, 0, true, false, k2P, kSmemCap, G>(pass_table(ptabI, S::llog(0)), ld_sm, st_sm);
     __syncthreads();
     pass<E2, 1, true, false, kSmemCap, kCanon, G>(pass_table(ptabI, S::llog(1)), ld_sm, st_out, NoFix(), flush);
+}
+
+template <int E1, int E2, bool HALFK>
+__global__ void __launch_bounds__(kLNT, LG<E2>::MINB)
+dec_4_kernel(const uint2* __restrict__ ptabI, uint32_t k, uint32_t L, uint32_t tps, uint32_t stripe0,
+             const uint32_t* __restrict__ Y3, uint16_t* __restrict__ out, EscOut esc_out,
+             const __grid_constant__ CUtensorMap in_map) {
+    constexpr uint32_t N = 1u << (E1 + E2);
+    dec_4_body<E1, E2, HALFK, 0>(ptabI, k, L, Y3, out, esc_out, &in_map, batch_unit<N>(tps, 1u << E1, stripe0, L));
+}
+
+// ------------------------------------------------------- streamed (L2) ----
+// One persistent launch runs every pass of every column block (64 codewords
+// of one stripe) with the uint32 intermediates in rings of R [N][64] slots
+// that stay in L2, instead of [stripes][N][L] HBM scratch between launches.
+// Units (phase, column block cb, inner index g) are claimed in ticket order
+// from one counter; step s of the order holds, last phase first, the units of
+// phase p for cb = s - (p-1) D. A unit waits (acquire spin) until
+//   * phase p-1 of its cb has finished (the transpose needs every unit), and
+//   * phase p+1 of cb - R has finished (it read the ring slot cb reuses);
+// both were claimed earlier (D < R), and units only wait on earlier tickets,
+// so the schedule cannot deadlock. done[p][cb] counts finished units.
+__device__ __forceinline__ void wait_at_least(const uint32_t* p, uint32_t target) {
+    uint32_t v;
+    for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+        if (v >= target) break;
+        __nanosleep(128);
+    }
+}
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+// Ticket claims, one ahead: the CTA claims its next unit as it starts the
+// current one, so the atomic's round trip overlaps the work. (Still no
+// deadlock: the smallest ticket being worked on only waits on smaller
+// tickets, and none of those can be a claimed-but-unstarted one.)
+struct Claims {
+    uint32_t* ticket;
+    uint32_t* s_next;  // shared slot
+    __device__ __forceinline__ uint32_t first() {
+        if (threadIdx.x == 0) *s_next = atomicAdd(ticket, 1u);
+        __syncthreads();
+        return *s_next;
+    }
+    // after every thread has read the current ticket: claim the following one
+    __device__ __forceinline__ void prefetch() {
+        __syncthreads();
+        if (threadIdx.x == 0) *s_next = atomicAdd(ticket, 1u);
+    }
+    __device__ __forceinline__ uint32_t next() {
+        __syncthreads();
+        return *s_next;
+    }
+};
+
+
+// every thread's global writes of the unit, then one count: the barrier
+// orders the CTA's writes before thread 0's gpu-scope fence, which is
+// cumulative, then the counter update (the release pattern of CUTLASS's
+// semaphore)
+__device__ __forceinline__ void unit_done(uint32_t* counter, bool tma_stored) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (tma_stored) {
+            bulk_wait_all();  // the unit's TMA store has landed in global memory
+            fence_proxy_async_global();
+        }
+        __threadfence();
+        atomicAdd(counter, 1u);
+    }
+}
+
+template <int E1, int E2>
+struct StreamGeom {
+    static constexpr uint32_t N1 = 1u << E1, N2 = 1u << E2, N = N1 * N2;
+    static constexpr int MINB = LG<(E1 > E2 ? E1 : E2)>::MINB;
+};
+
+template <int E1, int E2, bool HALFK, bool PUNCT>
+__global__ void __launch_bounds__(kLNT, StreamGeom<E1, E2>::MINB)
+enc_stream_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, uint32_t k, uint32_t n, uint32_t L,
+                  uint32_t tps, uint32_t ncb, uint32_t R, uint32_t D, const uint16_t* __restrict__ src, EscIn esc_in,
+                  uint16_t* __restrict__ out, EscOut esc_out, uint32_t* __restrict__ Y, uint32_t* __restrict__ ctl,
+                  const __grid_constant__ CUtensorMap out_map, const __grid_constant__ CUtensorMap in_map) {
+    using SG = StreamGeom<E1, E2>;
+    constexpr uint32_t N1 = SG::N1, N2 = SG::N2, N = SG::N, U = N1 + N2;
+    uint32_t* done1 = ctl + 1;
+    uint32_t* done2 = done1 + ncb;
+    const uint32_t total = (ncb + D) * U;
+    __shared__ uint32_t s_next;
+    Claims cl{ctl, &s_next};
+    for (uint32_t t = cl.first(); t < total; t = cl.next()) {
+        cl.prefetch();
+        const uint32_t step = t / U, r = t - step * U;
+        const bool p2 = r < N1;  // [phase 2: N1 units][phase 1: N2 units]
+        const uint32_t g = p2 ? r : r - N1;
+        if (p2 && step < D) continue;
+        const uint32_t cb = p2 ? step - D : step;
+        if (cb >= ncb) continue;
+        const uint32_t slot = cb % R;
+        const Unit u{cb / tps, g, (cb % tps) * kLW, uint64_t(slot) * N * kLW, 0u, slot * N};
+        if (threadIdx.x == 0) {
+            if (p2) {
+                wait_at_least(done1 + cb, N2);
+                fence_proxy_async_global();
+            } else if (cb >= R) {
+                wait_at_least(done2 + cb - R, N1);
+            }
+        }
+        __syncthreads();
+        if (p2) {
+            enc_b_body<E1, E2, PUNCT, false, kLW>(ptab, n, L, Y, out, esc_out, &out_map, &in_map, u);
+            unit_done(done2 + cb, false);
+        } else {
+            enc_a_body<E1, E2, HALFK, kLW>(ptab, bigF, k, L, src, esc_in, Y, u);
+            unit_done(done1 + cb, false);
+        }
+    }
+}
+
+template <int E1, int E2, bool HALFK>
+__global__ void __launch_bounds__(kLNT, StreamGeom<E1, E2>::MINB)
+dec_stream_kernel(const uint2* __restrict__ ptabF, const uint2* __restrict__ ptabI, const uint2* __restrict__ bigF,
+                  const uint2* __restrict__ bigI, const uint2* __restrict__ rowmap, const uint2* __restrict__ ahat2,
+                  uint32_t k, uint32_t L, uint32_t tps, uint32_t ncb, uint32_t R, uint32_t D,
+                  const uint32_t* __restrict__ stripe_pattern, const uint16_t* __restrict__ rx, EscIn esc_in,
+                  uint16_t* __restrict__ out, EscOut esc_out, uint32_t* __restrict__ Y1, uint32_t* __restrict__ Y2,
+                  uint32_t* __restrict__ Y3, uint32_t* __restrict__ ctl, const __grid_constant__ CUtensorMap map1,
+                  const __grid_constant__ CUtensorMap map2, const __grid_constant__ CUtensorMap map3o,
+                  const __grid_constant__ CUtensorMap map3) {
+    using SG = StreamGeom<E1, E2>;
+    constexpr uint32_t N1 = SG::N1, N2 = SG::N2, N = SG::N, U = 2 * (N1 + N2);
+    uint32_t* done = ctl + 1;  // done[(p - 1) * ncb + cb]
+    const uint32_t total = (ncb + 3 * D) * U;
+    __shared__ uint32_t s_next;
+    Claims cl{ctl, &s_next};
+    for (uint32_t t = cl.first(); t < total; t = cl.next()) {
+        cl.prefetch();
+        const uint32_t step = t / U, r = t - step * U;
+        // [phase 4: N1][phase 3: N2][phase 2: N1][phase 1: N2]
+        uint32_t p, g;
+        if (r < N1) p = 4, g = r;
+        else if (r < N1 + N2) p = 3, g = r - N1;
+        else if (r < 2 * N1 + N2) p = 2, g = r - N1 - N2;
+        else p = 1, g = r - 2 * N1 - N2;
+        const uint32_t lag = (p - 1) * D;
+        if (step < lag) continue;
+        const uint32_t cb = step - lag;
+        if (cb >= ncb) continue;
+        const uint32_t slot = cb % R;
+        const Unit u{cb / tps, g, (cb % tps) * kLW, uint64_t(slot) * N * kLW, 0u, slot * N};
+        if (threadIdx.x == 0) {
+            if (p > 1) wait_at_least(done + (p - 2) * ncb + cb, (p - 1) % 2 ? N2 : N1);  // phases 1, 3: N2 units
+            if (p < 4 && cb >= R) wait_at_least(done + p * ncb + cb - R, (p + 1) % 2 ? N2 : N1);
+            fence_proxy_async_global();
+        }
+        __syncthreads();
+        switch (p) {
+            case 1:
+                dec_1_body<E1, E2, kLW>(ptabF, bigF, rowmap, k, L, stripe_pattern, rx, esc_in, Y1, u);
+                break;
+            case 2:
+                dec_2_body<E1, E2, HALFK, kLW>(ptabF, bigF, k, L, Y1, Y2, &map1, u);
+                break;
+            case 3:
+                dec_3_body<E1, E2, kLW>(ptabF, ptabI, bigI, ahat2, L, stripe_pattern, Y2, Y3, &map2, &map3o, u);
+                break;
+            default:
+                dec_4_body<E1, E2, HALFK, kLW>(ptabI, k, L, Y3, out, esc_out, &map3, u);
+                break;
+        }
+        unit_done(done + (p - 1) * ncb + cb, p == 3);
+    }
 }
 
 // (L, m1, m2, stripe) view of an unpunctured output [stripes][N1 N2][L]: row m1 + N1 m2
@@ -635,6 +885,81 @@ cudaError_t run_decode(const FastTables& t, const FastPlanView& pv, uint32_t str
     return cudaGetLastError();
 }
 
+// ring depth R and phase lag D (column blocks) of the streamed kernels: the
+// rings (3 for decode, 1 for encode) of R slots of N x 64 words stay well
+// inside the 126 MB L2 (C4, N = 16384: 4 MB a slot; C3, N = 65536: 16 MB)
+struct StreamShape {
+    uint32_t R, D;
+};
+StreamShape stream_shape(uint32_t N, bool decode) {
+    if (const char* e = std::getenv("FNTRS_STREAM_RD")) {  // "R,D" override (A/B)
+        unsigned r = 0, d = 0;
+        if (std::sscanf(e, "%u,%u", &r, &d) == 2 && d < r) return {r, d};
+    }
+    if (N <= 16384) return {4, 2};
+    return decode ? StreamShape{2, 1} : StreamShape{3, 1};
+}
+
+template <class K>
+cudaError_t stream_grid(K kernel, size_t smem, uint32_t& grid) {
+    int dev = 0, sms = 0, occ = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (!e) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (!e) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kLNT, smem);
+    grid = uint32_t(sms) * uint32_t(occ > 0 ? occ : 1);
+    return e;
+}
+
+template <int E1, int E2>
+cudaError_t stream_encode(const FastTables& t, uint32_t k, uint32_t n, uint32_t stripes, uint32_t L,
+                          const uint16_t* src, EscIn ein, uint16_t* out, EscOut eout, uint32_t* Y, uint32_t* ctl,
+                          StreamShape sh, cudaStream_t st) {
+    constexpr uint32_t N1 = 1u << E1, N2 = 1u << E2, N = N1 * N2;
+    const uint32_t tps = L / kLW, ncb = stripes * tps;
+    const size_t sm = size_t(N1 > N2 ? N1 : N2) * kLW * 4;
+    const bool half = k == N / 2, punct = n < N;
+    auto kern = half ? (punct ? enc_stream_kernel<E1, E2, true, true> : enc_stream_kernel<E1, E2, true, false>)
+                     : (punct ? enc_stream_kernel<E1, E2, false, true> : enc_stream_kernel<E1, E2, false, false>);
+    cudaError_t err;
+    if ((err = prep(kern, sm))) return err;
+    CUtensorMap omap, ymap;
+    std::memset(&omap, 0, sizeof(omap));
+    if ((err = make_u32_map(&ymap, Y, uint64_t(sh.R) * N, kLW, N2))) return err;
+    if ((err = cudaMemsetAsync(ctl, 0, (1 + 2 * size_t(ncb)) * 4, st))) return err;
+    uint32_t grid = 0;
+    if ((err = stream_grid(kern, sm, grid))) return err;
+    kern<<<grid, kLNT, sm, st>>>(t.ptab_fwd, t.big_fwd, k, n, L, tps, ncb, sh.R, sh.D, src, ein, out, eout, Y, ctl,
+                                 omap, ymap);
+    return cudaGetLastError();
+}
+
+template <int E1, int E2>
+cudaError_t stream_decode(const FastTables& t, const FastPlanView& pv, uint32_t stripes, uint32_t L,
+                          const uint32_t* sp, const uint16_t* rx, EscIn ein, uint16_t* out, EscOut eout,
+                          uint32_t* Y, uint32_t* ctl, StreamShape sh, cudaStream_t st) {
+    constexpr uint32_t N1 = 1u << E1, N2 = 1u << E2, N = N1 * N2;
+    const uint32_t tps = L / kLW, ncb = stripes * tps;
+    const size_t sm = size_t(N1 > N2 ? N1 : N2) * kLW * 4;
+    auto kern = pv.k == N / 2 ? dec_stream_kernel<E1, E2, true> : dec_stream_kernel<E1, E2, false>;
+    cudaError_t err;
+    if ((err = prep(kern, sm))) return err;
+    const uint64_t ring = uint64_t(sh.R) * N * kLW;
+    uint32_t *Y1 = Y, *Y2 = Y + ring, *Y3 = Y + 2 * ring;
+    CUtensorMap m1, m2, m3o, m3;  // D2 reads N2-row blocks of Y1, D3 N1-row blocks of Y2 and writes
+                                  // Y3 rows t1 N2 + q2 (strided view), D4 reads N2-row blocks of Y3
+    if ((err = make_u32_map(&m1, Y1, uint64_t(sh.R) * N, kLW, N2)) ||
+        (err = make_u32_map(&m2, Y2, uint64_t(sh.R) * N, kLW, N1)) ||
+        (err = make_u32_strided_map(&m3o, Y3, uint64_t(sh.R) * N1, N2, kLW, N1)) ||
+        (err = make_u32_map(&m3, Y3, uint64_t(sh.R) * N, kLW, N2)))
+        return err;
+    if ((err = cudaMemsetAsync(ctl, 0, (1 + 4 * size_t(ncb)) * 4, st))) return err;
+    uint32_t grid = 0;
+    if ((err = stream_grid(kern, sm, grid))) return err;
+    kern<<<grid, kLNT, sm, st>>>(t.ptab_fwd, t.ptab_inv, t.big_fwd, t.big_inv, pv.rowmap, pv.ahat2, pv.k, L, tps, ncb,
+                                 sh.R, sh.D, sp, rx, ein, out, eout, Y1, Y2, Y3, ctl, m1, m2, m3o, m3);
+    return cudaGetLastError();
+}
+
 __global__ void big_tables_kernel(uint2* fwd, uint2* inv) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0 || i >= (1u << 17)) return;
@@ -673,6 +998,51 @@ cudaError_t launch_encode_large(const FastTables& t, uint32_t k, uint32_t n, uin
         case 16384: return run_encode<7, 7>(t, k, n, stripes, L, src, ein, out, eout, Y, batch, st);
         case 32768: return run_encode<8, 7>(t, k, n, stripes, L, src, ein, out, eout, Y, batch, st);
         case 65536: return run_encode<8, 8>(t, k, n, stripes, L, src, ein, out, eout, Y, batch, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+// Off by default: measured slower than the batched kernels although its DRAM
+// traffic is ~1.5x algorithmic instead of ~7x (C4 decode 131 vs 147 GB/s,
+// encode 346 vs 415; C3 decode 118 vs 135): the four-step kernels are bound
+// by instruction issue, not HBM, and the transpose dependencies add barrier
+// stalls (every unit of a pass must finish before any of the next starts on
+// that column block). FNTRS_STREAM=1 selects it (profiles/README.md).
+bool stream_enabled() {
+    const char* e = std::getenv("FNTRS_STREAM");
+    return e && e[0] == '1';
+}
+
+size_t stream_scratch_words(uint32_t N, uint32_t stripes, uint32_t L, bool decode) {
+    const StreamShape sh = stream_shape(N, decode);
+    const uint64_t ncb = uint64_t(stripes) * (L / kLW);
+    return size_t(decode ? 3 : 1) * sh.R * N * kLW + 1 + (decode ? 4 : 2) * ncb + 64;
+}
+
+cudaError_t launch_encode_stream(const FastTables& t, uint32_t k, uint32_t n, uint32_t N, uint32_t stripes,
+                                 uint32_t L, const uint16_t* src, EscIn ein, uint16_t* out, EscOut eout,
+                                 uint32_t* scratch, cudaStream_t st) {
+    const StreamShape sh = stream_shape(N, false);
+    uint32_t* ctl = scratch + size_t(sh.R) * N * kLW;
+    switch (N) {
+        case 8192: return stream_encode<7, 6>(t, k, n, stripes, L, src, ein, out, eout, scratch, ctl, sh, st);
+        case 16384: return stream_encode<7, 7>(t, k, n, stripes, L, src, ein, out, eout, scratch, ctl, sh, st);
+        case 32768: return stream_encode<8, 7>(t, k, n, stripes, L, src, ein, out, eout, scratch, ctl, sh, st);
+        case 65536: return stream_encode<8, 8>(t, k, n, stripes, L, src, ein, out, eout, scratch, ctl, sh, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_decode_stream(const FastTables& t, const FastPlanView& pv, uint32_t stripes, uint32_t L,
+                                 const uint32_t* sp, const uint16_t* rx, EscIn ein, uint16_t* out, EscOut eout,
+                                 uint32_t* scratch, cudaStream_t st) {
+    const StreamShape sh = stream_shape(pv.N, true);
+    uint32_t* ctl = scratch + 3 * size_t(sh.R) * pv.N * kLW;
+    switch (pv.N) {
+        case 8192: return stream_decode<7, 6>(t, pv, stripes, L, sp, rx, ein, out, eout, scratch, ctl, sh, st);
+        case 16384: return stream_decode<7, 7>(t, pv, stripes, L, sp, rx, ein, out, eout, scratch, ctl, sh, st);
+        case 32768: return stream_decode<8, 7>(t, pv, stripes, L, sp, rx, ein, out, eout, scratch, ctl, sh, st);
+        case 65536: return stream_decode<8, 8>(t, pv, stripes, L, sp, rx, ein, out, eout, scratch, ctl, sh, st);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -152,6 +152,16 @@ cudaError_t build_large_tables(FastTables& t, cudaStream_t st);
 int large_supported(uint32_t N);
 uint32_t large_tile_columns();
 uint32_t large_batch(uint32_t N, uint32_t L, size_t scratch_bytes);  // stripes per scratch buffer
+// streamed four-step (codec_large.cu): one persistent launch, intermediates in
+// L2-resident rings; FNTRS_STREAM=0 selects the batched four-kernel path
+bool stream_enabled();
+size_t stream_scratch_words(uint32_t N, uint32_t stripes, uint32_t L, bool decode);
+cudaError_t launch_encode_stream(const FastTables& t, uint32_t k, uint32_t n, uint32_t N, uint32_t stripes,
+                                 uint32_t L, const uint16_t* src, EscIn ein, uint16_t* out, EscOut eout,
+                                 uint32_t* scratch, cudaStream_t st);
+cudaError_t launch_decode_stream(const FastTables& t, const FastPlanView& pv, uint32_t stripes, uint32_t L,
+                                 const uint32_t* sp, const uint16_t* rx, EscIn ein, uint16_t* out, EscOut eout,
+                                 uint32_t* scratch, cudaStream_t st);
 cudaError_t launch_encode_large(const FastTables& t, uint32_t k, uint32_t n, uint32_t N, uint32_t stripes, uint32_t L,
                                 const uint16_t* src, EscIn ein, uint16_t* out, EscOut eout, uint32_t* Y,
                                 uint32_t batch, cudaStream_t st);

@@ -597,3 +597,29 @@ def test_wide_stripe_offsets_beyond_32_bits(codec, oracle):
     assert torch.equal(dec[0, :, tail], src[0, :, tail])
     assert torch.equal(dec[0, :, :4096], src[0, :, :4096])
     assert escapes_to_numpy(de, dc).size == 0
+
+
+@pytest.mark.parametrize("k,n,L,S", [(4096, 8192, 64, 3), (8192, 16384, 128, 2), (5000, 16384, 64, 2),
+                                     (5000, 10000, 64, 2), (16384, 32768, 64, 1), (32768, 65536, 64, 1)])
+def test_streamed_four_step_matches_batched(codec, monkeypatch, k, n, L, S):
+    """The streamed four-step kernels (one persistent launch, L2 rings,
+    FNTRS_STREAM=1) give the batched kernels' payloads and escape lists."""
+    from paper_0907_1788_b200 import escapes_to_numpy, workload as W
+    src = torch.from_numpy(W.symbols(k * 7 + n, 0, S * k * L).view(np.int16).reshape(S, k, L)).cuda()
+    rng = np.random.default_rng(k + n)
+    pats = np.stack([np.sort(rng.choice(n, k, replace=False)) for _ in range(S)]).astype(np.uint32)
+    sp = np.arange(S, dtype=np.uint32)
+    res = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("FNTRS_STREAM", mode)
+        out, oe, cnt = codec.encode(k, n, src)
+        rx, rxe = W.received_packets(out, oe, cnt, pats, sp, n)
+        rx[:, 0, :7] = 0  # a few zero words; some become escapes below
+        rxe = rxe if rxe is not None else torch.zeros(0, dtype=torch.int64, device="cuda")
+        rxe = torch.unique(torch.cat([rxe, torch.arange(3, device="cuda", dtype=torch.int64)]))
+        plans = codec.plans(k, n, pats)
+        dec, de, dc = codec.decode(plans, torch.from_numpy(sp.view(np.int32)).cuda(), rx, rxe)
+        res[mode] = (out.cpu(), escapes_to_numpy(oe, cnt), dec.cpu(), escapes_to_numpy(de, dc))
+        plans.close()
+    for a, b in zip(res["0"], res["1"]):
+        assert (torch.equal(a, b) if isinstance(a, torch.Tensor) else np.array_equal(a, b))
