@@ -41,60 +41,66 @@ PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback, only if MEASURED_PEAKS.json is absent
 
 
-PROFILE_CSV = {"decode": "r01_ncu_full_raw.csv", "encode": "r01_ncu_full_enc_raw.csv"}
+# Committed ncu --set full captures of the current build (scripts/prof_round2.sh,
+# summarised by scripts/ncu_summary.py into profiles/r02_ncu_summary.csv): one
+# launch of each kernel per config, with the codewords that launch coded.
+PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "r02_ncu_summary.csv")
+PROFILE_CODEWORDS = {"C2": 8192 * 2048, "C3": 1 * 2048, "C4": 32 * 1024, "C5": 256 * 1024}
+SYS_PROFILE = os.path.join(ROOT, "profiles", "r01_ncu_full_sysdec_raw.csv")  # systematic C2 decode, 8192 stripes
 
 
-def _profile_row(cfg, chunk, systematic, kernel="decode"):
-    """Header, units and values of the committed ncu --set full capture
-    (profiles/r01_ncu_full_raw.csv: dec_fast_kernel<8>; r01_ncu_full_enc_raw.csv:
-    enc_fast_kernel<8>; one 8192-stripe C2 chunk each) when this run's launch
-    has that exact shape."""
-    if systematic or cfg.name != "C2" or chunk != 8192:
-        return None
+def kernel_label(cfg, what, systematic):
+    """The kernel(s) behind one encode / decode call of this config."""
+    E = cfg.n.bit_length() - 1 if cfg.n & (cfg.n - 1) == 0 else cfg.n.bit_length()
+    if cfg.n <= 4096:
+        if what == "decode":
+            return (f"dec_fast_kernel<{E}> MODE 3 (fused systematic decode: one cyclic convolution, two transforms)"
+                    if systematic else f"dec_fast_kernel<{E}> (fused decode: 3 transforms, one launch per call)")
+        return f"enc_fast_kernel<{E}> (fused encode, one launch per call)"
+    if what == "decode":
+        return "dec_1..dec_4_kernel (four-step decode: 4 launches per 32-stripe batch; values summed over the four)"
+    return "enc_a + enc_b_kernel (four-step encode: 2 launches per batch; values summed over the two)"
+
+
+def _summary_rows(cfg, what):
+    import csv
     try:
-        import csv
-        rows = list(csv.reader(open(os.path.join(ROOT, "profiles", PROFILE_CSV[kernel]))))
-        return rows[0], rows[1], rows[2]
+        rows = list(csv.DictReader(open(PROFILE_SUMMARY)))
     except Exception:
-        return None
+        return []
+    tag = f"prof_{cfg.name}_{'dec' if what == 'decode' else 'enc'}_raw.csv"
+    return [r for r in rows if r["report"] == tag]
 
 
-def profiled_traffic(cfg, chunk, systematic, kernel="decode"):
-    """DRAM bytes (read + write) per launch from the committed capture."""
-    row = _profile_row(cfg, chunk, systematic, kernel)
-    if row is None:
-        return None
-    h, u, v = row
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    try:
-        return int(sum(float(v[h.index(m)]) * scale[u[h.index(m)]]
-                       for m in ("dram__bytes_read.sum", "dram__bytes_write.sum")))
-    except Exception:
-        return None
-
-
-def profiled_pct(cfg, chunk, systematic, metric, kernel="decode"):
-    """A percentage metric of the launch from the committed capture, as a fraction."""
-    row = _profile_row(cfg, chunk, systematic, kernel)
-    if row is None:
-        return None
-    h, u, v = row
-    try:
-        return round(float(v[h.index(metric)]) / 100.0, 4)
-    except Exception:
-        return None
-
-
-def profiled_issue(cfg, chunk, systematic, kernel="decode"):
-    """The kernel's SM issue-slot utilisation from the committed capture."""
-    return profiled_pct(cfg, chunk, systematic, "smsp__issue_active.avg.pct_of_peak_sustained_active", kernel)
-
-
-def profiled_multiplier(cfg, chunk, systematic, kernel="decode"):
-    """The kernel's busiest unit, the integer multiplier (FMA-heavy) pipe:
-    its binding roofline in place of HBM (same capture)."""
-    return profiled_pct(cfg, chunk, systematic, "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed",
-                        kernel)
+def profiled(cfg, what, systematic, codewords):
+    """Per-call DRAM traffic (read + write, scaled from the captured launch(es)
+    to this call's codewords) and the issue / multiplier-pipe fractions
+    (duration-weighted over the kernels of the call) from the committed capture."""
+    if systematic:
+        if cfg.name != "C2" or what != "decode":
+            return {}
+        try:
+            import csv
+            r = list(csv.reader(open(SYS_PROFILE)))
+            h, u, v = r[0], r[1], r[2]
+            sc = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            tr = sum(float(v[h.index(m)]) * sc[u[h.index(m)]] for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+            return {"traffic": int(tr * codewords / (8192 * 2048)),
+                    "traffic_source": "profiles/r01_ncu_full_sysdec_raw.csv (8192-stripe C2 launch, scaled)"}
+        except Exception:
+            return {}
+    rows = _summary_rows(cfg, what)
+    if not rows or cfg.name not in PROFILE_CODEWORDS:
+        return {}
+    dur = sum(float(r["dur_us"]) for r in rows)
+    tr = sum((float(r["dram_rd_MB"]) + float(r["dram_wr_MB"])) * 1e6 for r in rows)
+    wavg = lambda k: round(sum(float(r[k]) * float(r["dur_us"]) for r in rows) / dur / 100.0, 4)
+    return {"traffic": int(tr * codewords / PROFILE_CODEWORDS[cfg.name]),
+            "traffic_source": f"ncu --set full dram__bytes_read.sum + dram__bytes_write.sum of "
+                              f"{len(rows)} kernel launch(es) coding {PROFILE_CODEWORDS[cfg.name]} codewords, scaled to "
+                              f"this call (profiles/r02_ncu_summary.csv, raw pages in profiles/r02_ncu/)",
+            "issue_active_frac": wavg("issue_pct"), "multiplier_pipe_busy_frac": wavg("fmaheavy_pct"),
+            "profiled_kernel_us": round(dur, 2)}
 
 
 def hbm_peak():
@@ -465,6 +471,13 @@ def run_gpu(args, rank, world, local_rank):
     enc_bytes = 2 * k * L * rows + 2 * n * L * rows  # read 2k + write 2n
     dec_achieved = dec_bytes / (dec_launch_ms * 1e-3) / 1e9
     enc_achieved = enc_bytes / (enc_launch_ms * 1e-3) / 1e9
+    dec_prof = profiled(cfg, "decode", SYSTEMATIC, rows * L)
+    enc_prof = profiled(cfg, "encode", SYSTEMATIC, rows * L)
+    if args.traffic is not None:
+        dec_prof["traffic"], dec_prof["traffic_source"] = args.traffic, "--traffic"
+    for pr, alg in ((dec_prof, dec_bytes), (enc_prof, enc_bytes)):
+        if pr.get("traffic"):
+            pr["traffic_over_algorithmic"] = round(pr["traffic"] / alg, 3)
     result = {
         "metric": "encode & decode GB/s of source data per GPU (1/2/4/8 B200), % of HBM roofline",
         "codec": "systematic" if SYSTEMATIC else "non-systematic",
@@ -495,30 +508,21 @@ def run_gpu(args, rank, world, local_rank):
         "encode_gbs": round(src_bytes_rank / (phase_ms[1] * 1e-3) / 1e9, 2),
         "decode_gbs": round(src_bytes_rank / (phase_ms[2] * 1e-3) / 1e9, 2),
         "decode_with_plans_gbs": round(src_bytes_rank / ((phase_ms[2] + phase_ms[0]) * 1e-3) / 1e9, 2),
-        "roofline": {
+        "roofline": dict({
             "bound": "hbm",
-            "kernel": ("dec_fast_kernel MODE 3 (fused systematic decode: one cyclic convolution, two transforms; one launch per chunk)" if SYSTEMATIC
-                       else "dec_fast_kernel (fused decode, one launch per chunk)"),
+            "kernel": kernel_label(cfg, "decode", SYSTEMATIC),
             "achieved": round(dec_achieved, 2), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
             "frac": round(dec_achieved / peak, 4),
-            "traffic": args.traffic if args.traffic is not None else profiled_traffic(cfg, chunk, SYSTEMATIC),
-            "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum per launch "
-                              "(profiles/r01_ncu_full_raw.csv)",
-            # what bounds it instead of HBM: the integer multiplier pipe and SM issue (same capture)
-            "issue_active_frac": profiled_issue(cfg, chunk, SYSTEMATIC),
-            "multiplier_pipe_busy_frac": profiled_multiplier(cfg, chunk, SYSTEMATIC),
             "algorithmic_bytes_per_launch": dec_bytes, "avg_launch_ms": round(dec_launch_ms, 4),
-        },
-        "roofline_encode": {
-            "bound": "hbm", "kernel": "enc_fast_kernel", "achieved": round(enc_achieved, 2), "peak": peak,
-            "unit": "GB/s", "frac": round(enc_achieved / peak, 4), "algorithmic_bytes_per_launch": enc_bytes,
-            "avg_launch_ms": round(enc_launch_ms, 4),
-            "traffic": profiled_traffic(cfg, chunk, SYSTEMATIC, "encode"),
-            "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum per launch "
-                              "(profiles/r01_ncu_full_enc_raw.csv)",
-            "issue_active_frac": profiled_issue(cfg, chunk, SYSTEMATIC, "encode"),
-            "multiplier_pipe_busy_frac": profiled_multiplier(cfg, chunk, SYSTEMATIC, "encode"),
-        },
+            "per_unit": "read 2k + write 2k bytes per codeword (SURVEY 8(d)); a launch = one decode call of "
+                        f"{rows} stripes x {L} codewords",
+        }, **dec_prof),
+        "roofline_encode": dict({
+            "bound": "hbm", "kernel": kernel_label(cfg, "encode", SYSTEMATIC), "achieved": round(enc_achieved, 2),
+            "peak": peak, "unit": "GB/s", "frac": round(enc_achieved / peak, 4),
+            "algorithmic_bytes_per_launch": enc_bytes, "avg_launch_ms": round(enc_launch_ms, 4),
+            "per_unit": "read 2k + write 2n bytes per codeword",
+        }, **enc_prof),
         "gpu_launches": int(gpu_launches),
         "verified": verified,
         "clocks": clocks.summary(),

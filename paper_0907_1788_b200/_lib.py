@@ -43,6 +43,15 @@ SIGNATURES = [
     ("fntrs_gpu_launch_count", _u64, [_vp]),
     ("fntrs_gpu_set_fast_path", _int, [_vp, _int]),
     ("fntrs_gpu_fill_symbols", _int, [_u64, _u64, _u64, _vp, _vp]),
+    ("fntrs_gpu_transform_counts", _int, [_vp, C.POINTER(_u64)]),
+    ("fntrs_gpu_naive_dft", _int, [_vp, _u32, _int, _u32, _vp, _vp, _vp]),
+    ("fntrs_gpu_transform_tables", _int, [_vp, _u32, _vp, _vp, _vp, _vp, _vp, _vp]),
+    ("fntrs_gpu_poly_products", _int, [_vp, _u32, _vp, _vp, _vp, _vp]),
+    ("fntrs_gpu_subproduct_tree_layout", _int, [_u32, _pu32, _pu32, _u32, _pu32, C.POINTER(_u64), C.POINTER(_u64)]),
+    ("fntrs_gpu_subproduct_tree", _int, [_vp, _u32, _vp, _vp, _vp]),
+    ("fntrs_gpu_lagrange", _int, [_vp, _u32, _vp, _vp, _vp, _vp]),
+    ("fntrs_gpu_poly_derivative", _int, [_vp, _u32, _vp, _vp, _vp]),
+    ("fntrs_gpu_poly_eval", _int, [_vp, _u32, _vp, _u32, _vp, _vp]),
 ]
 
 _lib = None

@@ -4,7 +4,7 @@ set -e
 mkdir -p gpurun_out
 for c in C1 C2 C3 C4 C5; do
   g=""; [ "$c" = C1 ] && g="--graph"  # launch-bound: whole-step CUDA-graph replay
-  python bench.py --config $c --steps 5 --warmup 3 --cpu-seconds 8 $g > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err || { echo "$c failed"; tail -5 gpurun_out/bench_$c.err; }
+  python bench.py --config $c --steps 5 --warmup 3 --cpu-seconds 8 --sweep none $g > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err || { echo "$c failed"; tail -5 gpurun_out/bench_$c.err; }
   python - "$c" << 'PY'
 import json, sys
 c = sys.argv[1]

@@ -73,3 +73,20 @@ def test_product_does_not_import_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 for bad in ("liboracle", "oracle_bind", "fntrs_oracle", "libfntrs_ref", "orc_", "import oracle"):
                     assert bad not in txt, (f, bad)
+
+
+def test_subproduct_tree_layout_host_only():
+    """Node lengths of the reference's tree shape (poly.cpp:216-242): leaves of
+    2 coefficients, adjacent pairs multiplied, an odd last node carried."""
+    from paper_0907_1788_b200 import _lib
+    lib = _lib.load()
+    nl, nn, nc = C.c_uint32(), C.c_uint64(), C.c_uint64()
+    assert lib.fntrs_gpu_subproduct_tree_layout(5, C.byref(nl), None, 0, None, C.byref(nn), C.byref(nc)) == 0
+    assert (nl.value, nn.value) == (4, 5 + 3 + 2 + 1)
+    lv = (C.c_uint32 * 4)()
+    lens = (C.c_uint32 * nn.value)()
+    assert lib.fntrs_gpu_subproduct_tree_layout(5, C.byref(nl), lv, 4, lens, C.byref(nn), C.byref(nc)) == 0
+    assert list(lv) == [5, 3, 2, 1]
+    assert list(lens) == [2] * 5 + [3, 3, 2] + [5, 2] + [6]
+    assert nc.value == sum(lens)
+    assert lib.fntrs_gpu_subproduct_tree_layout(0, None, None, 0, None, None, None) == 4  # SizeMismatch
