@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E, MODE>::MINB) dec_fast_kernel(
     constexpr bool CT = FNTRS_CONST_TW && E <= 8;
     const uint4* tF0 = CT ? pass_table(reinterpret_cast<const uint2*>(c_twF), S::llog(0)) : pass_table(ptabF, S::llog(0));
     const uint4* tI0 = CT ? pass_table(reinterpret_cast<const uint2*>(c_twI), S::llog(0)) : pass_table(ptabI, S::llog(0));
-    if constexpr (CT) ptabFT = reinterpret_cast<const uint2*>(c_twFT);
+    [[maybe_unused]] const uint2* twFT = CT ? reinterpret_cast<const uint2*>(c_twFT) : ptabFT;
     const bool esc_any = esc_in.n != 0;
     for (uint32_t iter = 0; tile < tiles; tile = next_tile[iter & 1], ++iter) {
         const uint32_t stripe = tile / tps;
@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(G::NT, DecOcc<E, MODE>::MINB) dec_fast_kernel(
                     // FNT2's last DIT pass pre-multiplies logical row t + s*sub0 by r^(t s);
                     // this element is t = q, s = N/R - 1 - g: apply it here, where the
                     // multiply also does the reduction the store needed anyway
-                    const uint4* tq = reinterpret_cast<const uint4*>(ptabFT + N + (uint32_t(N / RZ) - 1u - g) * RZ);
+                    const uint4* tq = reinterpret_cast<const uint4*>(twFT + N + (uint32_t(N / RZ) - 1u - g) * RZ);
 #pragma unroll
                     for (int q = 0; q < RZ; q += 2) {
                         const uint4 w = CT ? tq[q / 2] : __ldg(tq + q / 2);

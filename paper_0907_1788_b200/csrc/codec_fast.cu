@@ -68,13 +68,19 @@ namespace {
 // item (columns c and c + 32 share twiddle loads and addressing; C2 encode
 // 693 -> 716 GB/s); larger N keep the decode geometry (a 64-wide N = 512 tile
 // and its staging exceed shared memory).
+#ifndef FNTRS_ENC_CW
+#define FNTRS_ENC_CW 2
+#endif
+#ifndef FNTRS_ENC_NT
+#define FNTRS_ENC_NT 256
+#endif
 template <int E>
 struct EncPick {
-    static constexpr int CW = E <= 8 ? 2 : 1;
+    static constexpr int CW = E <= 8 ? FNTRS_ENC_CW : 1;
     // output rows through shared memory + one TMA store per tile: C2 encode
     // 711 -> 819 GB/s (per-symbol 2-byte stores were the bottleneck); not at N = 32 (-2 %)
     static constexpr bool TS = E >= 6;
-    using G = typename std::conditional<(E <= 8), Geom<E, 64, 256, 2>, typename Pick<E>::G>::type;
+    using G = typename std::conditional<(E <= 8), Geom<E, 64, FNTRS_ENC_NT, 2>, typename Pick<E>::G>::type;
 };
 
 // TS: single input stage + the n output rows staged in shared memory and
