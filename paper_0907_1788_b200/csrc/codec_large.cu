@@ -132,7 +132,7 @@ __device__ __forceinline__ void enc_a_body(const uint2* __restrict__ ptab, const
         if ((HALFK && q >= R0 / 2) || (!HALFK && row >= k)) return 0u;
         if (!kStep) return srcp[row * L + col];
         sq = q == 0 ? srcp + (row * L + col) : step_ptr(sq, sstep);
-        return *sq;
+        return __ldcs(sq);  // global state space (the laundered pointer would load generically)
     };
     auto fix = [&](uint32_t (&v)[R0], uint32_t base, uint32_t, uint32_t col) {
         if (!esc_any || !any_zero(v)) return;
@@ -167,7 +167,7 @@ __device__ __forceinline__ void enc_a_body(const uint2* __restrict__ ptab, const
             tix += i2 << (E1 - RLZ);
         }
         const uint2 w = ldg_alu(bigN, tix & (N - 1));
-        *yq = mulws(y, w.x, w.y);
+        __stcg(yq, mulws(y, w.x, w.y));
         return 0u;
     };
     pass<E1, 0, false, false, kP64, kSmemCap, G>(pass_table(ptab, S::llog(0)), ld, st_sm, fix);
@@ -281,9 +281,10 @@ __device__ __forceinline__ void dec_1_body(const uint2* __restrict__ ptab, const
     auto ld = [&](uint32_t i1, uint32_t, int, uint32_t col) -> uint32_t {
         const uint2 m = __ldg(rm + i1 * N2 + i2);  // erased: {~0, 0}
         const uint32_t row = m.x == 0xFFFFFFFFu ? 0u : m.x;
-        const uint32_t raw = rxp[row * L + col];
+        const uint32_t raw = __ldcs(rxp + (row * L + col));
         zflag |= (raw == 0u) & (m.y != 0u);
-        return mulws(raw, m.y, m.y * 65535u);
+        // raw <= 65535, |1/A'| <= p/2 (balanced): the product is exact in 32 signed bits
+        return reds(raw * m.y);
     };
     auto fix = [&](uint32_t (&v)[R0], uint32_t base, uint32_t, uint32_t col) {
         const uint32_t any = zflag;
@@ -322,7 +323,7 @@ __device__ __forceinline__ void dec_1_body(const uint2* __restrict__ ptab, const
             tix += i2 << (E1 - RLZ);
         }
         const uint2 w = ldg_alu(bigN, tix & (N - 1));
-        *yq = mulws(y, w.x, w.y);
+        __stcg(yq, mulws(y, w.x, w.y));
         return 0u;
     };
     pass<E1, 0, false, false, k2P, kSmemCap, G>(pass_table(ptab, S::llog(0)), ld, st_sm, fix);
@@ -382,7 +383,7 @@ __device__ __forceinline__ void dec_2_body(const uint2* __restrict__ ptab, const
             tix += i1p << S::slog(0);
         }
         const uint2 w = ldg_alu(bigN, tix & (N - 1));
-        *yq = mulws(y, w.x, w.y);
+        __stcg(yq, mulws(y, w.x, w.y));
         return 0u;
     };
     // FNT1 pass B, first radix pass (input block by TMA)
