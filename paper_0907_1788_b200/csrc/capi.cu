@@ -6,7 +6,6 @@
 // codec arithmetic runs in the CUDA kernels; there is no CPU path.
 #include <cuda_runtime.h>
 
-#include <cub/device/device_radix_sort.cuh>
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
@@ -111,11 +110,6 @@ struct DeviceGuard {
     }
 };
 
-int end_bit_for(uint64_t max_key) {
-    int b = 1;
-    while (b < 64 && (max_key >> b)) ++b;
-    return b;
-}
 
 // Small escape buffers: one CTA sorts them in shared memory (bitonic network).
 // The kernel reads the device-side escape count, so it sorts only the next
@@ -148,10 +142,108 @@ __global__ void __launch_bounds__(1024) small_sort_kernel(unsigned long long* ke
     for (uint32_t i = threadIdx.x; i < live; i += blockDim.x) keys[i] = s[i];
 }
 
+// Larger escape lists: our own merge sort over the live keys [0, min(count,
+// cap)) (the device-side count is read by the kernels, so no host sync):
+// tiles of kTile keys are sorted in shared memory (bitonic), then runs are
+// merged pairwise by merge path -- every CTA owns kMTile consecutive outputs of
+// a merged pair, finds where they start in the two runs by a diagonal binary
+// search, stages both pieces in shared memory and merges them, each thread
+// again splitting its kMergePer outputs by a diagonal search. The passes the
+// capacity could need are launched; a pass whose run width already covers the
+// live keys exits at once, and a last kernel moves the result back into the
+// caller's buffer if it ended in the scratch one. Keys are distinct symbol
+// indices, so stability does not matter.
+constexpr uint32_t kTile = 4096, kSortThreads = 512, kMTile = 2048, kMergePer = kMTile / kSortThreads;
+
+__device__ __forceinline__ uint32_t live_keys(const unsigned long long* count, uint64_t cap) {
+    const unsigned long long c = *count;
+    return uint32_t(c < cap ? c : cap);
+}
+
+__global__ void __launch_bounds__(kSortThreads) tile_sort_kernel(unsigned long long* keys,
+                                                                 const unsigned long long* count, uint64_t cap) {
+    __shared__ unsigned long long s[kTile];
+    const uint32_t live = live_keys(count, cap), t0 = blockIdx.x * kTile;
+    if (t0 >= live || live <= 1) return;
+    const uint32_t n = min(kTile, live - t0);
+    for (uint32_t i = threadIdx.x; i < kTile; i += kSortThreads) s[i] = i < n ? keys[t0 + i] : ~0ull;
+    __syncthreads();
+    for (uint32_t size = 2; size <= kTile; size <<= 1)
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t i = threadIdx.x; i < kTile / 2; i += kSortThreads) {
+                const uint32_t lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const unsigned long long a = s[lo], b = s[hi];
+                if ((a > b) == up) {
+                    s[lo] = b;
+                    s[hi] = a;
+                }
+            }
+            __syncthreads();
+        }
+    for (uint32_t i = threadIdx.x; i < n; i += kSortThreads) keys[t0 + i] = s[i];
+}
+
+// number of elements taken from A among the first d outputs of merge(A, B)
+__device__ __forceinline__ uint32_t merge_split(const unsigned long long* A, uint32_t na,
+                                                const unsigned long long* B, uint32_t nb, uint32_t d) {
+    uint32_t lo = d > nb ? d - nb : 0u, hi = min(d, na);
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;  // take mid from A, d - mid from B
+        if (A[mid] < B[d - mid - 1])
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(kSortThreads) merge_pass_kernel(const unsigned long long* in,
+                                                                  unsigned long long* out,
+                                                                  const unsigned long long* count, uint64_t cap,
+                                                                  uint32_t width, uint32_t* passes) {
+    __shared__ unsigned long long sa[kMTile], sb[kMTile];
+    const uint32_t live = live_keys(count, cap);
+    if (width >= live) return;  // already one run: nothing to merge (and no pass counted)
+    const uint32_t o0 = blockIdx.x * kMTile;
+    if (o0 >= live) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(passes, 1u);
+    const uint32_t pair = o0 / (2 * width) * (2 * width);
+    const uint32_t na = min(width, live - pair), nb = live - pair > width ? min(width, live - pair - width) : 0u;
+    const unsigned long long* A = in + pair;
+    const unsigned long long* B = A + na;
+    const uint32_t d0 = o0 - pair, d1 = min(d0 + kMTile, na + nb);
+    __shared__ uint32_t s_split[2];
+    if (threadIdx.x < 2) s_split[threadIdx.x] = merge_split(A, na, B, nb, threadIdx.x ? d1 : d0);
+    __syncthreads();
+    const uint32_t a0 = s_split[0], a1 = s_split[1], b0 = d0 - a0, b1 = d1 - a1;
+    const uint32_t ma = a1 - a0, mb = b1 - b0;
+    for (uint32_t i = threadIdx.x; i < ma; i += kSortThreads) sa[i] = A[a0 + i];
+    for (uint32_t i = threadIdx.x; i < mb; i += kSortThreads) sb[i] = B[b0 + i];
+    __syncthreads();
+    const uint32_t d = threadIdx.x * kMergePer;
+    if (d >= ma + mb) return;
+    uint32_t i = merge_split(sa, ma, sb, mb, d), j = d - i;
+    const uint32_t e = min(d + kMergePer, ma + mb);
+    for (uint32_t o = d; o < e; ++o) {
+        const bool takeA = j >= mb || (i < ma && sa[i] < sb[j]);
+        out[pair + d0 + o] = takeA ? sa[i++] : sb[j++];
+    }
+}
+
+// the result is in the scratch buffer after an odd number of effective passes
+__global__ void copy_back_kernel(unsigned long long* keys, const unsigned long long* alt,
+                                 const unsigned long long* count, uint64_t cap, const uint32_t* passes) {
+    if (!(*passes & 1u)) return;
+    const uint32_t live = live_keys(count, cap);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < live; i += gridDim.x * blockDim.x) keys[i] = alt[i];
+}
+
 // Escape finalisation: keys[0..cap) were pre-filled with ~0 and partially
 // overwritten by the kernel's appends; sorting puts the real indices first,
 // ascending (the reference's per-shard order).
 int sort_escapes(fntrs_ctx* ctx, const EscOut& eout, uint64_t max_key, cudaStream_t st) {
+    (void)max_key;
     const uint64_t cap = eout.cap;
     unsigned long long* keys = eout.keys;
     if (cap <= 1) return FNTRS_OK;
@@ -168,23 +260,26 @@ int sort_escapes(fntrs_ctx* ctx, const EscOut& eout, uint64_t max_key, cudaStrea
         return FNTRS_OK;
     }
     if (cap > 0x7FFFFFFFull) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "escape capacity too large");
-    // Real keys are < max_key, so only bits [0, end_bit) need sorting; the ~0
-    // fill has all of those bits set and still sorts last (and keeps its value).
-    const int end_bit = end_bit_for(max_key);
     // per-call, stream-ordered scratch: calls on different streams never share it
     unsigned long long* alt = nullptr;
-    void* tmp = nullptr;
-    size_t need = 0;
-    CK(cudaMallocAsync(&alt, cap * sizeof(unsigned long long), st), "escape scratch");
-    cub::DoubleBuffer<unsigned long long> db(keys, alt);
-    CK(cub::DeviceRadixSort::SortKeys(nullptr, need, db, int(cap), 0, end_bit, st), "escape sort size");
-    CK(cudaMallocAsync(&tmp, need, st), "escape sort scratch");
-    CK(cub::DeviceRadixSort::SortKeys(tmp, need, db, int(cap), 0, end_bit, st), "escape sort");
-    ctx->launches += 2 + (end_bit + 7) / 8;  // onesweep: histogram + exclusive scan + one pass per 8 bits
-    if (db.Current() != keys)
-        CK(cudaMemcpyAsync(keys, db.Current(), cap * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st),
-           "escape copy");
-    cudaFreeAsync(tmp, st);
+    CK(cudaMallocAsync(&alt, cap * sizeof(unsigned long long) + 16, st), "escape scratch");
+    uint32_t* passes = reinterpret_cast<uint32_t*>(alt + cap);
+    CK(cudaMemsetAsync(passes, 0, sizeof(uint32_t), st), "escape sort");
+    const uint32_t tiles = uint32_t((cap + kTile - 1) / kTile);
+    tile_sort_kernel<<<tiles, kSortThreads, 0, st>>>(keys, eout.count, cap);
+    unsigned long long *a = keys, *b = alt;
+    int launched = 1;
+    const uint32_t mtiles = uint32_t((cap + kMTile - 1) / kMTile);
+    for (uint64_t w = kTile; w < cap; w *= 2) {
+        merge_pass_kernel<<<mtiles, kSortThreads, 0, st>>>(a, b, eout.count, cap, uint32_t(w), passes);
+        std::swap(a, b);
+        ++launched;
+    }
+    // passes the live count did not need exit before writing: the effective ones
+    // alternate buffers from `keys`, so an odd count leaves the result in `alt`
+    copy_back_kernel<<<148, 256, 0, st>>>(keys, alt, eout.count, cap, passes);
+    CK(cudaGetLastError(), "escape sort");
+    ctx->launches += launched + 1;
     cudaFreeAsync(alt, st);
     return FNTRS_OK;
 }

@@ -542,8 +542,11 @@ def test_plan_methods_agree(codec, oracle, k, n, P, monkeypatch):
     (64, 256, 2, 200, 16384),      # 12800 escapes, single-CTA sort at its 16K limit
     (64, 256, 2, 256, 16384),      # exactly 16384 = cap
     (256, 512, 2, 300, None),      # 76800 escapes > default cap: count reports the overflow
-    (256, 512, 2, 300, 80000),     # 76800 escapes, radix sort on the key bits below S*n*L
-    (256, 512, 4, 5, 80000),       # few escapes in a large buffer (radix sort, mostly ~0 fill)
+    (256, 512, 2, 300, 80000),     # 76800 escapes: tile sort + 5 merge passes
+    (256, 512, 4, 5, 80000),       # few escapes in a large buffer (merge sort, mostly ~0 fill)
+    (256, 512, 2, 40, 80000),      # 10240 live keys: tile sort + 2 merge passes (even: result in place)
+    (256, 512, 2, 79, 80000),      # 20224 live keys: 3 merge passes (odd: copied back from scratch)
+    (256, 1024, 4, 1000, 300000),  # 256000 live keys: 6 merge passes over 125 merge tiles
 ])
 def test_escape_sort_paths(codec, n, L, S, hot, cap):
     """k = 1: every output of a codeword equals its source symbol, so `hot`
