@@ -5,6 +5,8 @@
 //
 //   fntrs encode <input> [-o DIR] -k K -n N [--systematic|--non-systematic] [--seed S] [--path P] [--jobs J]
 //   fntrs decode <manifest|dir> -o OUT [--path P] [--jobs J]
+//   fntrs bench [--grid k1,k2,..] [-k K] [-n N] [--reps R]   (CSV, batched GPU timing)
+//   fntrs selftest [--seed S]
 //
 // The reference codes S = ceil(ceil(len/2)/k) one-codeword stripes and shard j
 // carries symbol j of every stripe. Here that is ONE batched stripe of k
@@ -27,6 +29,7 @@
 
 #include "fntrs/codec.hpp"
 #include "fntrs/errors.hpp"
+#include "fntrs/interp.hpp"
 #include "fntrs/shardio.hpp"
 #include "fntrs_gpu.h"
 #include "shard_detail.h"
@@ -214,10 +217,183 @@ int cmd_decode(const std::string& input, const std::string& output) {
     return 0;
 }
 
+// ---- bench: the reference CLI's CSV (variant,k,n,bytes,seconds,MBps,fnt_equivalents;
+// fntrs_main.cpp:255-303), measured on the batched GPU path: `seconds` is the device time
+// per codeword over a batch of 64 stripes x 256 codewords (CUDA events around `reps`
+// stream-ordered calls), bytes = 2k of source per codeword, fnt_equivalents from the
+// library's transform tally (fntrs_gpu_transform_counts) per codeword.
+uint64_t splitmix(uint64_t& s) {
+    uint64_t z = (s += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+int cmd_bench(const std::vector<std::pair<uint32_t, uint32_t>>& sizes, int reps, uint64_t seed) {
+    std::printf("variant,k,n,bytes,seconds,MBps,fnt_equivalents\n");
+    Gpu g;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    for (const auto& [k, n] : sizes) {
+        uint32_t nd = 1;
+        while (nd < n) nd <<= 1;
+        const uint32_t L = 256, S = 64;
+        const uint64_t cw = uint64_t(S) * L;
+        std::vector<uint16_t> src(size_t(S) * k * L);
+        for (auto& w : src) w = uint16_t(splitmix(seed));
+        uint16_t* d_src = g.alloc<uint16_t>(src.size());
+        uint16_t* d_enc = g.alloc<uint16_t>(size_t(S) * n * L);
+        uint16_t* d_rx = g.alloc<uint16_t>(size_t(S) * k * L);
+        uint16_t* d_dec = g.alloc<uint16_t>(size_t(S) * k * L);
+        const uint64_t cap = uint64_t(S) * n * L / 1024 + 4096;
+        uint64_t* d_esc = g.alloc<uint64_t>(cap + 1);
+        uint32_t* d_sp = g.alloc<uint32_t>(S);
+        g.copy(d_src, src.data(), src.size() * 2, cudaMemcpyHostToDevice);
+        if (cudaMemsetAsync(d_sp, 0, S * 4, g.st)) throw Error("fntrs: memset failed");
+        // no-shortcut reception as in the reference's bench: position 0 erased, survivors 1..k
+        std::vector<uint32_t> pos(k);
+        const uint32_t shift = n > k ? 1u : 0u;
+        for (uint32_t i = 0; i < k; ++i) pos[i] = i + shift;
+        fntrs_plans* pl = nullptr;
+        g.check(fntrs_gpu_plans_create(g.ctx, k, n, k, 1, pos.data(), &pl, g.st));
+        auto line = [&](const char* variant, auto&& op) {
+            uint64_t before[17], after[17];
+            op();  // warm (tables, the context's cached systematic plan)
+            g.sync();
+            g.check(fntrs_gpu_transform_counts(g.ctx, before));
+            cudaEventRecord(e0, g.st);
+            for (int r = 0; r < reps; ++r) op();
+            cudaEventRecord(e1, g.st);
+            g.sync();
+            g.check(fntrs_gpu_transform_counts(g.ctx, after));
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            double eq = 0;
+            for (int e = 0; e < 17; ++e) eq += double(after[e] - before[e]) * double(1u << e);
+            const double per = std::max(double(ms) * 1e-3 / reps / double(cw), 1e-15);
+            std::printf("%s,%u,%u,%u,%.9e,%.3f,%.3f\n", variant, k, n, 2 * k, per, 2.0 * k / per / 1e6,
+                        eq / nd / double(reps) / double(cw));
+        };
+        line("encode_nonsystematic", [&] {
+            g.check(fntrs_gpu_encode(g.ctx, k, n, S, L, d_src, nullptr, 0, d_enc, d_esc, cap, d_esc + cap, g.st));
+        });
+        line("encode_systematic", [&] {
+            g.check(fntrs_gpu_encode_systematic(g.ctx, k, n, S, L, d_src, nullptr, 0, d_enc, d_esc, cap,
+                                                d_esc + cap, g.st));
+        });
+        // received rows = encoded rows shift..shift+k-1 (their rare escapes do not change the timing)
+        g.check(fntrs_gpu_encode(g.ctx, k, n, S, L, d_src, nullptr, 0, d_enc, d_esc, cap, d_esc + cap, g.st));
+        for (uint32_t s2 = 0; s2 < S; ++s2)
+            g.copy(d_rx + size_t(s2) * k * L, d_enc + (size_t(s2) * n + shift) * L, size_t(k) * L * 2,
+                   cudaMemcpyDeviceToDevice);
+        line("decode_nonsystematic", [&] {
+            g.check(fntrs_gpu_decode(g.ctx, pl, S, L, d_sp, d_rx, nullptr, 0, d_dec, d_esc, cap, d_esc + cap, g.st));
+        });
+        line("decode_systematic", [&] {
+            g.check(fntrs_gpu_decode_systematic(g.ctx, pl, S, L, d_sp, d_rx, nullptr, 0, d_dec, d_esc, cap,
+                                                d_esc + cap, g.st));
+        });
+        g.sync();
+        fntrs_gpu_plans_destroy(pl);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return 0;
+}
+
+// ---- selftest: MDS-exhaustive decoding of small codes, then randomized
+// equivalence of the fast interpolation with the quadratic oracle and of every
+// encoder / decoder variant (the reference CLI's two suites,
+// fntrs_main.cpp:305-405), through the drop-in API on the GPU.
+std::vector<Fe> random_fe(uint32_t count, uint64_t& st) {
+    std::vector<Fe> v(count);
+    for (auto& x : v) x = Fe(splitmix(st) % 65537);
+    return v;
+}
+
+std::vector<uint32_t> random_subset(uint32_t k, uint32_t n, uint64_t& st) {
+    std::vector<uint32_t> all(n);
+    for (uint32_t i = 0; i < n; ++i) all[i] = i;
+    for (uint32_t i = 0; i < k; ++i) std::swap(all[i], all[i + uint32_t(splitmix(st) % (n - i))]);
+    all.resize(k);
+    return all;
+}
+
+int cmd_selftest(uint64_t seed) {
+    uint64_t st = seed;
+    bool ok = true;
+    const std::pair<uint32_t, uint32_t> codes[] = {{4, 2}, {8, 4}, {8, 5}, {16, 12}};  // (n, k)
+    for (const auto& [n, k] : codes) {
+        const auto sys = codec::CodeParams::make(k, n, true), non = codec::CodeParams::make(k, n, false);
+        const auto src = random_fe(k, st);
+        const auto es = codec::encode_systematic(sys, src), en = codec::encode_nonsystematic(non, src);
+        uint64_t patterns = 0, failures = 0;
+        for (uint32_t mask = 0; mask < (1u << n); ++mask) {
+            if (uint32_t(__builtin_popcount(mask)) < k) continue;
+            ++patterns;
+            codec::Codeword rs, rn;
+            for (uint32_t j = 0; j < n; ++j)
+                if (mask >> j & 1u) {
+                    rs.push_back({j, es[j]});
+                    rn.push_back({j, en[j]});
+                }
+            failures += codec::decode_systematic(sys, rs, codec::Path::Fast) != src ||
+                        codec::decode_direct(sys, rs) != src ||
+                        codec::decode_nonsystematic(non, rn, codec::Path::Fast) != src ||
+                        codec::decode_direct(non, rn) != src;
+        }
+        std::printf("selftest: mds (%u,%u): %llu patterns, %llu failures\n", n, k,
+                    static_cast<unsigned long long>(patterns), static_cast<unsigned long long>(failures));
+        ok = ok && failures == 0;
+    }
+    const int instances = 100;
+    int passed = 0;
+    for (int t = 0; t < instances; ++t) {
+        const uint32_t k = 1 + uint32_t(splitmix(st) % 128);
+        uint32_t nd = 2;
+        while (nd < k) nd <<= 1;
+        if ((splitmix(st) & 1) && nd < 1024) nd <<= 1;
+        const auto positions = random_subset(k, nd, st);
+        const auto values = random_fe(k, st);
+        auto fast = interp::interpolate(interp::build_plan(nd, positions), values);
+        std::vector<std::pair<Fe, Fe>> points(k);
+        const Fe r = gf::root_of_unity(nd, false);
+        for (uint32_t j = 0; j < k; ++j) points[j] = {gf::pow(r, positions[j]), values[j]};
+        auto slow = interp::lagrange_oracle(points);
+        fast.resize(k, 0);
+        slow.resize(k, 0);
+        bool good = fast == slow;
+        const uint32_t n = k + uint32_t(splitmix(st) % (512 - k + 1));
+        const auto sys = codec::CodeParams::make(k, n, true), non = codec::CodeParams::make(k, n, false);
+        const auto src = random_fe(k, st);
+        const auto es = codec::encode_systematic(sys, src, codec::Path::Fast);
+        good = good && es == codec::encode_systematic_direct(sys, src) &&
+               es == codec::encode_systematic_intermediate_direct(sys, src);
+        const auto en = codec::encode_nonsystematic(non, src);
+        const auto keep = random_subset(k, n, st);
+        codec::Codeword rs(k), rn(k);
+        for (uint32_t j = 0; j < k; ++j) {
+            rs[j] = {keep[j], es[keep[j]]};
+            rn[j] = {keep[j], en[keep[j]]};
+        }
+        good = good && codec::decode_systematic(sys, rs, codec::Path::Fast) == src &&
+               codec::decode_direct(sys, rs) == src &&
+               codec::decode_nonsystematic(non, rn, codec::Path::Fast) == src && codec::decode_direct(non, rn) == src;
+        passed += good;
+    }
+    std::printf("selftest: oracle equivalence: %d/%d instances ok\n", passed, instances);
+    ok = ok && passed == instances;
+    std::printf("selftest: %s\n", ok ? "PASS" : "FAIL");
+    return ok ? 0 : 2;
+}
+
 [[noreturn]] void usage(const char* msg) {
     std::fprintf(stderr,
                  "%s\nusage: fntrs encode <input> [-o DIR] -k K -n N [--systematic|--non-systematic] [--seed S]\n"
-                 "       fntrs decode <manifest|dir> -o OUT\n",
+                 "       fntrs decode <manifest|dir> -o OUT\n"
+                 "       fntrs bench [--grid k1,k2,..] [-k K] [-n N] [--reps R] [--seed S]\n"
+                 "       fntrs selftest [--seed S]\n",
                  msg);
     std::exit(1);
 }
@@ -239,7 +415,8 @@ int main(int argc, char** argv) {
     if (argc < 2) usage("missing subcommand");
     const std::string cmd = argv[1];
     std::string input, output = ".";
-    uint64_t k = 0, n = 0, seed = 1;
+    uint64_t k = 0, n = 0, seed = 1, reps = 5;
+    std::vector<uint32_t> grid;
     bool systematic = true, have_out = false, have_k = false, have_n = false;
     for (int i = 2; i < argc; ++i) {
         const std::string a = argv[i];
@@ -257,6 +434,15 @@ int main(int argc, char** argv) {
             const std::string p = value("--path");
             if (p != "auto" && p != "fast" && p != "direct") usage("--path must be auto, fast or direct");
         } else if (a == "--jobs") (void)to_u64(value("--jobs"), "--jobs");
+        else if (a == "--reps") reps = to_u64(value("--reps"), "--reps");
+        else if (a == "--grid") {
+            const std::string gs = value("--grid");
+            for (size_t p = 0; p <= gs.size();) {
+                const size_t q = std::min(gs.find(',', p), gs.size());
+                grid.push_back(uint32_t(to_u64(gs.substr(p, q - p), "--grid")));
+                p = q + 1;
+            }
+        }
         else if (!a.empty() && a[0] == '-') usage(("unknown option " + a).c_str());
         else if (input.empty()) input = a;
         else usage(("unexpected argument " + a).c_str());
@@ -272,6 +458,25 @@ int main(int argc, char** argv) {
             if (input.empty() || !have_out) usage("decode needs <input> and --out");
             return cmd_decode(input, output);
         }
+        if (cmd == "bench") {  // fntrs_main.cpp:444-472: a grid of k (n = 2k), one size, or a default set
+            std::vector<std::pair<uint32_t, uint32_t>> sizes;
+            if (!grid.empty()) {
+                for (uint32_t g : grid) {
+                    if (g < 1 || g > 32768) usage("grid k values must be in [1, 32768]");
+                    sizes.emplace_back(g, 2 * g);
+                }
+            } else if (!have_k && !have_n) {
+                sizes = {{256, 512}, {1024, 2048}, {4096, 8192}};
+            } else {
+                if (!have_n) n = 2 * k;
+                if (!have_k) k = n / 2;
+                if (k < 1 || k > n || n > 65536) usage("need 1 <= k <= n <= 65536");
+                sizes = {{uint32_t(k), uint32_t(n)}};
+            }
+            if (reps < 1) usage("--reps must be positive");
+            return cmd_bench(sizes, int(reps), seed);
+        }
+        if (cmd == "selftest") return cmd_selftest(seed);
         usage(("unknown subcommand " + cmd).c_str());
     } catch (const Error& e) {
         std::fprintf(stderr, "error: %s\n", e.what());

@@ -92,3 +92,29 @@ def test_cli_files_byte_identical_to_reference(tmp_path, k, n, length, systemati
     assert (d / f"{4242:016x}.manifest.fnt").read_bytes() == manifest
     for j, want in enumerate(shards):
         assert (d / f"{4242:016x}.{j}.fnt").read_bytes() == want, j
+
+
+def test_cli_selftest_and_bench():
+    """The reference CLI's other two commands: `selftest` (MDS-exhaustive small
+    codes + randomized oracle equivalence through the drop-in API) passes, and
+    `bench` prints the reference's CSV columns with sane values (batched GPU
+    timing; FNT_n equivalents per codeword from the library's tally)."""
+    cli = _binary("fntrs", "cli")
+    r = subprocess.run([cli, "selftest", "--seed", "9"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "selftest: PASS" in r.stdout, r.stdout + r.stderr
+    assert r.stdout.count("0 failures") == 4
+    r = subprocess.run([cli, "bench", "--grid", "128,2048", "--reps", "3"], capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr
+    lines = r.stdout.strip().splitlines()
+    assert lines[0] == "variant,k,n,bytes,seconds,MBps,fnt_equivalents"
+    rows = [ln.split(",") for ln in lines[1:]]
+    assert [x[0] for x in rows[:4]] == ["encode_nonsystematic", "encode_systematic", "decode_nonsystematic",
+                                        "decode_systematic"]
+    assert len(rows) == 8
+    for v, k, n, b, sec, mbps, eq in rows:
+        assert int(n) == 2 * int(k) and float(sec) > 0 and float(mbps) > 0
+        if v == "encode_nonsystematic":
+            assert abs(float(eq) - 1.0) < 1e-9  # one FNT_n per codeword
+        if v == "decode_nonsystematic":
+            assert abs(float(eq) - 3.0) < 1e-9  # FNT_n + FNT_M + inverse FNT_M, M = n
