@@ -90,3 +90,24 @@ def test_subproduct_tree_layout_host_only():
     assert list(lens) == [2] * 5 + [3, 3, 2] + [5, 2] + [6]
     assert nc.value == sum(lens)
     assert lib.fntrs_gpu_subproduct_tree_layout(0, None, None, 0, None, None, None) == 4  # SizeMismatch
+
+
+def test_cli_usage_errors_without_gpu(tmp_path):
+    """The `fntrs` CLI rejects bad arguments with exit code 1 before touching
+    a device (the reference CLI's CLI11 validation, fntrs_main.cpp:413-444),
+    and a codec call without a device fails loudly with exit code 2."""
+    import subprocess
+    exe = os.path.join(ROOT, "build", "fntrs")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-C", ROOT, "cli"], check=True, capture_output=True)
+    src = tmp_path / "f.bin"
+    src.write_bytes(b"abc")
+    for args in (["encode", str(src), "--k", "5", "--n", "4"], ["encode", str(src), "--k", "65536", "--n", "65536"],
+                 ["encode", str(src)], ["decode", str(tmp_path)], ["frobnicate"], ["bench", "--grid", "0"],
+                 ["encode", str(src), "--k", "x", "--n", "4"]):
+        r = subprocess.run([exe, *args], capture_output=True, text=True, timeout=60)
+        assert r.returncode == 1, (args, r.returncode, r.stderr)
+        assert "usage" in r.stderr
+    r = subprocess.run([exe, "decode", str(tmp_path), "-o", str(tmp_path / "o")], capture_output=True, text=True,
+                       timeout=60)
+    assert r.returncode == 2 and "no *.manifest.fnt" in r.stderr
