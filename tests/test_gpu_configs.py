@@ -8,11 +8,12 @@ and SURVEY.md 8(d)'s bit-exact plan:
     comparison covers exactly the same codewords), C2 on a stratified 1/32
     sample (32 blocks of 64 consecutive stripes spread over all 65536, both
     pattern classes);
-  * decode compared in full on C1 and C3; on per-class samples of C4 (uniform,
-    parity-only, bursts), C2 (shared and distinct patterns) and C5; each from
-    the codewords AND from tampered received rows (non-codewords: the decoder
-    must return the same unique interpolant as the reference, escapes
-    included).
+  * decode compared in full on C1, C3, C4 (every stripe of the three erasure
+    classes: uniform, parity-only, bursts) and C5, and on the same 1/32 sample
+    of C2 (shared and distinct patterns); from the codewords, and on a subset
+    of stripes of every config from tampered received rows (non-codewords:
+    the decoder must return the same unique interpolant as the reference,
+    escapes included).
 Source symbols are generated on the device by the product's generator
 (fntrs_gpu_fill_symbols, itself checked against numpy in
 test_gpu_parity.py::test_device_generator_matches_numpy) at the global symbol
@@ -119,26 +120,21 @@ def sub_patterns(pats_all, sp_all, stripes):
     return pats_all[used], sp.astype(np.uint32)
 
 
-def decode_sample(codec, reflib, cfg, stripes, src_h, enc_h, esc_h, pats_all, sp_all, tamper_seed):
-    """Decode the listed stripes (their encoded rows given) from codewords and
-    from tampered rows; both against the reference."""
+def decode_sample(codec, reflib, cfg, stripes, src_h, enc_h, esc_h, pats_all, sp_all, tamper_seed, tampered=None):
+    """Decode the listed stripes (their encoded rows given) from codewords and,
+    for the first `tampered` of them (all by default), from tampered rows; both
+    against the reference."""
     from oracle_bind import gather_received
     pats, sp = sub_patterns(pats_all, sp_all, stripes)
     rx, rxe = gather_received(enc_h, esc_h, pats, sp)
     got, got_esc = check_decode(codec, reflib, cfg, pats, sp, rx, rxe, "codewords")
     assert np.array_equal(got, src_h) and got_esc.size == 0
-    trx, trxe = tamper(rx, rxe, tamper_seed)
-    check_decode(codec, reflib, cfg, pats, sp, trx, trxe, "tampered rows")
-
-
-def restrict_esc(esc, S_all, n, L, idx):
-    """Escape keys of the listed stripes, renumbered as if they were stripes 0..len-1."""
-    per = n * L
-    out = []
-    for j, s in enumerate(idx):
-        e = esc[(esc >= s * per) & (esc < (s + 1) * per)]
-        out.append(e - np.uint64(s * per) + np.uint64(j * per))
-    return np.concatenate(out) if out else np.zeros(0, np.uint64)
+    t = len(stripes) if tampered is None else min(tampered, len(stripes))
+    if t:
+        pats_t, sp_t = sub_patterns(pats_all, sp_all, np.asarray(stripes)[:t])
+        esc_t = rxe[rxe < np.uint64(t * cfg.k * cfg.L)]
+        trx, trxe = tamper(rx[:t], esc_t, tamper_seed)
+        check_decode(codec, reflib, cfg, pats_t, sp_t, trx, trxe, "tampered rows")
 
 
 # --------------------------------------------------------------------- C1 ----
@@ -163,50 +159,48 @@ def test_c3_full(codec, reflib):
 
 
 # --------------------------------------------------------------------- C4 ----
-def test_c4_encode_full_decode_per_class(codec, reflib):
-    """All 256 stripes encoded (chunks of 32) against the reference; decode on
-    4 stripes of each erasure class (uniform, parity only, 1024-bursts)."""
+def test_c4_full(codec, reflib):
+    """All 256 stripes encoded AND decoded (chunks of 32) against the
+    reference: every stripe of the three erasure classes (uniform, parity
+    only, 1024-bursts); tampered rows on 6 stripes (two per class) per chunk."""
     from paper_0907_1788_b200 import workload as W
     cfg = W.CONFIGS["C4"]
     pats_all, sp_all = W.patterns(cfg)
     chunk = 32
-    for s0 in range(0, cfg.stripes, chunk):
+    for c, s0 in enumerate(range(0, cfg.stripes, chunk)):
         src, enc, esc = check_encode_chunk(codec, reflib, cfg, s0, chunk)
-        if s0 == 0:  # stripes 0..11: four of each class (s % 3)
-            idx = np.arange(12)
-            decode_sample(codec, reflib, cfg, idx, src[idx], enc[idx], restrict_esc(esc, chunk, cfg.n, cfg.L, idx),
-                          pats_all, sp_all, 44)
-    assert {int(s) % 3 for s in range(12)} == {0, 1, 2}
+        idx = np.arange(chunk)
+        decode_sample(codec, reflib, cfg, s0 + idx, src, enc, esc, pats_all, sp_all, 44 + c, tampered=6)
+    assert {int(s) % 3 for s in range(6)} == {0, 1, 2}
 
 
 # --------------------------------------------------------------------- C5 ----
-def test_c5_encode_full_decode_sample(codec, reflib):
-    """All 2048 stripes (8 GiB of source) encoded in chunks of 128 against the
-    reference; decode of 8 stripes from each of 4 chunks spread over the range."""
+def test_c5_full(codec, reflib):
+    """All 2048 stripes (8 GiB of source) encoded AND decoded in chunks of 128
+    against the reference; tampered rows on 8 stripes of every fourth chunk."""
     from paper_0907_1788_b200 import workload as W
     cfg = W.CONFIGS["C5"]
     pats_all, sp_all = W.patterns(cfg)
     chunk = 128
     for c, s0 in enumerate(range(0, cfg.stripes, chunk)):
         src, enc, esc = check_encode_chunk(codec, reflib, cfg, s0, chunk)
-        if c % 4 == 1:
-            idx = np.arange(0, chunk, chunk // 8)
-            decode_sample(codec, reflib, cfg, s0 + idx, src[idx], enc[idx],
-                          restrict_esc(esc, chunk, cfg.n, cfg.L, idx), pats_all, sp_all, 55 + c)
+        idx = np.arange(chunk)
+        decode_sample(codec, reflib, cfg, s0 + idx, src, enc, esc, pats_all, sp_all, 55 + c,
+                      tampered=8 if c % 4 == 1 else 0)
 
 
 # --------------------------------------------------------------------- C2 ----
 def test_c2_stratified_sample(codec, reflib):
     """1/32 of C2 (32 blocks of 64 consecutive stripes, one block every 2048
-    stripes): encode payload + escapes of every sampled stripe; decode of 16
-    stripes per block (8 on the shared pattern P0, 8 on distinct patterns)."""
+    stripes): encode payload + escapes and decode of every sampled stripe
+    (even stripes on the shared pattern P0, odd on distinct patterns); tampered
+    rows on 16 stripes per block."""
     from paper_0907_1788_b200 import workload as W
     cfg = W.CONFIGS["C2"]
     pats_all, sp_all = W.patterns(cfg)
     block = 64
     for b, s0 in enumerate(range(0, cfg.stripes, 2048)):
         src, enc, esc = check_encode_chunk(codec, reflib, cfg, s0, block)
-        idx = np.arange(16)
+        idx = np.arange(block)
         assert (sp_all[s0 + idx][0::2] == 0).all() and (sp_all[s0 + idx][1::2] != 0).all()
-        decode_sample(codec, reflib, cfg, s0 + idx, src[idx], enc[idx], restrict_esc(esc, block, cfg.n, cfg.L, idx),
-                      pats_all, sp_all, 200 + b)
+        decode_sample(codec, reflib, cfg, s0 + idx, src, enc, esc, pats_all, sp_all, 200 + b, tampered=16)
