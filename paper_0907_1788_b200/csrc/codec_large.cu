@@ -87,7 +87,11 @@ __device__ __forceinline__ Unit batch_unit(uint32_t tps, uint32_t ng, uint32_t s
 
 // A consumed intermediate block is dead: drop its L2 lines without a write
 // back (each block is read by exactly one unit, after its TMA load landed).
+#ifndef FNTRS_STREAM_DISCARD
+#define FNTRS_STREAM_DISCARD 1
+#endif
 __device__ __forceinline__ void discard_block(const uint32_t* base, uint32_t bytes) {
+    if constexpr (!FNTRS_STREAM_DISCARD) return;
     for (uint32_t off = threadIdx.x * 128u; off < bytes; off += kLNT * 128u)
         asm volatile("discard.global.L2 [%0], 128;" ::"l"(reinterpret_cast<const char*>(base) + off) : "memory");
 }
@@ -616,28 +620,29 @@ __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence
 // tickets, and none of those can be a claimed-but-unstarted one.)
 struct Claims {
     uint32_t* ticket;
-    uint32_t* s_next;  // shared slot
+    uint32_t* s;  // two shared slots, used alternately
+    uint32_t it = 0;
     __device__ __forceinline__ uint32_t first() {
-        if (threadIdx.x == 0) *s_next = atomicAdd(ticket, 1u);
+        if (threadIdx.x == 0) s[0] = atomicAdd(ticket, 1u);
         __syncthreads();
-        return *s_next;
+        return s[0];
     }
-    // after every thread has read the current ticket: claim the following one
+    // thread 0 claims the following ticket into the other slot; every thread read
+    // that slot's previous ticket before the barriers of the current unit
     __device__ __forceinline__ void prefetch() {
-        __syncthreads();
-        if (threadIdx.x == 0) *s_next = atomicAdd(ticket, 1u);
+        if (threadIdx.x == 0) s[(it + 1) & 1u] = atomicAdd(ticket, 1u);
     }
+    // after a barrier that followed prefetch()
     __device__ __forceinline__ uint32_t next() {
-        __syncthreads();
-        return *s_next;
+        ++it;
+        return s[it & 1u];
     }
 };
-
 
 // every thread's global writes of the unit, then one count: the barrier
 // orders the CTA's writes before thread 0's gpu-scope fence, which is
 // cumulative, then the counter update (the release pattern of CUTLASS's
-// semaphore)
+// semaphore). The same barrier publishes the prefetched ticket.
 __device__ __forceinline__ void unit_done(uint32_t* counter, bool tma_stored) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -659,7 +664,8 @@ struct StreamGeom {
 template <int E1, int E2, bool HALFK, bool PUNCT>
 __global__ void __launch_bounds__(kLNT, StreamGeom<E1, E2>::MINB)
 enc_stream_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF, uint32_t k, uint32_t n, uint32_t L,
-                  uint32_t tps, uint32_t ncb, uint32_t R, uint32_t D, const uint16_t* __restrict__ src, EscIn esc_in,
+                  uint32_t tps, int tsh, uint32_t ncb, uint32_t R, uint32_t D, const uint16_t* __restrict__ src,
+                  EscIn esc_in,
                   uint16_t* __restrict__ out, EscOut esc_out, uint32_t* __restrict__ Y, uint32_t* __restrict__ ctl,
                   const __grid_constant__ CUtensorMap out_map, const __grid_constant__ CUtensorMap in_map) {
     using SG = StreamGeom<E1, E2>;
@@ -667,18 +673,21 @@ enc_stream_kernel(const uint2* __restrict__ ptab, const uint2* __restrict__ bigF
     uint32_t* done1 = ctl + 1;
     uint32_t* done2 = done1 + ncb;
     const uint32_t total = (ncb + D) * U;
-    __shared__ uint32_t s_next;
-    Claims cl{ctl, &s_next};
+    __shared__ uint32_t s_tk[2];
+    Claims cl{ctl, s_tk};
     for (uint32_t t = cl.first(); t < total; t = cl.next()) {
         cl.prefetch();
         const uint32_t step = t / U, r = t - step * U;
         const bool p2 = r < N1;  // [phase 2: N1 units][phase 1: N2 units]
         const uint32_t g = p2 ? r : r - N1;
-        if (p2 && step < D) continue;
         const uint32_t cb = p2 ? step - D : step;
-        if (cb >= ncb) continue;
-        const uint32_t slot = cb % R;
-        const Unit u{cb / tps, g, (cb % tps) * kLW, uint64_t(slot) * N * kLW, 0u, slot * N};
+        if ((p2 && step < D) || cb >= ncb) {  // outside the schedule: publish the next ticket only
+            __syncthreads();
+            continue;
+        }
+        const uint32_t slot = cb & (R - 1u);  // R is a power of two
+        const uint32_t stripe = tsh >= 0 ? cb >> tsh : cb / tps, ct = cb - stripe * tps;
+        const Unit u{stripe, g, ct * kLW, uint64_t(slot) * N * kLW, 0u, slot * N};
         if (threadIdx.x == 0) {
             if (p2) {
                 wait_at_least(done1 + cb, N2);
@@ -702,7 +711,7 @@ template <int E1, int E2, bool HALFK>
 __global__ void __launch_bounds__(kLNT, StreamGeom<E1, E2>::MINB)
 dec_stream_kernel(const uint2* __restrict__ ptabF, const uint2* __restrict__ ptabI, const uint2* __restrict__ bigF,
                   const uint2* __restrict__ bigI, const uint2* __restrict__ rowmap, const uint2* __restrict__ ahat2,
-                  uint32_t k, uint32_t L, uint32_t tps, uint32_t ncb, uint32_t R, uint32_t D,
+                  uint32_t k, uint32_t L, uint32_t tps, int tsh, uint32_t ncb, uint32_t R, uint32_t D,
                   const uint32_t* __restrict__ stripe_pattern, const uint16_t* __restrict__ rx, EscIn esc_in,
                   uint16_t* __restrict__ out, EscOut esc_out, uint32_t* __restrict__ Y1, uint32_t* __restrict__ Y2,
                   uint32_t* __restrict__ Y3, uint32_t* __restrict__ ctl, const __grid_constant__ CUtensorMap map1,
@@ -712,8 +721,8 @@ dec_stream_kernel(const uint2* __restrict__ ptabF, const uint2* __restrict__ pta
     constexpr uint32_t N1 = SG::N1, N2 = SG::N2, N = SG::N, U = 2 * (N1 + N2);
     uint32_t* done = ctl + 1;  // done[(p - 1) * ncb + cb]
     const uint32_t total = (ncb + 3 * D) * U;
-    __shared__ uint32_t s_next;
-    Claims cl{ctl, &s_next};
+    __shared__ uint32_t s_tk[2];
+    Claims cl{ctl, s_tk};
     for (uint32_t t = cl.first(); t < total; t = cl.next()) {
         cl.prefetch();
         const uint32_t step = t / U, r = t - step * U;
@@ -724,11 +733,14 @@ dec_stream_kernel(const uint2* __restrict__ ptabF, const uint2* __restrict__ pta
         else if (r < 2 * N1 + N2) p = 2, g = r - N1 - N2;
         else p = 1, g = r - 2 * N1 - N2;
         const uint32_t lag = (p - 1) * D;
-        if (step < lag) continue;
         const uint32_t cb = step - lag;
-        if (cb >= ncb) continue;
-        const uint32_t slot = cb % R;
-        const Unit u{cb / tps, g, (cb % tps) * kLW, uint64_t(slot) * N * kLW, 0u, slot * N};
+        if (step < lag || cb >= ncb) {  // outside the schedule: publish the next ticket only
+            __syncthreads();
+            continue;
+        }
+        const uint32_t slot = cb & (R - 1u);  // R is a power of two
+        const uint32_t stripe = tsh >= 0 ? cb >> tsh : cb / tps, ct = cb - stripe * tps;
+        const Unit u{stripe, g, ct * kLW, uint64_t(slot) * N * kLW, 0u, slot * N};
         if (threadIdx.x == 0) {
             if (p > 1) wait_at_least(done + (p - 2) * ncb + cb, (p - 1) % 2 ? N2 : N1);  // phases 1, 3: N2 units
             if (p < 4 && cb >= R) wait_at_least(done + p * ncb + cb - R, (p + 1) % 2 ? N2 : N1);
@@ -892,13 +904,17 @@ cudaError_t run_decode(const FastTables& t, const FastPlanView& pv, uint32_t str
 struct StreamShape {
     uint32_t R, D;
 };
+int pow2_shift(uint32_t v) {  // log2(v) for a power of two, else -1
+    return v && !(v & (v - 1)) ? 31 - __builtin_clz(v) : -1;
+}
+
 StreamShape stream_shape(uint32_t N, bool decode) {
-    if (const char* e = std::getenv("FNTRS_STREAM_RD")) {  // "R,D" override (A/B)
+    if (const char* e = std::getenv("FNTRS_STREAM_RD")) {  // "R,D" override (A/B); R a power of two
         unsigned r = 0, d = 0;
-        if (std::sscanf(e, "%u,%u", &r, &d) == 2 && d < r) return {r, d};
+        if (std::sscanf(e, "%u,%u", &r, &d) == 2 && d < r && pow2_shift(r) >= 0) return {r, d};
     }
-    if (N <= 16384) return {4, 2};
-    return decode ? StreamShape{2, 1} : StreamShape{3, 1};
+    if (N <= 16384) return {8, 4};  // C4: 3 rings x 8 slots x 4 MB = 96 MB of L2
+    return decode ? StreamShape{2, 1} : StreamShape{4, 2};
 }
 
 template <class K>
@@ -929,8 +945,8 @@ cudaError_t stream_encode(const FastTables& t, uint32_t k, uint32_t n, uint32_t 
     if ((err = cudaMemsetAsync(ctl, 0, (1 + 2 * size_t(ncb)) * 4, st))) return err;
     uint32_t grid = 0;
     if ((err = stream_grid(kern, sm, grid))) return err;
-    kern<<<grid, kLNT, sm, st>>>(t.ptab_fwd, t.big_fwd, k, n, L, tps, ncb, sh.R, sh.D, src, ein, out, eout, Y, ctl,
-                                 omap, ymap);
+    kern<<<grid, kLNT, sm, st>>>(t.ptab_fwd, t.big_fwd, k, n, L, tps, pow2_shift(tps), ncb, sh.R, sh.D, src, ein, out,
+                                 eout, Y, ctl, omap, ymap);
     return cudaGetLastError();
 }
 
@@ -956,8 +972,8 @@ cudaError_t stream_decode(const FastTables& t, const FastPlanView& pv, uint32_t 
     if ((err = cudaMemsetAsync(ctl, 0, (1 + 4 * size_t(ncb)) * 4, st))) return err;
     uint32_t grid = 0;
     if ((err = stream_grid(kern, sm, grid))) return err;
-    kern<<<grid, kLNT, sm, st>>>(t.ptab_fwd, t.ptab_inv, t.big_fwd, t.big_inv, pv.rowmap, pv.ahat2, pv.k, L, tps, ncb,
-                                 sh.R, sh.D, sp, rx, ein, out, eout, Y1, Y2, Y3, ctl, m1, m2, m3o, m3);
+    kern<<<grid, kLNT, sm, st>>>(t.ptab_fwd, t.ptab_inv, t.big_fwd, t.big_inv, pv.rowmap, pv.ahat2, pv.k, L, tps,
+                                 pow2_shift(tps), ncb, sh.R, sh.D, sp, rx, ein, out, eout, Y1, Y2, Y3, ctl, m1, m2, m3o, m3);
     return cudaGetLastError();
 }
 
