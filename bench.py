@@ -46,7 +46,6 @@ FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback, only if MEASURED_PEAKS.
 # launch of each kernel per config, with the codewords that launch coded.
 PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "r02_ncu_summary.csv")
 PROFILE_CODEWORDS = {"C2": 8192 * 2048, "C3": 1 * 2048, "C4": 32 * 1024, "C5": 256 * 1024}
-SYS_PROFILE = os.path.join(ROOT, "profiles", "r01_ncu_full_sysdec_raw.csv")  # systematic C2 decode, 8192 stripes
 
 
 def kernel_label(cfg, what, systematic):
@@ -68,7 +67,8 @@ def _summary_rows(cfg, what):
         rows = list(csv.DictReader(open(PROFILE_SUMMARY)))
     except Exception:
         return []
-    tag = f"prof_{cfg.name}_{'dec' if what == 'decode' else 'enc'}_raw.csv"
+    short = {"decode": "dec", "encode": "enc"}.get(what, what)
+    tag = f"prof_{cfg.name}_{short}_raw.csv"
     return [r for r in rows if r["report"] == tag]
 
 
@@ -76,19 +76,10 @@ def profiled(cfg, what, systematic, codewords):
     """Per-call DRAM traffic (read + write, scaled from the captured launch(es)
     to this call's codewords) and the issue / multiplier-pipe fractions
     (duration-weighted over the kernels of the call) from the committed capture."""
-    if systematic:
-        if cfg.name != "C2" or what != "decode":
+    if systematic:  # the fused systematic kernels (MODE 3 decode / MODE 4 encode), captured for C2
+        if cfg.name != "C2":
             return {}
-        try:
-            import csv
-            r = list(csv.reader(open(SYS_PROFILE)))
-            h, u, v = r[0], r[1], r[2]
-            sc = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-            tr = sum(float(v[h.index(m)]) * sc[u[h.index(m)]] for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-            return {"traffic": int(tr * codewords / (8192 * 2048)),
-                    "traffic_source": "profiles/r01_ncu_full_sysdec_raw.csv (8192-stripe C2 launch, scaled)"}
-        except Exception:
-            return {}
+        what = "sysdec" if what == "decode" else "sysenc"
     rows = _summary_rows(cfg, what)
     if not rows or cfg.name not in PROFILE_CODEWORDS:
         return {}

@@ -19,3 +19,5 @@ run C5 256 dec "dec_fast_kernel" 1 1
 run C5 256 enc "enc_fast_kernel" 1 1
 run C2 8192 dec "dec_fast_kernel" 1 1
 run C2 8192 enc "enc_fast_kernel" 1 1
+run C2 8192 sysdec "dec_fast_kernel" 1 3   # skip the two MODE 4 encodes and the first decode
+run C2 8192 sysenc "dec_fast_kernel" 1 1   # the systematic encode is MODE 4 of the decode kernel
