@@ -80,9 +80,12 @@ namespace {
 #ifndef FNTRS_SYS_MINB
 #define FNTRS_SYS_MINB 4
 #endif
+#ifndef FNTRS_DEC_MINB
+#define FNTRS_DEC_MINB 5
+#endif
 template <int E, int MODE = 0>
 struct DecOcc {
-    static constexpr int MINB = (E <= 8) ? (MODE >= 3 ? FNTRS_SYS_MINB : 5) : Pick<E>::MINB;
+    static constexpr int MINB = (E <= 8) ? (MODE >= 3 ? FNTRS_SYS_MINB : FNTRS_DEC_MINB) : Pick<E>::MINB;
 };
 
 // MODE 0: decode (interp::interpolate, the k coefficients out).
