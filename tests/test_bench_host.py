@@ -53,3 +53,24 @@ def test_cpu_info_block():
     info = bench.cpu_info()
     assert info["logical_cores"] == os.cpu_count()
     assert set(info) == {"cpu_model", "logical_cores", "avx2_path"}
+
+
+def test_reference_arm_line(tmp_path):
+    """`bench.py --impl reference` (the reference library on the host cores)
+    prints one JSON line with the contract's keys: impl, the metric and unit of
+    the GPU arm, a cpu_baseline block and an e2e block with zero PCIe bytes."""
+    import json
+    import subprocess
+    from oracle_bind import RefLib
+    if not RefLib.available():
+        pytest.skip("reference library (oracle/_ref) not built")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "C1",
+                        "--steps", "1", "--warmup", "3", "--ref-step-seconds", "0.3"], capture_output=True, text=True,
+                       timeout=600, cwd=ROOT, env={k: v for k, v in os.environ.items() if k != "WORLD_SIZE"})
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert d["impl"] == "reference" and d["unit"] == "GB/s" and d["higher_is_better"] is True
+    assert d["value"] > 0 and d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
+    assert d["cpu_baseline"]["path"] == "fast" and d["cpu_baseline"]["other_path"]["path"] == "auto"
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert d["metric"].startswith("encode & decode GB/s")
