@@ -247,6 +247,26 @@ int fntrs_gpu_subproduct_tree(fntrs_ctx* ctx, uint32_t k, const uint32_t* points
 int fntrs_gpu_lagrange(fntrs_ctx* ctx, uint32_t k, const uint32_t* xs, const uint32_t* vs, uint32_t* out,
                        void* stream);
 
+/* Evaluation at geometric points (proj/include/fntrs/geom.hpp, proj/src/geom.cpp):
+ * fntrs_gpu_chirp_table fills the reference's ChirpTable vectors for size n
+ * (power of two <= 65536) and any root: b[2n-1] (b_i = root^(i(i-1)/2)),
+ * b_inverse[n], and b_spectrum[2n] = FNT_2n(b zero-padded) in NATURAL order
+ * (any pointer may be NULL; n = 65536 is the full-domain case: nothing to
+ * fill). fntrs_gpu_geom_eval writes out[n] = a(root^i), i < n, for a of len <=
+ * n coefficients, by the chirp (two FNT_2n and a pointwise product), or for n
+ * = 65536 by the transform itself (root must be the domain root or its
+ * inverse: InvalidTransformSize otherwise). fntrs_gpu_geom_eval_negative:
+ * out[j] = a(root^-(j+1)). All buffers DEVICE. */
+int fntrs_gpu_chirp_table(fntrs_ctx* ctx, uint32_t n, uint32_t root, uint32_t* b, uint32_t* b_inverse,
+                          uint32_t* b_spectrum, void* stream);
+int fntrs_gpu_geom_eval(fntrs_ctx* ctx, uint32_t n, uint32_t root, const uint32_t* a, uint32_t len,
+                        const uint32_t* b_inverse, const uint32_t* b_spectrum, uint32_t* out, void* stream);
+int fntrs_gpu_geom_eval_negative(fntrs_ctx* ctx, uint32_t n, uint32_t root, const uint32_t* a, uint32_t len,
+                                 const uint32_t* b_inverse, const uint32_t* b_spectrum, uint32_t* out, void* stream);
+/* (b_inverse / b_spectrum: a cached chirp table of `root` -- for the negative
+ * direction, of root^-1 -- as fntrs_gpu_chirp_table fills it, or NULL to build
+ * one: with a cached table an evaluation runs two FNT_2n, as the reference's.) */
+
 /* poly::derivative (out[len-1]) and poly::eval_horner (*out = a(x)),
  * proj/src/poly.cpp:201-214. */
 int fntrs_gpu_poly_derivative(fntrs_ctx* ctx, uint32_t len, const uint32_t* a, uint32_t* out, void* stream);

@@ -50,6 +50,9 @@ SIGNATURES = [
     ("fntrs_gpu_subproduct_tree_layout", _int, [_u32, _pu32, _pu32, _u32, _pu32, C.POINTER(_u64), C.POINTER(_u64)]),
     ("fntrs_gpu_subproduct_tree", _int, [_vp, _u32, _vp, _vp, _vp]),
     ("fntrs_gpu_lagrange", _int, [_vp, _u32, _vp, _vp, _vp, _vp]),
+    ("fntrs_gpu_chirp_table", _int, [_vp, _u32, _u32, _vp, _vp, _vp, _vp]),
+    ("fntrs_gpu_geom_eval", _int, [_vp, _u32, _u32, _vp, _u32, _vp, _vp, _vp, _vp]),
+    ("fntrs_gpu_geom_eval_negative", _int, [_vp, _u32, _u32, _vp, _u32, _vp, _vp, _vp, _vp]),
     ("fntrs_gpu_poly_derivative", _int, [_vp, _u32, _vp, _vp, _vp]),
     ("fntrs_gpu_poly_eval", _int, [_vp, _u32, _vp, _u32, _vp, _vp]),
 ]

@@ -1171,6 +1171,104 @@ int fntrs_gpu_lagrange(fntrs_ctx* ctx, uint32_t k, const uint32_t* xs, const uin
     return FNTRS_OK;
 }
 
+int fntrs_gpu_chirp_table(fntrs_ctx* ctx, uint32_t n, uint32_t root, uint32_t* b, uint32_t* b_inverse,
+                          uint32_t* b_spectrum, void* stream) {  // geom.cpp:13-41
+    if (!ctx) return FNTRS_E_INVALID_ARGUMENT;
+    if (n == 0 || n > 65536 || (n & (n - 1)))
+        return fail(ctx, FNTRS_E_INVALID_TRANSFORM_SIZE, "chirp table size must be a power of two in [1, 65536]");
+    if (n == 65536) return FNTRS_OK;  // full domain: evaluation is the transform itself
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Scratch sc;
+    int rc = get_scratch(ctx, sc, size_t(4) * n * 4 + 256, 1, st);
+    if (rc) return rc;
+    uint32_t* bb = b ? b : sc.p[0];
+    cudaError_t e = launch_chirp(n, root, bb, b_inverse, st);
+    ctx->launches += 1;
+    if (!e && b_spectrum) {  // b zero-padded to 2n, forward spectrum
+        uint32_t* pad = sc.p[0] + 2 * n;
+        e = cudaMemsetAsync(pad, 0, size_t(2) * n * 4, st);
+        if (!e) e = cudaMemcpyAsync(pad, bb, size_t(2 * n - 1) * 4, cudaMemcpyDeviceToDevice, st);
+        if (!e) rc = fntrs_gpu_fnt(ctx, 2 * n, 0, 1, pad, b_spectrum, stream);
+    }
+    release_scratch(sc, st);
+    if (rc) return rc;
+    CK(e, "chirp table");
+    return FNTRS_OK;
+}
+
+int fntrs_gpu_geom_eval(fntrs_ctx* ctx, uint32_t n, uint32_t root, const uint32_t* a, uint32_t len,
+                        const uint32_t* b_inverse, const uint32_t* b_spectrum, uint32_t* out,
+                        void* stream) {  // geom.cpp:59-99
+    if (!ctx) return FNTRS_E_INVALID_ARGUMENT;
+    if (n == 0 || n > 65536 || (n & (n - 1)))
+        return fail(ctx, FNTRS_E_INVALID_TRANSFORM_SIZE, "chirp table size must be a power of two in [1, 65536]");
+    if (len > n) return fail(ctx, FNTRS_E_SIZE_MISMATCH, "geom_eval: polynomial has more coefficients than points");
+    if (!out || (len && !a)) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "null buffer");
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    root %= kP;
+    Scratch sc;
+    int rc = get_scratch(ctx, sc, size_t(8) * n * 4 + 256, 1, st);
+    if (rc) return rc;
+    cudaError_t e = cudaSuccess;
+    if (n == 65536) {  // eval_full_domain: the transform (forward), or its unscaled inverse for the inverse root
+        const bool fwd = root == croot(n, false), inv = root == croot(n, true);
+        if (!fwd && !inv) {
+            release_scratch(sc, st);
+            return fail(ctx, FNTRS_E_INVALID_TRANSFORM_SIZE, "full-domain evaluation needs the transform root");
+        }
+        uint32_t* pad = sc.p[0];
+        e = cudaMemsetAsync(pad, 0, size_t(n) * 4, st);
+        if (!e && len) e = cudaMemcpyAsync(pad, a, size_t(len) * 4, cudaMemcpyDeviceToDevice, st);
+        // sum a_j root^-(ij) = n * fnt_inverse = -fnt_inverse (65536 = -1): the unscaled inverse
+        if (!e) rc = fntrs_gpu_fnt(ctx, n, fwd ? 0 : 2, 1, pad, out, stream);
+    } else {
+        const uint32_t m = 2 * n;
+        uint32_t *binv = sc.p[0], *B = binv + n, *c = B + m, *c2 = c + m;
+        if (b_inverse && b_spectrum) {  // the caller's cached table
+            binv = const_cast<uint32_t*>(b_inverse);
+            B = const_cast<uint32_t*>(b_spectrum);
+        } else {
+            e = launch_chirp(n, root, c2, binv, st);  // b into c2 (2n - 1), then its padded spectrum
+            if (!e) e = cudaMemsetAsync(c2 + (m - 1), 0, 4, st);
+            if (!e) rc = fntrs_gpu_fnt(ctx, m, 0, 1, c2, B, stream);
+        }
+        if (!e && !rc) e = launch_geom_pre(n, len, a, binv, c, st);
+        if (!e && !rc) rc = fntrs_gpu_fnt(ctx, m, 0, 1, c, c2, stream);
+        if (!e && !rc) e = launch_pointwise(m, c2, B, st);
+        if (!e && !rc) rc = fntrs_gpu_fnt(ctx, m, 1, 1, c2, c, stream);  // inverse, 1/m
+        if (!e && !rc) e = launch_geom_post(n, c, binv, out, st);
+        ctx->launches += 4;
+    }
+    release_scratch(sc, st);
+    if (rc) return rc;
+    CK(e, "geom eval");
+    return FNTRS_OK;
+}
+
+int fntrs_gpu_geom_eval_negative(fntrs_ctx* ctx, uint32_t n, uint32_t root, const uint32_t* a, uint32_t len,
+                                 const uint32_t* b_inverse, const uint32_t* b_spectrum, uint32_t* out,
+                                 void* stream) {  // geom.cpp:101-116
+    if (!ctx) return FNTRS_E_INVALID_ARGUMENT;
+    if (len > n)
+        return fail(ctx, FNTRS_E_SIZE_MISMATCH, "geom_eval_negative: polynomial has more coefficients than points");
+    if (!out || (len && !a)) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "null buffer");
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const uint32_t rho = cpow(root % kP, kP - 2);
+    Scratch sc;
+    int rc = get_scratch(ctx, sc, size_t(len) * 4 + 256, 1, st);
+    if (rc) return rc;
+    cudaError_t e = launch_powers_scale(len, rho, a, sc.p[0], st);
+    ctx->launches += 1;
+    if (!e) rc = fntrs_gpu_geom_eval(ctx, n, rho, sc.p[0], len, b_inverse, b_spectrum, out, stream);
+    release_scratch(sc, st);
+    if (rc) return rc;
+    CK(e, "geom eval negative");
+    return FNTRS_OK;
+}
+
 int fntrs_gpu_poly_derivative(fntrs_ctx* ctx, uint32_t len, const uint32_t* a, uint32_t* out, void* stream) {
     if (!ctx) return FNTRS_E_INVALID_ARGUMENT;
     if (len > 1 && (!a || !out)) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "null buffer");

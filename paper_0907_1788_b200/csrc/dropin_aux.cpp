@@ -10,11 +10,13 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <map>
 #include <string>
 #include <vector>
 
 #include "dropin_shared.h"
 #include "fntrs/errors.hpp"
+#include "fntrs/geom.hpp"
 #include "fntrs/poly.hpp"
 #include "fntrs/shardio.hpp"
 #include "fntrs_gpu.h"
@@ -170,6 +172,112 @@ SubproductTree build_subproduct_tree(std::span<const Fe> points) {  // poly.cpp:
 }
 
 }  // namespace poly
+
+// ---- geom.hpp ---------------------------------------------------------------
+namespace geom {
+
+ChirpTable build_chirp(std::uint32_t n, Fe root) {  // geom.cpp:13-41
+    ChirpTable t;
+    t.n = n;
+    t.root = root;
+    Shared& S = shared();
+    std::lock_guard<std::mutex> lock(S.mu);
+    S.ensure();
+    if (n == 65536) {
+        S.check(fntrs_gpu_chirp_table(S.ctx, n, root, nullptr, nullptr, nullptr, S.stream));  // validates only
+        t.full_domain = true;
+        return t;
+    }
+    if (n == 0 || n > 65536 || (n & (n - 1))) S.check(fntrs_gpu_chirp_table(S.ctx, n, root, nullptr, nullptr, nullptr,
+                                                                          S.stream));  // throws
+    DevBuf d(size_t(5) * n * 4, S.stream);
+    uint32_t* p = d.as<uint32_t>();
+    S.check(fntrs_gpu_chirp_table(S.ctx, n, root, p, p + 2 * n, p + 3 * n, S.stream));
+    t.b.resize(2 * n - 1);
+    t.b_inverse.resize(n);
+    std::vector<Fe> spec(2 * n);
+    download(S, t.b.data(), d, 2 * n - 1, 0);
+    download(S, t.b_inverse.data(), d, n, 2 * n);
+    download(S, spec.data(), d, 2 * n, 3 * n);
+    S.sync();
+    S.note_transforms();
+    // dif_forward leaves the spectrum in bit-reversed order (transform.hpp)
+    t.b_fnt.resize(2 * n);
+    uint32_t lg = 0;
+    while ((1u << lg) < 2 * n) ++lg;
+    for (uint32_t i = 0; i < 2 * n; ++i) {
+        uint32_t r = 0;
+        for (uint32_t bit = 0; bit < lg; ++bit) r |= ((i >> bit) & 1u) << (lg - 1 - bit);
+        t.b_fnt[i] = spec[r];
+    }
+    return t;
+}
+
+std::shared_ptr<const ChirpTable> chirp_for(std::uint32_t n, Fe root) {  // geom.cpp:43-53
+    static std::mutex mu;
+    static std::map<std::pair<std::uint32_t, Fe>, std::shared_ptr<const ChirpTable>> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find({n, root});
+    if (it != cache.end()) return it->second;
+    auto t = std::make_shared<const ChirpTable>(build_chirp(n, root));
+    cache.emplace(std::make_pair(n, root), t);
+    return t;
+}
+
+namespace {
+// a(root^i) on the device with a table's b_inverse and its spectrum (natural
+// order: the inverse of dif_forward's bit reversal); full-domain tables have none
+std::vector<Fe> eval_with_table(std::span<const Fe> a, const ChirpTable& t, bool negative, Fe root) {
+    const uint32_t n = t.n, m = 2 * n;
+    Shared& S = shared();
+    std::lock_guard<std::mutex> lock(S.mu);
+    S.ensure();
+    const bool tab = !t.full_domain && t.b_inverse.size() == n && t.b_fnt.size() == m;
+    DevBuf d((a.size() + n + (tab ? n + m : 0) + 1) * 4, S.stream);
+    uint32_t* p = d.as<uint32_t>();
+    upload(S, d, a.data(), a.size());
+    uint32_t *binv = nullptr, *spec = nullptr;
+    if (tab) {
+        binv = p + a.size() + n;
+        spec = binv + n;
+        std::vector<Fe> nat(m);
+        uint32_t lg = 0;
+        while ((1u << lg) < m) ++lg;
+        for (uint32_t i = 0; i < m; ++i) {
+            uint32_t r = 0;
+            for (uint32_t bit = 0; bit < lg; ++bit) r |= ((i >> bit) & 1u) << (lg - 1 - bit);
+            nat[r] = t.b_fnt[i];
+        }
+        if (cudaMemcpyAsync(binv, t.b_inverse.data(), size_t(n) * 4, cudaMemcpyHostToDevice, S.stream) ||
+            cudaMemcpyAsync(spec, nat.data(), size_t(m) * 4, cudaMemcpyHostToDevice, S.stream))
+            throw Error("fntrs: host-to-device copy failed");
+        S.sync();  // `nat` is a host temporary
+    }
+    if (negative)
+        S.check(fntrs_gpu_geom_eval_negative(S.ctx, n, root, p, uint32_t(a.size()), binv, spec, p + a.size(),
+                                             S.stream));
+    else
+        S.check(fntrs_gpu_geom_eval(S.ctx, n, t.root, p, uint32_t(a.size()), binv, spec, p + a.size(), S.stream));
+    std::vector<Fe> out(n);
+    download(S, out.data(), d, n, a.size());
+    S.sync();
+    S.note_transforms();
+    return out;
+}
+}  // namespace
+
+std::vector<Fe> geom_eval(std::span<const Fe> a, const ChirpTable& table) {  // geom.cpp:75-99
+    if (a.size() > table.n) throw SizeMismatch("geom_eval: polynomial has more coefficients than points");
+    return eval_with_table(a, table, false, table.root);
+}
+
+std::vector<Fe> geom_eval_negative(std::span<const Fe> a, std::uint32_t n, Fe root) {  // geom.cpp:101-116
+    if (a.size() > n) throw SizeMismatch("geom_eval_negative: polynomial has more coefficients than points");
+    // the table of rho = 1/root, cached like the reference's chirp_for
+    return eval_with_table(a, *chirp_for(n, gf::inv(root)), true, root);
+}
+
+}  // namespace geom
 
 // ---- shardio.hpp ------------------------------------------------------------
 namespace shardio {

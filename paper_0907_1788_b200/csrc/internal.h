@@ -71,6 +71,13 @@ cudaError_t launch_subproduct_tree(uint32_t k, const uint32_t* xs, uint32_t* coe
 cudaError_t launch_lagrange(uint32_t k, const uint32_t* xs, const uint32_t* vs, uint32_t* out, cudaStream_t st);
 cudaError_t launch_derivative(uint32_t len, const uint32_t* a, uint32_t* out, cudaStream_t st);
 cudaError_t launch_eval(uint32_t len, uint32_t x, const uint32_t* a, uint32_t* out, cudaStream_t st);
+cudaError_t launch_chirp(uint32_t n, uint32_t root, uint32_t* b, uint32_t* binv, cudaStream_t st);
+cudaError_t launch_geom_pre(uint32_t n, uint32_t len, const uint32_t* a, const uint32_t* binv, uint32_t* c,
+                            cudaStream_t st);
+cudaError_t launch_pointwise(uint32_t m, uint32_t* c, const uint32_t* B, cudaStream_t st);
+cudaError_t launch_geom_post(uint32_t n, const uint32_t* c, const uint32_t* binv, uint32_t* out, cudaStream_t st);
+cudaError_t launch_powers_scale(uint32_t len, uint32_t rho, const uint32_t* a, uint32_t* out, cudaStream_t st);
+cudaError_t launch_negate(uint32_t n, uint32_t* x, cudaStream_t st);
 
 cudaError_t launch_fnt_tile(const Tables& t, uint32_t m, bool inverse, uint32_t scale, uint32_t L,
                             const uint32_t* in, uint32_t* out, cudaStream_t st);

@@ -170,7 +170,86 @@ __global__ void eval_kernel(uint32_t len, uint32_t x, const uint32_t* __restrict
     }
 }
 
+// ---- chirp (Bluestein) evaluation at geometric points (proj/src/geom.cpp) ----
+// b_i = root^(i (i-1) / 2) (b_0 = 1, b_{i+1} = b_i root^i), b_inverse_i = 1 / b_i
+__global__ void chirp_kernel(uint32_t n, uint32_t root, uint32_t* __restrict__ b, uint32_t* __restrict__ binv) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i + 1 < 2 * n; i += gridDim.x * blockDim.x) {
+        const uint64_t e = uint64_t(i) * (i - (i ? 1u : 0u)) / 2;
+        // root^65536 = 1 for root != 0 (Fermat); root = 0 gives b = 1, 1, 0, 0, ...
+        const uint32_t v = root % kP ? cpow(root % kP, e % 65536u) : (i < 2 ? 1u : 0u);
+        b[i] = v;
+        if (i < n && binv) binv[i] = cpow(v, kP - 2);
+    }
+}
+
+// c[n-1-j] = a_j / b_j for j < len, 0 elsewhere (2n entries)
+__global__ void geom_pre_kernel(uint32_t n, uint32_t len, const uint32_t* __restrict__ a,
+                                const uint32_t* __restrict__ binv, uint32_t* __restrict__ c) {
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < 2 * n; t += gridDim.x * blockDim.x) {
+        uint32_t v = 0;
+        if (t < n) {
+            const uint32_t j = n - 1 - t;
+            if (j < len) v = cmul(a[j] % kP, binv[j]);
+        }
+        c[t] = v;
+    }
+}
+
+__global__ void pointwise_kernel(uint32_t m, uint32_t* __restrict__ c, const uint32_t* __restrict__ B) {
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < m; t += gridDim.x * blockDim.x)
+        c[t] = cmul(c[t], B[t]);
+}
+
+// out_i = c[n-1+i] / b_i
+__global__ void geom_post_kernel(uint32_t n, const uint32_t* __restrict__ c, const uint32_t* __restrict__ binv,
+                                 uint32_t* __restrict__ out) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        out[i] = cmul(c[n - 1 + i], binv[i]);
+}
+
+// out_i = a_i rho^i (geom_eval_negative folds one power of rho into the coefficients)
+__global__ void powers_scale_kernel(uint32_t len, uint32_t rho, const uint32_t* __restrict__ a,
+                                    uint32_t* __restrict__ out) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x)
+        out[i] = cmul(a[i] % kP, cpow(rho, i));
+}
+
+// out_i = p - x_i (negation of canonical values)
+__global__ void negate_kernel(uint32_t n, uint32_t* __restrict__ x) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        x[i] = x[i] ? kP - x[i] : 0u;
+}
+
 }  // namespace
+
+unsigned grid_for(uint64_t n) { return unsigned(std::max<uint64_t>(1, std::min<uint64_t>(592, (n + 255) / 256))); }
+
+cudaError_t launch_chirp(uint32_t n, uint32_t root, uint32_t* b, uint32_t* binv, cudaStream_t st) {
+    chirp_kernel<<<grid_for(2ull * n), 256, 0, st>>>(n, root, b, binv);
+    return cudaGetLastError();
+}
+cudaError_t launch_geom_pre(uint32_t n, uint32_t len, const uint32_t* a, const uint32_t* binv, uint32_t* c,
+                            cudaStream_t st) {
+    geom_pre_kernel<<<grid_for(2ull * n), 256, 0, st>>>(n, len, a, binv, c);
+    return cudaGetLastError();
+}
+cudaError_t launch_pointwise(uint32_t m, uint32_t* c, const uint32_t* B, cudaStream_t st) {
+    pointwise_kernel<<<grid_for(m), 256, 0, st>>>(m, c, B);
+    return cudaGetLastError();
+}
+cudaError_t launch_geom_post(uint32_t n, const uint32_t* c, const uint32_t* binv, uint32_t* out, cudaStream_t st) {
+    geom_post_kernel<<<grid_for(n), 256, 0, st>>>(n, c, binv, out);
+    return cudaGetLastError();
+}
+cudaError_t launch_powers_scale(uint32_t len, uint32_t rho, const uint32_t* a, uint32_t* out, cudaStream_t st) {
+    if (!len) return cudaSuccess;
+    powers_scale_kernel<<<grid_for(len), 256, 0, st>>>(len, rho, a, out);
+    return cudaGetLastError();
+}
+cudaError_t launch_negate(uint32_t n, uint32_t* x, cudaStream_t st) {
+    negate_kernel<<<grid_for(n), 256, 0, st>>>(n, x);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_naive_dft(uint32_t r, uint32_t scale, uint32_t n, const uint32_t* in, uint32_t* out,
                              cudaStream_t st) {

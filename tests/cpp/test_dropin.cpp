@@ -14,6 +14,7 @@
 
 #include "fntrs/codec.hpp"
 #include "fntrs/instrument.hpp"
+#include "fntrs/geom.hpp"
 #include "fntrs/interp.hpp"
 #include "fntrs/poly.hpp"
 #include "fntrs/shardio.hpp"
@@ -439,6 +440,66 @@ int main() {
         const shardio::ChunkManifest man{9, 5, 2, 65536, 2, false};
         CHECK(shardio::read_manifest(shardio::write_manifest(man)) == man);
         CHECK(shardio::shard_filename(255, 3) == "00000000000000ff.3.fnt");
+    }
+    // geom.hpp: chirp evaluation (test_geom.cpp goldens and identities)
+    {
+        auto t4 = geom::build_chirp(4, gf::root_of_unity(4));
+        CHECK(geom::geom_eval(std::vector<Fe>{9}, t4) == (std::vector<Fe>{9, 9, 9, 9}));
+        CHECK(geom::geom_eval(std::vector<Fe>{5, 7}, geom::build_chirp(2, 65536)) == (std::vector<Fe>{12, 65535}));
+        auto t1 = geom::build_chirp(1, 1);
+        CHECK(geom::geom_eval(std::vector<Fe>{42}, t1) == (std::vector<Fe>{42}));
+        CHECK(geom::geom_eval(std::vector<Fe>{}, t1) == (std::vector<Fe>{0}));
+        auto t8 = geom::build_chirp(8, gf::root_of_unity(8));
+        const std::vector<Fe> a{11, 22, 33, 44, 55, 66, 77, 88};
+        CHECK(geom::geom_eval(a, t8) == (std::vector<Fe>{396, 26903, 11220, 4375, 65493, 61074, 54229, 38546}));
+        CHECK(geom::geom_eval_negative(a, 8, gf::root_of_unity(8)) ==
+              (std::vector<Fe>{38546, 54229, 61074, 65493, 4375, 11220, 26903, 396}));
+        CHECK(geom::geom_eval_negative(std::vector<Fe>{0, 1}, 2, 65536) == (std::vector<Fe>{65536, 1}));
+        CHECK(t8.b.size() == 15 && t8.b_inverse.size() == 8 && t8.b_fnt.size() == 16 && t8.b[0] == 1 && t8.b[1] == 1 &&
+              t8.b[2] == gf::root_of_unity(8) && gf::mul(t8.b[5], t8.b_inverse[5]) == 1);
+        CHECK(throws_as<SizeMismatch>([&] { geom::geom_eval(std::vector<Fe>(9, 1), t8); }));
+        CHECK(throws_as<InvalidTransformSize>([] { geom::build_chirp(6, 3); }));
+        std::mt19937_64 rng(31);
+        for (uint32_t n = 1; n <= 256; n <<= 1) {  // any root, against Horner
+            const Fe root = gf::root_of_unity(std::max(n, 4u));
+            auto t = geom::build_chirp(n, root);
+            std::vector<Fe> c(n);
+            for (auto& x : c) x = Fe(rng() % 65537);
+            auto got = geom::geom_eval(c, t);
+            bool ok = true;
+            for (uint32_t i = 0; i < n; ++i) ok = ok && got[i] == poly::eval_horner(c, gf::pow(root, i));
+            CHECK(ok);
+        }
+        {
+            std::vector<Fe> c(64);
+            for (auto& x : c) x = Fe(rng() % 65537);
+            CHECK(geom::geom_eval(c, geom::build_chirp(64, plan_for(64).root)) == fnt_forward(plan_for(64), c));
+        }
+        // cached table: two transforms per evaluation; the full domain: one
+        auto t256 = geom::chirp_for(256, gf::root_of_unity(256));
+        FntCounter c2;
+        {
+            FntScope scope(c2);
+            geom::geom_eval(std::vector<Fe>(100, 3), *t256);
+        }
+        CHECK(c2.total() == 2 && c2.count(512) == 2);
+        auto full = geom::chirp_for(65536, gf::root_of_unity(65536));
+        CHECK(full->full_domain);
+        std::vector<Fe> c(100);
+        for (auto& x : c) x = Fe(rng() % 65537);
+        FntCounter c1;
+        std::vector<Fe> got;
+        {
+            FntScope scope(c1);
+            got = geom::geom_eval(c, *full);
+        }
+        CHECK(c1.total() == 1 && c1.count(65536) == 1);
+        const Fe r = gf::root_of_unity(65536), rinv = gf::inv(r);
+        bool ok = true;
+        for (uint32_t i : {0u, 1u, 2u, 100u, 65535u}) ok = ok && got[i] == poly::eval_horner(c, gf::pow(r, i));
+        auto neg = geom::geom_eval_negative(c, 65536, r);
+        for (uint32_t j : {0u, 1u, 7u, 65535u}) ok = ok && neg[j] == poly::eval_horner(c, gf::pow(rinv, j + 1));
+        CHECK(ok);
     }
     std::printf("drop-in C++ API: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail ? 1 : 0;
