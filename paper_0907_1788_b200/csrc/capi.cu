@@ -567,18 +567,23 @@ int fntrs_gpu_plans_create(fntrs_ctx* ctx, uint32_t k, uint32_t n, uint32_t kp, 
     // shapes neither the fused nor the tile kernels take: the general column path
     const bool cols = split || (!large && (N > kTileMaxN || (!full && M > kTileMaxN)));
     if (npatterns && !positions) return fail(ctx, FNTRS_E_INVALID_ARGUMENT, "positions is null");
-    // validation (codec.cpp:32-48 order: range first, then duplicates)
-    std::vector<uint8_t> seen(n);
+    // validation (codec.cpp:32-48 order: range first, then duplicates); the
+    // duplicate check stamps positions with the pattern number, so nothing is
+    // cleared between patterns (O(kp) host work per pattern)
+    std::vector<uint32_t> seen(n, 0xFFFFFFFFu);
     for (uint32_t p = 0; p < npatterns; ++p) {
         const uint32_t* z = positions + size_t(p) * kp;
-        for (uint32_t i = 0; i < kp; ++i)
-            if (z[i] >= n)
-                return fail(ctx, FNTRS_E_POSITION_OUT_OF_RANGE, "received position " + std::to_string(z[i]) +
-                                                                   " not below n = " + std::to_string(n));
-        std::fill(seen.begin(), seen.end(), 0);
+        uint32_t zmax = 0;
+        for (uint32_t i = 0; i < kp; ++i) zmax = std::max(zmax, z[i]);
+        if (kp && zmax >= n)
+            for (uint32_t i = 0; i < kp; ++i)
+                if (z[i] >= n)
+                    return fail(ctx, FNTRS_E_POSITION_OUT_OF_RANGE, "received position " + std::to_string(z[i]) +
+                                                                       " not below n = " + std::to_string(n));
         for (uint32_t i = 0; i < kp; ++i) {
-            if (seen[z[i]]) return fail(ctx, FNTRS_E_DUPLICATE_POSITION, "received position " + std::to_string(z[i]) + " repeats");
-            seen[z[i]] = 1;
+            if (seen[z[i]] == p)
+                return fail(ctx, FNTRS_E_DUPLICATE_POSITION, "received position " + std::to_string(z[i]) + " repeats");
+            seen[z[i]] = p;
         }
     }
     DeviceGuard g(ctx->device);
