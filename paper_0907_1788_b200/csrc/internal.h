@@ -77,7 +77,6 @@ cudaError_t launch_geom_pre(uint32_t n, uint32_t len, const uint32_t* a, const u
 cudaError_t launch_pointwise(uint32_t m, uint32_t* c, const uint32_t* B, cudaStream_t st);
 cudaError_t launch_geom_post(uint32_t n, const uint32_t* c, const uint32_t* binv, uint32_t* out, cudaStream_t st);
 cudaError_t launch_powers_scale(uint32_t len, uint32_t rho, const uint32_t* a, uint32_t* out, cudaStream_t st);
-cudaError_t launch_negate(uint32_t n, uint32_t* x, cudaStream_t st);
 
 cudaError_t launch_fnt_tile(const Tables& t, uint32_t m, bool inverse, uint32_t scale, uint32_t L,
                             const uint32_t* in, uint32_t* out, cudaStream_t st);

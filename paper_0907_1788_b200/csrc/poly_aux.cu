@@ -1,9 +1,11 @@
 // poly_aux.cu -- the rest of the reference's public API on the GPU: the
 // quadratic cross-checks (naive_dft, proj/src/transform.cpp:325-343;
 // interp::lagrange_oracle, proj/src/interp.cpp:139-171), the TransformPlan
-// tables (transform.cpp:31-63), and the polynomial helpers behind poly.hpp
+// tables (transform.cpp:31-63), the polynomial helpers behind poly.hpp
 // (products, the subproduct tree, derivative, evaluation;
-// proj/src/poly.cpp:22-242). None of these is on the batched codec path
+// proj/src/poly.cpp:22-242) and the element-wise steps of geom.hpp's chirp
+// evaluation (proj/src/geom.cpp:13-116; its transforms are fntrs_gpu_fnt
+// calls, capi.cu). None of these is on the batched codec path
 // (the decoder replaces the tree by a log-domain convolution, DESIGN 4.4);
 // they let the reference's own consumers (proj/tests/acceptance.cpp) link
 // against the drop-in and get the reference's values, computed on the device.
@@ -214,12 +216,6 @@ __global__ void powers_scale_kernel(uint32_t len, uint32_t rho, const uint32_t* 
         out[i] = cmul(a[i] % kP, cpow(rho, i));
 }
 
-// out_i = p - x_i (negation of canonical values)
-__global__ void negate_kernel(uint32_t n, uint32_t* __restrict__ x) {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-        x[i] = x[i] ? kP - x[i] : 0u;
-}
-
 }  // namespace
 
 unsigned grid_for(uint64_t n) { return unsigned(std::max<uint64_t>(1, std::min<uint64_t>(592, (n + 255) / 256))); }
@@ -244,10 +240,6 @@ cudaError_t launch_geom_post(uint32_t n, const uint32_t* c, const uint32_t* binv
 cudaError_t launch_powers_scale(uint32_t len, uint32_t rho, const uint32_t* a, uint32_t* out, cudaStream_t st) {
     if (!len) return cudaSuccess;
     powers_scale_kernel<<<grid_for(len), 256, 0, st>>>(len, rho, a, out);
-    return cudaGetLastError();
-}
-cudaError_t launch_negate(uint32_t n, uint32_t* x, cudaStream_t st) {
-    negate_kernel<<<grid_for(n), 256, 0, st>>>(n, x);
     return cudaGetLastError();
 }
 
