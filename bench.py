@@ -735,6 +735,7 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    args.steps = max(1, args.steps)
     global SYSTEMATIC
     SYSTEMATIC = args.codec == "systematic"
 
